@@ -1,0 +1,156 @@
+/*
+ * cascade.h -- C ABI of the B200 (sm_100a) fast-cascade library  libcascade_b200.so
+ *
+ * Implements the time-domain cascade of G. Beylkin, "Fast convolution algorithm for state
+ * space models", arXiv 2411.17729 (PAPER.md in the reference tree; line numbers below).
+ *
+ *   Problem (§3): given the discrete LTI system of Eq. 2,
+ *     x_l = Abar x_{l-1} + Bbar u_l,   y_l = C x_l + D u_l,   x_{-1} = 0,
+ *   produce {y_l}_{l=0}^{L-1} for the truncated transfer function H_N of Eq. 5
+ *   (PAPER.md:132-135):  H_N(z) = C prod_{n=0}^{N} [I + (z^-1 Abar)^(2^n)] Bbar + D.
+ *   Method: v^(0)_l = Bbar u_l; for k = 0..N (N+1 stages, R1),
+ *     v_l <- v_l + Abar^(2^k) v_{l-2^k}  for l >= 2^k (out of place; l < 2^k unchanged);
+ *     y_l = C v_l + D u_l.
+ *   The powers Abar^(2^k) come from repeated squaring.
+ *
+ * Conventions for every entry point
+ *   - Plain pointers and sizes only; no torch or CUDA types. `stream` is a cudaStream_t
+ *     passed as void* (NULL = legacy default stream).
+ *   - Ownership: the caller allocates every buffer (device memory unless stated) including
+ *     the workspace, sized by the matching *_bytes query. The library never allocates or
+ *     frees device memory inside an apply call and keeps no state between calls
+ *     (stateless; thread-safe for distinct workspaces).
+ *   - Asynchrony: all device work is enqueued on `stream`; no host synchronisation inside
+ *     casc_powers / casc_apply / casc_apply_bank. casc_run_host synchronises `stream` once
+ *     at its end (its output lives in host memory).
+ *   - Errors: returned as casc_status; nothing is thrown across the ABI. Arguments are
+ *     validated before any work is enqueued. There is NO CPU fallback: a shape or mode the
+ *     GPU kernels do not cover returns CASC_ERR_UNSUPPORTED.
+ *   - Precision modes: CASC_FP32 stores signals and states in fp32 and computes with fp32
+ *     accuracy (3xTF32 tensor-core products, fp32 accumulation; tolerance 1e-5 relative L2,
+ *     BASELINE north_star); CASC_BF16 stores signals/states in bf16 and accumulates in fp32
+ *     (tolerance 2e-2). Model parameters (Abar, Bbar, C, D) are always passed in float64 and
+ *     rounded once, inside the library, to the format the kernels consume.
+ *   - Layouts (row-major, C order): Abar [n_sys][m][m]; Bbar [n_sys][m][p]; C [n_sys][q][m];
+ *     D [n_sys][q][p] (may be NULL = 0); u [n_sys][batch][L][p]; y [n_sys][batch][L][q].
+ *     Time is the second-fastest axis of a signal; the shift by 2^k stays inside one
+ *     sequence (one (system, batch) pair) and reads zeros before l = 0.
+ */
+#ifndef CASCADE_B200_H
+#define CASCADE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum casc_status {
+  CASC_OK = 0,
+  CASC_ERR_ARG = 1,          /* null pointer, m/p/q/L/batch < 1, N < 0, bad mode            */
+  CASC_ERR_DIM = 2,          /* inconsistent dimensions (e.g. p > m, N > N_max)               */
+  CASC_ERR_NONSQUARE = 3,    /* reserved: Abar is square by construction of the ABI          */
+  CASC_ERR_UNSUPPORTED = 4,  /* valid request the sm_100a kernels do not cover                */
+  CASC_ERR_WORKSPACE = 5,    /* ws_bytes smaller than the *_bytes query                       */
+  CASC_ERR_CUDA = 6,         /* a CUDA runtime call failed (launch, copy, device mismatch)    */
+  CASC_ERR_NCCL = 7          /* reserved for the sequence-sharded path                        */
+} casc_status;
+
+typedef enum casc_mode {
+  CASC_FP32 = 0,             /* fp32 storage, fp32-accurate math (3xTF32 tensor cores)        */
+  CASC_BF16 = 1              /* bf16 storage, fp32 accumulation                               */
+} casc_mode;
+
+/* Human-readable name of a status code (static string). */
+const char* casc_status_str(int status);
+
+/* Library version (major*10000 + minor*100 + patch) and the compute capability it targets
+ * (100 = sm_100a). */
+int casc_version(void);
+int casc_target_sm(void);
+
+/* ----------------------------------------------------------------------------------------
+ * a1  Powers by repeated squaring -- PAPER.md:164-166 ("we need to compute the powers of
+ *     the matrix Abar, Abar^2, Abar^4, Abar^8, ..."); accuracy remark PAPER.md:274-277.
+ *
+ * For each system s: P_0 = Abar_s, P_{k+1} = P_k P_k (float64 throughout, k < N_s), then
+ * each P_k (k <= N_s) is rounded once to the storage format of `mode` (fp32: tf32 hi + tf32
+ * lo pair, round-to-nearest-away; bf16: round-to-nearest-even).
+ *   n_sys   number of independent systems (1 for a single MIMO system).
+ *   m       state dimension (Abar is m x m).
+ *   N_host  HOST int array [n_sys]: truncation order N_s (0 <= N_s <= N_max).
+ *   N_max   slot count of the pack (pack holds N_max+1 powers per system).
+ *   Abar    DEVICE float64 [n_sys][m][m], read only.
+ *   pack    DEVICE buffer of casc_pack_bytes(n_sys, m, N_max, mode) bytes, written. Opaque:
+ *           consumed only by casc_apply / casc_apply_bank with the same (n_sys, m, N_max, mode).
+ * Errors: CASC_ERR_ARG (null, m < 1, n_sys < 1, N_max < 0), CASC_ERR_DIM (N_s out of range),
+ *         CASC_ERR_UNSUPPORTED (m > 4096), CASC_ERR_CUDA.
+ * -------------------------------------------------------------------------------------- */
+size_t casc_pack_bytes(int n_sys, int m, int N_max, int mode);
+int casc_powers(int n_sys, int m, const int* N_host, int N_max, const double* Abar, int mode,
+                void* pack, void* stream);
+
+/* ----------------------------------------------------------------------------------------
+ * a2-a5  Apply one LTI system (MIMO or SISO) to `batch` sequences of length L --
+ *     PAPER.md:185-229 (§3): v^(0) = Bbar u (:187), N+1 out-of-place shifted stages
+ *     (:193-225, general step :217-225), y = C v + D u (:226-229). Stages with 2^k >= L are
+ *     the identity and are skipped (R20).
+ *   m, p, q   state / input / output dimensions (1 <= p, q <= m).
+ *   L, batch  sequence length and number of sequences.
+ *   N         truncation order (N+1 stages); pack must come from casc_powers with N_s = N.
+ *   mode      CASC_FP32 (u, y are float32) or CASC_BF16 (u, y are bf16 bit patterns).
+ *   pack      DEVICE, from casc_powers(1, m, &N, N_max, ...) (N_max is read from the call
+ *             that built it: pass it again as N_max).
+ *   Bbar, C, D  DEVICE float64 [m][p], [q][m], [q][p] (D may be NULL meaning D = 0).
+ *   u         DEVICE [batch][L][p];  y  DEVICE [batch][L][q] (written).
+ *   ws        DEVICE workspace of >= casc_apply_workspace_bytes(...) bytes.
+ *   effective_stages  HOST int* (may be NULL): #{k <= N : 2^k < L}.
+ * Errors: CASC_ERR_ARG, CASC_ERR_DIM (p > m or q > m), CASC_ERR_WORKSPACE,
+ *         CASC_ERR_UNSUPPORTED, CASC_ERR_CUDA.
+ * -------------------------------------------------------------------------------------- */
+size_t casc_apply_workspace_bytes(int m, int p, int q, int64_t L, int batch, int N, int mode);
+int casc_apply(int m, int p, int q, int64_t L, int batch, int N, int N_max, int mode,
+               const void* pack, const double* Bbar, const double* C, const double* D,
+               const void* u, void* y, void* ws, size_t ws_bytes, int* effective_stages,
+               void* stream);
+
+/* ----------------------------------------------------------------------------------------
+ * a6  Bank of independent SISO channels (p = q = 1), each with its own (Abar_c, Bbar_c,
+ *     C_c, D_c, N_c) -- the HiPPO example of PAPER.md:253-273 (Eq. 9-10) applied per
+ *     channel with the cascade of PAPER.md:185-229.
+ *   n_ch      number of channels; N_host HOST int [n_ch]; pack from
+ *             casc_powers(n_ch, m, N_host, N_max, ...).
+ *   Bbar      DEVICE float64 [n_ch][m]; C DEVICE float64 [n_ch][m]; D DEVICE float64 [n_ch]
+ *             (may be NULL = 0).
+ *   u, y      DEVICE [n_ch][batch][L] in the storage dtype of `mode`.
+ * Errors as casc_apply.
+ * -------------------------------------------------------------------------------------- */
+size_t casc_bank_workspace_bytes(int n_ch, int m, int64_t L, int batch, int N_max, int mode);
+int casc_apply_bank(int n_ch, int m, int64_t L, int batch, const int* N_host, int N_max,
+                    int mode, const void* pack, const double* Bbar, const double* C,
+                    const double* D, const void* u, void* y, void* ws, size_t ws_bytes,
+                    void* stream);
+
+/* ----------------------------------------------------------------------------------------
+ * End-to-end entry with HOST buffers: copies Abar, Bbar, C, D (float64) and u (storage
+ * dtype) host -> device, runs casc_powers + casc_apply / casc_apply_bank, copies y back to
+ * host, and synchronises `stream`. Host buffers should be pinned for asynchronous copies.
+ *   n_sys == 1 with any (p, q) runs the single-system path; n_sys > 1 requires p = q = 1
+ *   (bank). dev_ws: DEVICE buffer of casc_run_host_bytes(...) bytes.
+ * -------------------------------------------------------------------------------------- */
+size_t casc_run_host_bytes(int n_sys, int m, int p, int q, int64_t L, int batch, int N_max,
+                           int mode);
+int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const int* N_host,
+                  int N_max, int mode, const double* Abar_h, const double* Bbar_h,
+                  const double* C_h, const double* D_h, const void* u_h, void* y_h,
+                  void* dev_ws, size_t dev_ws_bytes, void* stream);
+
+/* Number of kernel launches the last successful apply/powers call on this host thread
+ * enqueued (bench evidence for "gpu_launches"). */
+int casc_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CASCADE_B200_H */

@@ -1,0 +1,392 @@
+// C ABI of libcascade_b200 (declared in include/cascade.h) and the host-side engine that
+// sequences the kernels of the cascade on one stream.
+//
+// Step schedule for system s with effective order Ne = min(N_s, floor(log2(L-1))) (stages with
+// 2^k >= L are identities, R20):
+//   derived   (fp64)   Abar Bbar, C P_Ne, C Bbar + D, C Abar Bbar              (tiny GEMMs)
+//   first     (a2)     v^(1)_l = Bbar u_l + Abar Bbar u_{l-1}        = stages "B u" and k = 0
+//   stage k   (a4)     v^(k+1)_l = v^(k)_l + P_k v^(k)_{l-2^k}           k = 1 .. Ne-1
+//   last      (a5)     y_l = C v_l + (C P_Ne) v_{l-2^Ne} + D u_l           = stage Ne and y
+//   Ne == 0            y_l = (C Bbar + D) u_l + C Abar Bbar u_{l-1}      (one kernel)
+// The fused first/last forms are exact regroupings of PAPER.md:187 / :217-228 (associativity;
+// DESIGN.md R21). v^(k) ping-pongs between two workspace buffers: after stage k it sits in
+// buffer k % 2.
+#include <cstring>
+#include <vector>
+#include <numeric>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "engine.cuh"
+
+namespace casc {
+thread_local int g_launches = 0;
+
+static int eff_order(int N, int64_t L) {
+  if (L <= 2) return 0;
+  int kstar = 0;                                   // largest k with 2^k < L
+  while (((int64_t)1 << (kstar + 1)) < L) ++kstar;
+  return N < kstar ? N : kstar;
+}
+
+struct ApplyWs {
+  int* meta;                        // Neff | order | direct | groupA | groupB   (5 n ints)
+  double *AB64, *CP64, *CBD64, *CAB64;
+  float *Bb32, *AB32, *C32, *CP32, *D32, *CBD32, *CAB32;
+  void *Va, *Vb;
+  size_t bytes;
+};
+
+static ApplyWs carve_apply(void* ws, int n, int m, int p, int q, int64_t L, int batch, int mode) {
+  Carver c(ws);
+  ApplyWs w{};
+  const size_t es = (mode == CASC_BF16) ? 2 : 4;
+  w.meta = c.take<int>((size_t)5 * n);
+  w.AB64 = c.take<double>((size_t)n * m * p);
+  w.CP64 = c.take<double>((size_t)n * q * m);
+  w.CBD64 = c.take<double>((size_t)n * q * p);
+  w.CAB64 = c.take<double>((size_t)n * q * p);
+  w.Bb32 = c.take<float>((size_t)n * m * p);
+  w.AB32 = c.take<float>((size_t)n * m * p);
+  w.C32 = c.take<float>((size_t)n * q * m);
+  w.CP32 = c.take<float>((size_t)n * q * m);
+  w.D32 = c.take<float>((size_t)n * q * p);
+  w.CBD32 = c.take<float>((size_t)n * q * p);
+  w.CAB32 = c.take<float>((size_t)n * q * p);
+  const size_t vbytes = (size_t)n * batch * (size_t)L * m * es;
+  w.Va = c.take<char>(vbytes);
+  w.Vb = c.take<char>(vbytes);
+  w.bytes = c.bytes();
+  return w;
+}
+
+size_t apply_ws_bytes(int n, int m, int p, int q, int64_t L, int batch, int mode) {
+  return carve_apply(nullptr, n, m, p, q, L, batch, mode).bytes;
+}
+
+int validate_common(int n, int m, int p, int q, int64_t L, int batch, int N_max, int mode) {
+  if (n < 1 || m < 1 || p < 1 || q < 1 || L < 1 || batch < 1 || N_max < 0) return CASC_ERR_ARG;
+  if (mode != CASC_FP32 && mode != CASC_BF16) return CASC_ERR_ARG;
+  if (p > m || q > m) return CASC_ERR_DIM;
+  if (N_max > 62) return CASC_ERR_DIM;
+  if (m > 4096) return CASC_ERR_UNSUPPORTED;
+  return CASC_OK;
+}
+
+// The engine: n systems sharing (m, p, q), per-system N_host[s].
+int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_host, int N_max,
+                 int mode, const void* pack, const double* Bbar, const double* C, const double* D,
+                 const void* u, void* y, void* ws, size_t ws_bytes, cudaStream_t st) {
+  int rc = validate_common(n, m, p, q, L, batch, N_max, mode);
+  if (rc) return rc;
+  if (!N_host || !pack || !Bbar || !C || !u || !y || !ws) return CASC_ERR_ARG;
+  for (int s = 0; s < n; ++s)
+    if (N_host[s] < 0 || N_host[s] > N_max) return CASC_ERR_DIM;
+  ApplyWs w = carve_apply(ws, n, m, p, q, L, batch, mode);
+  if (ws_bytes < w.bytes) return CASC_ERR_WORKSPACE;
+  PackLayout P = pack_layout(const_cast<void*>(pack), n, m, N_max, mode);
+  const bool bf = (mode == CASC_BF16);
+  const int64_t mm = (int64_t)m * m;
+
+  // ---- host metadata: effective orders and launch lists
+  std::vector<int> meta((size_t)5 * n);
+  int* Neff = meta.data();
+  int *order = Neff + n, *direct = Neff + 2 * n, *gA = Neff + 3 * n, *gB = Neff + 4 * n;
+  int maxNe = 0;
+  for (int s = 0; s < n; ++s) {
+    Neff[s] = eff_order(N_host[s], L);
+    maxNe = std::max(maxNe, Neff[s]);
+  }
+  int n1 = 0, n0 = 0, na = 0, nb = 0;
+  std::vector<int> idx(n);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return Neff[a] > Neff[b]; });
+  for (int s : idx) {
+    if (Neff[s] >= 1) {
+      order[n1++] = s;
+      if ((Neff[s] - 1) % 2 == 0) gA[na++] = s; else gB[nb++] = s;
+    } else {
+      direct[n0++] = s;
+    }
+  }
+  CASC_TRY(cudaMemcpyAsync(w.meta, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  const int* dNeff = w.meta;
+  const int *dorder = w.meta + n, *ddirect = w.meta + 2 * n, *dgA = w.meta + 3 * n, *dgB = w.meta + 4 * n;
+
+  // ---- derived float64 matrices (tiny)
+  {
+    DgemmArg a{};
+    // AB = P_0 Bbar  (m x p)
+    a = DgemmArg{};
+    a.M = m; a.N = p; a.K = m;
+    a.A = P.p64; a.lda = m; a.sA = (N_max + 1) * mm;
+    a.B = Bbar; a.ldb = p; a.sB = (int64_t)m * p;
+    a.C = w.AB64; a.ldc = p; a.sC = (int64_t)m * p;
+    if ((rc = launch_dgemm(a, n, st))) return rc;
+    // CP = C P_Ne  (q x m)
+    a = DgemmArg{};
+    a.M = q; a.N = m; a.K = m;
+    a.A = C; a.lda = m; a.sA = (int64_t)q * m;
+    a.B = P.p64; a.ldb = m; a.sB = (N_max + 1) * mm; a.nB = mm; a.selB = dNeff;
+    a.C = w.CP64; a.ldc = m; a.sC = (int64_t)q * m;
+    if ((rc = launch_dgemm(a, n, st))) return rc;
+    // CBD = C Bbar + D  (q x p)
+    a = DgemmArg{};
+    a.M = q; a.N = p; a.K = m;
+    a.A = C; a.lda = m; a.sA = (int64_t)q * m;
+    a.B = Bbar; a.ldb = p; a.sB = (int64_t)m * p;
+    a.C = w.CBD64; a.ldc = p; a.sC = (int64_t)q * p;
+    a.Cadd = D; a.sCadd = (int64_t)q * p;
+    if ((rc = launch_dgemm(a, n, st))) return rc;
+    // CAB = C (Abar Bbar)  (q x p)
+    a = DgemmArg{};
+    a.M = q; a.N = p; a.K = m;
+    a.A = C; a.lda = m; a.sA = (int64_t)q * m;
+    a.B = w.AB64; a.ldb = p; a.sB = (int64_t)m * p;
+    a.C = w.CAB64; a.ldc = p; a.sC = (int64_t)q * p;
+    if ((rc = launch_dgemm(a, n, st))) return rc;
+  }
+  if ((rc = launch_f64_to_f32(Bbar, w.Bb32, (int64_t)n * m * p, st))) return rc;
+  if ((rc = launch_f64_to_f32(w.AB64, w.AB32, (int64_t)n * m * p, st))) return rc;
+  if ((rc = launch_f64_to_f32(C, w.C32, (int64_t)n * q * m, st))) return rc;
+  if ((rc = launch_f64_to_f32(w.CP64, w.CP32, (int64_t)n * q * m, st))) return rc;
+  if ((rc = launch_f64_to_f32(w.CBD64, w.CBD32, (int64_t)n * q * p, st))) return rc;
+  if ((rc = launch_f64_to_f32(w.CAB64, w.CAB32, (int64_t)n * q * p, st))) return rc;
+  if (D) {
+    if ((rc = launch_f64_to_f32(D, w.D32, (int64_t)n * q * p, st))) return rc;
+  } else {
+    CASC_TRY(cudaMemsetAsync(w.D32, 0, sizeof(float) * (size_t)n * q * p, st));
+  }
+
+  const int64_t u_sys = (int64_t)batch * L * p, y_sys = (int64_t)batch * L * q;
+  const int64_t v_sys = (int64_t)batch * L * m;
+  auto base = [&](GemmArg& g) {
+    g = GemmArg{};
+    g.L = L; g.batch = batch; g.Neff = dNeff;
+  };
+  auto src = [&](SrcArg& sa, const void* A, int64_t A_sys, int K, const void* W, int64_t W_sys,
+                 int w_bf16, const float* Wlo, int64_t shift, int from_N) {
+    sa.A = A; sa.A_sys = A_sys; sa.K = K; sa.a_bf16 = bf;
+    sa.W = W; sa.W_sys = W_sys; sa.w_bf16 = w_bf16; sa.Wlo = Wlo;
+    sa.shift = shift; sa.shift_from_N = from_N;
+  };
+
+  // ---- Ne == 0 systems: y = (C Bbar + D) u_l + (C Abar Bbar) u_{l-1}
+  if (n0 > 0) {
+    GemmArg g; base(g);
+    src(g.src[0], u, u_sys, p, w.CBD32, (int64_t)q * p, 0, nullptr, 0, 0);
+    src(g.src[1], u, u_sys, p, w.CAB32, (int64_t)q * p, 0, nullptr, 1, 0);
+    g.n_src = 2;
+    g.out = y; g.out_sys = y_sys; g.out_bf16 = bf; g.n_out = q;
+    g.sys_list = ddirect; g.n_list = n0;
+    if ((rc = launch_simt_gemm(g, st))) return rc;
+  }
+  if (n1 == 0) return CASC_OK;
+
+  // ---- first (a2): v^(1) = Bbar u_l + Abar Bbar u_{l-1}  -> Va
+  {
+    GemmArg g; base(g);
+    src(g.src[0], u, u_sys, p, w.Bb32, (int64_t)m * p, 0, nullptr, 0, 0);
+    src(g.src[1], u, u_sys, p, w.AB32, (int64_t)m * p, 0, nullptr, 1, 0);
+    g.n_src = 2;
+    g.out = w.Va; g.out_sys = v_sys; g.out_bf16 = bf; g.n_out = m;
+    g.sys_list = dorder; g.n_list = n1;
+    if ((rc = launch_simt_gemm(g, st))) return rc;
+  }
+  // ---- stages k = 1 .. maxNe-1 (a4) over the systems with Neff >= k+1 (a prefix of order)
+  for (int k = 1; k <= maxNe - 1; ++k) {
+    int cnt = 0;
+    while (cnt < n1 && Neff[order[cnt]] >= k + 1) ++cnt;
+    void* Vs = (k - 1) % 2 == 0 ? w.Va : w.Vb;
+    void* Vd = (k % 2 == 0) ? w.Va : w.Vb;
+    GemmArg g; base(g);
+    if (bf) {
+      src(g.src[0], Vs, v_sys, m, P.b16 + k * mm, (N_max + 1) * mm, 1, nullptr, (int64_t)1 << k, 0);
+    } else {
+      const float* hi = P.f32 + (int64_t)k * 2 * mm;
+      src(g.src[0], Vs, v_sys, m, hi, (N_max + 1) * 2 * mm, 0, hi + mm, (int64_t)1 << k, 0);
+    }
+    g.n_src = 1;
+    g.R = Vs; g.R_sys = v_sys;
+    g.out = Vd; g.out_sys = v_sys; g.out_bf16 = bf; g.n_out = m;
+    g.sys_list = dorder; g.n_list = cnt;
+    if ((rc = launch_simt_gemm(g, st))) return rc;
+  }
+  // ---- last (a5): y = C v + (C P_Ne) v_{l-2^Ne} + D u, per buffer parity group
+  for (int grp = 0; grp < 2; ++grp) {
+    const int cnt = grp == 0 ? na : nb;
+    if (cnt == 0) continue;
+    void* V = grp == 0 ? w.Va : w.Vb;
+    GemmArg g; base(g);
+    src(g.src[0], V, v_sys, m, w.C32, (int64_t)q * m, 0, nullptr, 0, 0);
+    src(g.src[1], V, v_sys, m, w.CP32, (int64_t)q * m, 0, nullptr, 0, 1);
+    src(g.src[2], u, u_sys, p, w.D32, (int64_t)q * p, 0, nullptr, 0, 0);
+    g.n_src = D ? 3 : 2;
+    g.out = y; g.out_sys = y_sys; g.out_bf16 = bf; g.n_out = q;
+    g.sys_list = grp == 0 ? dgA : dgB; g.n_list = cnt;
+    if ((rc = launch_simt_gemm(g, st))) return rc;
+  }
+  return CASC_OK;
+}
+
+int engine_powers(int n, int m, const int* N_host, int N_max, const double* Abar, int mode,
+                  void* pack, cudaStream_t st) {
+  if (n < 1 || m < 1 || N_max < 0 || !N_host || !Abar || !pack) return CASC_ERR_ARG;
+  if (mode != CASC_FP32 && mode != CASC_BF16) return CASC_ERR_ARG;
+  if (N_max > 62) return CASC_ERR_DIM;
+  if (m > 4096) return CASC_ERR_UNSUPPORTED;
+  for (int s = 0; s < n; ++s)
+    if (N_host[s] < 0 || N_host[s] > N_max) return CASC_ERR_DIM;
+  PackLayout P = pack_layout(pack, n, m, N_max, mode);
+  const int64_t mm = (int64_t)m * m, sys = (N_max + 1) * mm;
+  CASC_TRY(cudaMemcpyAsync(P.hdr, N_host, sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  // P_0 = Abar (strided copy into slot 0 of every system)
+  CASC_TRY(cudaMemcpy2DAsync(P.p64, sys * sizeof(double), Abar, mm * sizeof(double),
+                             mm * sizeof(double), n, cudaMemcpyDeviceToDevice, st));
+  int maxN = *std::max_element(N_host, N_host + n);
+  for (int k = 1; k <= maxN; ++k) {               // P_k = P_{k-1} P_{k-1}
+    DgemmArg a{};
+    a.M = m; a.N = m; a.K = m;
+    a.A = P.p64 + (k - 1) * mm; a.lda = m; a.sA = sys;
+    a.B = P.p64 + (k - 1) * mm; a.ldb = m; a.sB = sys;
+    a.C = P.p64 + k * mm; a.ldc = m; a.sC = sys;
+    a.skip_below = P.hdr; a.level = k;
+    int rc = launch_dgemm(a, n, st);
+    if (rc) return rc;
+  }
+  return launch_pack(P, n, N_max, m, st);
+}
+
+}  // namespace casc
+
+using namespace casc;
+
+extern "C" {
+
+const char* casc_status_str(int s) {
+  switch (s) {
+    case CASC_OK: return "CASC_OK";
+    case CASC_ERR_ARG: return "CASC_ERR_ARG";
+    case CASC_ERR_DIM: return "CASC_ERR_DIM";
+    case CASC_ERR_NONSQUARE: return "CASC_ERR_NONSQUARE";
+    case CASC_ERR_UNSUPPORTED: return "CASC_ERR_UNSUPPORTED";
+    case CASC_ERR_WORKSPACE: return "CASC_ERR_WORKSPACE";
+    case CASC_ERR_CUDA: return "CASC_ERR_CUDA";
+    case CASC_ERR_NCCL: return "CASC_ERR_NCCL";
+    default: return "CASC_ERR_UNKNOWN";
+  }
+}
+
+int casc_version(void) { return 100; }
+int casc_target_sm(void) { return 100; }
+int casc_last_launch_count(void) { return g_launches; }
+
+size_t casc_pack_bytes(int n_sys, int m, int N_max, int mode) {
+  if (n_sys < 1 || m < 1 || N_max < 0) return 0;
+  return pack_layout(nullptr, n_sys, m, N_max, mode).bytes;
+}
+
+int casc_powers(int n_sys, int m, const int* N_host, int N_max, const double* Abar, int mode,
+                void* pack, void* stream) {
+  g_launches = 0;
+  return engine_powers(n_sys, m, N_host, N_max, Abar, mode, pack, (cudaStream_t)stream);
+}
+
+size_t casc_apply_workspace_bytes(int m, int p, int q, int64_t L, int batch, int N, int mode) {
+  (void)N;
+  if (m < 1 || p < 1 || q < 1 || L < 1 || batch < 1) return 0;
+  return apply_ws_bytes(1, m, p, q, L, batch, mode);
+}
+
+int casc_apply(int m, int p, int q, int64_t L, int batch, int N, int N_max, int mode,
+               const void* pack, const double* Bbar, const double* C, const double* D,
+               const void* u, void* y, void* ws, size_t ws_bytes, int* effective_stages,
+               void* stream) {
+  g_launches = 0;
+  if (N < 0) return CASC_ERR_ARG;
+  int rc = engine_apply(1, m, p, q, L, batch, &N, N_max, mode, pack, Bbar, C, D, u, y, ws,
+                        ws_bytes, (cudaStream_t)stream);
+  if (rc == CASC_OK && effective_stages) {
+    int e = 0;
+    for (int k = 0; k <= N; ++k)
+      if (((int64_t)1 << k) < L) ++e;
+    *effective_stages = e;
+  }
+  return rc;
+}
+
+size_t casc_bank_workspace_bytes(int n_ch, int m, int64_t L, int batch, int N_max, int mode) {
+  (void)N_max;
+  if (n_ch < 1 || m < 1 || L < 1 || batch < 1) return 0;
+  return apply_ws_bytes(n_ch, m, 1, 1, L, batch, mode);
+}
+
+int casc_apply_bank(int n_ch, int m, int64_t L, int batch, const int* N_host, int N_max,
+                    int mode, const void* pack, const double* Bbar, const double* C,
+                    const double* D, const void* u, void* y, void* ws, size_t ws_bytes,
+                    void* stream) {
+  g_launches = 0;
+  return engine_apply(n_ch, m, 1, 1, L, batch, N_host, N_max, mode, pack, Bbar, C, D, u, y, ws,
+                      ws_bytes, (cudaStream_t)stream);
+}
+
+struct HostWs {
+  double *Abar, *Bbar, *C, *D;
+  void *u, *y, *pack, *apply_ws;
+  size_t apply_bytes, bytes;
+};
+
+static HostWs carve_host(void* base, int n, int m, int p, int q, int64_t L, int batch, int N_max,
+                         int mode) {
+  Carver c(base);
+  HostWs h{};
+  const size_t es = (mode == CASC_BF16) ? 2 : 4;
+  h.Abar = c.take<double>((size_t)n * m * m);
+  h.Bbar = c.take<double>((size_t)n * m * p);
+  h.C = c.take<double>((size_t)n * q * m);
+  h.D = c.take<double>((size_t)n * q * p);
+  h.u = c.take<char>((size_t)n * batch * L * p * es);
+  h.y = c.take<char>((size_t)n * batch * L * q * es);
+  h.pack = c.take<char>(pack_layout(nullptr, n, m, N_max, mode).bytes);
+  h.apply_bytes = apply_ws_bytes(n, m, p, q, L, batch, mode);
+  h.apply_ws = c.take<char>(h.apply_bytes);
+  h.bytes = c.bytes();
+  return h;
+}
+
+size_t casc_run_host_bytes(int n_sys, int m, int p, int q, int64_t L, int batch, int N_max,
+                           int mode) {
+  if (n_sys < 1 || m < 1 || p < 1 || q < 1 || L < 1 || batch < 1 || N_max < 0) return 0;
+  return carve_host(nullptr, n_sys, m, p, q, L, batch, N_max, mode).bytes;
+}
+
+int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const int* N_host,
+                  int N_max, int mode, const double* Abar_h, const double* Bbar_h,
+                  const double* C_h, const double* D_h, const void* u_h, void* y_h,
+                  void* dev_ws, size_t dev_ws_bytes, void* stream) {
+  int rc = validate_common(n_sys, m, p, q, L, batch, N_max, mode);
+  if (rc) return rc;
+  if (!N_host || !Abar_h || !Bbar_h || !C_h || !u_h || !y_h || !dev_ws) return CASC_ERR_ARG;
+  if (n_sys > 1 && (p != 1 || q != 1)) return CASC_ERR_UNSUPPORTED;
+  HostWs h = carve_host(dev_ws, n_sys, m, p, q, L, batch, N_max, mode);
+  if (dev_ws_bytes < h.bytes) return CASC_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t es = (mode == CASC_BF16) ? 2 : 4;
+  CASC_TRY(cudaMemcpyAsync(h.Abar, Abar_h, sizeof(double) * n_sys * m * m, cudaMemcpyHostToDevice, st));
+  CASC_TRY(cudaMemcpyAsync(h.Bbar, Bbar_h, sizeof(double) * n_sys * m * p, cudaMemcpyHostToDevice, st));
+  CASC_TRY(cudaMemcpyAsync(h.C, C_h, sizeof(double) * n_sys * q * m, cudaMemcpyHostToDevice, st));
+  if (D_h) CASC_TRY(cudaMemcpyAsync(h.D, D_h, sizeof(double) * n_sys * q * p, cudaMemcpyHostToDevice, st));
+  CASC_TRY(cudaMemcpyAsync(h.u, u_h, es * n_sys * batch * L * p, cudaMemcpyHostToDevice, st));
+  rc = engine_powers(n_sys, m, N_host, N_max, h.Abar, mode, h.pack, st);
+  if (rc) return rc;
+  const int launches_powers = g_launches;
+  rc = engine_apply(n_sys, m, p, q, L, batch, N_host, N_max, mode, h.pack, h.Bbar, h.C,
+                    D_h ? h.D : nullptr, h.u, h.y, h.apply_ws, h.apply_bytes, st);
+  if (rc) return rc;
+  CASC_TRY(cudaMemcpyAsync(y_h, h.y, es * n_sys * batch * L * q, cudaMemcpyDeviceToHost, st));
+  CASC_TRY(cudaStreamSynchronize(st));
+  (void)launches_powers;
+  return CASC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,85 @@
+// Shared device/host helpers of libcascade_b200 (internal; not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stddef.h>
+
+#include "../../include/cascade.h"
+
+namespace casc {
+
+// per-host-thread launch counter (casc_last_launch_count)
+extern thread_local int g_launches;
+inline void count_launch(int n = 1) { g_launches += n; }
+
+#define CASC_TRY(expr)                                      \
+  do {                                                      \
+    cudaError_t e__ = (expr);                               \
+    if (e__ != cudaSuccess) return CASC_ERR_CUDA;           \
+  } while (0)
+
+#define CASC_LAUNCHED()                                     \
+  do {                                                      \
+    ::casc::count_launch();                                 \
+    if (cudaPeekAtLastError() != cudaSuccess) {             \
+      (void)cudaGetLastError();                             \
+      return CASC_ERR_CUDA;                                 \
+    }                                                       \
+  } while (0)
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Bump allocator used both to size (base == nullptr) and to carve a workspace.
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base(static_cast<char*>(b)) {}
+  template <class T>
+  T* take(size_t count) {
+    off = align_up(off, 256);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+  size_t bytes() const { return align_up(off, 256); }
+};
+
+// Pack layout (opaque to callers):
+//   header  : int N_s[n_sys]
+//   p64     : double [n_sys][N_max+1][m][m]          float64 powers P_k = Abar^(2^k)
+//   fp32    : float  [n_sys][N_max+1][2][m][m]       tf32 hi, tf32 lo   (mode FP32)
+//   bf16    : bf16   [n_sys][N_max+1][m][m]          (mode BF16)
+struct PackLayout {
+  int* hdr;
+  double* p64;
+  float* f32;
+  __nv_bfloat16* b16;
+  size_t bytes;
+};
+
+inline PackLayout pack_layout(void* pack, int n_sys, int m, int N_max, int mode) {
+  Carver c(pack);
+  PackLayout L{};
+  const size_t mm = (size_t)m * m, slots = (size_t)n_sys * (N_max + 1);
+  L.hdr = c.take<int>(n_sys);
+  L.p64 = c.take<double>(slots * mm);
+  L.f32 = nullptr;
+  L.b16 = nullptr;
+  if (mode == CASC_FP32) L.f32 = c.take<float>(slots * 2 * mm);
+  else L.b16 = c.take<__nv_bfloat16>(slots * mm);
+  L.bytes = c.bytes();
+  return L;
+}
+
+__device__ __forceinline__ float to_f32(float x) { return x; }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+}  // namespace casc

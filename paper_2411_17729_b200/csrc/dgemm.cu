@@ -1,0 +1,135 @@
+// Batched float64 GEMM used for (a1) the repeated squaring P_{k+1} = P_k P_k of
+// PAPER.md:164-166 and for the small derived products of the fused first / last stages
+// (Abar Bbar, C P_N, C Bbar + D, C Abar Bbar). Powers are formed in float64 and rounded
+// once afterwards, as PAPER.md:275-277 suggests ("powers ... can always be computed with a
+// large number of accurate digits and used with as many digits as the application requires").
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace casc {
+
+// 64x64 output tile per 256-thread block, 4x4 register micro-tile, K chunks of 16.
+__global__ void __launch_bounds__(256) dgemm_batched_kernel(DgemmArg a) {
+  const int s = blockIdx.z;
+  if (a.skip_below && a.skip_below[s] < a.level) return;
+  const int64_t selA = a.selA ? a.selA[s] : 0, selB = a.selB ? a.selB[s] : 0;
+  const double* A = a.A + s * a.sA + selA * a.nA;
+  const double* B = a.B + s * a.sB + selB * a.nB;
+  double* C = a.C + s * a.sC;
+  const double* Cadd = a.Cadd ? a.Cadd + s * a.sCadd : nullptr;
+
+  __shared__ double As[16][64 + 1];
+  __shared__ double Bs[16][64 + 1];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int row0 = blockIdx.y * 64, col0 = blockIdx.x * 64;
+  double acc[4][4] = {};
+  for (int k0 = 0; k0 < a.K; k0 += 16) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int e = tid + i * 256;             // 1024 elements of a 64x16 A chunk
+      int r = e / 16, kk = e % 16;
+      int gr = row0 + r, gk = k0 + kk;
+      As[kk][r] = (gr < a.M && gk < a.K) ? A[(int64_t)gr * a.lda + gk] : 0.0;
+      int kb = e / 64, c = e % 64;       // 16x64 B chunk
+      int gkb = k0 + kb, gc = col0 + c;
+      Bs[kb][c] = (gkb < a.K && gc < a.N) ? B[(int64_t)gkb * a.ldb + gc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int gr = row0 + ty * 4 + i;
+    if (gr >= a.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int gc = col0 + tx * 4 + j;
+      if (gc >= a.N) continue;
+      double v = acc[i][j];
+      if (Cadd) v += Cadd[(int64_t)gr * a.ldc + gc];
+      C[(int64_t)gr * a.ldc + gc] = v;
+    }
+  }
+}
+
+int launch_dgemm(const DgemmArg& a, int n_sys, cudaStream_t st) {
+  if (a.M <= 0 || a.N <= 0 || n_sys <= 0) return CASC_OK;
+  dim3 grid((unsigned)ceil_div(a.N, 64), (unsigned)ceil_div(a.M, 64), (unsigned)n_sys);
+  dgemm_batched_kernel<<<grid, 256, 0, st>>>(a);
+  CASC_LAUNCHED();
+  return CASC_OK;
+}
+
+// Round each float64 power once to the storage format (R17):
+//   FP32 mode: hi = rna_tf32(fp32(P)), lo = rna_tf32(fp32(P - hi))  -> P ~ hi + lo to ~2^-22
+//   BF16 mode: RN-even bf16 of fp32(P)
+__global__ void pack_powers_kernel(const int* hdr, const double* p64, float* f32,
+                                   __nv_bfloat16* b16, int n_sys, int N_max, int m) {
+  const int64_t mm = (int64_t)m * m;
+  const int64_t total = (int64_t)n_sys * (N_max + 1) * mm;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t slot = e / mm, ij = e % mm;
+    const int s = (int)(slot / (N_max + 1)), k = (int)(slot % (N_max + 1));
+    if (k > hdr[s]) continue;
+    const double p = p64[e];
+    if (f32) {
+      float hi = tf32_rna((float)p);
+      float lo = tf32_rna((float)(p - (double)hi));
+      f32[slot * 2 * mm + ij] = hi;
+      f32[slot * 2 * mm + mm + ij] = lo;
+    } else {
+      b16[e] = __float2bfloat16_rn((float)p);
+    }
+  }
+}
+
+int launch_pack(const PackLayout& P, int n_sys, int N_max, int m, cudaStream_t st) {
+  const int64_t total = (int64_t)n_sys * (N_max + 1) * m * m;
+  int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
+  pack_powers_kernel<<<blocks, 256, 0, st>>>(P.hdr, P.p64, P.f32, P.b16, n_sys, N_max, m);
+  CASC_LAUNCHED();
+  return CASC_OK;
+}
+
+__global__ void f64_to_f32_kernel(const double* src, float* dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = (float)src[i];
+}
+
+int launch_f64_to_f32(const double* src, float* dst, int64_t n, cudaStream_t st) {
+  if (n <= 0) return CASC_OK;
+  int blocks = (int)std::min<int64_t>(ceil_div(n, 256), 148 * 8);
+  f64_to_f32_kernel<<<blocks, 256, 0, st>>>(src, dst, n);
+  CASC_LAUNCHED();
+  return CASC_OK;
+}
+
+__global__ void fill_f64_kernel(double* dst, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = v;
+}
+
+int launch_fill_f64(double* dst, int64_t n, double v, cudaStream_t st) {
+  if (n <= 0) return CASC_OK;
+  int blocks = (int)std::min<int64_t>(ceil_div(n, 256), 148 * 8);
+  fill_f64_kernel<<<blocks, 256, 0, st>>>(dst, n, v);
+  CASC_LAUNCHED();
+  return CASC_OK;
+}
+
+}  // namespace casc

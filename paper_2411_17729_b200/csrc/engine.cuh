@@ -1,0 +1,13 @@
+// Host engine entry points (internal).
+#pragma once
+#include "common.cuh"
+
+namespace casc {
+size_t apply_ws_bytes(int n, int m, int p, int q, int64_t L, int batch, int mode);
+int validate_common(int n, int m, int p, int q, int64_t L, int batch, int N_max, int mode);
+int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_host, int N_max,
+                 int mode, const void* pack, const double* Bbar, const double* C, const double* D,
+                 const void* u, void* y, void* ws, size_t ws_bytes, cudaStream_t st);
+int engine_powers(int n, int m, const int* N_host, int N_max, const double* Abar, int mode,
+                  void* pack, cudaStream_t st);
+}  // namespace casc

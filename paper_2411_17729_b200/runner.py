@@ -1,0 +1,76 @@
+"""Map a synth.Workload onto the C-ABI calls (device upload + powers + apply).
+
+Used by the GPU tests, bench.py and __graft_entry__.smoke(). Marshalling only; no arithmetic
+of the method happens here.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import api
+
+
+def storage_to_torch(arr: np.ndarray, mode: str) -> torch.Tensor:
+    """synth storage array (float32, or uint16 bf16 bits) -> CPU torch tensor of that dtype."""
+    if mode == "fp32":
+        return torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32))
+    return torch.from_numpy(np.ascontiguousarray(arr).view(np.int16)).view(torch.bfloat16)
+
+
+class DeviceWorkload:
+    """Inputs of a workload resident in HBM, plus preallocated outputs / workspace."""
+
+    def __init__(self, wl, device="cuda", u_host: np.ndarray | None = None, channels=None):
+        self.wl = wl
+        self.device = device
+        ch = list(range(wl.n_ch)) if channels is None else list(channels)
+        self.channels = ch
+        self.bank = wl.kind == "bank"
+        self.N = [int(wl.N[c]) for c in ch]
+        self.N_max = max(self.N)
+        d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
+        self.Abar = d(wl.Abar[ch])
+        if self.bank:
+            self.Bbar, self.C, self.D = d(wl.Bbar[ch, :, 0]), d(wl.C[ch, 0, :]), d(wl.D[ch, 0, 0])
+        else:
+            self.Bbar, self.C, self.D = d(wl.Bbar[ch[0]]), d(wl.C[ch[0]]), d(wl.D[ch[0]])
+            if not np.any(wl.D[ch[0]]):
+                self.D = None
+        if u_host is None:
+            u_host = wl.u_storage(ch[0], ch[-1] + 1) if ch == list(range(ch[0], ch[-1] + 1)) \
+                else np.stack([wl.u_storage(c, c + 1)[0] for c in ch])
+        u = storage_to_torch(u_host, wl.mode)
+        if self.bank:
+            u = u.reshape(len(ch), wl.batch, wl.L)
+        else:
+            u = u.reshape(wl.batch, wl.L, wl.p)
+        self.u = u.to(device)
+        md = api._mode(wl.mode)
+        n = len(ch)
+        if self.bank:
+            self.y = torch.empty((n, wl.batch, wl.L), dtype=api.STORAGE[md], device=device)
+            wsb = api.bank_workspace_bytes(n, wl.m, wl.L, wl.batch, self.N_max, md)
+        else:
+            self.y = torch.empty((wl.batch, wl.L, wl.q), dtype=api.STORAGE[md], device=device)
+            wsb = api.apply_workspace_bytes(wl.m, wl.p, wl.q, wl.L, wl.batch, self.N[0], md)
+        self.ws = torch.empty(wsb, dtype=torch.uint8, device=device)
+        self.pack = torch.empty(api.pack_bytes(n, wl.m, self.N_max, md), dtype=torch.uint8, device=device)
+        self.pw = None
+
+    def step(self, stream=None):
+        """One pass of the hot path: powers (a1) + apply (a2..a6)."""
+        self.pw = api.powers(self.Abar, self.N, self.wl.mode, N_max=self.N_max, stream=stream, out=self.pack)
+        launches = api.last_launch_count()
+        if self.bank:
+            api.apply_bank(self.pw, self.Bbar, self.C, self.D, self.u, y=self.y, ws=self.ws, stream=stream)
+        else:
+            api.apply(self.pw, self.Bbar, self.C, self.D, self.u, y=self.y, ws=self.ws, stream=stream)
+        return launches + api.last_launch_count()
+
+    def y_f64(self) -> np.ndarray:
+        """y as float64 [n][batch][L][q] (CPU)."""
+        y = self.y.float().cpu().double().numpy()
+        if self.bank:
+            return y[..., None]
+        return y[None]

@@ -1,0 +1,72 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol include/cascade.h
+declares, size queries are consistent, and argument validation answers before any device work."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2411_17729_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "cascade.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(casc_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(_lib.LIB_PATH):
+        from paper_2411_17729_b200 import build
+        build.build()
+    return _lib.lib()
+
+
+def test_every_header_symbol_is_exported_and_bound(lib):
+    names = header_functions()
+    assert len(names) >= 12
+    for n in names:
+        assert hasattr(lib, n), n
+        assert n in _lib.SIGNATURES, f"{n} missing from the Python binding"
+
+
+def test_version_and_status_strings(lib):
+    assert lib.casc_target_sm() == 100
+    assert lib.casc_status_str(0) == b"CASC_OK"
+    assert lib.casc_status_str(4) == b"CASC_ERR_UNSUPPORTED"
+    assert lib.casc_status_str(99) == b"CASC_ERR_UNKNOWN"
+
+
+def test_size_queries(lib):
+    a = lib.casc_pack_bytes(1, 64, 13, 0)
+    b = lib.casc_pack_bytes(1, 64, 13, 1)
+    assert a > b > 14 * 64 * 64 * 8           # fp64 powers + storage copy
+    assert lib.casc_pack_bytes(0, 64, 13, 0) == 0
+    ws = lib.casc_apply_workspace_bytes(256, 64, 64, 65536, 16, 13, 0)
+    assert ws >= 2 * 65536 * 16 * 256 * 4      # two fp32 state buffers
+    wsb = lib.casc_bank_workspace_bytes(256, 64, 16384, 4, 13, 0)
+    assert wsb >= 2 * 256 * 4 * 16384 * 64 * 4
+    assert lib.casc_run_host_bytes(1, 16, 1, 1, 4096, 1, 11, 0) > 0
+
+
+def test_argument_validation_without_gpu(lib):
+    N = _lib.int_array([3])
+    # errors are detected before any CUDA call, so these are safe on a CPU-only host
+    assert lib.casc_powers(1, 0, N, 3, ctypes.c_void_p(8), 0, ctypes.c_void_p(8), None) == 1
+    assert lib.casc_powers(1, 4, N, 2, ctypes.c_void_p(8), 0, ctypes.c_void_p(8), None) == 2   # N > N_max
+    assert lib.casc_powers(1, 4, N, 3, ctypes.c_void_p(8), 7, ctypes.c_void_p(8), None) == 1   # bad mode
+    v = ctypes.c_void_p(8)
+    # p > m
+    assert lib.casc_apply(4, 5, 1, 10, 1, 3, 3, 0, v, v, v, None, v, v, v, 1 << 30, None, None) == 2
+    # L < 1
+    assert lib.casc_apply(4, 1, 1, 0, 1, 3, 3, 0, v, v, v, None, v, v, v, 1 << 30, None, None) == 1
+    # workspace too small
+    assert lib.casc_apply(4, 1, 1, 10, 1, 3, 3, 0, v, v, v, None, v, v, v, 16, None, None) == 5
+    # bank with N_c > N_max
+    Nb = _lib.int_array([1, 9])
+    assert lib.casc_apply_bank(2, 8, 10, 1, Nb, 3, 0, v, v, v, None, v, v, v, 1 << 30, None) == 2
+    # run_host: bank requires SISO
+    assert lib.casc_run_host(2, 8, 2, 1, 10, 1, Nb, 9, 0, v, v, v, None, v, v, v, 1 << 40, None) == 4

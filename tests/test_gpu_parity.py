@@ -1,0 +1,177 @@
+"""GPU parity: the CUDA path (through the C ABI) against the float64 oracle on the same seeded
+inputs. Tolerances (BASELINE north_star): relative L2 <= 1e-5 in fp32 mode, <= 2e-2 in bf16
+mode, on y and on the state part y - D u (R15); the impulse tail is exactly zero."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import configs as S
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": 1e-5, "bf16": 2e-2}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2411_17729_b200 as pk
+    pk.lib()                                 # fails loudly if the library is missing
+
+
+def rel(a, b):
+    return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300))
+
+
+def run_gpu(wl, channels=None):
+    from paper_2411_17729_b200.runner import DeviceWorkload
+    dw = DeviceWorkload(wl, channels=channels)
+    dw.step()
+    torch.cuda.synchronize()
+    return dw.y_f64(), dw
+
+
+def oracle_y(wl, channels=None):
+    chans = range(wl.n_ch) if channels is None else channels
+    u = wl.u_all()
+    return oracle.apply_workload(wl, u=u, channels=chans), u
+
+
+def check_parity(wl, channels=None, tol=None):
+    tol = TOL[wl.mode] if tol is None else tol
+    y_gpu, _ = run_gpu(wl, channels)
+    y_ref, u = oracle_y(wl, channels)
+    chans = list(range(wl.n_ch)) if channels is None else list(channels)
+    assert np.all(np.isfinite(y_gpu))
+    e = rel(y_gpu, y_ref)
+    Du = np.stack([u[c] @ wl.D[c].T for c in chans])
+    es = rel(y_gpu - Du, y_ref - Du)
+    assert e <= tol, f"rel err {e:.3e} > {tol}"
+    assert es <= tol, f"state-part rel err {es:.3e} > {tol}"
+    return e, es
+
+
+# ------------------------------------------------------------------ powers (a1)
+@pytest.mark.parametrize("m,N", [(16, 11), (64, 13), (100, 15), (256, 5)])
+def test_powers_fp64_match_oracle(m, N):
+    import paper_2411_17729_b200 as pk
+    if m == 100:
+        Abar, _ = S.trapezoid(S.hippo(100), None, 5e-4)
+    else:
+        Abar = S.make_random_mimo(m, 1, 1, 8, 1, 0, rho=0.99).Abar[0]
+    pw = pk.powers(torch.from_numpy(Abar).cuda(), N, "fp32")
+    torch.cuda.synchronize()
+    mm = m * m
+    hdr = 256                                                   # header padded to 256 B
+    p64 = pw.pack[hdr:hdr + (N + 1) * mm * 8].view(torch.float64).reshape(N + 1, m, m).cpu().numpy()
+    ref = oracle.powers(Abar, N)
+    for k in range(N + 1):
+        scale = max(np.max(np.abs(ref[k])), 1e-300)
+        assert np.max(np.abs(p64[k] - ref[k])) <= 1e-12 * max(scale, 1.0) * (1 + k)
+    if m == 100:   # the paper's pin: (Abar^(2^15))_11 ~ 5.87548e-15
+        assert abs(p64[15][0, 0] / 5.87548e-15 - 1) < 2e-5
+
+
+# ------------------------------------------------------------------ configs (scaled to oracle-sized runs)
+def test_E1_full_size():
+    e, es = check_parity(S.make_E1())
+    print(f"E1 rel {e:.2e} state {es:.2e}")
+
+
+def test_E2_reduced_bank():
+    wl = S.make_E2(n_ch=12, L=4096, batch=2)
+    check_parity(wl)
+
+
+def test_E2_full_shape_sampled_channels():
+    """Full E2 sizes (256 ch, L=16384, batch 4) on the GPU; oracle on 6 channels spanning N."""
+    wl = S.make_E2()
+    y_gpu, _ = run_gpu(wl)
+    order = np.argsort(wl.N)
+    pick = [int(order[0]), int(order[len(order) // 3]), int(order[len(order) // 2]),
+            int(order[-1]), 0, wl.n_ch - 1]
+    y_ref, u = oracle_y(wl, pick)
+    for i, c in enumerate(pick):
+        e = rel(y_gpu[c], y_ref[i])
+        es = rel(y_gpu[c] - u[c] * wl.D[c, 0, 0], y_ref[i] - u[c] * wl.D[c, 0, 0])
+        assert e <= 1e-5 and es <= 1e-5, (c, int(wl.N[c]), e, es)
+
+
+def test_E3_reduced_mimo():
+    wl = S.make_E3(L=4096, batch=2)
+    check_parity(wl)
+
+
+def test_E4_reduced_bf16():
+    wl = S.make_E4(L=4096, batch=1, N=11)
+    check_parity(wl)
+
+
+@pytest.mark.parametrize("mode", ["fp32", "bf16"])
+def test_random_mimo_ragged(mode):
+    wl = S.make_random_mimo(48, 5, 7, L=1000, batch=3, N=6, mode=mode)
+    check_parity(wl)
+
+
+# ------------------------------------------------------------------ edge cases
+@pytest.mark.parametrize("L", [1, 2, 3, 4, 5, 63, 64, 65, 127, 128, 129, 1023, 1024, 1025])
+def test_lengths_and_skipped_stages(L):
+    wl = S.make_random_mimo(16, 2, 3, L=L, batch=2, N=12, mode="fp32")
+    check_parity(wl)
+
+
+@pytest.mark.parametrize("N", [0, 1, 2, 7])
+def test_small_N_and_zero_D(N):
+    wl = S.make_random_mimo(32, 3, 2, L=300, batch=1, N=N, zero_D=True)
+    check_parity(wl)
+
+
+def test_impulse_exact_zero_tail():
+    """T10 on the GPU: the cascade is a polynomial of degree 2^(N+1)-1, so an impulse at l=0
+    produces exactly 0.0 for l >= 2^(N+1) (0 + P 0 = 0 in any arithmetic)."""
+    import paper_2411_17729_b200 as pk
+    wl = S.make_random_mimo(16, 1, 1, L=600, batch=1, N=5, zero_D=True)
+    u = torch.zeros((1, 600, 1), dtype=torch.float32, device="cuda")
+    u[0, 0, 0] = 1.0
+    pw = pk.powers(torch.from_numpy(wl.Abar[0]).cuda(), 5)
+    y = pk.apply(pw, torch.from_numpy(wl.Bbar[0]).cuda(), torch.from_numpy(wl.C[0]).cuda(), None, u)
+    yc = y.cpu().double().numpy()[0, :, 0]
+    assert np.all(yc[64:] == 0.0)
+    assert yc[63] != 0.0
+    ref = oracle.cascade(oracle.powers(wl.Abar[0], 5), wl.Bbar[0], wl.C[0], np.zeros((1, 1)),
+                         u.cpu().double().numpy(), 5)[0, :, 0]
+    assert rel(yc, ref) < 1e-5
+
+
+def test_effective_stages_reported():
+    import paper_2411_17729_b200 as pk
+    wl = S.make_random_mimo(8, 1, 1, L=100, batch=1, N=12)
+    pw = pk.powers(torch.from_numpy(wl.Abar[0]).cuda(), 12)
+    u = torch.randn((1, 100, 1), device="cuda")
+    _, eff = pk.apply(pw, torch.from_numpy(wl.Bbar[0]).cuda(), torch.from_numpy(wl.C[0]).cuda(),
+                      torch.from_numpy(wl.D[0]).cuda(), u, return_stages=True)
+    assert eff == oracle.effective_stages(100, 12) == 7
+
+
+def test_run_host_matches_device_path():
+    import paper_2411_17729_b200 as pk
+    from paper_2411_17729_b200.runner import storage_to_torch
+    wl = S.make_E2(n_ch=5, L=2048, batch=2)
+    y_dev, _ = run_gpu(wl)
+    n = wl.n_ch
+    u_h = storage_to_torch(wl.u_storage(), "fp32").reshape(n, wl.batch, wl.L, 1).pin_memory()
+    y_h = torch.empty_like(u_h).pin_memory()
+    f = lambda a: torch.from_numpy(np.ascontiguousarray(a))  # noqa: E731
+    ws = torch.empty(pk.run_host_bytes(n, wl.m, 1, 1, wl.L, wl.batch, int(wl.N.max()), "fp32"),
+                     dtype=torch.uint8, device="cuda")
+    pk.run_host(f(wl.Abar), f(wl.Bbar), f(wl.C), f(wl.D), u_h, y_h, list(wl.N), "fp32", ws)
+    assert np.array_equal(y_h.double().numpy(), y_dev)
+
+
+def test_determinism_bitwise():
+    wl = S.make_E2(n_ch=4, L=2048, batch=2)
+    a, _ = run_gpu(wl)
+    b, _ = run_gpu(wl)
+    assert np.array_equal(a, b)
