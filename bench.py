@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark of the fast cascade (arXiv 2411.17729) on B200 -- prints ONE JSON line (rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config E2]
+
+A step is one pass of the whole hot path over one batch of synthetic input: powers by repeated
+squaring (a1) + apply (first stage, stages, last stage with y = Cv + Du),
+inputs resident in HBM. The default workload is BASELINE.json configs[1] (E2: 256 HiPPO-LegS
+SISO channels, m=64, L=16384, batch 4, fp32). With N GPUs (torchrun) every rank runs its own
+E2-sized share of a 256*N-channel bank (channel sharding: no collective; weak scaling); the time
+is the max over ranks of the device-timed steps.
+
+`--impl reference` times the float64 oracle (oracle/) on this host's cores on a bounded sample
+of the same workload (rank 0 only). The oracle is test infrastructure; this flag and the
+cpu_baseline field are the only places bench.py executes it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cascade GFLOP/s & output samples/s vs tensor/HBM roofline at 1/2/4/8 B200"
+CONFIG_INDEX = {"E1": 0, "E2": 1, "E3": 2, "E4": 3, "E5": 4}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="E2", choices=list(CONFIG_INDEX))
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle CPU baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- workloads
+def make_workload(cfg: str, world: int, rank: int):
+    """Return (workload, channel list of this rank, description dict)."""
+    from synth import configs as S
+    if cfg == "E1":
+        wl = S.make_E1()
+        return wl, [0], {"workload": "E1", "m": 16, "L": wl.L, "batch": wl.batch, "N": 11}
+    if cfg == "E2":
+        wl = S.make_E2(n_ch=256 * world)
+        chans = list(range(256 * rank, 256 * (rank + 1)))
+        Ns = wl.N[chans]
+        return wl, chans, {"workload": "E2", "n_ch_per_gpu": 256, "n_ch_total": 256 * world, "m": 64,
+                           "p": 1, "q": 1, "L": wl.L, "batch": wl.batch,
+                           "N_c_range": [int(Ns.min()), int(Ns.max())], "stages_per_gpu": int((Ns + 1).sum()),
+                           "parallelism": f"channel-sharded x{world} (no collective)"}
+    if cfg == "E3":
+        wl = S.make_E3()
+        return wl, [0], {"workload": "E3", "m": 256, "p": 64, "q": 64, "L": wl.L, "batch": wl.batch, "N": 13,
+                         "parallelism": "replica per GPU" if world > 1 else "single"}
+    if cfg == "E4":
+        wl = S.make_E4()
+        return wl, [0], {"workload": "E4", "m": 1024, "p": 256, "q": 256, "L": wl.L, "batch": wl.batch,
+                         "N": int(wl.N[0]), "parallelism": "replica per GPU" if world > 1 else "single"}
+    raise SystemExit(f"config {cfg} is not runnable on one GPU in this build (E5 needs channel waves)")
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id = gpu_id
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.gpu_id, f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons, n = [], [], set(), 0
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                s, mx = float(parts[1]), float(parts[2])
+            except ValueError:
+                continue
+            n += 1
+            smax.append(mx)
+            if s > 400:          # under load (idle clocks are ~120 MHz)
+                sm.append(s)
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": n, "samples_under_load": len(sm)}
+
+
+def gpu_smi_id(torch, dev: int) -> str:
+    try:
+        u = str(torch.cuda.get_device_properties(dev).uuid)
+        return u if u.startswith("GPU-") else "GPU-" + u
+    except Exception:
+        return str(dev)
+
+
+# ----------------------------------------------------------------------------- peaks
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+def ncu_traffic(kernel_class: str, cfg: str):
+    """dram bytes per launch of `kernel_class` from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(path))
+        return d.get(cfg, {}).get(kernel_class)
+    except Exception:
+        return None
+
+
+def roofline(prof: dict, mode: str, cfg: str):
+    """Roofline of the dominant kernel class (largest total device time in the timed region)."""
+    if not prof:
+        return None
+    cls, r = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    pk = peaks()
+    t = r["ms"] / r["launches"] / 1e3                      # average launch duration, s
+    by, fl = r["bytes"] / r["launches"], r["flops"] / r["launches"]
+    tensor_classes = ("mimo_tc_stage", "mimo_tc_first", "mimo_tc_last")
+    if cls in tensor_classes:
+        if mode == "bf16":
+            peak, note = pk["bf16_tflops_sustained"], "bf16 sustained (%s)" % pk["source"]
+        else:
+            peak = pk["bf16_tflops_sustained"] * 0.5 / 3.0
+            note = "3xTF32 useful-flop peak = sustained bf16 x 0.5 (tf32/bf16 nominal) / 3 (%s)" % pk["source"]
+        ach = fl / t / 1e12
+        out = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak}
+    else:
+        ach = by / t / 1e9
+        peak = pk["hbm_gbs"]
+        note = "HBM copy bandwidth (%s)" % pk["source"]
+        out = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak}
+    out.update({"traffic": ncu_traffic(cls, cfg), "kernel": cls, "launches_timed": r["launches"],
+                "avg_launch_ms": t * 1e3, "algorithmic_bytes_per_launch": by,
+                "algorithmic_flops_per_launch": fl, "peak_note": note})
+    return out
+
+
+# ----------------------------------------------------------------------------- oracle (CPU)
+def oracle_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        n = [p.get("num_threads", 1) for p in threadpool_info() if p.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_sample(wl, chans, budget_s: float, max_units: int | None = None):
+    """Run the float64 oracle cascade on whole channels (bank) or on exact windows (MIMO) of the
+    workload until `budget_s` is spent. Returns (flops_ns, samples, seconds, description)."""
+    import numpy as np
+    import oracle
+    t0 = time.perf_counter()
+    flops = samples = 0.0
+    units = 0
+    if wl.kind == "bank":
+        for c in chans:
+            u = wl.u_all_channel(c) if hasattr(wl, "u_all_channel") else \
+                np.stack([wl.u_window(c, b, 0, wl.L) for b in range(wl.batch)])
+            N = int(wl.N[c])
+            oracle.cascade(oracle.powers(wl.Abar[c], N), wl.Bbar[c], wl.C[c], wl.D[c], u, N)
+            flops += 2.0 * wl.m * wl.m * wl.L * wl.batch * (N + 1)
+            samples += wl.L * wl.batch
+            units += 1
+            if time.perf_counter() - t0 > budget_s or (max_units and units >= max_units):
+                break
+        desc = f"{units} whole channels of {wl.name} (all {wl.batch} sequences, full L={wl.L}), float64 cascade"
+    else:
+        N = int(wl.N[0])
+        P = oracle.powers(wl.Abar[0], N)
+        W = 4096
+        rng = np.random.default_rng(0)
+        while True:
+            b = int(rng.integers(wl.batch))
+            l0 = int(rng.integers(0, max(1, wl.L - W)))
+            lo = oracle.window_start(l0, N)
+            uw = wl.u_window(0, b, lo, l0 + W)[None]
+            oracle.cascade_window(P, wl.Bbar[0], wl.C[0], wl.D[0], uw, N, l0, lo)
+            flops += 2.0 * wl.m * wl.m * W * (N + 1)           # useful work of the W outputs
+            samples += W
+            units += 1
+            if time.perf_counter() - t0 > budget_s or (max_units and units >= max_units):
+                break
+        desc = f"{units} exact windows of {W} outputs of {wl.name} (window property, halo 2^(N+1)-1), float64"
+    return flops, samples, time.perf_counter() - t0, desc
+
+
+# ----------------------------------------------------------------------------- arms
+def run_reference(args, world, rank):
+    """--impl reference: the float64 oracle on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    wl, chans, cfgd = make_workload(args.config, 1, 0)
+    per_step = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(wl, chans, per_step / 4, max_units=1)
+    tot_f = tot_s = tot_t = 0.0
+    desc = ""
+    for i in range(args.steps):
+        off = (i * 7) % len(chans)
+        f, s, t, desc = oracle_sample(wl, chans[off:] + chans[:off], per_step)
+        tot_f, tot_s, tot_t = tot_f + f, tot_s + s, tot_t + t
+    value = tot_f / tot_t / 1e9
+    cores = oracle_threads()
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
+            "samples_per_s": tot_s / tot_t, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE recipe)", "config": cfgd,
+            "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                             "sample": desc + f"; each step a bounded sample (~{per_step:.0f}s)"},
+            "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local_rank):
+    import torch
+    import torch.distributed as dist
+    import numpy as np
+    import paper_2411_17729_b200 as pk
+    from paper_2411_17729_b200.runner import DeviceWorkload, storage_to_torch
+
+    dev = local_rank
+    torch.cuda.set_device(dev)
+    pk.lib()
+    wl, chans, cfgd = make_workload(args.config, world, rank)
+    dw = DeviceWorkload(wl, device=f"cuda:{dev}", channels=chans)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{dev}")   # > 126 MB L2
+
+    launches = 0
+    for _ in range(max(3, args.warmup)):
+        dw.step()
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(gpu_smi_id(torch, dev))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    pk.profile_reset()
+    pk.profile_enable(True)
+    for i in range(args.steps):
+        flush.zero_()                                  # L2 flush between timed steps (not timed)
+        ev[i][0].record(stream)
+        launches += dw.step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    pk.profile_enable(False)
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    prof = pk.profile_read()
+    ms_steps = [a.elapsed_time(b) for a, b in ev]
+    ms_total = sum(ms_steps)
+    t = torch.tensor([ms_total], dtype=torch.float64, device=f"cuda:{dev}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    flops_rank = 2.0 * wl.m * wl.m * wl.L * wl.batch * float(sum(int(wl.N[c]) + 1 for c in chans))
+    samples_rank = wl.L * wl.batch * len(chans)
+    value = flops_rank * world * args.steps / (ms_max / 1e3) / 1e9
+    sps = samples_rank * world * args.steps / (ms_max / 1e3)
+
+    # ---- e2e: the public host-buffer C-ABI call, H2D + compute + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        n = len(chans)
+        f = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        Ab_h, Bb_h, C_h = f(wl.Abar[chans]), f(wl.Bbar[chans]), f(wl.C[chans])
+        D_h = f(wl.D[chans]) if np.any(wl.D[chans]) else None
+        u_h = dw.u.cpu().reshape(n, wl.batch, wl.L, wl.p).pin_memory()
+        y_h = torch.empty((n, wl.batch, wl.L, wl.q), dtype=u_h.dtype).pin_memory()
+        Ns = [int(wl.N[c]) for c in chans]
+        ws = torch.empty(pk.run_host_bytes(n, wl.m, wl.p, wl.q, wl.L, wl.batch, max(Ns), wl.mode),
+                         dtype=torch.uint8, device=f"cuda:{dev}")
+        pk.run_host(Ab_h, Bb_h, C_h, D_h, u_h, y_h, Ns, wl.mode, ws)
+        del dw
+        e2e_ms = []
+        for _ in range(args.e2e_steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if world > 1:
+                dist.barrier()
+            a.record(stream)
+            pk.run_host(Ab_h, Bb_h, C_h, D_h, u_h, y_h, Ns, wl.mode, ws)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms.append(a.elapsed_time(b))
+        te = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=f"cuda:{dev}")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        h2d = sum(t.numel() * t.element_size() for t in (Ab_h, Bb_h, C_h, u_h) + ((D_h,) if D_h is not None else ()))
+        d2h = y_h.numel() * y_h.element_size()
+        e2e = {"value": flops_rank * world * args.e2e_steps / (float(te.item()) / 1e3) / 1e9, "unit": "GFLOP/s",
+               "samples_per_s": samples_rank * world * args.e2e_steps / (float(te.item()) / 1e3),
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": float(te.item()) / args.e2e_steps,
+               "api": "casc_run_host (pinned host buffers; copies + powers + apply + copy-back)"}
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        f_s, s_s, t_s, desc = oracle_sample(wl, chans, args.cpu_seconds)
+        cpu = {"value": f_s / t_s / 1e9, "unit": "GFLOP/s", "samples_per_s": s_s / t_s,
+               "cores": oracle_threads(), "kind": "oracle", "sample": desc, "seconds": t_s}
+    cfgd = dict(cfgd)
+    cfgd["l2"] = "512 MiB buffer written between timed steps (flush); state buffers also exceed L2"
+    cfgd["timed_step"] = "powers (fp64 squaring + pack) + apply (all stages, y = Cv + Du)"
+    line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "samples_per_s": sps, "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if wl.mode == "fp32" else "bf16",
+            "data": "synthetic (seeded BASELINE recipe; no dataset in the paper)", "config": cfgd,
+            "roofline": roofline(prof, wl.mode, args.config), "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clocks,
+            "kernels": {k: {"launches": v["launches"], "ms": v["ms"]} for k, v in prof.items()},
+            "flops_per_step_ns": flops_rank * world}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    try:
+        run_ours(args, world, rank, local_rank)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -150,6 +150,21 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
  * enqueued (bench evidence for "gpu_launches"). */
 int casc_last_launch_count(void);
 
+/* ----------------------------------------------------------------------------------------
+ * Optional per-kernel-class timing (measurement support, bench.py). When enabled on the
+ * calling host thread, every launch the library enqueues is bracketed by CUDA events
+ * recorded on its own stream and tagged with its kernel class and ALGORITHMIC bytes / flops.
+ * casc_profile_read synchronises the recorded events of one class and returns the launch
+ * count, summed device milliseconds, bytes and flops (any pointer may be NULL).
+ * casc_profile_reset drops all records. Classes: 0 .. casc_profile_num_classes()-1, named by
+ * casc_profile_class_name (static strings).
+ * -------------------------------------------------------------------------------------- */
+int casc_profile_enable(int on);
+int casc_profile_reset(void);
+int casc_profile_num_classes(void);
+const char* casc_profile_class_name(int cls);
+int casc_profile_read(int cls, int* launches, double* ms, double* bytes, double* flops);
+
 #ifdef __cplusplus
 }
 #endif

@@ -4,6 +4,6 @@ The compute lives in libcascade_b200.so (C ABI: include/cascade.h); this package
 torch-facing binding. There is no CPU fallback.
 """
 from .api import (MODES, STORAGE, Powers, apply, apply_bank, apply_workspace_bytes,  # noqa: F401
-                  bank_workspace_bytes, last_launch_count, pack_bytes, powers, run_host,
-                  run_host_bytes)
+                  bank_workspace_bytes, last_launch_count, pack_bytes, powers, profile_enable,
+                  profile_read, profile_reset, run_host, run_host_bytes)
 from ._lib import CascadeError, LIB_PATH, lib  # noqa: F401

@@ -30,6 +30,12 @@ SIGNATURES = {
     "casc_run_host": (c_int, [c_int, c_int, c_int, c_int, c_int64, c_int, P_int, c_int, c_int,
                               c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                               c_void_p, c_size_t, c_void_p]),
+    "casc_profile_enable": (c_int, [c_int]),
+    "casc_profile_reset": (c_int, []),
+    "casc_profile_num_classes": (c_int, []),
+    "casc_profile_class_name": (c_char_p, [c_int]),
+    "casc_profile_read": (c_int, [c_int, P_int, ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
 }
 
 _lib = None

@@ -150,3 +150,26 @@ def run_host(Abar_h, Bbar_h, C_h, D_h, u_h, y_h, N, mode, dev_ws, stream=None):
 
 def last_launch_count() -> int:
     return int(lib().casc_last_launch_count())
+
+
+# ------------------------------------------------------------------ in-library kernel timing
+def profile_enable(on: bool = True) -> None:
+    lib().casc_profile_enable(1 if on else 0)
+
+
+def profile_reset() -> None:
+    lib().casc_profile_reset()
+
+
+def profile_read() -> dict:
+    """{class_name: {launches, ms, bytes, flops}} for classes with at least one launch."""
+    out = {}
+    L = lib()
+    for c in range(L.casc_profile_num_classes()):
+        n, ms, by, fl = ctypes.c_int(0), ctypes.c_double(0), ctypes.c_double(0), ctypes.c_double(0)
+        check(L.casc_profile_read(c, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(by), ctypes.byref(fl)),
+              "casc_profile_read")
+        if n.value:
+            out[L.casc_profile_class_name(c).decode()] = {"launches": n.value, "ms": ms.value,
+                                                          "bytes": by.value, "flops": fl.value}
+    return out

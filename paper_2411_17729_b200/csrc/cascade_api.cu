@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "engine.cuh"
+#include "profile.cuh"
 
 namespace casc {
 thread_local int g_launches = 0;
@@ -87,6 +88,7 @@ int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_
   PackLayout P = pack_layout(const_cast<void*>(pack), n, m, N_max, mode);
   const bool bf = (mode == CASC_BF16);
   const int64_t mm = (int64_t)m * m;
+  const double es = bf ? 2.0 : 4.0;
 
   // ---- host metadata: effective orders and launch lists
   std::vector<int> meta((size_t)5 * n);
@@ -115,6 +117,7 @@ int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_
 
   // ---- derived float64 matrices (tiny)
   {
+    ProfScope ps(st, K_DERIVED, 0.0, 2.0 * n * ((double)m * m * p + (double)q * m * m + 2.0 * q * m * p));
     DgemmArg a{};
     // AB = P_0 Bbar  (m x p)
     a = DgemmArg{};
@@ -146,6 +149,8 @@ int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_
     a.C = w.CAB64; a.ldc = p; a.sC = (int64_t)q * p;
     if ((rc = launch_dgemm(a, n, st))) return rc;
   }
+  {
+  ProfScope ps(st, K_CONVERT, 0.0, 0.0);
   if ((rc = launch_f64_to_f32(Bbar, w.Bb32, (int64_t)n * m * p, st))) return rc;
   if ((rc = launch_f64_to_f32(w.AB64, w.AB32, (int64_t)n * m * p, st))) return rc;
   if ((rc = launch_f64_to_f32(C, w.C32, (int64_t)n * q * m, st))) return rc;
@@ -156,6 +161,7 @@ int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_
     if ((rc = launch_f64_to_f32(D, w.D32, (int64_t)n * q * p, st))) return rc;
   } else {
     CASC_TRY(cudaMemsetAsync(w.D32, 0, sizeof(float) * (size_t)n * q * p, st));
+  }
   }
 
   const int64_t u_sys = (int64_t)batch * L * p, y_sys = (int64_t)batch * L * q;
@@ -179,6 +185,7 @@ int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_
     g.n_src = 2;
     g.out = y; g.out_sys = y_sys; g.out_bf16 = bf; g.n_out = q;
     g.sys_list = ddirect; g.n_list = n0;
+    ProfScope ps(st, K_DIRECT, (double)n0 * batch * L * (p + q) * es, (double)n0 * batch * L * 4.0 * q * p);
     if ((rc = launch_simt_gemm(g, st))) return rc;
   }
   if (n1 == 0) return CASC_OK;
@@ -191,6 +198,7 @@ int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_
     g.n_src = 2;
     g.out = w.Va; g.out_sys = v_sys; g.out_bf16 = bf; g.n_out = m;
     g.sys_list = dorder; g.n_list = n1;
+    ProfScope ps(st, K_FIRST, (double)n1 * batch * L * (p + m) * es, (double)n1 * batch * L * 4.0 * m * p);
     if ((rc = launch_simt_gemm(g, st))) return rc;
   }
   // ---- stages k = 1 .. maxNe-1 (a4) over the systems with Neff >= k+1 (a prefix of order)
@@ -210,6 +218,7 @@ int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_
     g.R = Vs; g.R_sys = v_sys;
     g.out = Vd; g.out_sys = v_sys; g.out_bf16 = bf; g.n_out = m;
     g.sys_list = dorder; g.n_list = cnt;
+    ProfScope ps(st, K_STAGE, 2.0 * cnt * batch * L * m * es, 2.0 * cnt * batch * L * (double)m * m);
     if ((rc = launch_simt_gemm(g, st))) return rc;
   }
   // ---- last (a5): y = C v + (C P_Ne) v_{l-2^Ne} + D u, per buffer parity group
@@ -224,6 +233,8 @@ int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_
     g.n_src = D ? 3 : 2;
     g.out = y; g.out_sys = y_sys; g.out_bf16 = bf; g.n_out = q;
     g.sys_list = grp == 0 ? dgA : dgB; g.n_list = cnt;
+    ProfScope ps(st, K_LAST, (double)cnt * batch * L * (m + p + q) * es,
+                 (double)cnt * batch * L * (4.0 * q * m + 2.0 * q * p));
     if ((rc = launch_simt_gemm(g, st))) return rc;
   }
   return CASC_OK;
@@ -245,6 +256,9 @@ int engine_powers(int n, int m, const int* N_host, int N_max, const double* Abar
                              mm * sizeof(double), n, cudaMemcpyDeviceToDevice, st));
   int maxN = *std::max_element(N_host, N_host + n);
   for (int k = 1; k <= maxN; ++k) {               // P_k = P_{k-1} P_{k-1}
+    int cnt = 0;
+    for (int s = 0; s < n; ++s) cnt += N_host[s] >= k;
+    ProfScope ps(st, K_POWERS, 16.0 * cnt * mm, 2.0 * cnt * (double)mm * m);
     DgemmArg a{};
     a.M = m; a.N = m; a.K = m;
     a.A = P.p64 + (k - 1) * mm; a.lda = m; a.sA = sys;
@@ -254,6 +268,7 @@ int engine_powers(int n, int m, const int* N_host, int N_max, const double* Abar
     int rc = launch_dgemm(a, n, st);
     if (rc) return rc;
   }
+  ProfScope ps(st, K_PACK, 0.0, 0.0);
   return launch_pack(P, n, N_max, m, st);
 }
 

@@ -1,0 +1,94 @@
+// Optional per-kernel-class timing: when enabled on the calling host thread, each launch of
+// the engine is bracketed by CUDA events recorded on the launch stream, and tagged with the
+// algorithmic bytes / flops of that launch. bench.py reads these to report the dominant
+// kernel's achieved bandwidth or throughput (roofline) from live, in-run measurements.
+#include <vector>
+#include "common.cuh"
+#include "profile.cuh"
+
+namespace casc {
+
+struct ProfRec {
+  cudaEvent_t a, b;
+  int cls;
+  double bytes, flops;
+};
+struct ProfState {
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+static thread_local ProfState g_prof;
+
+ProfScope::ProfScope(cudaStream_t st, int cls, double bytes, double flops) : st_(st), idx_(-1) {
+  if (!g_prof.on) return;
+  ProfRec r{g_prof.get(), g_prof.get(), cls, bytes, flops};
+  cudaEventRecord(r.a, st);
+  g_prof.recs.push_back(r);
+  idx_ = (int)g_prof.recs.size() - 1;
+}
+ProfScope::~ProfScope() {
+  if (idx_ >= 0) cudaEventRecord(g_prof.recs[idx_].b, st_);
+}
+
+static const char* kNames[K_NCLASS] = {"powers_square", "powers_pack", "derived", "first_stage",
+                                       "stage", "last_stage", "direct", "convert",
+                                       "bank_head", "bank_stage", "bank_tail", "mimo_tc_stage",
+                                       "mimo_tc_first", "mimo_tc_last"};
+
+}  // namespace casc
+
+using namespace casc;
+extern "C" {
+
+int casc_profile_enable(int on) {
+  g_prof.on = on != 0;
+  return CASC_OK;
+}
+
+int casc_profile_reset(void) {
+  for (auto& r : g_prof.recs) {
+    g_prof.pool.push_back(r.a);
+    g_prof.pool.push_back(r.b);
+  }
+  g_prof.recs.clear();
+  return CASC_OK;
+}
+
+int casc_profile_num_classes(void) { return K_NCLASS; }
+
+const char* casc_profile_class_name(int cls) {
+  return (cls >= 0 && cls < K_NCLASS) ? kNames[cls] : "unknown";
+}
+
+int casc_profile_read(int cls, int* launches, double* ms, double* bytes, double* flops) {
+  int n = 0;
+  double t = 0, by = 0, fl = 0;
+  for (auto& r : g_prof.recs) {
+    if (r.cls != cls) continue;
+    if (cudaEventSynchronize(r.b) != cudaSuccess) return CASC_ERR_CUDA;
+    float e = 0.f;
+    if (cudaEventElapsedTime(&e, r.a, r.b) != cudaSuccess) return CASC_ERR_CUDA;
+    ++n;
+    t += e;
+    by += r.bytes;
+    fl += r.flops;
+  }
+  if (launches) *launches = n;
+  if (ms) *ms = t;
+  if (bytes) *bytes = by;
+  if (flops) *flops = fl;
+  return CASC_OK;
+}
+
+}  // extern "C"
