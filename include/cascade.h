@@ -165,6 +165,15 @@ int casc_profile_num_classes(void);
 const char* casc_profile_class_name(int cls);
 int casc_profile_read(int cls, int* launches, double* ms, double* bytes, double* flops);
 
+/* ----------------------------------------------------------------------------------------
+ * Hardware self-test of the tensor-core building block (diagnostics; used by tests/):
+ *   D[128][64] = A[off:off+128][0:64] . B[0:64][0:64]^T on tcgen05 kind::tf32, fp32 accumulate,
+ *   operands staged in shared memory in the K-major no-swizzle layout the cascade kernels use.
+ *   prep: 0 raw fp32 bits, 1 pre-truncated to tf32, 2 rounded (rna) to tf32.
+ *   A DEVICE float [144][64], B DEVICE float [64][64], D DEVICE float [128][64]; 0 <= off <= 16.
+ * -------------------------------------------------------------------------------------- */
+int casc_selftest_umma(int prep, int off, const float* A, const float* B, float* D, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,6 +30,7 @@ SIGNATURES = {
     "casc_run_host": (c_int, [c_int, c_int, c_int, c_int, c_int64, c_int, P_int, c_int, c_int,
                               c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                               c_void_p, c_size_t, c_void_p]),
+    "casc_selftest_umma": (c_int, [c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "casc_profile_enable": (c_int, [c_int]),
     "casc_profile_reset": (c_int, []),
     "casc_profile_num_classes": (c_int, []),

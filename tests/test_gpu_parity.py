@@ -122,6 +122,21 @@ def test_lengths_and_skipped_stages(L):
     check_parity(wl)
 
 
+@pytest.mark.parametrize("m", [16, 32, 64])
+@pytest.mark.parametrize("L,N", [(1, 3), (2, 0), (3, 1), (100, 12), (129, 7), (300, 8), (1000, 9), (2049, 11)])
+def test_bank_tensor_core_path_edges(m, L, N):
+    """SISO systems take the tcgen05 bank path (Krylov head, streaming stages, fused tail)."""
+    wl = S.make_random_mimo(m, 1, 1, L=L, batch=2, N=N, rho=0.97, mode="fp32")
+    check_parity(wl)
+
+
+def test_bank_mixed_orders_and_ragged_length():
+    """Channels with N from 0 to 13 in one bank, L not a multiple of the 128-step tile."""
+    wl = S.make_E2(n_ch=14, L=3000, batch=3)
+    wl.N[:] = np.arange(14)
+    check_parity(wl)
+
+
 @pytest.mark.parametrize("N", [0, 1, 2, 7])
 def test_small_N_and_zero_D(N):
     wl = S.make_random_mimo(32, 3, 2, L=300, batch=1, N=N, zero_D=True)
