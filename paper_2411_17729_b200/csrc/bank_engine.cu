@@ -140,10 +140,15 @@ int engine_bank_tc(int n, int m, int64_t L, int batch, const int* N_host, int N_
     a.Vs = static_cast<const float*>(j % 2 == 0 ? w.Va : w.Vb);
     a.Vd = static_cast<float*>(j % 2 == 0 ? w.Vb : w.Va);
     a.P = P.f32; a.k = k; a.slots = N_max + 1;
+    a.copy_from = (k == kHeadK) ? 0 : ((int64_t)1 << (k - 1));
     a.sys_list = dorder; a.n_list = cnt; a.L = L; a.batch = batch;
     a.tiles_per_cta = pick_group(ntiles, (int64_t)cnt * batch, 8);
     ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt * batch * L * m * 4.0, 2.0 * cnt * batch * L * (double)mm);
-    if ((rc = launch_bank_stage(m, a, st))) return rc;
+    static const bool use_ws = [] {
+      const char* e = getenv("CASC_BANK_STAGE");
+      return e && e[0] == 'w';
+    }();
+    if ((rc = use_ws ? launch_bank_stage_ws(m, a, st) : launch_bank_stage_rp(m, a, st))) return rc;
   }
   // ---- tail: stage Ne + y = C v + D u
   {

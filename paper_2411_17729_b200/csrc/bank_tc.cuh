@@ -14,7 +14,7 @@ struct BankHeadArg {
 struct BankStageArg {
   const float* Vs; float* Vd;   // [n_ch][batch][L][MS]
   const float* P;               // pack fp32 region: [n_ch][slots][2][MS][MS]
-  int k; int slots;
+  int k; int slots; int64_t copy_from;    // rows [copy_from, 2^k) are copies
   const int* sys_list; int n_list;
   int64_t L; int batch; int tiles_per_cta;
 };
@@ -28,7 +28,8 @@ struct BankTailArg {
 
 bool bank_tc_supported(int m);
 int launch_bank_head(int m, const BankHeadArg& a, cudaStream_t st);
-int launch_bank_stage(int m, const BankStageArg& a, cudaStream_t st);
+int launch_bank_stage_ws(int m, const BankStageArg& a, cudaStream_t st);
+int launch_bank_stage_rp(int m, const BankStageArg& a, cudaStream_t st);
 int launch_bank_tail(int m, const BankTailArg& a, cudaStream_t st);
 int launch_kr_init(const double* Bbar, double* Kr, int n, int ms, cudaStream_t st);
 int launch_kr_split(const double* Kr, const int* Kc, float* krT, int n, int ms, cudaStream_t st);
