@@ -109,6 +109,15 @@ def test_E4_reduced_bf16():
     check_parity(wl)
 
 
+@pytest.mark.parametrize("m,p,q,L,batch,N", [(128, 64, 64, 1000, 3, 6), (64, 64, 64, 300, 2, 0),
+                                              (256, 128, 64, 4096, 2, 11), (192, 64, 128, 129, 1, 3),
+                                              (128, 64, 64, 2, 2, 5), (128, 64, 64, 1, 1, 2)])
+def test_mimo_bf16_tensor_core_path(m, p, q, L, batch, N):
+    """bf16 MIMO systems with m, p, q multiples of 64 take the TMA + tcgen05 GEMM path."""
+    wl = S.make_random_mimo(m, p, q, L=L, batch=batch, N=N, rho=0.98, mode="bf16")
+    check_parity(wl)
+
+
 @pytest.mark.parametrize("mode", ["fp32", "bf16"])
 def test_random_mimo_ragged(mode):
     wl = S.make_random_mimo(48, 5, 7, L=1000, batch=3, N=6, mode=mode)
