@@ -170,12 +170,24 @@ class Workload:
         c1 = self.n_ch if c1 is None else c1
         per_ch = self.batch * self.L * self.p
         n = (c1 - c0) * per_ch
-        buf = np.empty(n, dtype=np.float32)
-        _rng.normal_chunked(self.u_seed, self.u_stream, c0 * per_ch, n, buf)
         shape = (c1 - c0, self.batch, self.L, self.p)
         if self.mode == "fp32":
+            buf = np.empty(n, dtype=np.float32)
+            _rng.normal_chunked(self.u_seed, self.u_stream, c0 * per_ch, n, buf)
             return buf.reshape(shape)
-        return bf16_bits_from_f32(buf).reshape(shape)
+        out = np.empty(n, dtype=np.uint16)
+        chunk = 1 << 22
+        start = c0 * per_ch
+
+        def work(o):
+            c = min(chunk, n - o)
+            out[o:o + c] = bf16_bits_from_f32(_rng.normal32(self.u_seed, self.u_stream, start + o, c))
+
+        from concurrent.futures import ThreadPoolExecutor
+        import os
+        with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+            list(ex.map(work, range(0, n, chunk)))
+        return out.reshape(shape)
 
     def flops_ns(self) -> float:
         """BASELINE north_star count F = sum_c 2 m^2 L batch (N_c + 1)."""
