@@ -4,8 +4,6 @@
 
 namespace casc {
 
-__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
-__device__ __forceinline__ float tf32_lo(float x) { return x - tf32_trunc(x); }
 
 template <int MS>
 struct TmemCols {

@@ -105,10 +105,9 @@ __global__ void __launch_bounds__(128) bank_stage_rp_kernel(BankStageArg a) {
     for (int it = 0; it < NLD; ++it) {
       const int e = it * 128 + tid;
       const int rem = e % (8 * CH), ch = rem / 8, r = (e / (8 * CH)) * 8 + rem % 8;
-      const float4 v = areg[it];
-      *reinterpret_cast<float4*>(Ahi + (ch * TM + r) * 4) = v;
-      *reinterpret_cast<float4*>(Alo + (ch * TM + r) * 4) =
-          make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+      const float4 v = areg[it], h = tf32_hi4(v);
+      *reinterpret_cast<float4*>(Ahi + (ch * TM + r) * 4) = h;
+      *reinterpret_cast<float4*>(Alo + (ch * TM + r) * 4) = tf32_lo4(v, h);
     }
     fence_async_smem();
     tc_fence_before();

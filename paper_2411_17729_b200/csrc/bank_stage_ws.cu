@@ -26,7 +26,6 @@ constexpr int TM = 128;          // time rows per tile
 constexpr int NS = 3;            // shifted-tile ring depth
 constexpr int GT = 16;           // tiles per work block
 
-__device__ __forceinline__ float lo_part(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // Deterministic walk over this CTA's tiles (both warp groups run their own copy).
@@ -149,10 +148,11 @@ __global__ void __launch_bounds__(256, 1) bank_stage_ws_kernel(BankStageArg a) {
       named_sync(1, 128);
       const bool mma = src0 >= 0;
       if (mma) {
-        const float* ar = Araw + (i % NS) * TM * MS;
+        float* ar = Araw + (i % NS) * TM * MS;
         for (int e = pt; e < TM * CH; e += 128) {
-          const float4 v = *reinterpret_cast<const float4*>(ar + e * 4);
-          *reinterpret_cast<float4*>(Alo + e * 4) = make_float4(lo_part(v.x), lo_part(v.y), lo_part(v.z), lo_part(v.w));
+          const float4 v = *reinterpret_cast<const float4*>(ar + e * 4), h = tf32_hi4(v);
+          *reinterpret_cast<float4*>(ar + e * 4) = h;
+          *reinterpret_cast<float4*>(Alo + e * 4) = tf32_lo4(v, h);
         }
         fence_async_smem();
       }

@@ -93,10 +93,9 @@ __global__ void __launch_bounds__(128) bank_head_kernel(BankHeadArg a) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int w = tid + 128 * h;
-      const float* z = zr[h];
-      *reinterpret_cast<float4*>(zh + w * 4) = make_float4(z[0], z[1], z[2], z[3]);
-      *reinterpret_cast<float4*>(zl + w * 4) =
-          make_float4(tf32_lo(z[0]), tf32_lo(z[1]), tf32_lo(z[2]), tf32_lo(z[3]));
+      const float4 z = make_float4(zr[h][0], zr[h][1], zr[h][2], zr[h][3]), zhi = tf32_hi4(z);
+      *reinterpret_cast<float4*>(zh + w * 4) = zhi;
+      *reinterpret_cast<float4*>(zl + w * 4) = tf32_lo4(z, zhi);
     }
     fence_async_smem();
     tc_fence_before();

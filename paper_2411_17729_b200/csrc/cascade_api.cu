@@ -63,7 +63,7 @@ static ApplyWs carve_apply(void* ws, int n, int m, int p, int q, int64_t L, int 
 
 size_t apply_ws_bytes(int n, int m, int p, int q, int64_t L, int batch, int mode) {
   if (bank_tc_path(m, p, q, mode)) return bank_ws_bytes(n, m, L, batch);
-  if (mimo_tc_path(n, m, p, q, mode)) return mimo_ws_bytes(m, p, q, L, batch);
+  if (mimo_tc_path(n, m, p, q, mode)) return mimo_ws_bytes(m, p, q, L, batch, mode);
   return carve_apply(nullptr, n, m, p, q, L, batch, mode).bytes;
 }
 
@@ -88,7 +88,7 @@ int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_
   if (bank_tc_path(m, p, q, mode))
     return engine_bank_tc(n, m, L, batch, N_host, N_max, pack, Bbar, C, D, u, y, ws, ws_bytes, st);
   if (mimo_tc_path(n, m, p, q, mode))
-    return engine_mimo_tc(m, p, q, L, batch, N_host[0], N_max, pack, Bbar, C, D, u, y, ws, ws_bytes, st);
+    return engine_mimo_tc(m, p, q, L, batch, N_host[0], N_max, mode, pack, Bbar, C, D, u, y, ws, ws_bytes, st);
   ApplyWs w = carve_apply(ws, n, m, p, q, L, batch, mode);
   if (ws_bytes < w.bytes) return CASC_ERR_WORKSPACE;
   PackLayout P = pack_layout(const_cast<void*>(pack), n, m, N_max, mode);

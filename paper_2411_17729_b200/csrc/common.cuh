@@ -81,5 +81,13 @@ __device__ __forceinline__ float tf32_rna(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
+// 3xTF32 split of a streaming fp32 operand (R17): hi = rna_tf32(x), lo = rna_tf32(x - hi)
+// (x - hi is exact in fp32), so x = hi + lo to ~2^-23 relative with an unbiased rounding.
+__device__ __forceinline__ float4 tf32_hi4(float4 v) {
+  return make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+}
+__device__ __forceinline__ float4 tf32_lo4(float4 v, float4 h) {
+  return make_float4(tf32_rna(v.x - h.x), tf32_rna(v.y - h.y), tf32_rna(v.z - h.z), tf32_rna(v.w - h.w));
+}
 
 }  // namespace casc

@@ -1,4 +1,4 @@
-// MIMO cascade stages on the sm_100a tensor cores (bf16 storage, fp32 accumulation).
+// MIMO cascade stages on the sm_100a tensor cores.
 //
 // One kernel computes every step of PAPER.md:185-229 for a single system as a shifted
 // multi-source GEMM with a fused residual epilogue:
@@ -9,12 +9,18 @@
 // The time shift is a TMA coordinate offset; rows l - shift < 0 fall outside the tensor and
 // TMA zero-fills them, which is exactly "columns l < 2^k are left unchanged".
 //
-// Persistent CTAs (one per SM), 6 warps:
-//   warp 0      TMA producer: 4-stage ring of {A 128x64, W BNx64} bf16 tiles (SWIZZLE_128B)
-//   warp 1      MMA issuer: tcgen05.mma kind::f16, M=128, N=BN, K=16, into one of two TMEM
-//               accumulators (2 x BN columns), commit -> smem slot free / accumulator full
-//   warps 2-5   epilogue: TMEM -> registers (lane = time row), + residual tile (TMA-loaded,
-//               SW128), convert to bf16 in place, TMA store; accumulator released to warp 1.
+// Two precisions (template TF32):
+//   bf16   : kind::f16, bf16 tiles of 128 x 64 (128-B rows), fp32 accumulation, bf16 output.
+//   3xTF32 : kind::tf32 with hi.hi + lo.hi + hi.lo, fp32 tiles of 128 x 32 (128-B rows). The
+//            constant W comes as tf32 hi/lo pairs; the streaming A tile is used raw (the tensor
+//            core truncates it to its tf32 hi) and transform warps write lo = x - trunc(x).
+//
+// Persistent CTAs (one per SM):
+//   warp 0      TMA producer: ring of {A, W (hi[, lo])} tiles (SWIZZLE_128B)
+//   warp 1      MMA issuer: M=128, N=BN, into one of two TMEM accumulators (2 x BN columns)
+//   warps 2-5   epilogue: TMEM -> registers (lane = time row), + residual tile (TMA-loaded),
+//               convert in place, TMA store; accumulator released to warp 1.
+//   warps 6-9   (3xTF32 only) lo-part transform of each landed A tile.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -26,18 +32,12 @@ namespace casc {
 using namespace sm100;
 
 namespace {
-constexpr int BM = 128, BK = 64, STAGES = 4;
-constexpr uint32_t A_BYTES = BM * BK * 2;          // 16 KB
+constexpr int BM = 128;
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
       ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2) : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
-      ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1) : "memory");
 }
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];"
@@ -73,21 +73,47 @@ __device__ __forceinline__ float2 unpack_bf16(uint32_t u) {
   __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&u);
   return __bfloat1622float2(h);
 }
+
+template <int BN, bool TF32>
+struct Cfg {
+  static constexpr int ES = TF32 ? 4 : 2;                 // element size
+  static constexpr int BK = 128 / ES;                     // K per stage: 128-byte rows
+  static constexpr uint32_t A_BYTES = BM * 128;           // 16 KB
+  static constexpr uint32_t W_BYTES = BN * 128;           // one of hi / lo
+  static constexpr int NW = TF32 ? 2 : 1;                 // weight tiles per stage
+  static constexpr uint32_t STAGE_BYTES = A_BYTES * (TF32 ? 2 : 1) + W_BYTES * NW;   // (A, Alo,) W...
+  static constexpr uint32_t TMA_BYTES = A_BYTES + W_BYTES * NW;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES < 4 ? (200 * 1024) / STAGE_BYTES : 4;
+  static constexpr int CW = 128 / ES;                     // epilogue chunk width (columns)
+  static constexpr uint32_t R_BYTES = BM * 128;           // 16 KB
+  static constexpr int THREADS = TF32 ? 320 : 192;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 2 * R_BYTES;
+};
 }  // namespace
 
-template <int BN>
-__global__ void __launch_bounds__(192, 1) mimo_gemm_bf16_kernel(const __grid_constant__ MimoMaps maps, MimoArg a) {
-  constexpr uint32_t B_BYTES = BN * BK * 2;
-  constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
-  constexpr int TCOLS = 2 * BN < 32 ? 32 : 2 * BN;
-  constexpr uint32_t R_BYTES = BM * 64 * 2;       // 16 KB epilogue chunk (128 rows x 64 cols)
+template <int BN, bool TF32>
+__global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(const __grid_constant__ MimoMaps maps,
+                                                                              MimoArg a) {
+  using C = Cfg<BN, TF32>;
+  constexpr int STAGES = C::STAGES, BK = C::BK;
+  // TMEM: two accumulator buffers of ACOLS columns. 3xTF32 keeps hi.hi in [0, BN) ("main") and
+  // the two correction products in [BN, 2BN) ("corr"): the tensor core's fp32 accumulator
+  // truncates at every MMA, so the error grows with the number of MMAs chained into one
+  // accumulator (measured ~2e-8 per MMA); splitting keeps the main chain at K/8 MMAs and the
+  // corr chain's error is 2^-11 smaller. The epilogue sums main + corr with round-to-nearest.
+  constexpr int ACOLS = TF32 ? 2 * BN : BN;
+  static_assert(2 * ACOLS <= 512, "TMEM holds 512 columns");
+  constexpr int TCOLS = 2 * ACOLS < 32 ? 32 : 2 * ACOLS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;                              // [STAGES][A_BYTES]
-  uint8_t* sB = smem + STAGES * A_BYTES;           // [STAGES][B_BYTES]
-  uint8_t* sR = sB + STAGES * B_BYTES;             // [2][R_BYTES]
-  __shared__ uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2], rfull[2];
+  // per stage: [A][W hi][(W lo)][(A lo)]
+  uint8_t* sR = smem + STAGES * C::STAGE_BYTES;      // [2][R_BYTES]
+  __shared__ uint64_t full[STAGES], empty[STAGES], lo_ready[STAGES], tfull[2], tempty[2], rfull[2];
   __shared__ uint32_t tmem_base;
+  auto stA = [&](int s) { return smem + s * C::STAGE_BYTES; };
+  auto stW = [&](int s) { return smem + s * C::STAGE_BYTES + C::A_BYTES; };
+  auto stWlo = [&](int s) { return smem + s * C::STAGE_BYTES + C::A_BYTES + C::W_BYTES; };
+  auto stAlo = [&](int s) { return smem + s * C::STAGE_BYTES + C::A_BYTES + C::NW * C::W_BYTES; };
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t mt_per_b = (a.L + BM - 1) / BM;
@@ -96,7 +122,7 @@ __global__ void __launch_bounds__(192, 1) mimo_gemm_bf16_kernel(const __grid_con
   const int64_t n_tiles = n_mblk * n_nblk;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); mbar_init(&lo_ready[s], 128); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); mbar_init(&rfull[s], 1); }
     fence_mbar_init();
   }
@@ -125,9 +151,10 @@ __global__ void __launch_bounds__(192, 1) mimo_gemm_bf16_kernel(const __grid_con
           const int nk = a.K[src] / BK;
           for (int kc = 0; kc < nk; ++kc) {
             mbar_wait(&empty[s], ph ^ 1);
-            mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-            tma_load_3d(sA + s * A_BYTES, &maps.A[src], &full[s], kc * BK, l0 - (int)a.shift[src], b);
-            tma_load_2d(sB + s * B_BYTES, &maps.W[src], &full[s], kc * BK, nb * BN);
+            mbar_arrive_expect_tx(&full[s], C::TMA_BYTES);
+            tma_load_3d(stA(s), &maps.A[src], &full[s], kc * BK, l0 - (int)a.shift[src], b);
+            tma_load_3d(stW(s), &maps.W[src], &full[s], kc * BK, nb * BN, 0);
+            if (TF32) tma_load_3d(stWlo(s), &maps.W[src], &full[s], kc * BK, nb * BN, 1);
             if (++s == STAGES) { s = 0; ph ^= 1; }
           }
         }
@@ -136,28 +163,36 @@ __global__ void __launch_bounds__(192, 1) mimo_gemm_bf16_kernel(const __grid_con
   } else if (warp == 1) {
     // =========================================================== MMA issuer
     if (lane == 0) {
-      const uint32_t idesc = make_idesc(FMT_BF16, BM, BN);
+      const uint32_t idesc = make_idesc(TF32 ? FMT_TF32 : FMT_BF16, BM, BN);
       int s = 0;
       uint32_t ph = 0;
       int64_t t_local = 0;
       for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t_local) {
         const int acc = (int)(t_local & 1);
-        const uint32_t aph = (uint32_t)((t_local >> 1) & 1);
-        mbar_wait(&tempty[acc], aph ^ 1);
+        mbar_wait(&tempty[acc], (uint32_t)((t_local >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tbase + acc * BN;
+        const uint32_t d = tbase + acc * ACOLS, dc = d + BN;
         bool first = true;
         for (int src = 0; src < a.n_src; ++src) {
           const int nk = a.K[src] / BK;
           for (int kc = 0; kc < nk; ++kc) {
-            mbar_wait(&full[s], ph);
+            if (TF32) mbar_wait(&lo_ready[s], ph);
+            else mbar_wait(&full[s], ph);
             tc_fence_after();
-            const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+            const uint32_t a0 = smem_u32(stA(s)), w0 = smem_u32(stW(s));
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k) {
+            for (int k = 0; k < 4; ++k) {               // 4 x 32 B = one 128-B row per stage
               const uint64_t ad = make_sdesc(a0 + k * 32, 16, 1024, LAYOUT_SW128);
-              const uint64_t bd = make_sdesc(b0 + k * 32, 16, 1024, LAYOUT_SW128);
-              mma_f16(d, ad, bd, idesc, first ? 0u : 1u);
+              const uint64_t wd = make_sdesc(w0 + k * 32, 16, 1024, LAYOUT_SW128);
+              if (TF32) {
+                const uint64_t ald = make_sdesc(smem_u32(stAlo(s)) + k * 32, 16, 1024, LAYOUT_SW128);
+                const uint64_t wld = make_sdesc(smem_u32(stWlo(s)) + k * 32, 16, 1024, LAYOUT_SW128);
+                mma_tf32(d, ad, wd, idesc, first ? 0u : 1u);      // main: hi.hi
+                mma_tf32(dc, ald, wd, idesc, first ? 0u : 1u);    // corr: lo.hi + hi.lo
+                mma_tf32(dc, ad, wld, idesc, 1u);
+              } else {
+                mma_f16(d, ad, wd, idesc, first ? 0u : 1u);
+              }
               first = false;
             }
             mma_commit(&empty[s]);
@@ -165,6 +200,32 @@ __global__ void __launch_bounds__(192, 1) mimo_gemm_bf16_kernel(const __grid_con
           }
         }
         mma_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp >= 6) {
+    // =========================================================== lo transform (3xTF32)
+    if (TF32) {
+      const int t = threadIdx.x - 192;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        for (int src = 0; src < a.n_src; ++src) {
+          const int nk = a.K[src] / BK;
+          for (int kc = 0; kc < nk; ++kc) {
+            mbar_wait(&full[s], ph);
+            float4* hi = reinterpret_cast<float4*>(stA(s));
+            float4* out = reinterpret_cast<float4*>(stAlo(s));
+#pragma unroll
+            for (int e = t; e < (int)(C::A_BYTES / 16); e += 128) {
+              const float4 v = hi[e], h = tf32_hi4(v);
+              hi[e] = h;                                // hi in place (the MMA waits for lo_ready)
+              out[e] = tf32_lo4(v, h);
+            }
+            fence_async_smem();
+            mbar_arrive(&lo_ready[s]);
+            if (++s == STAGES) { s = 0; ph ^= 1; }
+          }
+        }
       }
     }
   } else {
@@ -182,39 +243,53 @@ __global__ void __launch_bounds__(192, 1) mimo_gemm_bf16_kernel(const __grid_con
       const int acc = (int)(t_local & 1);
       mbar_wait(&tfull[acc], (uint32_t)((t_local >> 1) & 1));
       tc_fence_after();
-      for (int j = 0; j < BN / 64; ++j, ++chunk_ctr) {
+      for (int j = 0; j < BN / C::CW; ++j, ++chunk_ctr) {
         const int rb = (int)(chunk_ctr & 1);
-        uint8_t* rbuf = sR + rb * R_BYTES;
-        const int n0 = nb * BN + j * 64;
+        uint8_t* rbuf = sR + rb * C::R_BYTES;
+        const int n0 = nb * BN + j * C::CW;
         if (leader) {
           bulk_wait_read<1>();                     // the store that last used rbuf[rb] has read it
           if (a.has_residual) {
-            mbar_arrive_expect_tx(&rfull[rb], R_BYTES);
+            mbar_arrive_expect_tx(&rfull[rb], C::R_BYTES);
             tma_load_3d(rbuf, &maps.R, &rfull[rb], n0, l0, b);
           }
         }
         uint32_t v[64];
-        const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + acc * BN + j * 64;
+        const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + acc * ACOLS + j * C::CW;
         tmem_ld32(taddr, v);
-        tmem_ld32(taddr + 32, v + 32);
+        tmem_ld32(taddr + (TF32 ? BN : 32), v + 32);     // 3xTF32: the corr accumulator
         tmem_wait_ld();
+        if (TF32) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) + __uint_as_float(v[32 + e]));
+        }
         if (a.has_residual) mbar_wait(&rfull[rb], (chunk_ctr >> 1) & 1);
         else named_sync(2, 128);                   // rbuf free (leader waited for the old store)
-        // row `row` of the SW128 tile: 8 chunks of 16 B at ((c ^ (row % 8)) * 16)
-        uint8_t* rrow = rbuf + row * 128;
+        uint8_t* rrow = rbuf + row * 128;          // SW128: 16-B chunk c at ((c ^ (row % 8)) * 16)
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           uint4* p = reinterpret_cast<uint4*>(rrow + ((c ^ (row & 7)) * 16));
-          float f[8];
+          if (TF32) {
+            float f[4];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[c * 8 + e]);
-          if (a.has_residual) {
-            const uint4 r = *p;
-            const float2 r0 = unpack_bf16(r.x), r1 = unpack_bf16(r.y), r2 = unpack_bf16(r.z), r3 = unpack_bf16(r.w);
-            f[0] += r0.x; f[1] += r0.y; f[2] += r1.x; f[3] += r1.y;
-            f[4] += r2.x; f[5] += r2.y; f[6] += r3.x; f[7] += r3.y;
+            for (int e = 0; e < 4; ++e) f[e] = __uint_as_float(v[c * 4 + e]);
+            if (a.has_residual) {
+              const float4 r = *reinterpret_cast<const float4*>(p);
+              f[0] += r.x; f[1] += r.y; f[2] += r.z; f[3] += r.w;
+            }
+            *reinterpret_cast<float4*>(p) = make_float4(f[0], f[1], f[2], f[3]);
+          } else {
+            float f[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[c * 8 + e]);
+            if (a.has_residual) {
+              const uint4 r = *p;
+              const float2 r0 = unpack_bf16(r.x), r1 = unpack_bf16(r.y), r2 = unpack_bf16(r.z), r3 = unpack_bf16(r.w);
+              f[0] += r0.x; f[1] += r0.y; f[2] += r1.x; f[3] += r1.y;
+              f[4] += r2.x; f[5] += r2.y; f[6] += r3.x; f[7] += r3.y;
+            }
+            *p = make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
           }
-          *p = make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
         }
         fence_async_smem();
         named_sync(1, 128);
@@ -245,37 +320,25 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 3-D bf16 signal [batch][L][K], box {64, rows, 1}, SWIZZLE_128B
-static bool map_signal(CUtensorMap* m, const void* base, int64_t K, int64_t L, int64_t batch, int rows) {
+// 3-D tensor [d2][d1][d0] (d0 contiguous) with a box {128-B row, rows, 1}, SWIZZLE_128B.
+static bool map3d(CUtensorMap* m, const void* base, bool f32, int64_t d0, int64_t d1, int64_t d2, int rows) {
   auto fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)L, (cuuint64_t)batch};
-  cuuint64_t strides[2] = {(cuuint64_t)(K * 2), (cuuint64_t)(L * K * 2)};
-  cuuint32_t box[3] = {64, (cuuint32_t)rows, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-// 2-D bf16 weight [n_out][K], box {64, BN}, SWIZZLE_128B
-static bool map_weight(CUtensorMap* m, const void* base, int64_t K, int64_t n_out, int bn) {
-  auto fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)n_out};
-  cuuint64_t strides[1] = {(cuuint64_t)(K * 2)};
-  cuuint32_t box[2] = {64, (cuuint32_t)bn};
-  cuuint32_t es[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const int64_t es = f32 ? 4 : 2;
+  cuuint64_t dims[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
+  cuuint64_t strides[2] = {(cuuint64_t)(d0 * es), (cuuint64_t)(d1 * d0 * es)};
+  cuuint32_t box[3] = {(cuuint32_t)(128 / es), (cuuint32_t)rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base),
+            dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-bool mimo_tc_supported(int m, int p, int q) {
-  return m % 64 == 0 && p % 64 == 0 && q % 64 == 0 && m >= 64;
-}
+bool mimo_tc_supported(int m, int p, int q) { return m % 64 == 0 && p % 64 == 0 && q % 64 == 0 && m >= 64; }
 
-template <int BN>
-static int launch_bn(const MimoGemm& g, cudaStream_t st) {
+template <int BN, bool TF32>
+static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
+  using C = Cfg<BN, TF32>;
   MimoMaps maps;
   memset(&maps, 0, sizeof(maps));
   MimoArg a{};
@@ -284,30 +347,35 @@ static int launch_bn(const MimoGemm& g, cudaStream_t st) {
   a.batch = g.batch;
   a.n_out = g.n_out;
   for (int s = 0; s < g.n_src; ++s) {
-    if (g.src[s].K % BK) return CASC_ERR_UNSUPPORTED;
+    if (g.src[s].K % C::BK) return CASC_ERR_UNSUPPORTED;
     a.K[s] = g.src[s].K;
     a.shift[s] = g.src[s].shift;
-    if (!map_signal(&maps.A[s], g.src[s].A, g.src[s].K, g.L, g.batch, BM)) return CASC_ERR_CUDA;
-    if (!map_weight(&maps.W[s], g.src[s].W, g.src[s].K, g.n_out, BN)) return CASC_ERR_CUDA;
+    if (!map3d(&maps.A[s], g.src[s].A, TF32, g.src[s].K, g.L, g.batch, BM)) return CASC_ERR_CUDA;
+    // weights: bf16 [n_out][K]; 3xTF32: [2 (hi, lo)][n_out][K]
+    if (!map3d(&maps.W[s], g.src[s].W, TF32, g.src[s].K, g.n_out, TF32 ? 2 : 1, BN)) return CASC_ERR_CUDA;
   }
   a.has_residual = g.R != nullptr;
-  if (g.R && !map_signal(&maps.R, g.R, g.n_out, g.L, g.batch, BM)) return CASC_ERR_CUDA;
-  if (!map_signal(&maps.out, g.out, g.n_out, g.L, g.batch, BM)) return CASC_ERR_CUDA;
-  const size_t smem = 1024 + STAGES * (A_BYTES + (size_t)BN * BK * 2) + 2 * BM * 64 * 2;
-  if (cudaFuncSetAttribute(mimo_gemm_bf16_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
+  if (g.R && !map3d(&maps.R, g.R, TF32, g.n_out, g.L, g.batch, BM)) return CASC_ERR_CUDA;
+  if (!map3d(&maps.out, g.out, TF32, g.n_out, g.L, g.batch, BM)) return CASC_ERR_CUDA;
+  if (cudaFuncSetAttribute(mimo_gemm_kernel<BN, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)C::SMEM) != cudaSuccess)
     return CASC_ERR_CUDA;
   const int64_t tiles = ceil_div(g.L, BM) * g.batch * ceil_div(g.n_out, BN);
   const int grid = (int)std::min<int64_t>(tiles, 148);
-  mimo_gemm_bf16_kernel<BN><<<grid, 192, smem, st>>>(maps, a);
+  mimo_gemm_kernel<BN, TF32><<<grid, C::THREADS, C::SMEM, st>>>(maps, a);
   CASC_LAUNCHED();
   return CASC_OK;
 }
 
-int launch_mimo_gemm_bf16(const MimoGemm& g, cudaStream_t st) {
-  if (g.n_out % 256 == 0) return launch_bn<256>(g, st);
-  if (g.n_out % 128 == 0) return launch_bn<128>(g, st);
-  if (g.n_out % 64 == 0) return launch_bn<64>(g, st);
+int launch_mimo_gemm(const MimoGemm& g, bool tf32, cudaStream_t st) {
+  if (tf32) {
+    if (g.n_out % 128 == 0) return launch_cfg<128, true>(g, st);   // main + corr accumulators
+    if (g.n_out % 64 == 0) return launch_cfg<64, true>(g, st);
+  } else {
+    if (g.n_out % 256 == 0) return launch_cfg<256, false>(g, st);
+    if (g.n_out % 128 == 0) return launch_cfg<128, false>(g, st);
+    if (g.n_out % 64 == 0) return launch_cfg<64, false>(g, st);
+  }
   return CASC_ERR_UNSUPPORTED;
 }
 

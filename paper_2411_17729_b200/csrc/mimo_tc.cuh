@@ -23,7 +23,7 @@ struct MimoGemm {
 };
 
 bool mimo_tc_supported(int m, int p, int q);
-int launch_mimo_gemm_bf16(const MimoGemm& g, cudaStream_t st);
-int launch_f64_to_bf16(const double* src, __nv_bfloat16* dst, int64_t n, cudaStream_t st);
+// tf32 = true: 3xTF32 (fp32 signals, weights as [2][n_out][K] tf32 hi/lo); else bf16.
+int launch_mimo_gemm(const MimoGemm& g, bool tf32, cudaStream_t st);
 
 }  // namespace casc

@@ -112,9 +112,11 @@ def test_E4_reduced_bf16():
 @pytest.mark.parametrize("m,p,q,L,batch,N", [(128, 64, 64, 1000, 3, 6), (64, 64, 64, 300, 2, 0),
                                               (256, 128, 64, 4096, 2, 11), (192, 64, 128, 129, 1, 3),
                                               (128, 64, 64, 2, 2, 5), (128, 64, 64, 1, 1, 2)])
-def test_mimo_bf16_tensor_core_path(m, p, q, L, batch, N):
-    """bf16 MIMO systems with m, p, q multiples of 64 take the TMA + tcgen05 GEMM path."""
-    wl = S.make_random_mimo(m, p, q, L=L, batch=batch, N=N, rho=0.98, mode="bf16")
+@pytest.mark.parametrize("mode", ["bf16", "fp32"])
+def test_mimo_tensor_core_path(m, p, q, L, batch, N, mode):
+    """MIMO systems with m, p, q multiples of 64 take the TMA + tcgen05 GEMM path
+    (kind::f16 in bf16 mode, 3xTF32 in fp32 mode)."""
+    wl = S.make_random_mimo(m, p, q, L=L, batch=batch, N=N, rho=0.98, mode=mode)
     check_parity(wl)
 
 
