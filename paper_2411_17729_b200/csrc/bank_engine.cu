@@ -13,6 +13,7 @@
 #include "bank_tc.cuh"
 #include "profile.cuh"
 #include "engine.cuh"
+#include "mimo_tc.cuh"
 
 namespace casc {
 
@@ -144,11 +145,27 @@ int engine_bank_tc(int n, int m, int64_t L, int batch, const int* N_host, int N_
     a.sys_list = dorder; a.n_list = cnt; a.L = L; a.batch = batch;
     a.tiles_per_cta = pick_group(ntiles, (int64_t)cnt * batch, 8);
     ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt * batch * L * m * 4.0, 2.0 * cnt * batch * L * (double)mm);
-    static const bool use_ws = [] {
+    // Kernel choice (CASC_BANK_STAGE for A/B measurements): the TMA-pipelined shifted GEMM
+    // (mimo_tc.cu, 3xTF32, per-channel weight planes) for m % 64 == 0, else the
+    // register-prefetch kernel; "rp" / "ws" force the older variants.
+    static const char mode_env = [] {
       const char* e = getenv("CASC_BANK_STAGE");
-      return e && e[0] == 'w';
+      return e ? e[0] : 't';
     }();
-    if ((rc = use_ws ? launch_bank_stage_ws(m, a, st) : launch_bank_stage_rp(m, a, st))) return rc;
+    if (mode_env == 'w') {
+      rc = launch_bank_stage_ws(m, a, st);
+    } else if (mode_env == 'r' || m % 64 != 0) {
+      rc = launch_bank_stage_rp(m, a, st);
+    } else {
+      MimoGemm g{};
+      g.src[0].A = a.Vs; g.src[0].W = P.f32; g.src[0].K = m; g.src[0].shift = (int64_t)1 << k;
+      g.src[0].w_plane_off = 2 * k; g.src[0].w_planes = (int64_t)n * (N_max + 1) * 2;
+      g.n_src = 1; g.R = a.Vs; g.out = a.Vd; g.n_out = m; g.L = L; g.batch = batch;
+      g.sys_list = dorder; g.n_list = cnt; g.n_sys_total = n;
+      g.w_plane_stride = 2 * (N_max + 1); g.t_first = (int)(a.copy_from / 128);
+      rc = launch_mimo_gemm(g, true, st);
+    }
+    if (rc) return rc;
   }
   // ---- tail: stage Ne + y = C v + D u
   {

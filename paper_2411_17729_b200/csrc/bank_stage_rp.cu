@@ -63,7 +63,10 @@ __global__ void __launch_bounds__(128) bank_stage_rp_kernel(BankStageArg a) {
   uint32_t phase = 0;
 
   float4 areg[NLD];
-  float sreg[MS];
+  // self rows of this warp (rows 32*warp .. +31 of the tile) in the warp-coalesced mapping:
+  // sweep it covers RPS consecutive rows, lane -> (row it*RPS + lane/CH, 16-B chunk lane%CH)
+  constexpr int RPS = 32 / CH;
+  float4 s4[CH];
   // shifted tile rows [src0, src0+128): a warp moves 8 rows x 4 chunks (8 x 64 B) per load
   auto load_a = [&](int64_t src0) {
 #pragma unroll
@@ -74,14 +77,35 @@ __global__ void __launch_bounds__(128) bank_stage_rp_kernel(BankStageArg a) {
     }
   };
   auto load_s = [&](int64_t t0) {
-    const int64_t row = t0 + tid;
-    if (row < a.L) {
+    const int64_t r0 = t0 + warp * 32;
 #pragma unroll
-      for (int i = 0; i < MS; i += 4) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(Vs + row * MS + i));
-        sreg[i] = v.x; sreg[i + 1] = v.y; sreg[i + 2] = v.z; sreg[i + 3] = v.w;
-      }
+    for (int it = 0; it < CH; ++it) {
+      const int64_t row = r0 + it * RPS + lane / CH;
+      s4[it] = row < a.L ? __ldg(reinterpret_cast<const float4*>(Vs + row * MS + (lane % CH) * 4))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+  };
+  // store this warp's 32 rows: optional per-thread-row values v (TMEM lane order) are first
+  // transposed through the warp's swizzled smem slab, then added to s4 and written coalesced
+  auto store_rows = [&](float* slab, const float* v, int64_t r0, int valid) {
+    if (v) {
+#pragma unroll
+      for (int j = 0; j < CH; ++j)
+        *reinterpret_cast<float4*>(slab + lane * MS + ((j ^ (lane % CH)) * 4)) =
+            make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      __syncwarp();
+    }
+#pragma unroll
+    for (int it = 0; it < CH; ++it) {
+      const int r = it * RPS + lane / CH, j = lane % CH;
+      float4 o = s4[it];
+      if (v) {
+        const float4 p = *reinterpret_cast<const float4*>(slab + r * MS + ((j ^ (r % CH)) * 4));
+        o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+      }
+      if (r < valid) *reinterpret_cast<float4*>(Vd + (r0 + r) * MS + j * 4) = o;
+    }
+    __syncwarp();
   };
   if (tb * TM - shift >= 0) load_a(tb * TM - shift);
   load_s(tb * TM);
@@ -93,12 +117,11 @@ __global__ void __launch_bounds__(128) bank_stage_rp_kernel(BankStageArg a) {
     const int valid = (int)(rem_rows < 0 ? 0 : (rem_rows < 32 ? rem_rows : 32));
     const bool has_next = tile + 1 < tile_end;
     if (src0 < 0) {                                  // l < 2^k: column unchanged
-      warp_store_rows<MS>(Ahi + warp * 32 * MS, sreg, Vd + r0 * MS, lane, valid);
+      store_rows(nullptr, nullptr, r0, valid);
       if (has_next) {
         if (src0 + TM >= 0) load_a(src0 + TM);
         load_s(t0 + TM);
       }
-      __syncthreads();                               // staging slabs (in Ahi) free again
       continue;
     }
 #pragma unroll
@@ -135,10 +158,8 @@ __global__ void __launch_bounds__(128) bank_stage_rp_kernel(BankStageArg a) {
 #pragma unroll
     for (int c0 = 0; c0 < MS; c0 += 16) tmem_ld16(tacc + ((uint32_t)(warp * 32) << 16) + c0, v + c0);
     tc_fence_before();
-#pragma unroll
-    for (int i = 0; i < MS; ++i) v[i] += sreg[i];
+    store_rows(Ahi + warp * 32 * MS, v, r0, valid);   // slab in Ahi: free once the MMA completed
     if (has_next) load_s(t0 + TM);
-    warp_store_rows<MS>(Ahi + warp * 32 * MS, v, Vd + r0 * MS, lane, valid);   // Ahi free after the MMA
     __syncthreads();
   }
   __syncthreads();

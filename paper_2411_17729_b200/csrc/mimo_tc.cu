@@ -1,26 +1,30 @@
-// MIMO cascade stages on the sm_100a tensor cores.
+// Shifted multi-source GEMM on the sm_100a tensor cores: every dense cascade step.
 //
-// One kernel computes every step of PAPER.md:185-229 for a single system as a shifted
-// multi-source GEMM with a fused residual epilogue:
-//   out[b][l][n] = sum_src sum_k A_src[b][l - shift_src][k] W_src[n][k]  (+ R[b][l][n])
-//   first stage  (a2): (u, 0, Bbar), (u, 1, Abar Bbar)            -> v^(1)
-//   stage k      (a4): (v, 2^k, Abar^(2^k)) + residual v           -> v^(k+1)
-//   last stage   (a5): (v, 0, C), (v, 2^N, C Abar^(2^N)), (u, 0, D) -> y
+// One kernel computes the steps of PAPER.md:185-229 as
+//   out[s][l][n] = sum_src sum_k A_src[s][l - shift_src][k] W_src(s)[n][k]  (+ R[s][l][n])
+// over sequences s (a (system, batch) pair) and time steps l:
+//   MIMO first stage (a2): (u, 0, Bbar), (u, 1, Abar Bbar)            -> v^(1)
+//   MIMO / bank stage (a4): (v, 2^k, Abar^(2^k)) + residual v          -> v^(k+1)
+//   MIMO last stage  (a5): (v, 0, C), (v, 2^N, C Abar^(2^N)), (u, 0, D) -> y
 // The time shift is a TMA coordinate offset; rows l - shift < 0 fall outside the tensor and
 // TMA zero-fills them, which is exactly "columns l < 2^k are left unchanged".
+// For a bank of channels the weight W_src(s) is the power of the channel owning sequence s:
+// the weight tensor is a stack of planes and each tile selects its plane.
 //
 // Two precisions (template TF32):
 //   bf16   : kind::f16, bf16 tiles of 128 x 64 (128-B rows), fp32 accumulation, bf16 output.
-//   3xTF32 : kind::tf32 with hi.hi + lo.hi + hi.lo, fp32 tiles of 128 x 32 (128-B rows). The
-//            constant W comes as tf32 hi/lo pairs; the streaming A tile is used raw (the tensor
-//            core truncates it to its tf32 hi) and transform warps write lo = x - trunc(x).
+//   3xTF32 : kind::tf32 with hi.hi + lo.hi + hi.lo, fp32 tiles of 128 x 32 (128-B rows). W comes
+//            as tf32 hi/lo planes; transform warps split the landed A tile in shared memory into
+//            hi = rna(x) (in place) and lo = rna(x - hi). hi.hi and the two correction products
+//            accumulate in separate TMEM accumulators (see ACOLS below).
 //
 // Persistent CTAs (one per SM):
-//   warp 0      TMA producer: ring of {A, W (hi[, lo])} tiles (SWIZZLE_128B)
-//   warp 1      MMA issuer: M=128, N=BN, into one of two TMEM accumulators (2 x BN columns)
-//   warps 2-5   epilogue: TMEM -> registers (lane = time row), + residual tile (TMA-loaded),
-//               convert in place, TMA store; accumulator released to warp 1.
-//   warps 6-9   (3xTF32 only) lo-part transform of each landed A tile.
+//   warp 0      TMA producer: ring of {A, W (hi[, lo])} tiles (SWIZZLE_128B) and a separate ring
+//               of residual / staging chunks (128 rows x 128 B) fetched ahead of the epilogue
+//   warp 1      MMA issuer: M=128, N=BN, into one of two TMEM accumulator buffers
+//   warps 2-5   epilogue: TMEM -> registers (lane = time row), + residual chunk, convert in place,
+//               TMA store; accumulator released to warp 1, chunk slot released to warp 0.
+//   warps 6-9   (3xTF32 only) hi/lo split of each landed A tile.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -81,21 +85,41 @@ struct Cfg {
   static constexpr uint32_t A_BYTES = BM * 128;           // 16 KB
   static constexpr uint32_t W_BYTES = BN * 128;           // one of hi / lo
   static constexpr int NW = TF32 ? 2 : 1;                 // weight tiles per stage
-  static constexpr uint32_t STAGE_BYTES = A_BYTES * (TF32 ? 2 : 1) + W_BYTES * NW;   // (A, Alo,) W...
+  static constexpr uint32_t STAGE_BYTES = A_BYTES * (TF32 ? 2 : 1) + W_BYTES * NW;   // A, W hi, (W lo, A lo)
   static constexpr uint32_t TMA_BYTES = A_BYTES + W_BYTES * NW;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES < 4 ? (200 * 1024) / STAGE_BYTES : 4;
-  static constexpr int CW = 128 / ES;                     // epilogue chunk width (columns)
+  static constexpr int RS = (TF32 && BN == 64) ? 4 : 2;   // residual / staging chunk slots
   static constexpr uint32_t R_BYTES = BM * 128;           // 16 KB
-  static constexpr int THREADS = TF32 ? 320 : 192;
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + 2 * R_BYTES;
+  static constexpr int STAGES_FIT = (int)((226u * 1024u - 1024u - RS * R_BYTES) / STAGE_BYTES);
+  static constexpr int STAGES = STAGES_FIT < 4 ? STAGES_FIT : 4;
+  static constexpr int CW = 128 / ES;                     // epilogue chunk width (columns)
+  static constexpr int R_WARP = TF32 ? 10 : 6;            // residual / staging producer warp
+  static constexpr int THREADS = 32 * (R_WARP + 1);
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + RS * R_BYTES;
 };
+
+// Tile -> (sequence coordinate in the tensors, time tile, N block, weight plane base)
+struct TileCoord {
+  int seq, l0, nb, plane0;
+};
+__device__ __forceinline__ TileCoord decode(int64_t tile, const MimoArg& a, int n_nblk, int64_t nt_eff) {
+  TileCoord t;
+  t.nb = (int)(tile % n_nblk);
+  const int64_t r = tile / n_nblk;
+  t.l0 = (int)((a.t_first + r % nt_eff) * BM);
+  const int64_t sidx = r / nt_eff;
+  const int li = (int)(sidx / a.batch), b = (int)(sidx % a.batch);
+  const int sys = a.sys_list ? a.sys_list[li] : 0;
+  t.seq = sys * a.batch + b;
+  t.plane0 = sys * a.w_plane_stride;
+  return t;
+}
 }  // namespace
 
 template <int BN, bool TF32>
 __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(const __grid_constant__ MimoMaps maps,
                                                                               MimoArg a) {
   using C = Cfg<BN, TF32>;
-  constexpr int STAGES = C::STAGES, BK = C::BK;
+  constexpr int STAGES = C::STAGES, BK = C::BK, RS = C::RS;
   // TMEM: two accumulator buffers of ACOLS columns. 3xTF32 keeps hi.hi in [0, BN) ("main") and
   // the two correction products in [BN, 2BN) ("corr"): the tensor core's fp32 accumulator
   // truncates at every MMA, so the error grows with the number of MMAs chained into one
@@ -106,9 +130,8 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
   constexpr int TCOLS = 2 * ACOLS < 32 ? 32 : 2 * ACOLS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // per stage: [A][W hi][(W lo)][(A lo)]
-  uint8_t* sR = smem + STAGES * C::STAGE_BYTES;      // [2][R_BYTES]
-  __shared__ uint64_t full[STAGES], empty[STAGES], lo_ready[STAGES], tfull[2], tempty[2], rfull[2];
+  uint8_t* sR = smem + STAGES * C::STAGE_BYTES;      // [RS][R_BYTES]
+  __shared__ uint64_t full[STAGES], empty[STAGES], lo_ready[STAGES], tfull[2], tempty[2], rfull[RS], rempty[RS];
   __shared__ uint32_t tmem_base;
   auto stA = [&](int s) { return smem + s * C::STAGE_BYTES; };
   auto stW = [&](int s) { return smem + s * C::STAGE_BYTES + C::A_BYTES; };
@@ -117,13 +140,15 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t mt_per_b = (a.L + BM - 1) / BM;
-  const int64_t n_mblk = mt_per_b * a.batch;
+  const int64_t nt_eff = mt_per_b - a.t_first;
   const int n_nblk = (a.n_out + BN - 1) / BN;
-  const int64_t n_tiles = n_mblk * n_nblk;
+  const int64_t n_tiles = (int64_t)a.n_list * a.batch * nt_eff * n_nblk;
+  constexpr int NCH = BN / C::CW;                   // epilogue chunks per tile
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); mbar_init(&lo_ready[s], 128); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); mbar_init(&rfull[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
+    for (int s = 0; s < RS; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 1); }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<TCOLS>(&tmem_base);
@@ -143,20 +168,37 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
       int s = 0;
       uint32_t ph = 0;
       for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int64_t mb = tile / n_nblk;
-        const int nb = (int)(tile % n_nblk);
-        const int b = (int)(mb / mt_per_b);
-        const int l0 = (int)((mb % mt_per_b) * BM);
+        const TileCoord tc = decode(tile, a, n_nblk, nt_eff);
         for (int src = 0; src < a.n_src; ++src) {
           const int nk = a.K[src] / BK;
+          const int plane = tc.plane0 + a.w_plane_off[src];
           for (int kc = 0; kc < nk; ++kc) {
             mbar_wait(&empty[s], ph ^ 1);
             mbar_arrive_expect_tx(&full[s], C::TMA_BYTES);
-            tma_load_3d(stA(s), &maps.A[src], &full[s], kc * BK, l0 - (int)a.shift[src], b);
-            tma_load_3d(stW(s), &maps.W[src], &full[s], kc * BK, nb * BN, 0);
-            if (TF32) tma_load_3d(stWlo(s), &maps.W[src], &full[s], kc * BK, nb * BN, 1);
+            tma_load_3d(stA(s), &maps.A[src], &full[s], kc * BK, tc.l0 - (int)a.shift[src], tc.seq);
+            tma_load_3d(stW(s), &maps.W[src], &full[s], kc * BK, tc.nb * BN, plane);
+            if (TF32) tma_load_3d(stWlo(s), &maps.W[src], &full[s], kc * BK, tc.nb * BN, plane + 1);
             if (++s == STAGES) { s = 0; ph ^= 1; }
           }
+        }
+      }
+    }
+  } else if (warp == C::R_WARP) {
+    // =========================================================== residual / staging producer
+    if (lane == 0) {
+      int rs = 0;
+      uint32_t rph = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const TileCoord tc = decode(tile, a, n_nblk, nt_eff);
+        for (int j = 0; j < NCH; ++j) {
+          mbar_wait(&rempty[rs], rph ^ 1);
+          if (a.has_residual) {
+            mbar_arrive_expect_tx(&rfull[rs], C::R_BYTES);
+            tma_load_3d(sR + rs * C::R_BYTES, &maps.R, &rfull[rs], tc.nb * BN + j * C::CW, tc.l0, tc.seq);
+          } else {
+            mbar_arrive(&rfull[rs]);
+          }
+          if (++rs == RS) { rs = 0; rph ^= 1; }
         }
       }
     }
@@ -203,7 +245,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
       }
     }
   } else if (warp >= 6) {
-    // =========================================================== lo transform (3xTF32)
+    // =========================================================== hi/lo split (3xTF32, warps 6-9)
     if (TF32) {
       const int t = threadIdx.x - 192;
       int s = 0;
@@ -234,26 +276,15 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
     const int row = q * 32 + lane;                // tile row = TMEM lane
     const bool leader = (warp == 2 && lane == 0);
     int64_t t_local = 0;
-    uint32_t chunk_ctr = 0;
+    int rs = 0, prev_rs = -1;
+    uint32_t rph = 0;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t_local) {
-      const int64_t mb = tile / n_nblk;
-      const int nb = (int)(tile % n_nblk);
-      const int b = (int)(mb / mt_per_b);
-      const int l0 = (int)((mb % mt_per_b) * BM);
+      const TileCoord tc = decode(tile, a, n_nblk, nt_eff);
       const int acc = (int)(t_local & 1);
       mbar_wait(&tfull[acc], (uint32_t)((t_local >> 1) & 1));
       tc_fence_after();
-      for (int j = 0; j < BN / C::CW; ++j, ++chunk_ctr) {
-        const int rb = (int)(chunk_ctr & 1);
-        uint8_t* rbuf = sR + rb * C::R_BYTES;
-        const int n0 = nb * BN + j * C::CW;
-        if (leader) {
-          bulk_wait_read<1>();                     // the store that last used rbuf[rb] has read it
-          if (a.has_residual) {
-            mbar_arrive_expect_tx(&rfull[rb], C::R_BYTES);
-            tma_load_3d(rbuf, &maps.R, &rfull[rb], n0, l0, b);
-          }
-        }
+      for (int j = 0; j < NCH; ++j) {
+        uint8_t* rbuf = sR + rs * C::R_BYTES;
         uint32_t v[64];
         const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + acc * ACOLS + j * C::CW;
         tmem_ld32(taddr, v);
@@ -263,8 +294,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) + __uint_as_float(v[32 + e]));
         }
-        if (a.has_residual) mbar_wait(&rfull[rb], (chunk_ctr >> 1) & 1);
-        else named_sync(2, 128);                   // rbuf free (leader waited for the old store)
+        mbar_wait(&rfull[rs], rph);
         uint8_t* rrow = rbuf + row * 128;          // SW128: 16-B chunk c at ((c ^ (row % 8)) * 16)
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
@@ -291,15 +321,23 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
             *p = make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
           }
         }
+        if (j == NCH - 1) {                         // this tile's accumulator has been drained
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+        }
         fence_async_smem();
         named_sync(1, 128);
         if (leader) {
-          tma_store_3d(&maps.out, rbuf, n0, l0, b);
+          tma_store_3d(&maps.out, rbuf, tc.nb * BN + j * C::CW, tc.l0, tc.seq);
           bulk_commit();
+          if (prev_rs >= 0) {                       // the previous chunk's store has read its slot
+            bulk_wait_read<1>();
+            mbar_arrive(&rempty[prev_rs]);
+          }
         }
+        prev_rs = rs;
+        if (++rs == RS) { rs = 0; rph ^= 1; }
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
     }
     if (leader) bulk_wait<0>();
   }
@@ -346,21 +384,29 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
   a.L = g.L;
   a.batch = g.batch;
   a.n_out = g.n_out;
+  a.sys_list = g.sys_list;
+  a.n_list = g.sys_list ? g.n_list : 1;
+  a.w_plane_stride = g.w_plane_stride;
+  a.t_first = g.t_first;
+  const int64_t nseq_total = (int64_t)(g.n_sys_total > 0 ? g.n_sys_total : 1) * g.batch;
   for (int s = 0; s < g.n_src; ++s) {
     if (g.src[s].K % C::BK) return CASC_ERR_UNSUPPORTED;
     a.K[s] = g.src[s].K;
     a.shift[s] = g.src[s].shift;
-    if (!map3d(&maps.A[s], g.src[s].A, TF32, g.src[s].K, g.L, g.batch, BM)) return CASC_ERR_CUDA;
-    // weights: bf16 [n_out][K]; 3xTF32: [2 (hi, lo)][n_out][K]
-    if (!map3d(&maps.W[s], g.src[s].W, TF32, g.src[s].K, g.n_out, TF32 ? 2 : 1, BN)) return CASC_ERR_CUDA;
+    a.w_plane_off[s] = g.src[s].w_plane_off;
+    if (!map3d(&maps.A[s], g.src[s].A, TF32, g.src[s].K, g.L, nseq_total, BM)) return CASC_ERR_CUDA;
+    // weights: planes of [n_out][K] (bf16), or hi / lo planes of tf32 for 3xTF32
+    const int64_t planes = g.src[s].w_planes > 0 ? g.src[s].w_planes : (TF32 ? 2 : 1);
+    if (!map3d(&maps.W[s], g.src[s].W, TF32, g.src[s].K, g.n_out, planes, BN)) return CASC_ERR_CUDA;
   }
   a.has_residual = g.R != nullptr;
-  if (g.R && !map3d(&maps.R, g.R, TF32, g.n_out, g.L, g.batch, BM)) return CASC_ERR_CUDA;
-  if (!map3d(&maps.out, g.out, TF32, g.n_out, g.L, g.batch, BM)) return CASC_ERR_CUDA;
+  if (g.R && !map3d(&maps.R, g.R, TF32, g.n_out, g.L, nseq_total, BM)) return CASC_ERR_CUDA;
+  if (!map3d(&maps.out, g.out, TF32, g.n_out, g.L, nseq_total, BM)) return CASC_ERR_CUDA;
   if (cudaFuncSetAttribute(mimo_gemm_kernel<BN, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)C::SMEM) != cudaSuccess)
     return CASC_ERR_CUDA;
-  const int64_t tiles = ceil_div(g.L, BM) * g.batch * ceil_div(g.n_out, BN);
+  const int64_t tiles = (int64_t)a.n_list * g.batch * (ceil_div(g.L, BM) - g.t_first) * ceil_div(g.n_out, BN);
+  if (tiles <= 0) return CASC_OK;
   const int grid = (int)std::min<int64_t>(tiles, 148);
   mimo_gemm_kernel<BN, TF32><<<grid, C::THREADS, C::SMEM, st>>>(maps, a);
   CASC_LAUNCHED();

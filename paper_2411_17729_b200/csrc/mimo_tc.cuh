@@ -1,4 +1,5 @@
-// MIMO tensor-core path (bf16 storage): argument blocks and launchers (internal).
+// Tensor-core shifted multi-source GEMM (MIMO steps and bank streaming stages): argument
+// blocks and launchers (internal).
 #pragma once
 #include <cuda.h>
 #include "common.cuh"
@@ -6,24 +7,33 @@
 namespace casc {
 
 struct MimoMaps {                 // passed as one __grid_constant__ kernel parameter
-  CUtensorMap A[3];               // source signals [batch][L][K_src]   box {64, 128, 1}
-  CUtensorMap W[3];               // weights [n_out][K_src]             box {64, BN}
-  CUtensorMap R;                  // residual [batch][L][n_out]         box {64, 128, 1}
-  CUtensorMap out;                // output   [batch][L][n_out]         box {64, 128, 1}
+  CUtensorMap A[3];               // source signals [seq][L][K_src]    box {128 B, 128, 1}
+  CUtensorMap W[3];               // weight planes [plane][n_out][K]   box {128 B, BN, 1}
+  CUtensorMap R;                  // residual [seq][L][n_out]          box {128 B, 128, 1}
+  CUtensorMap out;                // output   [seq][L][n_out]          box {128 B, 128, 1}
 };
 struct MimoArg {
-  int n_src; int K[3]; int64_t shift[3];
+  int n_src; int K[3]; int64_t shift[3]; int w_plane_off[3];
   int64_t L; int batch; int n_out; int has_residual;
+  const int* sys_list; int n_list;   // systems processed (bank channels); null: one system
+  int w_plane_stride;                // weight planes per system (bank: slots * 2)
+  int t_first;                       // first 128-step time tile processed in each sequence
 };
-struct MimoSrc { const void* A; const void* W; int K; int64_t shift; };
+struct MimoSrc {
+  const void* A; const void* W; int K; int64_t shift;
+  int w_plane_off = 0;               // plane of this source's (hi) weight for system 0
+  int64_t w_planes = 0;              // planes in W (0: 1 for bf16, 2 for 3xTF32)
+};
 struct MimoGemm {
   MimoSrc src[3]; int n_src;
   const void* R; void* out; int n_out;
   int64_t L; int batch;
+  const int* sys_list = nullptr; int n_list = 1; int n_sys_total = 1;
+  int w_plane_stride = 0; int t_first = 0;
 };
 
 bool mimo_tc_supported(int m, int p, int q);
-// tf32 = true: 3xTF32 (fp32 signals, weights as [2][n_out][K] tf32 hi/lo); else bf16.
+// tf32 = true: 3xTF32 (fp32 signals, weights as tf32 hi/lo planes); else bf16.
 int launch_mimo_gemm(const MimoGemm& g, bool tf32, cudaStream_t st);
 
 }  // namespace casc
