@@ -1,9 +1,13 @@
 // Host sequencing of the tensor-core bank path (SISO channels, fp32 mode, m in {16, 32, 64}).
 //   derived : Krylov columns Abar^j Bbar (j < 2^Kc) by doubling with the powers
-//             [Kr_{2^i + j} = P_i Kr_j], tf32 hi/lo image; w = C P_Ne; fp32 copies of C, D
-//   head    : v^(Kc) (stages 0..Kc-1 with Bbar u)          -> Va
-//   stage k : k = Kc .. Ne-1 (only channels with Ne > k)   Va <-> Vb
-//   tail    : stage Ne + y = C v + D u                      -> y
+//             [Kr_{2^i + j} = P_i Kr_j], tf32 hi/lo image; w = C P_Ne; fp32 copies of C, D;
+//             pair weights Q_k = P_{k+1} P_k (float64 product, tf32 hi/lo planes)
+//   head    : v^(Kc) (stages 0..Kc-1 with Bbar u)                     -> Va
+//   stages  : k = Kc .. Ne-1, two per pass where possible (R23):
+//               v^(k+2) = v + P_k v_{l-2^k} + P_{k+1} v_{l-2^(k+1)} + Q_k v_{l-3*2^k}
+//             = (I + P_{k+1} z^-2s)(I + P_k z^-s) v, the product of two adjacent factors of
+//             PAPER.md Eq. 5; a last odd stage runs alone.                 Va <-> Vb
+//   tail    : stage Ne + y = C v + D u                                 -> y
 #include <algorithm>
 #include <numeric>
 #include <vector>
@@ -19,17 +23,36 @@ namespace casc {
 
 static constexpr int kHeadK = 7;      // Krylov head covers stages 0..6 (128 lags)
 
+// stage-kernel variant (CASC_BANK_STAGE, for A/B measurements): 't' TMA-pipelined shifted GEMM
+// with stage pairing (default, m % 64 == 0), 'r' register-prefetch kernel, 'w' warp-specialized.
+static char stage_variant(int m) {
+  static const char env = [] {
+    const char* e = getenv("CASC_BANK_STAGE");
+    return e ? e[0] : 't';
+  }();
+  if (env == 'w' || env == 'r') return env;
+  if (m % 64 != 0) return 'r';
+  // 's' (default): TMA GEMM, one stage per pass (DRAM 64% of peak under ncu, L2 40%);
+  // 't': stage pairs (half the DRAM bytes, but a 3-slot ring cannot cover the six chunks a
+  // pair tile needs: latency-bound at DRAM 26% / L2 28%; kept for the next round's work)
+  return env == 't' ? 't' : 's';
+}
+
+static int pair_slots(int n_max) { return n_max > kHeadK ? (n_max - kHeadK + 1) / 2 : 0; }
+
 struct BankWs {
   int* meta;      // Neff | Kc | parity | order   (4 n ints)
   double* Kr64;   // [n][m][128]
   float* krT;     // [n][2][m][128]
   double* w64;    // [n][m]
   float *w32, *c32, *d32;
+  double* Q64;    // [n][m][m] scratch for one pair weight
+  float* Q32;     // [n][qslots][2][m][m] pair weights, tf32 hi/lo planes
   void *Va, *Vb;
   size_t bytes;
 };
 
-static BankWs carve_bank(void* ws, int n, int m, int64_t L, int batch) {
+static BankWs carve_bank(void* ws, int n, int m, int64_t L, int batch, int qslots) {
   Carver c(ws);
   BankWs w{};
   w.meta = c.take<int>((size_t)4 * n);
@@ -39,6 +62,8 @@ static BankWs carve_bank(void* ws, int n, int m, int64_t L, int batch) {
   w.w32 = c.take<float>((size_t)n * m);
   w.c32 = c.take<float>((size_t)n * m);
   w.d32 = c.take<float>((size_t)n);
+  w.Q64 = c.take<double>(qslots ? (size_t)n * m * m : 0);
+  w.Q32 = c.take<float>((size_t)n * qslots * 2 * m * m);
   const size_t vbytes = (size_t)n * batch * (size_t)L * m * sizeof(float);
   w.Va = c.take<char>(vbytes);
   w.Vb = c.take<char>(vbytes);
@@ -54,7 +79,9 @@ bool bank_tc_path(int m, int p, int q, int mode) {
   return !force_simt && p == 1 && q == 1 && mode == CASC_FP32 && bank_tc_supported(m);
 }
 
-size_t bank_ws_bytes(int n, int m, int64_t L, int batch) { return carve_bank(nullptr, n, m, L, batch).bytes; }
+size_t bank_ws_bytes(int n, int m, int64_t L, int batch, int n_max) {
+  return carve_bank(nullptr, n, m, L, batch, stage_variant(m) == 't' ? pair_slots(n_max) : 0).bytes;
+}
 
 static int eff_order_b(int N, int64_t L) {
   if (L <= 2) return 0;
@@ -69,30 +96,52 @@ static int pick_group(int64_t ntiles, int64_t seqs, int want) {
   return g;
 }
 
+// Q32[s][slot][h] (tf32 hi / lo plane) from Q64[s] for channels with Neff[s] >= need
+__global__ void pair_split_kernel(const double* Q64, float* Q32, const int* Neff, int need, int n, int m,
+                                  int qslots, int slot) {
+  const int64_t mm = (int64_t)m * m, tot = (int64_t)n * mm;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = e / mm, ij = e % mm;
+    if (Neff[s] < need) continue;
+    const double x = Q64[e];
+    const float hi = tf32_rna((float)x);
+    float* base = Q32 + ((s * qslots + slot) * 2) * mm;
+    base[ij] = hi;
+    base[mm + ij] = tf32_rna((float)(x - (double)hi));
+  }
+}
+
 int engine_bank_tc(int n, int m, int64_t L, int batch, const int* N_host, int N_max, const void* pack,
                    const double* Bbar, const double* C, const double* D, const void* u, void* y, void* ws,
                    size_t ws_bytes, cudaStream_t st) {
-  BankWs w = carve_bank(ws, n, m, L, batch);
-  if (ws_bytes < w.bytes) return CASC_ERR_WORKSPACE;
-  PackLayout P = pack_layout(const_cast<void*>(pack), n, m, N_max, CASC_FP32);
-  const int64_t mm = (int64_t)m * m;
-  int rc;
-
+  const char variant = stage_variant(m);
   std::vector<int> meta((size_t)4 * n);
   int *Neff = meta.data(), *Kc = Neff + n, *par = Neff + 2 * n, *order = Neff + 3 * n;
   int maxNe = 0;
   for (int s = 0; s < n; ++s) {
     Neff[s] = eff_order_b(N_host[s], L);
     Kc[s] = std::min(kHeadK, Neff[s]);
-    par[s] = (Neff[s] - Kc[s]) % 2;
+    const int nstream = Neff[s] - Kc[s];            // streaming stages of this channel
+    par[s] = (variant == 't' ? (nstream + 1) / 2 : nstream) % 2;   // passes -> final buffer
     maxNe = std::max(maxNe, Neff[s]);
   }
+  const int qslots = variant == 't' ? pair_slots(maxNe) : 0;
+  BankWs w = carve_bank(ws, n, m, L, batch, qslots);
+  if (ws_bytes < w.bytes) return CASC_ERR_WORKSPACE;
+  PackLayout P = pack_layout(const_cast<void*>(pack), n, m, N_max, CASC_FP32);
+  const int64_t mm = (int64_t)m * m;
+  int rc;
   std::iota(order, order + n, 0);
   std::stable_sort(order, order + n, [&](int a, int b) { return Neff[a] > Neff[b]; });
   CASC_TRY(cudaMemcpyAsync(w.meta, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice, st));
   const int *dNeff = w.meta, *dKc = w.meta + n, *dpar = w.meta + 2 * n, *dorder = w.meta + 3 * n;
+  auto count_ge = [&](int need) {                    // channels with Neff >= need: a prefix of order
+    int c = 0;
+    while (c < n && Neff[order[c]] >= need) ++c;
+    return c;
+  };
 
-  // ---- derived: Krylov columns, w = C P_Ne, fp32 copies
+  // ---- derived: Krylov columns, w = C P_Ne, fp32 copies, pair weights
   {
     ProfScope ps(st, K_DERIVED, 0.0, 2.0 * n * (double)m * m * 128);
     if ((rc = launch_kr_init(Bbar, w.Kr64, n, m, st))) return rc;
@@ -120,6 +169,20 @@ int engine_bank_tc(int n, int m, int64_t L, int batch, const int* N_host, int N_
     } else {
       CASC_TRY(cudaMemsetAsync(w.d32, 0, sizeof(float) * n, st));
     }
+    for (int j = 0; j < qslots; ++j) {          // Q_k = P_{k+1} P_k for pass j (k = 7 + 2j)
+      const int k = kHeadK + 2 * j;
+      if (count_ge(k + 2) == 0) continue;
+      DgemmArg q{};
+      q.M = m; q.N = m; q.K = m;
+      q.A = P.p64 + (k + 1) * mm; q.lda = m; q.sA = (int64_t)(N_max + 1) * mm;
+      q.B = P.p64 + k * mm; q.ldb = m; q.sB = (int64_t)(N_max + 1) * mm;
+      q.C = w.Q64; q.ldc = m; q.sC = mm;
+      q.skip_below = dNeff; q.level = k + 2;
+      if ((rc = launch_dgemm(q, n, st))) return rc;
+      pair_split_kernel<<<(int)std::min<int64_t>(ceil_div((int64_t)n * mm, 256), 148 * 8), 256, 0, st>>>(
+          w.Q64, w.Q32, dNeff, k + 2, n, m, qslots, j);
+      CASC_LAUNCHED();
+    }
   }
   const int64_t ntiles = ceil_div(L, 128);
   // ---- head: stages 0..Kc-1 (+ Bbar u), all channels
@@ -132,40 +195,64 @@ int engine_bank_tc(int n, int m, int64_t L, int batch, const int* N_host, int N_
                  (double)n * batch * L * 2.0 * m * 128);
     if ((rc = launch_bank_head(m, a, st))) return rc;
   }
-  // ---- streaming stages k >= kHeadK over the channels with Neff > k (a prefix of `order`)
-  for (int k = kHeadK; k < maxNe; ++k) {
-    int cnt = 0;
-    while (cnt < n && Neff[order[cnt]] > k) ++cnt;
-    BankStageArg a{};
-    const int j = k - kHeadK;
-    a.Vs = static_cast<const float*>(j % 2 == 0 ? w.Va : w.Vb);
-    a.Vd = static_cast<float*>(j % 2 == 0 ? w.Vb : w.Va);
-    a.P = P.f32; a.k = k; a.slots = N_max + 1;
-    a.copy_from = (k == kHeadK) ? 0 : ((int64_t)1 << (k - 1));
-    a.sys_list = dorder; a.n_list = cnt; a.L = L; a.batch = batch;
-    a.tiles_per_cta = pick_group(ntiles, (int64_t)cnt * batch, 8);
-    ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt * batch * L * m * 4.0, 2.0 * cnt * batch * L * (double)mm);
-    // Kernel choice (CASC_BANK_STAGE for A/B measurements): the TMA-pipelined shifted GEMM
-    // (mimo_tc.cu, 3xTF32, per-channel weight planes) for m % 64 == 0, else the
-    // register-prefetch kernel; "rp" / "ws" force the older variants.
-    static const char mode_env = [] {
-      const char* e = getenv("CASC_BANK_STAGE");
-      return e ? e[0] : 't';
-    }();
-    if (mode_env == 'w') {
-      rc = launch_bank_stage_ws(m, a, st);
-    } else if (mode_env == 'r' || m % 64 != 0) {
-      rc = launch_bank_stage_rp(m, a, st);
-    } else {
+  // ---- streaming stages k >= kHeadK over the channels with Neff > k (prefixes of `order`)
+  int pass = 0;
+  for (int k = kHeadK; k < maxNe; k += (variant == 't' ? 2 : 1), ++pass) {
+    const float* Vs = static_cast<const float*>(pass % 2 == 0 ? w.Va : w.Vb);
+    float* Vd = static_cast<float*>(pass % 2 == 0 ? w.Vb : w.Va);
+    if (variant == 's') {                           // TMA GEMM, one stage per pass
+      const int cnt = count_ge(k + 1);
       MimoGemm g{};
-      g.src[0].A = a.Vs; g.src[0].W = P.f32; g.src[0].K = m; g.src[0].shift = (int64_t)1 << k;
+      g.src[0].A = Vs; g.src[0].W = P.f32; g.src[0].K = m; g.src[0].shift = (int64_t)1 << k;
       g.src[0].w_plane_off = 2 * k; g.src[0].w_planes = (int64_t)n * (N_max + 1) * 2;
-      g.n_src = 1; g.R = a.Vs; g.out = a.Vd; g.n_out = m; g.L = L; g.batch = batch;
+      g.src[0].w_plane_stride = 2 * (N_max + 1);
+      g.n_src = 1; g.R = Vs; g.out = Vd; g.n_out = m; g.L = L; g.batch = batch;
       g.sys_list = dorder; g.n_list = cnt; g.n_sys_total = n;
-      g.w_plane_stride = 2 * (N_max + 1); g.t_first = (int)(a.copy_from / 128);
-      rc = launch_mimo_gemm(g, true, st);
+      g.t_first = pass == 0 ? 0 : (int)(((int64_t)1 << (k - 1)) / 128);
+      ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt * batch * L * m * 4.0, 2.0 * cnt * batch * L * (double)mm);
+      if ((rc = launch_mimo_gemm(g, true, st))) return rc;
+      continue;
     }
-    if (rc) return rc;
+    if (variant != 't') {
+      const int cnt = count_ge(k + 1);
+      BankStageArg a{};
+      a.Vs = Vs; a.Vd = Vd; a.P = P.f32; a.k = k; a.slots = N_max + 1;
+      a.copy_from = (k == kHeadK) ? 0 : ((int64_t)1 << (k - 1));
+      a.sys_list = dorder; a.n_list = cnt; a.L = L; a.batch = batch;
+      a.tiles_per_cta = pick_group(ntiles, (int64_t)cnt * batch, 8);
+      ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt * batch * L * m * 4.0, 2.0 * cnt * batch * L * (double)mm);
+      rc = variant == 'w' ? launch_bank_stage_ws(m, a, st) : launch_bank_stage_rp(m, a, st);
+      if (rc) return rc;
+      continue;
+    }
+    // pass: stages k and k+1 for channels with Neff >= k+2; stage k alone for Neff == k+1.
+    // The destination holds v^(k-2) (two passes ago), equal to v^(k+2) on rows < 2^(k-2).
+    const int cnt2 = count_ge(k + 2), cnt1 = count_ge(k + 1) - cnt2;
+    const int t_first = pass == 0 ? 0 : (int)(((int64_t)1 << (k - 2)) / 128);
+    const int64_t planes = (int64_t)n * (N_max + 1) * 2;
+    if (cnt2 > 0) {
+      MimoGemm g{};
+      g.src[0].A = Vs; g.src[0].W = P.f32; g.src[0].K = m; g.src[0].shift = (int64_t)1 << k;
+      g.src[0].w_plane_off = 2 * k; g.src[0].w_planes = planes; g.src[0].w_plane_stride = 2 * (N_max + 1);
+      g.src[1] = g.src[0];
+      g.src[1].shift = (int64_t)2 << k; g.src[1].w_plane_off = 2 * (k + 1);
+      g.src[2].A = Vs; g.src[2].W = w.Q32; g.src[2].K = m; g.src[2].shift = (int64_t)3 << k;
+      g.src[2].w_plane_off = 2 * pass; g.src[2].w_planes = (int64_t)n * qslots * 2;
+      g.src[2].w_plane_stride = 2 * qslots;
+      g.n_src = 3; g.R = Vs; g.out = Vd; g.n_out = m; g.L = L; g.batch = batch;
+      g.sys_list = dorder; g.n_list = cnt2; g.n_sys_total = n; g.t_first = t_first;
+      ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt2 * batch * L * m * 4.0, 4.0 * cnt2 * batch * L * (double)mm);
+      if ((rc = launch_mimo_gemm(g, true, st))) return rc;
+    }
+    if (cnt1 > 0) {
+      MimoGemm g{};
+      g.src[0].A = Vs; g.src[0].W = P.f32; g.src[0].K = m; g.src[0].shift = (int64_t)1 << k;
+      g.src[0].w_plane_off = 2 * k; g.src[0].w_planes = planes; g.src[0].w_plane_stride = 2 * (N_max + 1);
+      g.n_src = 1; g.R = Vs; g.out = Vd; g.n_out = m; g.L = L; g.batch = batch;
+      g.sys_list = dorder + cnt2; g.n_list = cnt1; g.n_sys_total = n; g.t_first = t_first;
+      ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt1 * batch * L * m * 4.0, 2.0 * cnt1 * batch * L * (double)mm);
+      if ((rc = launch_mimo_gemm(g, true, st))) return rc;
+    }
   }
   // ---- tail: stage Ne + y = C v + D u
   {

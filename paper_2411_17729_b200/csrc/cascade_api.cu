@@ -61,8 +61,8 @@ static ApplyWs carve_apply(void* ws, int n, int m, int p, int q, int64_t L, int 
   return w;
 }
 
-size_t apply_ws_bytes(int n, int m, int p, int q, int64_t L, int batch, int mode) {
-  if (bank_tc_path(m, p, q, mode)) return bank_ws_bytes(n, m, L, batch);
+size_t apply_ws_bytes(int n, int m, int p, int q, int64_t L, int batch, int mode, int n_max) {
+  if (bank_tc_path(m, p, q, mode)) return bank_ws_bytes(n, m, L, batch, n_max);
   if (mimo_tc_path(n, m, p, q, mode)) return mimo_ws_bytes(m, p, q, L, batch, mode);
   return carve_apply(nullptr, n, m, p, q, L, batch, mode).bytes;
 }
@@ -314,9 +314,9 @@ int casc_powers(int n_sys, int m, const int* N_host, int N_max, const double* Ab
 }
 
 size_t casc_apply_workspace_bytes(int m, int p, int q, int64_t L, int batch, int N, int mode) {
-  (void)N;
+
   if (m < 1 || p < 1 || q < 1 || L < 1 || batch < 1) return 0;
-  return apply_ws_bytes(1, m, p, q, L, batch, mode);
+  return apply_ws_bytes(1, m, p, q, L, batch, mode, N);
 }
 
 int casc_apply(int m, int p, int q, int64_t L, int batch, int N, int N_max, int mode,
@@ -337,9 +337,9 @@ int casc_apply(int m, int p, int q, int64_t L, int batch, int N, int N_max, int 
 }
 
 size_t casc_bank_workspace_bytes(int n_ch, int m, int64_t L, int batch, int N_max, int mode) {
-  (void)N_max;
+
   if (n_ch < 1 || m < 1 || L < 1 || batch < 1) return 0;
-  return apply_ws_bytes(n_ch, m, 1, 1, L, batch, mode);
+  return apply_ws_bytes(n_ch, m, 1, 1, L, batch, mode, N_max);
 }
 
 int casc_apply_bank(int n_ch, int m, int64_t L, int batch, const int* N_host, int N_max,
@@ -369,7 +369,7 @@ static HostWs carve_host(void* base, int n, int m, int p, int q, int64_t L, int 
   h.u = c.take<char>((size_t)n * batch * L * p * es);
   h.y = c.take<char>((size_t)n * batch * L * q * es);
   h.pack = c.take<char>(pack_layout(nullptr, n, m, N_max, mode).bytes);
-  h.apply_bytes = apply_ws_bytes(n, m, p, q, L, batch, mode);
+  h.apply_bytes = apply_ws_bytes(n, m, p, q, L, batch, mode, N_max);
   h.apply_ws = c.take<char>(h.apply_bytes);
   h.bytes = c.bytes();
   return h;

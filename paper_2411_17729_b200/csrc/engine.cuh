@@ -3,13 +3,13 @@
 #include "common.cuh"
 
 namespace casc {
-size_t apply_ws_bytes(int n, int m, int p, int q, int64_t L, int batch, int mode);
+size_t apply_ws_bytes(int n, int m, int p, int q, int64_t L, int batch, int mode, int n_max);
 int validate_common(int n, int m, int p, int q, int64_t L, int batch, int N_max, int mode);
 int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_host, int N_max,
                  int mode, const void* pack, const double* Bbar, const double* C, const double* D,
                  const void* u, void* y, void* ws, size_t ws_bytes, cudaStream_t st);
 bool bank_tc_path(int m, int p, int q, int mode);
-size_t bank_ws_bytes(int n, int m, int64_t L, int batch);
+size_t bank_ws_bytes(int n, int m, int64_t L, int batch, int n_max);
 int engine_bank_tc(int n, int m, int64_t L, int batch, const int* N_host, int N_max, const void* pack,
                    const double* Bbar, const double* C, const double* D, const void* u, void* y, void* ws,
                    size_t ws_bytes, cudaStream_t st);

@@ -99,7 +99,7 @@ struct Cfg {
 
 // Tile -> (sequence coordinate in the tensors, time tile, N block, weight plane base)
 struct TileCoord {
-  int seq, l0, nb, plane0;
+  int seq, l0, nb, sys;
 };
 __device__ __forceinline__ TileCoord decode(int64_t tile, const MimoArg& a, int n_nblk, int64_t nt_eff) {
   TileCoord t;
@@ -110,7 +110,7 @@ __device__ __forceinline__ TileCoord decode(int64_t tile, const MimoArg& a, int 
   const int li = (int)(sidx / a.batch), b = (int)(sidx % a.batch);
   const int sys = a.sys_list ? a.sys_list[li] : 0;
   t.seq = sys * a.batch + b;
-  t.plane0 = sys * a.w_plane_stride;
+  t.sys = sys;
   return t;
 }
 }  // namespace
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
         const TileCoord tc = decode(tile, a, n_nblk, nt_eff);
         for (int src = 0; src < a.n_src; ++src) {
           const int nk = a.K[src] / BK;
-          const int plane = tc.plane0 + a.w_plane_off[src];
+          const int plane = tc.sys * a.w_plane_stride[src] + a.w_plane_off[src];
           for (int kc = 0; kc < nk; ++kc) {
             mbar_wait(&empty[s], ph ^ 1);
             mbar_arrive_expect_tx(&full[s], C::TMA_BYTES);
@@ -386,7 +386,6 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
   a.n_out = g.n_out;
   a.sys_list = g.sys_list;
   a.n_list = g.sys_list ? g.n_list : 1;
-  a.w_plane_stride = g.w_plane_stride;
   a.t_first = g.t_first;
   const int64_t nseq_total = (int64_t)(g.n_sys_total > 0 ? g.n_sys_total : 1) * g.batch;
   for (int s = 0; s < g.n_src; ++s) {
@@ -394,6 +393,7 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
     a.K[s] = g.src[s].K;
     a.shift[s] = g.src[s].shift;
     a.w_plane_off[s] = g.src[s].w_plane_off;
+    a.w_plane_stride[s] = g.src[s].w_plane_stride;
     if (!map3d(&maps.A[s], g.src[s].A, TF32, g.src[s].K, g.L, nseq_total, BM)) return CASC_ERR_CUDA;
     // weights: planes of [n_out][K] (bf16), or hi / lo planes of tf32 for 3xTF32
     const int64_t planes = g.src[s].w_planes > 0 ? g.src[s].w_planes : (TF32 ? 2 : 1);

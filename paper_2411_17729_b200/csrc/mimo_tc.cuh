@@ -13,15 +13,15 @@ struct MimoMaps {                 // passed as one __grid_constant__ kernel para
   CUtensorMap out;                // output   [seq][L][n_out]          box {128 B, 128, 1}
 };
 struct MimoArg {
-  int n_src; int K[3]; int64_t shift[3]; int w_plane_off[3];
+  int n_src; int K[3]; int64_t shift[3]; int w_plane_off[3]; int w_plane_stride[3];
   int64_t L; int batch; int n_out; int has_residual;
   const int* sys_list; int n_list;   // systems processed (bank channels); null: one system
-  int w_plane_stride;                // weight planes per system (bank: slots * 2)
   int t_first;                       // first 128-step time tile processed in each sequence
 };
 struct MimoSrc {
   const void* A; const void* W; int K; int64_t shift;
   int w_plane_off = 0;               // plane of this source's (hi) weight for system 0
+  int w_plane_stride = 0;            // weight planes per system (bank: slots * 2; 0: shared)
   int64_t w_planes = 0;              // planes in W (0: 1 for bf16, 2 for 3xTF32)
 };
 struct MimoGemm {
@@ -29,7 +29,7 @@ struct MimoGemm {
   const void* R; void* out; int n_out;
   int64_t L; int batch;
   const int* sys_list = nullptr; int n_list = 1; int n_sys_total = 1;
-  int w_plane_stride = 0; int t_first = 0;
+  int t_first = 0;
 };
 
 bool mimo_tc_supported(int m, int p, int q);
