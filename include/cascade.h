@@ -124,6 +124,10 @@ int casc_apply(int m, int p, int q, int64_t L, int batch, int N, int N_max, int 
  *   Bbar      DEVICE float64 [n_ch][m]; C DEVICE float64 [n_ch][m]; D DEVICE float64 [n_ch]
  *             (may be NULL = 0).
  *   u, y      DEVICE [n_ch][batch][L] in the storage dtype of `mode`.
+ *   ws_bytes  may be smaller than casc_bank_workspace_bytes(n_ch, ...): the channels are then
+ *             processed in consecutive waves of as many channels as fit (bounded memory, e.g.
+ *             BASELINE configs[4]: 4096 x 8 x 65536 x 64 fp32 states = 550 GB per buffer); at
+ *             least casc_bank_workspace_bytes(1, ...) is required.
  * Errors as casc_apply.
  * -------------------------------------------------------------------------------------- */
 size_t casc_bank_workspace_bytes(int n_ch, int m, int64_t L, int batch, int N_max, int mode);
@@ -137,7 +141,8 @@ int casc_apply_bank(int n_ch, int m, int64_t L, int batch, const int* N_host, in
  * dtype) host -> device, runs casc_powers + casc_apply / casc_apply_bank, copies y back to
  * host, and synchronises `stream`. Host buffers should be pinned for asynchronous copies.
  *   n_sys == 1 with any (p, q) runs the single-system path; n_sys > 1 requires p = q = 1
- *   (bank). dev_ws: DEVICE buffer of casc_run_host_bytes(...) bytes.
+ *   (bank). dev_ws: DEVICE buffer of casc_run_host_bytes(...) bytes; for banks a smaller
+ *   buffer is accepted (its tail becomes the apply workspace and the channels run in waves).
  * -------------------------------------------------------------------------------------- */
 size_t casc_run_host_bytes(int n_sys, int m, int p, int q, int64_t L, int batch, int N_max,
                            int mode);

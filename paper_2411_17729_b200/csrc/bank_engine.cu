@@ -9,6 +9,8 @@
 //             PAPER.md Eq. 5; a last odd stage runs alone.                 Va <-> Vb
 //   tail    : stage Ne + y = C v + D u                                 -> y
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
 #include <vector>
 
@@ -28,7 +30,7 @@ static constexpr int kHeadK = 7;      // Krylov head covers stages 0..6 (128 lag
 static char stage_variant(int m) {
   static const char env = [] {
     const char* e = getenv("CASC_BANK_STAGE");
-    return e ? e[0] : 't';
+    return e ? e[0] : 's';
   }();
   if (env == 'w' || env == 'r') return env;
   if (m % 64 != 0) return 'r';
@@ -111,9 +113,48 @@ __global__ void pair_split_kernel(const double* Q64, float* Q32, const int* Neff
   }
 }
 
+// One wave of n channels; Pw points at the wave's first channel inside the full pack.
+static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int N_max, const PackLayout& Pw,
+                     const double* Bbar, const double* C, const double* D, const float* u, float* y, void* ws,
+                     size_t ws_bytes, cudaStream_t st);
+
+// Bounded-memory bank: with a workspace smaller than the whole bank needs, the channels are
+// processed in consecutive waves of as many channels as fit (each wave is an independent bank).
 int engine_bank_tc(int n, int m, int64_t L, int batch, const int* N_host, int N_max, const void* pack,
                    const double* Bbar, const double* C, const double* D, const void* u, void* y, void* ws,
                    size_t ws_bytes, cudaStream_t st) {
+  int maxNe = 0;
+  for (int s = 0; s < n; ++s) maxNe = std::max(maxNe, eff_order_b(N_host[s], L));
+  const int qslots = stage_variant(m) == 't' ? pair_slots(maxNe) : 0;
+  int nw = n;
+  while (nw > 0 && carve_bank(nullptr, nw, m, L, batch, qslots).bytes > ws_bytes) {
+    const size_t per = carve_bank(nullptr, 1, m, L, batch, qslots).bytes;
+    const int guess = (int)std::min<size_t>((size_t)nw - 1, ws_bytes / std::max<size_t>(per, 1));
+    nw = guess;
+  }
+  if (nw < 1) {
+    if (getenv("CASC_DEBUG")) fprintf(stderr, "casc: bank wave does not fit: ws=%zu one=%zu\n", ws_bytes, carve_bank(nullptr, 1, m, L, batch, qslots).bytes);
+    return CASC_ERR_WORKSPACE;
+  }
+  PackLayout P = pack_layout(const_cast<void*>(pack), n, m, N_max, CASC_FP32);
+  const int64_t slot_mm = (int64_t)(N_max + 1) * m * m;
+  for (int c0 = 0; c0 < n; c0 += nw) {
+    const int cn = std::min(nw, n - c0);
+    PackLayout Pw = P;
+    Pw.p64 += c0 * slot_mm;
+    Pw.f32 += c0 * slot_mm * 2;
+    const int64_t sig = (int64_t)c0 * batch * L;
+    const int rc = bank_wave(cn, m, L, batch, N_host + c0, N_max, Pw, Bbar + (int64_t)c0 * m, C + (int64_t)c0 * m,
+                             D ? D + c0 : nullptr, static_cast<const float*>(u) + sig, static_cast<float*>(y) + sig,
+                             ws, ws_bytes, st);
+    if (rc) return rc;
+  }
+  return CASC_OK;
+}
+
+static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int N_max, const PackLayout& Pw,
+                     const double* Bbar, const double* C, const double* D, const float* u, float* y, void* ws,
+                     size_t ws_bytes, cudaStream_t st) {
   const char variant = stage_variant(m);
   std::vector<int> meta((size_t)4 * n);
   int *Neff = meta.data(), *Kc = Neff + n, *par = Neff + 2 * n, *order = Neff + 3 * n;
@@ -127,8 +168,11 @@ int engine_bank_tc(int n, int m, int64_t L, int batch, const int* N_host, int N_
   }
   const int qslots = variant == 't' ? pair_slots(maxNe) : 0;
   BankWs w = carve_bank(ws, n, m, L, batch, qslots);
-  if (ws_bytes < w.bytes) return CASC_ERR_WORKSPACE;
-  PackLayout P = pack_layout(const_cast<void*>(pack), n, m, N_max, CASC_FP32);
+  if (ws_bytes < w.bytes) {
+    if (getenv("CASC_DEBUG")) fprintf(stderr, "casc: bank wave ws=%zu need=%zu n=%d\n", ws_bytes, w.bytes, n);
+    return CASC_ERR_WORKSPACE;
+  }
+  const PackLayout& P = Pw;
   const int64_t mm = (int64_t)m * m;
   int rc;
   std::iota(order, order + n, 0);

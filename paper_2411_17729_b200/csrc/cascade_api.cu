@@ -12,6 +12,8 @@
 // DESIGN.md R21). v^(k) ping-pongs between two workspace buffers: after stage k it sits in
 // buffer k % 2.
 #include <cstring>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 #include <numeric>
 
@@ -390,7 +392,14 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
   if (!N_host || !Abar_h || !Bbar_h || !C_h || !u_h || !y_h || !dev_ws) return CASC_ERR_ARG;
   if (n_sys > 1 && (p != 1 || q != 1)) return CASC_ERR_UNSUPPORTED;
   HostWs h = carve_host(dev_ws, n_sys, m, p, q, L, batch, N_max, mode);
-  if (dev_ws_bytes < h.bytes) return CASC_ERR_WORKSPACE;
+  // the apply workspace is the last region: a smaller dev_ws leaves it short, which banks absorb
+  // by running in channel waves (engine_apply reports CASC_ERR_WORKSPACE otherwise)
+  const size_t fixed = (size_t)((char*)h.apply_ws - (char*)dev_ws);
+  if (dev_ws_bytes <= fixed) {
+    if (getenv("CASC_DEBUG")) fprintf(stderr, "casc: run_host ws=%zu fixed=%zu\n", dev_ws_bytes, fixed);
+    return CASC_ERR_WORKSPACE;
+  }
+  h.apply_bytes = std::min(h.apply_bytes, dev_ws_bytes - fixed);
   cudaStream_t st = (cudaStream_t)stream;
   const size_t es = (mode == CASC_BF16) ? 2 : 4;
   CASC_TRY(cudaMemcpyAsync(h.Abar, Abar_h, sizeof(double) * n_sys * m * m, cudaMemcpyHostToDevice, st));

@@ -21,7 +21,10 @@ def storage_to_torch(arr: np.ndarray, mode: str) -> torch.Tensor:
 class DeviceWorkload:
     """Inputs of a workload resident in HBM, plus preallocated outputs / workspace."""
 
-    def __init__(self, wl, device="cuda", u_host: np.ndarray | None = None, channels=None):
+    def __init__(self, wl, device="cuda", u_host: np.ndarray | None = None, channels=None,
+                 ws_budget: int | None = None):
+        """ws_budget: cap on the workspace bytes (banks then run in channel waves); default is
+        the full requirement, capped at 75% of the free device memory after inputs/outputs."""
         self.wl = wl
         self.device = device
         ch = list(range(wl.n_ch)) if channels is None else list(channels)
@@ -54,8 +57,12 @@ class DeviceWorkload:
         else:
             self.y = torch.empty((wl.batch, wl.L, wl.q), dtype=api.STORAGE[md], device=device)
             wsb = api.apply_workspace_bytes(wl.m, wl.p, wl.q, wl.L, wl.batch, self.N[0], md)
-        self.ws = torch.empty(wsb, dtype=torch.uint8, device=device)
         self.pack = torch.empty(api.pack_bytes(n, wl.m, self.N_max, md), dtype=torch.uint8, device=device)
+        if self.bank:
+            free = torch.cuda.mem_get_info(torch.device(device))[0]
+            cap = int(0.75 * free) if ws_budget is None else int(ws_budget)
+            wsb = min(wsb, max(cap, api.bank_workspace_bytes(1, wl.m, wl.L, wl.batch, self.N_max, md)))
+        self.ws = torch.empty(wsb, dtype=torch.uint8, device=device)
         self.pw = None
 
     def step(self, stream=None):

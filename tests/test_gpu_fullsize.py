@@ -49,6 +49,25 @@ def test_E3_full_size_sampled():
     sampled_windows(wl, dw, windows, 64, 1e-5)
 
 
+def test_E5_full_size_sampled_channels():
+    """configs[4]: 4096 HiPPO channels, L=65536, batch 8 -- states of 550 GB per buffer, so the
+    bank runs in channel waves inside the library; channels spanning N_c = min..15 are checked
+    over their whole length against the float64 oracle."""
+    wl = S.make_E5()
+    dw = run_full(wl)
+    order = np.argsort(wl.N, kind="stable")
+    pick = sorted({int(order[0]), int(order[len(order) // 2]), int(order[-1]), 0, wl.n_ch - 1})
+    for c in pick:
+        y = dw.y[c].float().cpu().double().numpy()                  # [batch][L]
+        u = np.stack([wl.u_window(c, b, 0, wl.L)[:, 0] for b in range(wl.batch)])
+        N = int(wl.N[c])
+        ref = oracle.cascade(oracle.powers(wl.Abar[c], N), wl.Bbar[c], wl.C[c], wl.D[c], u[:, :, None], N)[:, :, 0]
+        Du = u * wl.D[c, 0, 0]
+        e, es = rel(y, ref), rel(y - Du, ref - Du)
+        print(f"E5 channel {c} N={N}: rel {e:.3e} state {es:.3e}")
+        assert e <= 1e-5 and es <= 1e-5, (c, N, e, es)
+
+
 def test_E4_full_size_sampled():
     wl = S.make_E4()                                   # m=1024, p=q=256, L=2^20, batch=8, bf16
     dw = run_full(wl)

@@ -141,6 +141,23 @@ def test_bank_tensor_core_path_edges(m, L, N):
     check_parity(wl)
 
 
+def test_bank_channel_waves_bounded_memory():
+    """A workspace for ~3 channels forces the 10-channel bank through 4 waves; results must be
+    bitwise those of the single-wave run (each wave is an independent bank)."""
+    import paper_2411_17729_b200 as pk
+    from paper_2411_17729_b200.runner import DeviceWorkload
+    wl = S.make_E2(n_ch=10, L=3000, batch=2)
+    one = pk.bank_workspace_bytes(1, wl.m, wl.L, wl.batch, int(wl.N.max()), "fp32")
+    dw = DeviceWorkload(wl, ws_budget=3 * one + 4096)
+    dw.step()
+    torch.cuda.synchronize()
+    y_w = dw.y_f64()
+    y_full, _ = run_gpu(wl)
+    assert np.array_equal(y_w, y_full)
+    y_ref, _ = oracle_y(wl)
+    assert rel(y_w, y_ref) < 1e-5
+
+
 def test_bank_mixed_orders_and_ragged_length():
     """Channels with N from 0 to 13 in one bank, L not a multiple of the 128-step tile."""
     wl = S.make_E2(n_ch=14, L=3000, batch=3)
