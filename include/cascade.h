@@ -151,6 +151,33 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
                   const double* C_h, const double* D_h, const void* u_h, void* y_h,
                   void* dev_ws, size_t dev_ws_bytes, void* stream);
 
+/* ----------------------------------------------------------------------------------------
+ * a7  Sequence-sharded steps (BASELINE configs[3] "per-stage NCCL halo exchange").
+ *     Rank r owns time rows [r*L_loc, (r+1)*L_loc) of every sequence of ONE system
+ *     (m, p, q multiples of 64). The cascade's stage k reads v_{l-2^k}, so
+ *     before stage k each rank receives the last 2^k rows of v^(k) of rank r-1 (zeros on
+ *     rank 0); the exchange itself is done by the caller (paper_2411_17729_b200/seqshard.py,
+ *     NCCL through torch.distributed). Buffers carry the halo in front of the local rows:
+ *       u_ext [batch][1 + L_loc][p]   (row 0 = u_{-1} of this shard)
+ *       V     [batch][H + L_loc][m]   (rows [H - 2^k, H) = halo of stage k), H >= 2^Ne
+ *       y     [batch][L_loc][q]
+ *     Ne is the effective order for the GLOBAL length: min(N, floor(log2(L - 1))) (R20).
+ *   casc_seq_prepare : derived weights (Abar Bbar, C P_Ne, C Bbar + D, C Abar Bbar) into ws
+ *   casc_seq_first   : v^(1) = Bbar u_l + Abar Bbar u_{l-1} on the local rows
+ *   casc_seq_stage   : v^(k+1) = v^(k) + P_k v^(k)_{l-2^k} on the local rows (k >= 1)
+ *   casc_seq_last    : y = C v + (C P_Ne) v_{l-2^Ne} + D u  (Ne == 0: y = (C Bbar + D) u + C Abar Bbar u_{l-1})
+ * All pointers DEVICE; stream-ordered; errors as casc_apply (CASC_ERR_DIM if 2^k > H).
+ * -------------------------------------------------------------------------------------- */
+size_t casc_seq_workspace_bytes(int m, int p, int q, int mode);
+int casc_seq_prepare(int m, int p, int q, int Ne, int N_max, int mode, const void* pack, const double* Bbar,
+                     const double* C, const double* D, void* ws, size_t ws_bytes, void* stream);
+int casc_seq_first(int m, int p, int q, int64_t L_loc, int batch, int mode, const void* ws, const void* u_ext,
+                   int64_t H, void* V, void* stream);
+int casc_seq_stage(int m, int64_t L_loc, int batch, int k, int N_max, int mode, const void* pack, int64_t H,
+                   const void* V_src, void* V_dst, void* stream);
+int casc_seq_last(int m, int p, int q, int64_t L_loc, int batch, int Ne, int mode, const void* ws, int64_t H,
+                  const void* V, const void* u_ext, int has_D, void* y, void* stream);
+
 /* Number of kernel launches the last successful apply/powers call on this host thread
  * enqueued (bench evidence for "gpu_launches"). */
 int casc_last_launch_count(void);

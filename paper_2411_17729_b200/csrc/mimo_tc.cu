@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
           for (int kc = 0; kc < nk; ++kc) {
             mbar_wait(&empty[s], ph ^ 1);
             mbar_arrive_expect_tx(&full[s], C::TMA_BYTES);
-            tma_load_3d(stA(s), &maps.A[src], &full[s], kc * BK, tc.l0 - (int)a.shift[src], tc.seq);
+            tma_load_3d(stA(s), &maps.A[src], &full[s], kc * BK, a.a_row0[src] + tc.l0 - (int)a.shift[src], tc.seq);
             tma_load_3d(stW(s), &maps.W[src], &full[s], kc * BK, tc.nb * BN, plane);
             if (TF32) tma_load_3d(stWlo(s), &maps.W[src], &full[s], kc * BK, tc.nb * BN, plane + 1);
             if (++s == STAGES) { s = 0; ph ^= 1; }
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
           mbar_wait(&rempty[rs], rph ^ 1);
           if (a.has_residual) {
             mbar_arrive_expect_tx(&rfull[rs], C::R_BYTES);
-            tma_load_3d(sR + rs * C::R_BYTES, &maps.R, &rfull[rs], tc.nb * BN + j * C::CW, tc.l0, tc.seq);
+            tma_load_3d(sR + rs * C::R_BYTES, &maps.R, &rfull[rs], tc.nb * BN + j * C::CW, a.r_row0 + tc.l0, tc.seq);
           } else {
             mbar_arrive(&rfull[rs]);
           }
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
         fence_async_smem();
         named_sync(1, 128);
         if (leader) {
-          tma_store_3d(&maps.out, rbuf, tc.nb * BN + j * C::CW, tc.l0, tc.seq);
+          tma_store_3d(&maps.out, rbuf, tc.nb * BN + j * C::CW, a.out_row0 + tc.l0, tc.seq);
           bulk_commit();
           if (prev_rs >= 0) {                       // the previous chunk's store has read its slot
             bulk_wait_read<1>();
@@ -394,14 +394,17 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
     a.shift[s] = g.src[s].shift;
     a.w_plane_off[s] = g.src[s].w_plane_off;
     a.w_plane_stride[s] = g.src[s].w_plane_stride;
-    if (!map3d(&maps.A[s], g.src[s].A, TF32, g.src[s].K, g.L, nseq_total, BM)) return CASC_ERR_CUDA;
+    a.a_row0[s] = (int)g.src[s].row0;
+    if (!map3d(&maps.A[s], g.src[s].A, TF32, g.src[s].K, g.src[s].row0 + g.L, nseq_total, BM)) return CASC_ERR_CUDA;
     // weights: planes of [n_out][K] (bf16), or hi / lo planes of tf32 for 3xTF32
     const int64_t planes = g.src[s].w_planes > 0 ? g.src[s].w_planes : (TF32 ? 2 : 1);
     if (!map3d(&maps.W[s], g.src[s].W, TF32, g.src[s].K, g.n_out, planes, BN)) return CASC_ERR_CUDA;
   }
   a.has_residual = g.R != nullptr;
-  if (g.R && !map3d(&maps.R, g.R, TF32, g.n_out, g.L, nseq_total, BM)) return CASC_ERR_CUDA;
-  if (!map3d(&maps.out, g.out, TF32, g.n_out, g.L, nseq_total, BM)) return CASC_ERR_CUDA;
+  a.r_row0 = (int)g.R_row0;
+  a.out_row0 = (int)g.out_row0;
+  if (g.R && !map3d(&maps.R, g.R, TF32, g.n_out, g.R_row0 + g.L, nseq_total, BM)) return CASC_ERR_CUDA;
+  if (!map3d(&maps.out, g.out, TF32, g.n_out, g.out_row0 + g.L, nseq_total, BM)) return CASC_ERR_CUDA;
   if (cudaFuncSetAttribute(mimo_gemm_kernel<BN, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)C::SMEM) != cudaSuccess)
     return CASC_ERR_CUDA;

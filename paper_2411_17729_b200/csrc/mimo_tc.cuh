@@ -17,12 +17,14 @@ struct MimoArg {
   int64_t L; int batch; int n_out; int has_residual;
   const int* sys_list; int n_list;   // systems processed (bank channels); null: one system
   int t_first;                       // first 128-step time tile processed in each sequence
+  int a_row0[3], r_row0, out_row0;   // rows in front of local row 0 (sequence-shard halo)
 };
 struct MimoSrc {
   const void* A; const void* W; int K; int64_t shift;
   int w_plane_off = 0;               // plane of this source's (hi) weight for system 0
   int w_plane_stride = 0;            // weight planes per system (bank: slots * 2; 0: shared)
   int64_t w_planes = 0;              // planes in W (0: 1 for bf16, 2 for 3xTF32)
+  int64_t row0 = 0;                  // halo rows stored in front of local row 0 of A
 };
 struct MimoGemm {
   MimoSrc src[3]; int n_src;
@@ -30,6 +32,7 @@ struct MimoGemm {
   int64_t L; int batch;
   const int* sys_list = nullptr; int n_list = 1; int n_sys_total = 1;
   int t_first = 0;
+  int64_t R_row0 = 0, out_row0 = 0;  // halo rows in front of local row 0 of R / out
 };
 
 bool mimo_tc_supported(int m, int p, int q);
