@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle CPU baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-seqshard", action="store_true",
+                    help="E4: run the sequence-sharded code path even at one rank (validation)")
     return ap.parse_args()
 
 
@@ -69,7 +71,9 @@ def make_workload(cfg: str, world: int, rank: int):
     if cfg == "E4":
         wl = S.make_E4()
         return wl, [0], {"workload": "E4", "m": 1024, "p": 256, "q": 256, "L": wl.L, "batch": wl.batch,
-                         "N": int(wl.N[0]), "parallelism": "replica per GPU" if world > 1 else "single"}
+                         "N": int(wl.N[0]),
+                         "parallelism": (f"sequence-sharded x{world}: L_loc = {wl.L // world}, per-stage halo of "
+                                         "2^k rows from rank r-1 (NCCL P2P)") if world > 1 else "single"}
     if cfg == "E5":
         wl = S.make_E5()
         per = wl.n_ch // world
@@ -278,7 +282,12 @@ def run_ours(args, world, rank, local_rank):
     torch.cuda.set_device(dev)
     pk.lib()
     wl, chans, cfgd = make_workload(args.config, world, rank)
-    dw = DeviceWorkload(wl, device=f"cuda:{dev}", channels=chans)
+    sharded = args.config == "E4" and (world > 1 or args.force_seqshard)
+    if sharded:
+        from paper_2411_17729_b200.runner import SeqShardedWorkload
+        dw = SeqShardedWorkload(wl, rank, world, device=f"cuda:{dev}")
+    else:
+        dw = DeviceWorkload(wl, device=f"cuda:{dev}", channels=chans)
     stream = torch.cuda.current_stream()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{dev}")   # > 126 MB L2
 
@@ -314,14 +323,40 @@ def run_ours(args, world, rank, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
 
-    flops_rank = 2.0 * wl.m * wl.m * wl.L * wl.batch * float(sum(int(wl.N[c]) + 1 for c in chans))
-    samples_rank = wl.L * wl.batch * len(chans)
+    share = 1.0 / world if sharded else 1.0                   # a sequence shard does 1/world of the rows
+    flops_rank = share * 2.0 * wl.m * wl.m * wl.L * wl.batch * float(sum(int(wl.N[c]) + 1 for c in chans))
+    samples_rank = share * wl.L * wl.batch * len(chans)
     value = flops_rank * world * args.steps / (ms_max / 1e3) / 1e9
     sps = samples_rank * world * args.steps / (ms_max / 1e3)
 
     # ---- e2e: the public host-buffer C-ABI call, H2D + compute + D2H inside the timed region
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and sharded:
+        u_h = dw.u.cpu().pin_memory()
+        y_h = torch.empty(tuple(dw.y.shape), dtype=dw.y.dtype).pin_memory()
+        dw.run_host(u_h, y_h)
+        torch.cuda.synchronize()
+        e2e_ms = []
+        for _ in range(args.e2e_steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if world > 1:
+                dist.barrier()
+            a.record(stream)
+            dw.run_host(u_h, y_h)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e2e_ms.append(a.elapsed_time(b))
+        te = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=f"cuda:{dev}")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": flops_rank * world * args.e2e_steps / (float(te.item()) / 1e3) / 1e9, "unit": "GFLOP/s",
+               "samples_per_s": samples_rank * world * args.e2e_steps / (float(te.item()) / 1e3),
+               "h2d_bytes_per_step": int(u_h.numel() * u_h.element_size()),
+               "d2h_bytes_per_step": int(y_h.numel() * y_h.element_size()),
+               "ms_per_step": float(te.item()) / args.e2e_steps,
+               "api": "SeqShardedWorkload.run_host (pinned local u -> device, casc_seq_* steps with NCCL halos, y -> host)"}
+    elif not args.no_e2e:
         n = len(chans)
         f = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
         Ab_h, Bb_h, C_h = f(wl.Abar[chans]), f(wl.Bbar[chans]), f(wl.C[chans])
@@ -369,7 +404,8 @@ def run_ours(args, world, rank, local_rank):
     cfgd["timed_step"] = "powers (fp64 squaring + pack) + apply (all stages, y = Cv + Du)"
     line = {"metric": METRIC, "value": value, "unit": "GFLOP/s", "samples_per_s": sps, "n_gpus": world,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "strong" if args.config == "E5" else "weak",
+            "higher_is_better": True,
+            "scaling": "strong" if args.config == "E5" or sharded else "weak",
             "vs_baseline": None,
             "dtype": "f32" if wl.mode == "fp32" else "bf16",
             "data": "synthetic (seeded BASELINE recipe; no dataset in the paper)", "config": cfgd,

@@ -81,3 +81,47 @@ class DeviceWorkload:
         if self.bank:
             return y[..., None]
         return y[None]
+
+
+class SeqShardedWorkload:
+    """This rank's time shard of a single-system workload (BASELINE configs[3] at N > 1 GPUs):
+    rows [rank L_loc, (rank+1) L_loc) of every sequence, run with seqshard.run over DistComm
+    (per-stage halo exchange with the neighbouring ranks)."""
+
+    def __init__(self, wl, rank: int, world: int, device="cuda", group=None):
+        from . import seqshard
+        if wl.kind != "mimo" or wl.L % world:
+            raise ValueError("sequence sharding takes one system with L divisible by the rank count")
+        self.wl, self.rank, self.world = wl, rank, world
+        self.L_loc = wl.L // world
+        self.N = int(wl.N[0])
+        self.Ne = seqshard.effective_order(self.N, wl.L)
+        self.H = seqshard.shard_H(self.N, wl.L)
+        d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
+        self.Abar, self.Bbar, self.C = d(wl.Abar[0]), d(wl.Bbar[0]), d(wl.C[0])
+        self.D = d(wl.D[0]) if np.any(wl.D[0]) else None
+        l0 = rank * self.L_loc
+        u = np.stack([wl.u_window(0, b, l0, l0 + self.L_loc) for b in range(wl.batch)])   # storage-exact f64
+        self.u = torch.from_numpy(u).to(api.STORAGE[api._mode(wl.mode)]).to(device)
+        self.steps = seqshard.CudaSteps(wl.m, wl.p, wl.q, wl.mode, device)
+        self.shard = seqshard.make_shard(self.u, wl.m, wl.q, self.H)
+        self.comm = seqshard.DistComm(group) if world > 1 else seqshard.LocalComm()
+        self._seqshard = seqshard
+
+    @property
+    def y(self):
+        return self.shard.y
+
+    def step(self, stream=None) -> int:
+        """powers + derived weights + the sharded cascade; returns the number of kernel launches."""
+        launches = self.steps.prepare(self.Abar, self.Bbar, self.C, self.D, self.N, self.Ne, stream=stream)
+        launches += self.Ne + 1 if self.Ne > 0 else 1              # first + stages + last
+        self._seqshard.run(self.steps, self.comm, [self.shard], self.N, self.wl.L)
+        return launches
+
+    def run_host(self, u_h: torch.Tensor, y_h: torch.Tensor) -> int:
+        """End to end from pinned host buffers: H2D of the local u, step, D2H of the local y."""
+        self.shard.u_ext[:, 1:, :].copy_(u_h, non_blocking=True)
+        n = self.step()
+        y_h.copy_(self.shard.y, non_blocking=True)
+        return n

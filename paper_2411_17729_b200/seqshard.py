@@ -98,14 +98,17 @@ class CudaSteps:
         self.pw = None
         self.has_D = False
 
-    def prepare(self, Abar, Bbar, C, D, N: int, Ne: int, stream=None) -> None:
-        """Powers and the derived weights. Abar/Bbar/C/D float64 on device."""
+    def prepare(self, Abar, Bbar, C, D, N: int, Ne: int, stream=None) -> int:
+        """Powers and the derived weights. Abar/Bbar/C/D float64 on device.
+        Returns the number of kernel launches enqueued."""
         self.pw = api.powers(Abar, N, self.md, stream=stream)
+        n = api.last_launch_count()
         self.has_D = D is not None
         self.N_max = N
         check(lib().casc_seq_prepare(self.m, self.p, self.q, Ne, N, self.md, api._p(self.pw.pack), api._p(Bbar),
                                      api._p(C), api._p(D), api._p(self.ws), self.ws.numel(), api._stream(stream)),
               "casc_seq_prepare")
+        return n + api.last_launch_count()
 
     def first(self, sh: Shard, H: int, stream=None) -> None:
         batch, L_loc = sh.y.shape[0], sh.y.shape[1]
