@@ -42,6 +42,17 @@ static char stage_variant(int m) {
 
 static int pair_slots(int n_max) { return n_max > kHeadK ? (n_max - kHeadK + 1) / 2 : 0; }
 
+// Weight-resident GEMM mode for the stage (CASC_BANK_WRES=1). Measured slower on E2 (5.2 ms vs
+// 4.5 ms per step for the stages): the single weight buffer needs a pipeline drain at every
+// channel change, which costs more than the ring traffic it saves. Off by default.
+static int resident_weights() {
+  static const int on = [] {
+    const char* e = getenv("CASC_BANK_WRES");
+    return e && e[0] == '1' ? 1 : 0;
+  }();
+  return on;
+}
+
 struct BankWs {
   int* meta;      // Neff | Kc | parity | order   (4 n ints)
   double* Kr64;   // [n][m][128]
@@ -253,6 +264,7 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       g.n_src = 1; g.R = Vs; g.out = Vd; g.n_out = m; g.L = L; g.batch = batch;
       g.sys_list = dorder; g.n_list = cnt; g.n_sys_total = n;
       g.t_first = pass == 0 ? 0 : (int)(((int64_t)1 << (k - 1)) / 128);
+      g.w_resident = resident_weights();
       ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt * batch * L * m * 4.0, 2.0 * cnt * batch * L * (double)mm);
       if ((rc = launch_mimo_gemm(g, true, st))) return rc;
       continue;
@@ -284,7 +296,7 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       g.src[2].w_plane_off = 2 * pass; g.src[2].w_planes = (int64_t)n * qslots * 2;
       g.src[2].w_plane_stride = 2 * qslots;
       g.n_src = 3; g.R = Vs; g.out = Vd; g.n_out = m; g.L = L; g.batch = batch;
-      g.sys_list = dorder; g.n_list = cnt2; g.n_sys_total = n; g.t_first = t_first;
+      g.sys_list = dorder; g.n_list = cnt2; g.n_sys_total = n; g.t_first = t_first; g.w_resident = resident_weights();
       ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt2 * batch * L * m * 4.0, 4.0 * cnt2 * batch * L * (double)mm);
       if ((rc = launch_mimo_gemm(g, true, st))) return rc;
     }
@@ -293,7 +305,7 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       g.src[0].A = Vs; g.src[0].W = P.f32; g.src[0].K = m; g.src[0].shift = (int64_t)1 << k;
       g.src[0].w_plane_off = 2 * k; g.src[0].w_planes = planes; g.src[0].w_plane_stride = 2 * (N_max + 1);
       g.n_src = 1; g.R = Vs; g.out = Vd; g.n_out = m; g.L = L; g.batch = batch;
-      g.sys_list = dorder + cnt2; g.n_list = cnt1; g.n_sys_total = n; g.t_first = t_first;
+      g.sys_list = dorder + cnt2; g.n_list = cnt1; g.n_sys_total = n; g.t_first = t_first; g.w_resident = resident_weights();
       ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt1 * batch * L * m * 4.0, 2.0 * cnt1 * batch * L * (double)mm);
       if ((rc = launch_mimo_gemm(g, true, st))) return rc;
     }

@@ -27,6 +27,7 @@
 //   warps 6-9   (3xTF32 only) hi/lo split of each landed A tile.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -78,26 +79,37 @@ __device__ __forceinline__ float2 unpack_bf16(uint32_t u) {
   return __bfloat1622float2(h);
 }
 
-template <int BN, bool TF32>
+// Compile-time configuration. WCH > 0 selects the weight-resident mode: all K chunks of the
+// tile's weights (WCH at most) stay in a dedicated buffer and are reloaded only when the system
+// (bank channel) changes, so the ring carries A tiles only; 3xTF32 then splits into a separate
+// 2-slot lo ring. Used for the bank streaming stage, where one channel's P_k serves hundreds of
+// tiles and the bytes in flight decide the DRAM throughput.
+template <int BN, bool TF32, int RSO = 0, int WCH = 0>
 struct Cfg {
+  static constexpr bool WRES = WCH > 0;
   static constexpr int ES = TF32 ? 4 : 2;                 // element size
-  static constexpr int BK = 128 / ES;                     // K per stage: 128-byte rows
+  static constexpr int BK = 128 / ES;                     // K per chunk: 128-byte rows
   static constexpr uint32_t A_BYTES = BM * 128;           // 16 KB
   static constexpr uint32_t W_BYTES = BN * 128;           // one of hi / lo
-  static constexpr int NW = TF32 ? 2 : 1;                 // weight tiles per stage
-  static constexpr uint32_t STAGE_BYTES = A_BYTES * (TF32 ? 2 : 1) + W_BYTES * NW;   // A, W hi, (W lo, A lo)
-  static constexpr uint32_t TMA_BYTES = A_BYTES + W_BYTES * NW;
-  static constexpr int RS = (TF32 && BN == 64) ? 4 : 2;   // residual / staging chunk slots
+  static constexpr int NW = TF32 ? 2 : 1;                 // weight tiles per chunk
+  static constexpr uint32_t STAGE_BYTES =                 // ring slot: A[, A lo][, W hi[, W lo]]
+      WRES ? A_BYTES : A_BYTES * (TF32 ? 2 : 1) + W_BYTES * NW;
+  static constexpr uint32_t TMA_BYTES = WRES ? A_BYTES : A_BYTES + W_BYTES * NW;
+  static constexpr uint32_t WBUF = WRES ? (uint32_t)WCH * NW * W_BYTES : 0;
+  static constexpr int ALO = (WRES && TF32) ? 2 : 0;      // separate lo slots (weight-resident)
+  static constexpr int RS = RSO ? RSO : ((TF32 && BN == 64) ? 4 : 2);   // residual / staging chunks
   static constexpr uint32_t R_BYTES = BM * 128;           // 16 KB
-  static constexpr int STAGES_FIT = (int)((226u * 1024u - 1024u - RS * R_BYTES) / STAGE_BYTES);
-  static constexpr int STAGES = STAGES_FIT < 4 ? STAGES_FIT : 4;
+  static constexpr int STAGES_FIT =
+      (int)((226u * 1024u - 1024u - RS * R_BYTES - WBUF - ALO * A_BYTES) / STAGE_BYTES);
+  static constexpr int STAGES = STAGES_FIT < 8 ? STAGES_FIT : 8;
   static constexpr int CW = 128 / ES;                     // epilogue chunk width (columns)
   static constexpr int R_WARP = TF32 ? 10 : 6;            // residual / staging producer warp
   static constexpr int THREADS = 32 * (R_WARP + 1);
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + RS * R_BYTES;
+  static constexpr int GT = WRES ? 16 : 1;                // tiles per block of the tile walk
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + WBUF + ALO * A_BYTES + RS * R_BYTES;
 };
 
-// Tile -> (sequence coordinate in the tensors, time tile, N block, weight plane base)
+// Tile -> (sequence coordinate in the tensors, time tile, N block, system)
 struct TileCoord {
   int seq, l0, nb, sys;
 };
@@ -113,13 +125,28 @@ __device__ __forceinline__ TileCoord decode(int64_t tile, const MimoArg& a, int 
   t.sys = sys;
   return t;
 }
+
+// The CTA's walk over tiles: blocks of GT consecutive tiles dealt round-robin over the grid
+// (GT = 1: plain round-robin). Every role runs its own copy of the same walk.
+template <int GT>
+struct Walk {
+  int64_t blk, i, n_tiles;
+  __device__ Walk(int64_t n) : blk(blockIdx.x), i(0), n_tiles(n) {}
+  __device__ bool valid() const { return blk * GT + i < n_tiles; }
+  __device__ int64_t tile() const { return blk * GT + i; }
+  __device__ void next() {
+    if (++i == GT || blk * GT + i >= n_tiles) { i = 0; blk += gridDim.x; }
+  }
+};
 }  // namespace
 
-template <int BN, bool TF32>
-__global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(const __grid_constant__ MimoMaps maps,
-                                                                              MimoArg a) {
-  using C = Cfg<BN, TF32>;
+template <int BN, bool TF32, int RSO = 0, int WCH = 0>
+__global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
+    mimo_gemm_kernel(const __grid_constant__ MimoMaps maps, MimoArg a) {
+  using C = Cfg<BN, TF32, RSO, WCH>;
+  constexpr bool WRES = C::WRES;
   constexpr int STAGES = C::STAGES, BK = C::BK, RS = C::RS;
+  static_assert(STAGES >= 2, "shared memory too small for a 2-deep ring");
   // TMEM: two accumulator buffers of ACOLS columns. 3xTF32 keeps hi.hi in [0, BN) ("main") and
   // the two correction products in [BN, 2BN) ("corr"): the tensor core's fp32 accumulator
   // truncates at every MMA, so the error grows with the number of MMAs chained into one
@@ -130,8 +157,12 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
   constexpr int TCOLS = 2 * ACOLS < 32 ? 32 : 2 * ACOLS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sR = smem + STAGES * C::STAGE_BYTES;      // [RS][R_BYTES]
-  __shared__ uint64_t full[STAGES], empty[STAGES], lo_ready[STAGES], tfull[2], tempty[2], rfull[RS], rempty[RS];
+  uint8_t* sWres = smem + STAGES * C::STAGE_BYTES;           // [WCH][hi, lo] (weight-resident)
+  uint8_t* sAlo = sWres + C::WBUF;                           // [ALO] (weight-resident 3xTF32)
+  uint8_t* sR = sAlo + C::ALO * C::A_BYTES;                  // [RS][R_BYTES]
+  constexpr int NLO = WRES ? 2 : STAGES;                     // lo_ready barriers
+  __shared__ uint64_t full[STAGES], empty[STAGES], lo_ready[NLO], alo_free[2], tfull[2], tempty[2],
+      rfull[RS], rempty[RS], w_full;
   __shared__ uint32_t tmem_base;
   auto stA = [&](int s) { return smem + s * C::STAGE_BYTES; };
   auto stW = [&](int s) { return smem + s * C::STAGE_BYTES + C::A_BYTES; };
@@ -146,9 +177,11 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
   constexpr int NCH = BN / C::CW;                   // epilogue chunks per tile
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); mbar_init(&lo_ready[s], 128); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < NLO; ++s) mbar_init(&lo_ready[s], 128);
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); mbar_init(&alo_free[s], 1); }
     for (int s = 0; s < RS; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 1); }
+    mbar_init(&w_full, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<TCOLS>(&tmem_base);
@@ -165,10 +198,27 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
   if (warp == 0) {
     // =========================================================== TMA producer
     if (lane == 0) {
-      int s = 0;
-      uint32_t ph = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const TileCoord tc = decode(tile, a, n_nblk, nt_eff);
+      int s = 0, s_last = -1, cur_sys = -1;
+      uint32_t ph = 0, ph_last = 0;
+      for (Walk<C::GT> w(n_tiles); w.valid(); w.next()) {
+        const TileCoord tc = decode(w.tile(), a, n_nblk, nt_eff);
+        if (WRES && tc.sys != cur_sys) {
+          // every MMA issued so far must be done with the resident weights (MMAs complete in order)
+          if (s_last >= 0) mbar_wait(&empty[s_last], ph_last);
+          uint32_t bytes = 0;
+          for (int src = 0; src < a.n_src; ++src) bytes += (uint32_t)(a.K[src] / BK) * C::NW * C::W_BYTES;
+          mbar_arrive_expect_tx(&w_full, bytes);
+          int ci = 0;
+          for (int src = 0; src < a.n_src; ++src) {
+            const int plane = tc.sys * a.w_plane_stride[src] + a.w_plane_off[src];
+            for (int kc = 0; kc < a.K[src] / BK; ++kc, ++ci) {
+              uint8_t* wdst = sWres + ci * C::NW * C::W_BYTES;
+              tma_load_3d(wdst, &maps.W[src], &w_full, kc * BK, tc.nb * BN, plane);
+              if (TF32) tma_load_3d(wdst + C::W_BYTES, &maps.W[src], &w_full, kc * BK, tc.nb * BN, plane + 1);
+            }
+          }
+          cur_sys = tc.sys;
+        }
         for (int src = 0; src < a.n_src; ++src) {
           const int nk = a.K[src] / BK;
           const int plane = tc.sys * a.w_plane_stride[src] + a.w_plane_off[src];
@@ -176,8 +226,12 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
             mbar_wait(&empty[s], ph ^ 1);
             mbar_arrive_expect_tx(&full[s], C::TMA_BYTES);
             tma_load_3d(stA(s), &maps.A[src], &full[s], kc * BK, a.a_row0[src] + tc.l0 - (int)a.shift[src], tc.seq);
-            tma_load_3d(stW(s), &maps.W[src], &full[s], kc * BK, tc.nb * BN, plane);
-            if (TF32) tma_load_3d(stWlo(s), &maps.W[src], &full[s], kc * BK, tc.nb * BN, plane + 1);
+            if (!WRES) {
+              tma_load_3d(stW(s), &maps.W[src], &full[s], kc * BK, tc.nb * BN, plane);
+              if (TF32) tma_load_3d(stWlo(s), &maps.W[src], &full[s], kc * BK, tc.nb * BN, plane + 1);
+            }
+            s_last = s;
+            ph_last = ph;
             if (++s == STAGES) { s = 0; ph ^= 1; }
           }
         }
@@ -188,8 +242,8 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
     if (lane == 0) {
       int rs = 0;
       uint32_t rph = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const TileCoord tc = decode(tile, a, n_nblk, nt_eff);
+      for (Walk<C::GT> w(n_tiles); w.valid(); w.next()) {
+        const TileCoord tc = decode(w.tile(), a, n_nblk, nt_eff);
         for (int j = 0; j < NCH; ++j) {
           mbar_wait(&rempty[rs], rph ^ 1);
           if (a.has_residual) {
@@ -206,29 +260,42 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
     // =========================================================== MMA issuer
     if (lane == 0) {
       const uint32_t idesc = make_idesc(TF32 ? FMT_TF32 : FMT_BF16, BM, BN);
-      int s = 0;
-      uint32_t ph = 0;
-      int64_t t_local = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t_local) {
+      int s = 0, cur_sys = -1;
+      uint32_t ph = 0, wph = 0;
+      int64_t t_local = 0, j = 0;                 // tiles / chunks consumed by this CTA
+      for (Walk<C::GT> w(n_tiles); w.valid(); w.next(), ++t_local) {
+        const TileCoord tc = decode(w.tile(), a, n_nblk, nt_eff);
         const int acc = (int)(t_local & 1);
         mbar_wait(&tempty[acc], (uint32_t)((t_local >> 1) & 1) ^ 1);
+        if (WRES && tc.sys != cur_sys) {
+          mbar_wait(&w_full, wph);
+          wph ^= 1;
+          cur_sys = tc.sys;
+        }
         tc_fence_after();
         const uint32_t d = tbase + acc * ACOLS, dc = d + BN;
         bool first = true;
+        int ci = 0;
         for (int src = 0; src < a.n_src; ++src) {
           const int nk = a.K[src] / BK;
-          for (int kc = 0; kc < nk; ++kc) {
-            if (TF32) mbar_wait(&lo_ready[s], ph);
-            else mbar_wait(&full[s], ph);
+          for (int kc = 0; kc < nk; ++kc, ++ci, ++j) {
+            if (TF32) {
+              if (WRES) mbar_wait(&lo_ready[j & 1], (uint32_t)((j >> 1) & 1));
+              else mbar_wait(&lo_ready[s], ph);
+            } else {
+              mbar_wait(&full[s], ph);
+            }
             tc_fence_after();
-            const uint32_t a0 = smem_u32(stA(s)), w0 = smem_u32(stW(s));
+            const uint32_t a0 = smem_u32(stA(s));
+            const uint32_t w0 = WRES ? smem_u32(sWres + ci * C::NW * C::W_BYTES) : smem_u32(stW(s));
+            const uint32_t al0 = WRES ? smem_u32(sAlo + (j & 1) * C::A_BYTES) : smem_u32(stAlo(s));
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {               // 4 x 32 B = one 128-B row per stage
+            for (int k = 0; k < 4; ++k) {               // 4 x 32 B = one 128-B row per chunk
               const uint64_t ad = make_sdesc(a0 + k * 32, 16, 1024, LAYOUT_SW128);
               const uint64_t wd = make_sdesc(w0 + k * 32, 16, 1024, LAYOUT_SW128);
               if (TF32) {
-                const uint64_t ald = make_sdesc(smem_u32(stAlo(s)) + k * 32, 16, 1024, LAYOUT_SW128);
-                const uint64_t wld = make_sdesc(smem_u32(stWlo(s)) + k * 32, 16, 1024, LAYOUT_SW128);
+                const uint64_t ald = make_sdesc(al0 + k * 32, 16, 1024, LAYOUT_SW128);
+                const uint64_t wld = make_sdesc(w0 + C::W_BYTES + k * 32, 16, 1024, LAYOUT_SW128);
                 mma_tf32(d, ad, wd, idesc, first ? 0u : 1u);      // main: hi.hi
                 mma_tf32(dc, ald, wd, idesc, first ? 0u : 1u);    // corr: lo.hi + hi.lo
                 mma_tf32(dc, ad, wld, idesc, 1u);
@@ -238,6 +305,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
               first = false;
             }
             mma_commit(&empty[s]);
+            if (WRES && TF32) mma_commit(&alo_free[j & 1]);
             if (++s == STAGES) { s = 0; ph ^= 1; }
           }
         }
@@ -250,13 +318,15 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
       const int t = threadIdx.x - 192;
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      int64_t j = 0;
+      for (Walk<C::GT> w(n_tiles); w.valid(); w.next()) {
         for (int src = 0; src < a.n_src; ++src) {
           const int nk = a.K[src] / BK;
-          for (int kc = 0; kc < nk; ++kc) {
+          for (int kc = 0; kc < nk; ++kc, ++j) {
             mbar_wait(&full[s], ph);
+            if (WRES && j >= 2) mbar_wait(&alo_free[j & 1], (uint32_t)(((j - 2) >> 1) & 1));
             float4* hi = reinterpret_cast<float4*>(stA(s));
-            float4* out = reinterpret_cast<float4*>(stAlo(s));
+            float4* out = reinterpret_cast<float4*>(WRES ? sAlo + (j & 1) * C::A_BYTES : stAlo(s));
 #pragma unroll
             for (int e = t; e < (int)(C::A_BYTES / 16); e += 128) {
               const float4 v = hi[e], h = tf32_hi4(v);
@@ -264,7 +334,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
               out[e] = tf32_lo4(v, h);
             }
             fence_async_smem();
-            mbar_arrive(&lo_ready[s]);
+            mbar_arrive(&lo_ready[WRES ? (int)(j & 1) : s]);
             if (++s == STAGES) { s = 0; ph ^= 1; }
           }
         }
@@ -278,8 +348,8 @@ __global__ void __launch_bounds__(Cfg<BN, TF32>::THREADS, 1) mimo_gemm_kernel(co
     int64_t t_local = 0;
     int rs = 0, prev_rs = -1;
     uint32_t rph = 0;
-    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t_local) {
-      const TileCoord tc = decode(tile, a, n_nblk, nt_eff);
+    for (Walk<C::GT> w(n_tiles); w.valid(); w.next(), ++t_local) {
+      const TileCoord tc = decode(w.tile(), a, n_nblk, nt_eff);
       const int acc = (int)(t_local & 1);
       mbar_wait(&tfull[acc], (uint32_t)((t_local >> 1) & 1));
       tc_fence_after();
@@ -374,9 +444,9 @@ static bool map3d(CUtensorMap* m, const void* base, bool f32, int64_t d0, int64_
 
 bool mimo_tc_supported(int m, int p, int q) { return m % 64 == 0 && p % 64 == 0 && q % 64 == 0 && m >= 64; }
 
-template <int BN, bool TF32>
+template <int BN, bool TF32, int RSO = 0, int WCH = 0>
 static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
-  using C = Cfg<BN, TF32>;
+  using C = Cfg<BN, TF32, RSO, WCH>;
   MimoMaps maps;
   memset(&maps, 0, sizeof(maps));
   MimoArg a{};
@@ -405,13 +475,13 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
   a.out_row0 = (int)g.out_row0;
   if (g.R && !map3d(&maps.R, g.R, TF32, g.n_out, g.R_row0 + g.L, nseq_total, BM)) return CASC_ERR_CUDA;
   if (!map3d(&maps.out, g.out, TF32, g.n_out, g.out_row0 + g.L, nseq_total, BM)) return CASC_ERR_CUDA;
-  if (cudaFuncSetAttribute(mimo_gemm_kernel<BN, TF32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(mimo_gemm_kernel<BN, TF32, RSO, WCH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)C::SMEM) != cudaSuccess)
     return CASC_ERR_CUDA;
   const int64_t tiles = (int64_t)a.n_list * g.batch * (ceil_div(g.L, BM) - g.t_first) * ceil_div(g.n_out, BN);
   if (tiles <= 0) return CASC_OK;
-  const int grid = (int)std::min<int64_t>(tiles, 148);
-  mimo_gemm_kernel<BN, TF32><<<grid, C::THREADS, C::SMEM, st>>>(maps, a);
+  const int grid = (int)std::min<int64_t>(ceil_div(tiles, C::GT), 148);
+  mimo_gemm_kernel<BN, TF32, RSO, WCH><<<grid, C::THREADS, C::SMEM, st>>>(maps, a);
   CASC_LAUNCHED();
   return CASC_OK;
 }
@@ -419,7 +489,23 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
 int launch_mimo_gemm(const MimoGemm& g, bool tf32, cudaStream_t st) {
   if (tf32) {
     if (g.n_out % 128 == 0) return launch_cfg<128, true>(g, st);   // main + corr accumulators
-    if (g.n_out % 64 == 0) return launch_cfg<64, true>(g, st);
+    if (g.n_out % 64 == 0) {
+      // bank streaming stage: split of shared memory between the A/W ring and the residual
+      // ring (CASC_GEMM_RS = 2 | 4 | 6 residual chunks; default 4)
+      static const int rs = [] {
+        const char* e = getenv("CASC_GEMM_RS");
+        return e ? atoi(e) : 4;
+      }();
+      if (g.w_resident) {                         // weights resident across tiles (bank stage)
+        int chunks = 0;
+        for (int s = 0; s < g.n_src; ++s) chunks += g.src[s].K / 32;
+        if (chunks <= 2) return launch_cfg<64, true, 4, 2>(g, st);
+        if (chunks <= 6) return launch_cfg<64, true, 2, 6>(g, st);
+      }
+      if (rs == 2) return launch_cfg<64, true, 2>(g, st);
+      if (rs == 6) return launch_cfg<64, true, 6>(g, st);
+      return launch_cfg<64, true>(g, st);
+    }
   } else {
     if (g.n_out % 256 == 0) return launch_cfg<256, false>(g, st);
     if (g.n_out % 128 == 0) return launch_cfg<128, false>(g, st);

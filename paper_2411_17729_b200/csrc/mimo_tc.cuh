@@ -33,6 +33,7 @@ struct MimoGemm {
   const int* sys_list = nullptr; int n_list = 1; int n_sys_total = 1;
   int t_first = 0;
   int64_t R_row0 = 0, out_row0 = 0;  // halo rows in front of local row 0 of R / out
+  int w_resident = 0;                // keep the weights in shared memory across tiles
 };
 
 bool mimo_tc_supported(int m, int p, int q);
