@@ -248,7 +248,18 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     a.tiles_per_cta = pick_group(ntiles, (int64_t)n * batch, 16);
     ProfScope ps(st, K_BANK_HEAD, (double)n * batch * L * (1 + m) * 4.0,
                  (double)n * batch * L * 2.0 * m * 128);
-    if ((rc = launch_bank_head(m, a, st))) return rc;
+    // warp-specialized TMA-store head for m = 64 (CASC_BANK_HEAD=old selects the previous kernel)
+    static const bool old_head = [] {
+      const char* e = getenv("CASC_BANK_HEAD");
+      return e && e[0] == 'o';
+    }();
+    static const int head_group = [] {
+      const char* e = getenv("CASC_HEAD_GROUP");
+      return e ? atoi(e) : 64;
+    }();
+    if (m == 64 && !old_head) a.tiles_per_cta = pick_group(ntiles, (int64_t)n * batch, head_group);
+    rc = (m == 64 && !old_head) ? launch_bank_head_ws(m, a, (int64_t)n * batch, st) : launch_bank_head(m, a, st);
+    if (rc) return rc;
   }
   // ---- streaming stages k >= kHeadK over the channels with Neff > k (prefixes of `order`)
   int pass = 0;

@@ -28,6 +28,7 @@ struct BankTailArg {
 
 bool bank_tc_supported(int m);
 int launch_bank_head(int m, const BankHeadArg& a, cudaStream_t st);
+int launch_bank_head_ws(int m, const BankHeadArg& a, int64_t n_seq_total, cudaStream_t st);
 int launch_bank_stage_ws(int m, const BankStageArg& a, cudaStream_t st);
 int launch_bank_stage_rp(int m, const BankStageArg& a, cudaStream_t st);
 int launch_bank_tail(int m, const BankTailArg& a, cudaStream_t st);

@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
   static_assert(2 * ACOLS <= 512, "TMEM holds 512 columns");
   constexpr int TCOLS = 2 * ACOLS < 32 ? 32 : 2 * ACOLS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared state space (STS/LDS, not generic ST/LD)
   uint8_t* sWres = smem + STAGES * C::STAGE_BYTES;           // [WCH][hi, lo] (weight-resident)
   uint8_t* sAlo = sWres + C::WBUF;                           // [ALO] (weight-resident 3xTF32)
   uint8_t* sR = sAlo + C::ALO * C::A_BYTES;                  // [RS][R_BYTES]
@@ -429,7 +429,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 3-D tensor [d2][d1][d0] (d0 contiguous) with a box {128-B row, rows, 1}, SWIZZLE_128B.
-static bool map3d(CUtensorMap* m, const void* base, bool f32, int64_t d0, int64_t d1, int64_t d2, int rows) {
+bool map3d(CUtensorMap* m, const void* base, bool f32, int64_t d0, int64_t d1, int64_t d2, int rows) {
   auto fn = encode_fn();
   if (!fn) return false;
   const int64_t es = f32 ? 4 : 2;

@@ -37,6 +37,8 @@ struct MimoGemm {
 };
 
 bool mimo_tc_supported(int m, int p, int q);
+// 3-D tensor map [d2][d1][d0] (d0 contiguous), box {128 B, rows, 1}, SWIZZLE_128B (fp32 or bf16)
+bool map3d(CUtensorMap* m, const void* base, bool f32, int64_t d0, int64_t d1, int64_t d2, int rows);
 // tf32 = true: 3xTF32 (fp32 signals, weights as tf32 hi/lo planes); else bf16.
 int launch_mimo_gemm(const MimoGemm& g, bool tf32, cudaStream_t st);
 
