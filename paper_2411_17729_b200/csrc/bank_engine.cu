@@ -92,15 +92,191 @@ bool bank_tc_path(int m, int p, int q, int mode) {
   return !force_simt && p == 1 && q == 1 && mode == CASC_FP32 && bank_tc_supported(m);
 }
 
-size_t bank_ws_bytes(int n, int m, int64_t L, int batch, int n_max) {
-  return carve_bank(nullptr, n, m, L, batch, stage_variant(m) == 't' ? pair_slots(n_max) : 0).bytes;
-}
-
 static int eff_order_b(int N, int64_t L) {
   if (L <= 2) return 0;
   int kstar = 0;
   while (((int64_t)1 << (kstar + 1)) < L) ++kstar;
   return N < kstar ? N : kstar;
+}
+
+// ---------------------------------------------------------------- fused persistent path
+// bank_fused.cu: one launch for the whole bank, states in TMEM, levels exchanged through L2.
+// Opt-in (CASC_BANK_FUSED=1, read per call) for m = 64 when every channel has Ne >= 7: it is
+// correct (tests/test_gpu_bank_fused.py) but measured slower than the multi-kernel path on E2
+// (8.9 vs 6.4 ms for head + stages + tail): its tf32 N=64 MMAs are shared-memory-bound (48 cyc
+// each, 128 B/cyc) and the per-tile publication chain adds latency; see DESIGN.md.
+static bool fused_enabled() {
+  const char* e = getenv("CASC_BANK_FUSED");
+  return e && e[0] == '1';
+}
+static bool discard_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CASC_DISCARD");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+static constexpr int kFusedT = 6;           // tiles per chunk (TMEM: 6 x 64 state columns)
+
+struct FusedWs {
+  int* meta;        // Neff | Kc | order
+  double* Kr64;     // [n][64][128]
+  float* krimg;     // [n][16384]
+  double* w64;      // [n][64]
+  float *w32, *c32, *d32;
+  unsigned* done;   // [n*batch]
+  unsigned* flags;  // [S][ntiles]
+  float* pub;       // [S][NL][ntiles*128][64]
+  size_t bytes;
+};
+static FusedWs carve_fused(void* ws, int n, int64_t L, int batch, int S, int NL) {
+  Carver c(ws);
+  FusedWs w{};
+  const int64_t ntiles = ceil_div(L, 128);
+  w.meta = c.take<int>((size_t)3 * n);
+  w.Kr64 = c.take<double>((size_t)n * 64 * 128);
+  w.krimg = c.take<float>((size_t)n * 16384);
+  w.w64 = c.take<double>((size_t)n * 64);
+  w.w32 = c.take<float>((size_t)n * 64);
+  w.c32 = c.take<float>((size_t)n * 64);
+  w.d32 = c.take<float>((size_t)n);
+  w.done = c.take<unsigned>((size_t)n * batch);
+  w.flags = c.take<unsigned>((size_t)S * ntiles);
+  w.pub = c.take<float>((size_t)S * NL * ntiles * 128 * 64);
+  w.bytes = c.bytes();
+  return w;
+}
+static int sm_count() {
+  static const int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return n;
+}
+// sequence slots: enough for every sequence a CTA can be working on while others lag behind
+static int fused_slots(int64_t nchunk, int64_t Q) {
+  const int64_t s = 2 * ceil_div(148, nchunk) + 4;
+  return (int)std::min<int64_t>(Q, s);
+}
+static size_t fused_ws_bytes(int n, int m, int64_t L, int batch, int n_max) {
+  if (m != 64 || !fused_enabled()) return 0;
+  const int NL = eff_order_b(n_max, L) - 6;
+  if (NL < 1) return 0;
+  const int64_t nchunk = ceil_div(ceil_div(L, 128), kFusedT);
+  return carve_fused(nullptr, n, L, batch, fused_slots(nchunk, (int64_t)n * batch), NL).bytes;
+}
+
+size_t bank_ws_bytes(int n, int m, int64_t L, int batch, int n_max) {
+  return std::max(carve_bank(nullptr, n, m, L, batch, stage_variant(m) == 't' ? pair_slots(n_max) : 0).bytes,
+                  fused_ws_bytes(n, m, L, batch, n_max));
+}
+
+// Returns CASC_ERR_UNSUPPORTED when the fused path does not apply (caller falls back to the
+// multi-kernel path), CASC_ERR_WORKSPACE when not even one sequence slot fits.
+static int bank_fused(int n, int64_t L, int batch, const int* N_host, int N_max, const void* pack,
+                      const double* Bbar, const double* C, const double* D, const void* u, void* y, void* ws,
+                      size_t ws_bytes, cudaStream_t st) {
+  constexpr int m = 64;
+  if (!fused_enabled()) return CASC_ERR_UNSUPPORTED;
+  const int64_t Q = (int64_t)n * batch;
+  const int64_t ntiles = ceil_div(L, 128);
+  if (Q >= (1 << 26) || ntiles >= (1 << 24)) return CASC_ERR_UNSUPPORTED;
+  std::vector<int> meta((size_t)3 * n);
+  int *Neff = meta.data(), *Kc = Neff + n, *order = Neff + 2 * n;
+  int maxNe = 0;
+  double flops = 0, bytes = 0;
+  for (int s = 0; s < n; ++s) {
+    Neff[s] = eff_order_b(N_host[s], L);
+    if (Neff[s] < kHeadK) return CASC_ERR_UNSUPPORTED;
+    Kc[s] = kHeadK;
+    maxNe = std::max(maxNe, Neff[s]);
+    flops += 2.0 * m * m * (N_host[s] + 1) * (double)L * batch;          // PAPER count, SURVEY 8d
+    bytes += ((N_host[s] + 1) * 2.0 * m * 4.0 + 8.0) * (double)L * batch;  // unfused streaming bytes
+  }
+  std::iota(order, order + n, 0);
+  std::stable_sort(order, order + n, [&](int a, int b) { return Neff[a] > Neff[b]; });
+  const int NL = maxNe - 6;
+  int T = kFusedT;
+  if (const char* e = getenv("CASC_FUSED_T")) T = std::max(1, std::min(kFusedT, atoi(e)));
+  const int64_t nchunk = ceil_div(ntiles, T);
+  int S = fused_slots(nchunk, Q);
+  if (const char* e = getenv("CASC_FUSED_SLOTS")) S = std::max(1, std::min(S, atoi(e)));   // tests: force reuse
+  while (S > 1 && carve_fused(nullptr, n, L, batch, S, NL).bytes > ws_bytes) --S;
+  FusedWs w = carve_fused(ws, n, L, batch, S, NL);
+  if (w.bytes > ws_bytes) return CASC_ERR_WORKSPACE;
+  PackLayout P = pack_layout(const_cast<void*>(pack), n, m, N_max, CASC_FP32);
+  const int64_t mm = (int64_t)m * m;
+  int rc;
+  CASC_TRY(cudaMemcpyAsync(w.meta, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  const int *dNeff = w.meta, *dKc = w.meta + n, *dorder = w.meta + 2 * n;
+  {
+    // derived: Krylov columns Kr[:, j] = Abar^j Bbar (j < 128) by doubling with the powers
+    // (Kr_{2^i + j} = P_i Kr_j), their tf32 hi/lo smem image; w = C P_Ne; fp32 copies of C, D
+    ProfScope ps(st, K_DERIVED, 0.0, 2.0 * n * (double)m * m * 128);
+    if ((rc = launch_kr_init(Bbar, w.Kr64, n, m, st))) return rc;
+    for (int i = 0; i < kHeadK; ++i) {
+      DgemmArg a{};
+      a.M = m; a.N = 1 << i; a.K = m;
+      a.A = P.p64 + i * mm; a.lda = m; a.sA = (int64_t)(N_max + 1) * mm;
+      a.B = w.Kr64; a.ldb = 128; a.sB = (int64_t)m * 128;
+      a.C = w.Kr64 + (1 << i); a.ldc = 128; a.sC = (int64_t)m * 128;
+      if ((rc = launch_dgemm(a, n, st))) return rc;
+    }
+    if ((rc = launch_kr_image(w.Kr64, dKc, w.krimg, n, st))) return rc;
+    DgemmArg a{};                                // w = C P_Ne  (1 x m)
+    a.M = 1; a.N = m; a.K = m;
+    a.A = C; a.lda = m; a.sA = m;
+    a.B = P.p64; a.ldb = m; a.sB = (int64_t)(N_max + 1) * mm; a.nB = mm; a.selB = dNeff;
+    a.C = w.w64; a.ldc = m; a.sC = m;
+    if ((rc = launch_dgemm(a, n, st))) return rc;
+    if ((rc = launch_f64_to_f32(w.w64, w.w32, (int64_t)n * m, st))) return rc;
+    if ((rc = launch_f64_to_f32(C, w.c32, (int64_t)n * m, st))) return rc;
+    if (D) {
+      if ((rc = launch_f64_to_f32(D, w.d32, n, st))) return rc;
+    } else {
+      CASC_TRY(cudaMemsetAsync(w.d32, 0, sizeof(float) * n, st));
+    }
+  }
+  CASC_TRY(cudaMemsetAsync(w.done, 0, sizeof(unsigned) * (size_t)Q, st));
+  CASC_TRY(cudaMemsetAsync(w.flags, 0, sizeof(unsigned) * (size_t)S * ntiles, st));
+  BankFusedArg a{};
+  a.u = static_cast<const float*>(u); a.y = static_cast<float*>(y); a.krimg = w.krimg;
+  a.cvec = w.c32; a.wvec = w.w32; a.dvec = w.d32; a.order = dorder; a.Neff = dNeff;
+  a.flags = w.flags; a.done = w.done; a.pub = w.pub;
+  a.L = L; a.batch = batch; a.ntiles = (int)ntiles; a.T = T; a.nchunk = (int)nchunk; a.S = S; a.NL = NL;
+  a.planes_per_ch = 2 * (N_max + 1); a.total_chunks = Q * nchunk; a.discard = discard_enabled() ? 1 : 0;
+  const int grid = (int)std::min<int64_t>(a.total_chunks, sm_count());
+  if (getenv("CASC_DEBUG"))
+    fprintf(stderr, "casc: bank_fused n=%d L=%lld batch=%d ntiles=%lld nchunk=%lld S=%d NL=%d grid=%d ws=%zu\n", n,
+            (long long)L, batch, (long long)ntiles, (long long)nchunk, S, NL, grid, w.bytes);
+  static unsigned long long* dbg = nullptr;
+  const bool want_dbg = getenv("CASC_FUSED_DBG") != nullptr;
+  if (want_dbg) {
+    if (!dbg) CASC_TRY(cudaMalloc(&dbg, 24 * sizeof(unsigned long long)));
+    CASC_TRY(cudaMemsetAsync(dbg, 0, 24 * sizeof(unsigned long long), st));
+    a.dbg = dbg;
+  }
+  {
+    ProfScope ps(st, K_BANK_FUSED, bytes, flops);
+    rc = launch_bank_fused(a, P.f32, (int)((int64_t)n * (N_max + 1) * 2), grid, st);
+  }
+  if (want_dbg && rc == CASC_OK) {          // diagnostics only: synchronises and prints
+    unsigned long long h[24];
+    CASC_TRY(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CASC_TRY(cudaStreamSynchronize(st));
+    const double tot = (double)h[20] / grid;
+    static const char* nm[5][4] = {{"prod.wfree/done", "prod.flag", "prod.aempty", "-"},
+                                   {"mma.wfull", "mma.zfull", "mma.accempty", "mma.loready"},
+                                   {"xf.done", "xf.zempty", "xf.afull", "xf.lofree"},
+                                   {"epi.accfull", "epi.stg_empty", "epi.afull", "-"},
+                                   {"st.stg_full", "st.read", "st.release", "-"}};
+    fprintf(stderr, "casc fused dbg: grid %d, avg kernel cycles/CTA %.0f\n", grid, tot);
+    for (int r = 0; r < 5; ++r)
+      for (int i = 0; i < 4; ++i)
+        if (h[r * 4 + i]) fprintf(stderr, "  %-16s %6.1f%%\n", nm[r][i], 100.0 * h[r * 4 + i] / grid / tot);
+  }
+  return rc;
 }
 
 static int pick_group(int64_t ntiles, int64_t seqs, int want) {
@@ -134,6 +310,10 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
 int engine_bank_tc(int n, int m, int64_t L, int batch, const int* N_host, int N_max, const void* pack,
                    const double* Bbar, const double* C, const double* D, const void* u, void* y, void* ws,
                    size_t ws_bytes, cudaStream_t st) {
+  if (m == 64) {
+    const int rc = bank_fused(n, L, batch, N_host, N_max, pack, Bbar, C, D, u, y, ws, ws_bytes, st);
+    if (rc != CASC_ERR_UNSUPPORTED && rc != CASC_ERR_WORKSPACE) return rc;
+  }
   int maxNe = 0;
   for (int s = 0; s < n; ++s) maxNe = std::max(maxNe, eff_order_b(N_host[s], L));
   const int qslots = stage_variant(m) == 't' ? pair_slots(maxNe) : 0;

@@ -44,7 +44,7 @@ ProfScope::~ProfScope() {
 static const char* kNames[K_NCLASS] = {"powers_square", "powers_pack", "derived", "first_stage",
                                        "stage", "last_stage", "direct", "convert",
                                        "bank_head", "bank_stage", "bank_tail", "mimo_tc_stage",
-                                       "mimo_tc_first", "mimo_tc_last"};
+                                       "mimo_tc_first", "mimo_tc_last", "bank_fused"};
 
 }  // namespace casc
 

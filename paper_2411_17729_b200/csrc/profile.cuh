@@ -4,7 +4,7 @@
 namespace casc {
 enum KClass {
   K_POWERS = 0, K_PACK, K_DERIVED, K_FIRST, K_STAGE, K_LAST, K_DIRECT, K_CONVERT,
-  K_BANK_HEAD, K_BANK_STAGE, K_BANK_TAIL, K_MIMO_STAGE, K_MIMO_FIRST, K_MIMO_LAST, K_NCLASS
+  K_BANK_HEAD, K_BANK_STAGE, K_BANK_TAIL, K_MIMO_STAGE, K_MIMO_FIRST, K_MIMO_LAST, K_BANK_FUSED, K_NCLASS
 };
 
 // RAII: records a start event now and an end event when it goes out of scope (after the
