@@ -116,7 +116,7 @@ static bool discard_enabled() {
   }();
   return on;
 }
-static constexpr int kFusedT = 6;           // tiles per chunk (TMEM: 6 x 64 state columns)
+static constexpr int kFusedT = 4;           // tiles per chunk (TMEM: 4 x 64 state columns)
 
 struct FusedWs {
   int* meta;        // Neff | Kc | order
@@ -379,31 +379,9 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
   // ---- derived: Krylov columns, w = C P_Ne, fp32 copies, pair weights
   {
     ProfScope ps(st, K_DERIVED, 0.0, 2.0 * n * (double)m * m * 128);
-    if ((rc = launch_kr_init(Bbar, w.Kr64, n, m, st))) return rc;
-    const int maxKc = std::min(kHeadK, maxNe);
-    for (int i = 0; i < maxKc; ++i) {          // Kr[:, 2^i + j] = P_i Kr[:, j], j < 2^i
-      DgemmArg a{};
-      a.M = m; a.N = 1 << i; a.K = m;
-      a.A = P.p64 + i * mm; a.lda = m; a.sA = (int64_t)(N_max + 1) * mm;
-      a.B = w.Kr64; a.ldb = 128; a.sB = (int64_t)m * 128;
-      a.C = w.Kr64 + (1 << i); a.ldc = 128; a.sC = (int64_t)m * 128;
-      a.skip_below = dKc; a.level = i + 1;
-      if ((rc = launch_dgemm(a, n, st))) return rc;
-    }
-    if ((rc = launch_kr_split(w.Kr64, dKc, w.krT, n, m, st))) return rc;
-    DgemmArg a{};                                // w = C P_Ne  (1 x m)
-    a.M = 1; a.N = m; a.K = m;
-    a.A = C; a.lda = m; a.sA = m;
-    a.B = P.p64; a.ldb = m; a.sB = (int64_t)(N_max + 1) * mm; a.nB = mm; a.selB = dNeff;
-    a.C = w.w64; a.ldc = m; a.sC = m;
-    if ((rc = launch_dgemm(a, n, st))) return rc;
-    if ((rc = launch_f64_to_f32(w.w64, w.w32, (int64_t)n * m, st))) return rc;
-    if ((rc = launch_f64_to_f32(C, w.c32, (int64_t)n * m, st))) return rc;
-    if (D) {
-      if ((rc = launch_f64_to_f32(D, w.d32, n, st))) return rc;
-    } else {
-      CASC_TRY(cudaMemsetAsync(w.d32, 0, sizeof(float) * n, st));
-    }
+    if ((rc = launch_bank_derived(P.p64, N_max + 1, Bbar, C, D, dNeff, dKc, w.Kr64, w.krT, w.w64, w.w32, w.c32,
+                                  w.d32, n, m, st)))
+      return rc;
     for (int j = 0; j < qslots; ++j) {          // Q_k = P_{k+1} P_k for pass j (k = 7 + 2j)
       const int k = kHeadK + 2 * j;
       if (count_ge(k + 2) == 0) continue;
@@ -428,7 +406,9 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     a.tiles_per_cta = pick_group(ntiles, (int64_t)n * batch, 16);
     ProfScope ps(st, K_BANK_HEAD, (double)n * batch * L * (1 + m) * 4.0,
                  (double)n * batch * L * 2.0 * m * 128);
-    // warp-specialized TMA-store head for m = 64 (CASC_BANK_HEAD=old selects the previous kernel)
+    // warp-specialized TMA-store head for m = 64 (CASC_BANK_HEAD=old selects the previous kernel).
+    // A TMEM-operand (TS) variant was measured slower (2.0 vs 1.3 ms on E2): tcgen05 reads a
+    // TMEM A operand at ~64 B/cycle, below shared memory's 128 B/cycle.
     static const bool old_head = [] {
       const char* e = getenv("CASC_BANK_HEAD");
       return e && e[0] == 'o';

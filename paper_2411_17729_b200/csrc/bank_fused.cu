@@ -46,11 +46,11 @@ using namespace sm100;
 
 namespace {
 constexpr int TM = 128;                     // time rows per tile
-constexpr int NA = 4, NLO = 3;              // fp32/hi units, lo units (16 KB each)
+constexpr int NA = 6;                       // fp32 units (16 KB K-chunks of a shifted tile)
+constexpr int NAU = 2;                      // TMEM A units (tf32 hi | lo of one K-chunk)
 constexpr uint32_t UNIT = 16384;
 constexpr uint32_t OFF_A = 0;
-constexpr uint32_t OFF_LO = OFF_A + NA * UNIT;
-constexpr uint32_t OFF_W = OFF_LO + NLO * UNIT;      // 64 KB: Krylov hi | lo, or P_j in halves
+constexpr uint32_t OFF_W = OFF_A + NA * UNIT;        // 64 KB: Krylov hi | lo, or P_j in halves
 constexpr uint32_t OFF_Z = OFF_W + 65536;            // 2 slots x (hi 4 KB | lo 4 KB)
 constexpr uint32_t OFF_STG = OFF_Z + 16384;          // 2 x 16 KB publication staging slots
 constexpr uint32_t SMEM_USED = OFF_STG + 2 * UNIT;
@@ -60,8 +60,9 @@ constexpr size_t SMEM_BYTES = SMEM_USED;
 constexpr int STORE_WARP = 10;
 constexpr int THREADS = 32 * (STORE_WARP + 1);
 constexpr int PD = 4;                                // published tiles in flight per CTA
-constexpr int TMAX = 6;                              // tiles per chunk (TMEM state slots)
-constexpr uint32_t ACC0 = TMAX * 64;                 // TMEM: states [0, 384), two accumulators after
+constexpr int TMAX = 4;                              // tiles per chunk (TMEM state slots)
+constexpr uint32_t ACC0 = TMAX * 64;                 // TMEM: states [0, 256), two accumulators,
+constexpr uint32_t AU0 = ACC0 + 2 * 64;              // then NAU A units of 64 columns (hi | lo)
 
 __device__ __forceinline__ void named_sync_f(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
@@ -165,13 +166,12 @@ __global__ void __launch_bounds__(THREADS, 1) bank_fused_kernel(const __grid_con
   if (smem_u32(smem_raw) & 1023u) __trap();          // SW128 tiles need 1024-B alignment
   uint8_t* smem = smem_raw;
   uint8_t* sA = smem + OFF_A;
-  uint8_t* sLO = smem + OFF_LO;
   uint8_t* sW = smem + OFF_W;
   float* sZ = reinterpret_cast<float*>(smem + OFF_Z);
   uint8_t* sSTG = smem + OFF_STG;
   __shared__ float sCW[128];                         // c | w of the chunk's channel (tail)
   __shared__ StgDesc stg_desc[2];
-  __shared__ uint64_t afull[NA], aempty[NA], loready[NLO], lofree[NLO], wfull[2], wfree[2], zfull[2], zempty[2],
+  __shared__ uint64_t afull[NA], aempty[NA], auready[NAU], aufree[NAU], wfull[2], wfree[2], zfull[2], zempty[2],
       accfull[2], accempty[2], stg_full[2], stg_empty[2], tready[NA];
   __shared__ uint32_t tmem_base;
 
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(THREADS, 1) bank_fused_kernel(const __grid_con
   } while (0)
   if (threadIdx.x == 0) {
     for (int s = 0; s < NA; ++s) { mbar_init(&afull[s], 1); mbar_init(&aempty[s], 1); mbar_init(&tready[s], 1); }
-    for (int s = 0; s < NLO; ++s) { mbar_init(&loready[s], 128); mbar_init(&lofree[s], 1); }
+    for (int s = 0; s < NAU; ++s) { mbar_init(&auready[s], 128); mbar_init(&aufree[s], 1); }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&wfull[s], 1); mbar_init(&wfree[s], 1);
       mbar_init(&zfull[s], 128); mbar_init(&zempty[s], 1);
@@ -259,10 +259,10 @@ __global__ void __launch_bounds__(THREADS, 1) bank_fused_kernel(const __grid_con
       }
     }
   } else if (warp == 1) {
-    // ================================================================== MMA issuer
-    if (lane == 0) {
+    // ================================================================== MMA issuer (whole warp)
+    {
       const uint32_t idesc = make_idesc(FMT_TF32, TM, 64);
-      uint32_t nz = 0, na = 0, nlo = 0, nacc = 0, wu[2] = {0, 0};
+      uint32_t nz = 0, na = 0, nau = 0, nacc = 0, wu[2] = {0, 0};
       const uint32_t bh = smem_u32(sW), bl = bh + 32768;
       for (int64_t g = blockIdx.x; g < a.total_chunks; g += gridDim.x) {
         const Chunk k = chunk_of(g, a);
@@ -276,21 +276,19 @@ __global__ void __launch_bounds__(THREADS, 1) bank_fused_kernel(const __grid_con
           tc_fence_after();
           const uint32_t d = tbase + ACC0 + ac * 64;
           const uint32_t zh = smem_u32(sZ + zs * 2048), zl = zh + 4096;
-#pragma unroll 4
-          for (int ks = 0; ks < 16; ++ks) {
-            const uint64_t azh = make_sdesc(zh + ks * 128, 64, 128, LAYOUT_NONE);
-            const uint64_t azl = make_sdesc(zl + ks * 128, 64, 128, LAYOUT_NONE);
-            const uint64_t bdh = make_sdesc(bh + ks * 2 * 64 * 16, 64 * 16, 128, LAYOUT_NONE);
-            const uint64_t bdl = make_sdesc(bl + ks * 2 * 64 * 16, 64 * 16, 128, LAYOUT_NONE);
-            mma_tf32(d, azh, bdh, idesc, ks > 0);
-            mma_tf32(d, azl, bdh, idesc, 1);
-            mma_tf32(d, azh, bdl, idesc, 1);
+          const uint64_t azh0 = make_sdesc(zh, 64, 128, LAYOUT_NONE), azl0 = make_sdesc(zl, 64, 128, LAYOUT_NONE);
+          const uint64_t bdh0 = make_sdesc(bh, 64 * 16, 128, LAYOUT_NONE), bdl0 = make_sdesc(bl, 64 * 16, 128, LAYOUT_NONE);
+#pragma unroll
+          for (int ks = 0; ks < 16; ++ks) {          // descriptor start field advances by bytes >> 4
+            mma_tf32_w(d, azh0 + ks * 8, bdh0 + ks * 128, idesc, ks > 0);
+            mma_tf32_w(d, azl0 + ks * 8, bdh0 + ks * 128, idesc, 1);
+            mma_tf32_w(d, azh0 + ks * 8, bdl0 + ks * 128, idesc, 1);
           }
-          mma_commit(&zempty[zs]);
-          mma_commit(&accfull[ac]);
+          mma_commit_w(&zempty[zs]);
+          mma_commit_w(&accfull[ac]);
         }
-        mma_commit(&wfree[0]);
-        mma_commit(&wfree[1]);
+        mma_commit_w(&wfree[0]);
+        mma_commit_w(&wfree[1]);
         ++wu[0];
         ++wu[1];
         for (int j = 7; j <= k.Ne; ++j) {
@@ -311,31 +309,27 @@ __global__ void __launch_bounds__(THREADS, 1) bank_fused_kernel(const __grid_con
             tc_fence_after();
             const uint32_t d = tbase + ACC0 + ac * 64;
             bool first = true;
-            for (int kc = 0; kc < 2; ++kc, ++na, ++nlo) {
-              const int s = (int)(na % NA), ls = (int)(nlo % NLO);
-              TW(3, mbar_wait(&loready[ls], (nlo / NLO) & 1));
+            for (int kc = 0; kc < 2; ++kc, ++na, ++nau) {
+              const int au = (int)(nau % NAU);
+              TW(3, mbar_wait(&auready[au], (nau / NAU) & 1));
               tc_fence_after();
-              const uint32_t a0 = smem_u32(sA + s * UNIT), al = smem_u32(sLO + ls * UNIT);
-              const uint32_t w0 = smem_u32(sW + h * 32768 + kc * 8192), wl = w0 + 16384;
+              const uint32_t ah = tbase + AU0 + au * 64, al = ah + 32;
+              const uint64_t wd0 = make_sdesc(smem_u32(sW + h * 32768 + kc * 8192), 16, 1024, LAYOUT_SW128);
+              const uint64_t wl0 = wd0 + (16384 >> 4);
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {
-                const uint64_t ad = make_sdesc(a0 + kk * 32, 16, 1024, LAYOUT_SW128);
-                const uint64_t ald = make_sdesc(al + kk * 32, 16, 1024, LAYOUT_SW128);
-                const uint64_t wd = make_sdesc(w0 + kk * 32, 16, 1024, LAYOUT_SW128);
-                const uint64_t wld = make_sdesc(wl + kk * 32, 16, 1024, LAYOUT_SW128);
-                mma_tf32(d, ad, wd, idesc, first ? 0u : 1u);
-                mma_tf32(d, ald, wd, idesc, 1u);
-                mma_tf32(d, ad, wld, idesc, 1u);
+              for (int kk = 0; kk < 4; ++kk) {           // A (shifted state) from TMEM: no smem reads
+                mma_tf32_ts_w(d, ah + kk * 8, wd0 + 2 * kk, idesc, first ? 0u : 1u);
+                mma_tf32_ts_w(d, al + kk * 8, wd0 + 2 * kk, idesc, 1u);
+                mma_tf32_ts_w(d, ah + kk * 8, wl0 + 2 * kk, idesc, 1u);
                 first = false;
               }
-              mma_commit(&aempty[s]);
-              mma_commit(&lofree[ls]);
+              mma_commit_w(&aufree[au]);
             }
-            mma_commit(&accfull[ac]);
+            mma_commit_w(&accfull[ac]);
             ++nacc;
           }
           if (j < k.Ne) {
-            mma_commit(&wfree[h]);
+            mma_commit_w(&wfree[h]);
             ++wu[h];
           }
         }
@@ -344,7 +338,9 @@ __global__ void __launch_bounds__(THREADS, 1) bank_fused_kernel(const __grid_con
   } else if (warp >= 6 && warp < STORE_WARP) {
     // ================================================================== transform
     const int tt = threadIdx.x - 192;
-    uint32_t nz = 0, na = 0, nlo = 0, ntr = 0;
+    const int trow = (warp & 3) * 32 + lane;        // TMEM lane this warp may access
+    const uint32_t trow_t = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+    uint32_t nz = 0, na = 0, nau = 0, ntr = 0;
     for (int64_t g = blockIdx.x; g < a.total_chunks; g += gridDim.x) {
       const Chunk k = chunk_of(g, a);
       if (k.q >= a.S) {                 // slot reuse: sequence q - S must be complete
@@ -399,22 +395,32 @@ __global__ void __launch_bounds__(THREADS, 1) bank_fused_kernel(const __grid_con
             }
             continue;
           }
-          for (int kc = 0; kc < 2; ++kc, ++na, ++nlo) {
-            const int s = (int)(na % NA), ls = (int)(nlo % NLO);
+          for (int kc = 0; kc < 2; ++kc, ++na, ++nau) {
+            const int s = (int)(na % NA), au = (int)(nau % NAU);
             TW(2, mbar_wait(&afull[s], (na / NA) & 1));
-            TW(3, mbar_wait(&lofree[ls], ((nlo / NLO) & 1) ^ 1));
-            float4* hi = reinterpret_cast<float4*>(sA + s * UNIT);
-            float4* lo = reinterpret_cast<float4*>(sLO + ls * UNIT);
+            // this thread's row of the landed K-chunk (SW128: 16-B chunk c at (c ^ (row % 8)) * 16)
+            const uint8_t* rr = sA + s * UNIT + trow * 128;
+            uint32_t hv[32], lv[32];
 #pragma unroll
-            for (int e = tt; e < (int)(UNIT / 16); e += 128) {
-              const float4 v = hi[e], h = tf32_hi4(v);
-              hi[e] = h;
-              lo[e] = tf32_lo4(v, h);
+            for (int cc = 0; cc < 8; ++cc) {
+              const float4 v = *reinterpret_cast<const float4*>(rr + ((cc ^ (trow & 7)) * 16));
+              const float4 hh = tf32_hi4(v), ll = tf32_lo4(v, hh);
+              hv[4 * cc] = __float_as_uint(hh.x); hv[4 * cc + 1] = __float_as_uint(hh.y);
+              hv[4 * cc + 2] = __float_as_uint(hh.z); hv[4 * cc + 3] = __float_as_uint(hh.w);
+              lv[4 * cc] = __float_as_uint(ll.x); lv[4 * cc + 1] = __float_as_uint(ll.y);
+              lv[4 * cc + 2] = __float_as_uint(ll.z); lv[4 * cc + 3] = __float_as_uint(ll.w);
             }
-            if (a.discard)                              // line = half row (this K-chunk) of row tt
-              discard_line(a.pub + plane * pub_plane_floats + (ts * TM + tt) * 64 + kc * 32);
-            fence_async_smem();
-            mbar_arrive(&loready[ls]);
+            if (a.discard)                              // line = half row (this K-chunk) of row trow
+              discard_line(a.pub + plane * pub_plane_floats + (ts * TM + trow) * 64 + kc * 32);
+            named_sync_f(2, 128);                       // every row read: the smem unit is free
+            if (tt == 0) mbar_arrive(&aempty[s]);
+            TW(3, mbar_wait(&aufree[au], ((nau / NAU) & 1) ^ 1));
+            tc_fence_after();
+            tmem_st32f(trow_t + AU0 + au * 64, hv);
+            tmem_st32f(trow_t + AU0 + au * 64 + 32, lv);
+            tmem_wait_stf();
+            tc_fence_before();
+            mbar_arrive(&auready[au]);
           }
         }
       }

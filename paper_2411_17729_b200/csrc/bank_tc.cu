@@ -248,6 +248,67 @@ int launch_kr_split(const double* Kr, const int* Kc, float* krT, int n, int ms, 
   return CASC_OK;
 }
 
+// ============================================================================ fused derived data
+// One CTA per channel: Krylov columns Kr[:, j] = Abar^j Bbar (j < 2^Kc) by doubling with the
+// powers (Kr_{2^i + j} = P_i Kr_j, float64 FMA in ascending k as dgemm_batched_kernel), their
+// tf32 hi/lo transpose krT, w = C P_Ne, and fp32 copies of C and D -- one launch instead of ~12.
+__global__ void __launch_bounds__(256) bank_derived_kernel(const double* p64, int slots, const double* Bbar,
+                                                           const double* C, const double* D, const int* Neff,
+                                                           const int* Kc, double* Kr64, float* krT, double* w64,
+                                                           float* w32, float* c32, float* d32, int ms) {
+  extern __shared__ double dsm[];
+  double* Ps = dsm;                         // [ms][ms+1]
+  double* Kr = Ps + ms * (ms + 1);          // [ms][129]
+  const int s = blockIdx.x, tid = threadIdx.x;
+  const int64_t mm = (int64_t)ms * ms;
+  const int kc = Kc[s];
+  const double* Ps0 = p64 + (int64_t)s * slots * mm;
+  for (int e = tid; e < ms * 128; e += 256) Kr[(e / 128) * 129 + e % 128] = (e % 128 == 0) ? Bbar[(int64_t)s * ms + e / 128] : 0.0;
+  for (int i = 0; i < kc; ++i) {
+    __syncthreads();
+    for (int e = tid; e < ms * ms; e += 256) Ps[(e / ms) * (ms + 1) + e % ms] = Ps0[i * mm + e];
+    __syncthreads();
+    const int cols = 1 << i;
+    for (int e = tid; e < ms * cols; e += 256) {   // Kr[r][cols + j] = sum_k P_i[r][k] Kr[k][j]
+      const int r = e / cols, j = e % cols;
+      double acc = 0.0;
+      for (int k = 0; k < ms; ++k) acc = fma(Ps[r * (ms + 1) + k], Kr[k * 129 + j], acc);
+      Kr[r * 129 + cols + j] = acc;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < ms * 128; e += 256) {
+    const int r = e / 128, j = e % 128;
+    const double v = (j < (1 << kc)) ? Kr[r * 129 + j] : 0.0;
+    Kr64[((int64_t)s * ms + r) * 128 + j] = v;
+    const int kp = 127 - j;                        // krT[s][hi|lo][r][k'], k' = 127 - lag
+    const float hi = tf32_rna((float)v);
+    krT[(int64_t)s * 2 * ms * 128 + r * 128 + kp] = hi;
+    krT[(int64_t)s * 2 * ms * 128 + ms * 128 + r * 128 + kp] = tf32_rna((float)(v - (double)hi));
+  }
+  // w = C P_Ne (row vector times matrix), and fp32 copies
+  const double* PN = Ps0 + (int64_t)Neff[s] * mm;
+  for (int j = tid; j < ms; j += 256) {
+    double acc = 0.0;
+    for (int k = 0; k < ms; ++k) acc = fma(C[(int64_t)s * ms + k], PN[(int64_t)k * ms + j], acc);
+    w64[(int64_t)s * ms + j] = acc;
+    w32[(int64_t)s * ms + j] = (float)acc;
+    c32[(int64_t)s * ms + j] = (float)C[(int64_t)s * ms + j];
+  }
+  if (tid == 0) d32[s] = D ? (float)D[s] : 0.f;
+}
+
+int launch_bank_derived(const double* p64, int slots, const double* Bbar, const double* C, const double* D,
+                        const int* Neff, const int* Kc, double* Kr64, float* krT, double* w64, float* w32,
+                        float* c32, float* d32, int n, int ms, cudaStream_t st) {
+  const size_t smem = (size_t)(ms * (ms + 1) + ms * 129) * sizeof(double);
+  if (cudaFuncSetAttribute(bank_derived_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return CASC_ERR_CUDA;
+  bank_derived_kernel<<<n, 256, smem, st>>>(p64, slots, Bbar, C, D, Neff, Kc, Kr64, krT, w64, w32, c32, d32, ms);
+  CASC_LAUNCHED();
+  return CASC_OK;
+}
+
 // ============================================================================ launchers
 template <int MS>
 static int head_launch(const BankHeadArg& a, cudaStream_t st) {

@@ -50,6 +50,9 @@ int launch_bank_stage_ws(int m, const BankStageArg& a, cudaStream_t st);
 int launch_bank_stage_rp(int m, const BankStageArg& a, cudaStream_t st);
 int launch_bank_tail(int m, const BankTailArg& a, cudaStream_t st);
 int launch_kr_init(const double* Bbar, double* Kr, int n, int ms, cudaStream_t st);
+int launch_bank_derived(const double* p64, int slots, const double* Bbar, const double* C, const double* D,
+                        const int* Neff, const int* Kc, double* Kr64, float* krT, double* w64, float* w32,
+                        float* c32, float* d32, int n, int ms, cudaStream_t st);
 int launch_kr_split(const double* Kr, const int* Kc, float* krT, int n, int ms, cudaStream_t st);
 
 }  // namespace casc

@@ -259,6 +259,11 @@ int engine_powers(int n, int m, const int* N_host, int N_max, const double* Abar
   PackLayout P = pack_layout(pack, n, m, N_max, mode);
   const int64_t mm = (int64_t)m * m, sys = (N_max + 1) * mm;
   CASC_TRY(cudaMemcpyAsync(P.hdr, N_host, sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  if (m <= 64) {                                  // banks: all squarings + packing in one launch
+    int maxN = *std::max_element(N_host, N_host + n);
+    ProfScope ps(st, K_POWERS, 16.0 * n * mm * (maxN + 1), 2.0 * n * (double)mm * m * maxN);
+    return launch_powers_small(P, Abar, n, N_max, m, st);
+  }
   // P_0 = Abar (strided copy into slot 0 of every system)
   CASC_TRY(cudaMemcpy2DAsync(P.p64, sys * sizeof(double), Abar, mm * sizeof(double),
                              mm * sizeof(double), n, cudaMemcpyDeviceToDevice, st));

@@ -104,6 +104,64 @@ int launch_pack(const PackLayout& P, int n_sys, int N_max, int m, cudaStream_t s
   return CASC_OK;
 }
 
+// a1 for small systems (m <= 64, the HiPPO banks): one CTA per system squares P_k in shared
+// memory N_s times (float64 FMA in ascending k, the same order as dgemm_batched_kernel, so the
+// powers are bitwise those of the per-level launches) and writes each P_k and its storage image
+// as soon as it is formed -- one launch instead of N_max + 1.
+__global__ void __launch_bounds__(256) powers_small_kernel(const double* Abar, const int* hdr, double* p64,
+                                                           float* f32, __nv_bfloat16* b16, int N_max, int m) {
+  constexpr int LD = 65;
+  __shared__ double S[64 * LD];                          // P_k; P_{k+1} overwrites it in place
+  const int s = blockIdx.x, tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int64_t mm = (int64_t)m * m;
+  const int Ns = hdr[s];
+  const double* A0 = Abar + (int64_t)s * mm;
+  for (int e = tid; e < m * m; e += 256) S[(e / m) * LD + e % m] = A0[e];
+  __syncthreads();
+  for (int k = 0; k <= Ns; ++k) {
+    const double* Pk = S;
+    const int64_t slot = (int64_t)s * (N_max + 1) + k;
+    for (int e = tid; e < m * m; e += 256) {             // P_k out: float64 + storage image
+      const double p = Pk[(e / m) * LD + e % m];
+      p64[slot * mm + e] = p;
+      if (f32) {
+        const float hi = tf32_rna((float)p);
+        f32[slot * 2 * mm + e] = hi;
+        f32[slot * 2 * mm + mm + e] = tf32_rna((float)(p - (double)hi));
+      } else {
+        b16[slot * mm + e] = __float2bfloat16_rn((float)p);
+      }
+    }
+    if (k == Ns) break;
+    double acc[4][4] = {};                              // P_{k+1} = P_k P_k
+    for (int kk = 0; kk < m; ++kk) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = (ty * 4 + i < m) ? Pk[(ty * 4 + i) * LD + kk] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = (tx * 4 + j < m) ? Pk[kk * LD + tx * 4 + j] : 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();                                    // all reads of P_k done
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (ty * 4 + i < m && tx * 4 + j < m) S[(ty * 4 + i) * LD + tx * 4 + j] = acc[i][j];
+    __syncthreads();
+  }
+}
+
+int launch_powers_small(const PackLayout& P, const double* Abar, int n_sys, int N_max, int m, cudaStream_t st) {
+  if (m > 64) return CASC_ERR_UNSUPPORTED;
+  powers_small_kernel<<<n_sys, 256, 0, st>>>(Abar, P.hdr, P.p64, P.f32, P.b16, N_max, m);
+  CASC_LAUNCHED();
+  return CASC_OK;
+}
+
 __global__ void f64_to_f32_kernel(const double* src, float* dst, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)

@@ -257,8 +257,8 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // =========================================================== MMA issuer
-    if (lane == 0) {
+    // =========================================================== MMA issuer (whole warp, elected lane issues)
+    {
       const uint32_t idesc = make_idesc(TF32 ? FMT_TF32 : FMT_BF16, BM, BN);
       int s = 0, cur_sys = -1;
       uint32_t ph = 0, wph = 0;
@@ -289,27 +289,26 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
             const uint32_t a0 = smem_u32(stA(s));
             const uint32_t w0 = WRES ? smem_u32(sWres + ci * C::NW * C::W_BYTES) : smem_u32(stW(s));
             const uint32_t al0 = WRES ? smem_u32(sAlo + (j & 1) * C::A_BYTES) : smem_u32(stAlo(s));
+            const uint64_t ad0 = make_sdesc(a0, 16, 1024, LAYOUT_SW128), wd0 = make_sdesc(w0, 16, 1024, LAYOUT_SW128);
+            const uint64_t ald0 = make_sdesc(al0, 16, 1024, LAYOUT_SW128), wld0 = sdesc_add(wd0, C::W_BYTES);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {               // 4 x 32 B = one 128-B row per chunk
-              const uint64_t ad = make_sdesc(a0 + k * 32, 16, 1024, LAYOUT_SW128);
-              const uint64_t wd = make_sdesc(w0 + k * 32, 16, 1024, LAYOUT_SW128);
+              const uint64_t ad = sdesc_add(ad0, k * 32), wd = sdesc_add(wd0, k * 32);
               if (TF32) {
-                const uint64_t ald = make_sdesc(al0 + k * 32, 16, 1024, LAYOUT_SW128);
-                const uint64_t wld = make_sdesc(w0 + C::W_BYTES + k * 32, 16, 1024, LAYOUT_SW128);
-                mma_tf32(d, ad, wd, idesc, first ? 0u : 1u);      // main: hi.hi
-                mma_tf32(dc, ald, wd, idesc, first ? 0u : 1u);    // corr: lo.hi + hi.lo
-                mma_tf32(dc, ad, wld, idesc, 1u);
+                mma_tf32_w(d, ad, wd, idesc, first ? 0u : 1u);                      // main: hi.hi
+                mma_tf32_w(dc, sdesc_add(ald0, k * 32), wd, idesc, first ? 0u : 1u); // corr: lo.hi + hi.lo
+                mma_tf32_w(dc, ad, sdesc_add(wld0, k * 32), idesc, 1u);
               } else {
-                mma_f16(d, ad, wd, idesc, first ? 0u : 1u);
+                mma_f16_w(d, ad, wd, idesc, first ? 0u : 1u);
               }
               first = false;
             }
-            mma_commit(&empty[s]);
-            if (WRES && TF32) mma_commit(&alo_free[j & 1]);
+            mma_commit_w(&empty[s]);
+            if (WRES && TF32) mma_commit_w(&alo_free[j & 1]);
             if (++s == STAGES) { s = 0; ph ^= 1; }
           }
         }
-        mma_commit(&tfull[acc]);
+        mma_commit_w(&tfull[acc]);
       }
     }
   } else if (warp >= 6) {

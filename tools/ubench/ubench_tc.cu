@@ -85,7 +85,8 @@ __global__ void k_mma_w(int mode, int N, int iters, unsigned long long* out, int
   if (threadIdx.x < 32) tmem_dealloc<512>(tb);
 }
 
-// nw warps issue concurrently, warp w into accumulator columns [w*64, w*64+N)
+// nw warps issue concurrently, warp w into accumulator columns [w*128, w*128+N); TS: A in TMEM
+template <bool TS>
 __global__ void k_mma_mw(int N, int iters, unsigned long long* out, int nw) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint32_t tb;
@@ -104,7 +105,10 @@ __global__ void k_mma_mw(int N, int iters, unsigned long long* out, int nw) {
     const uint32_t dd = tb + (uint32_t)(warp * 128);
     for (int i = 0; i < iters; ++i) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) mma_ss_w(dd, ad0 + 2 * k, bd0 + 2 * k, idesc, 1);
+      for (int k = 0; k < 4; ++k) {
+        if (!TS) mma_ss_w(dd, ad0 + 2 * k, bd0 + 2 * k, idesc, 1);
+        else mma_ts_w(dd, tb + 384 + k * 8, bd0 + 2 * k, idesc, 1);
+      }
     }
     if (threadIdx.x % 32 == 0) mma_commit(&bar[warp]);
     __syncwarp();
@@ -267,15 +271,18 @@ int main() {
         printf("warp-issued mma tf32 %s M=128 N=%d nacc=%d: %.1f cyc/mma (floor %d) %s\n", mode ? "TS" : "SS", N, nacc,
                (double)h / (4.0 * it), 128 * N / 256, cudaGetErrorString(e));
       }
-  cudaFuncSetAttribute(k_mma_mw, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  for (int N : {64, 128})
-    for (int nw : {1, 2, 3, 4}) {
-      const int it = 2048;
-      k_mma_mw<<<1, 128, 64 * 1024>>>(N, it, d, nw);
-      cudaError_t e = cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-      printf("multi-issuer mma tf32 SS N=%d issuers=%d: %.1f cyc per mma (all issuers) %s\n", N, nw,
-             (double)h / (4.0 * it * nw), cudaGetErrorString(e));
-    }
+  cudaFuncSetAttribute(k_mma_mw<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  cudaFuncSetAttribute(k_mma_mw<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  for (int ts = 0; ts < 2; ++ts)
+    for (int N : {64, 128})
+      for (int nw : {1, 2}) {
+        const int it = 2048;
+        if (ts) k_mma_mw<true><<<1, 128, 64 * 1024>>>(N, it, d, nw);
+        else k_mma_mw<false><<<1, 128, 64 * 1024>>>(N, it, d, nw);
+        cudaError_t e = cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+        printf("mma tf32 %s N=%d issuers=%d: %.1f cyc per mma (all issuers) %s\n", ts ? "TS" : "SS", N, nw,
+               (double)h / (4.0 * it * nw), cudaGetErrorString(e));
+      }
   for (int nw : {1, 4, 8}) {
     const int it = 4096;
     k_tmem_ld64<<<1, 256>>>(nw, it, d, sink);
