@@ -69,6 +69,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+      ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+        "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),
+        "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -92,8 +103,13 @@ struct Cfg {
   static constexpr uint32_t A_BYTES = BM * 128;           // 16 KB
   static constexpr uint32_t W_BYTES = BN * 128;           // one of hi / lo
   static constexpr int NW = TF32 ? 2 : 1;                 // weight tiles per chunk
+  // TSA: 3xTF32 with the A operand (tf32 hi | lo) in TMEM, written by the transform warps
+  // (N = 64 tiles: the two accumulator buffers leave room for two A units of 64 columns).
+  // An SS tf32 MMA at N = 64 reads 6 KB of shared memory (48 cycles at 128 B/cycle vs the
+  // 32-cycle floor); with A in TMEM only W is read from shared memory.
+  static constexpr bool TSA = TF32 && BN == 64 && !WRES;
   static constexpr uint32_t STAGE_BYTES =                 // ring slot: A[, A lo][, W hi[, W lo]]
-      WRES ? A_BYTES : A_BYTES * (TF32 ? 2 : 1) + W_BYTES * NW;
+      WRES ? A_BYTES : A_BYTES * ((TF32 && !TSA) ? 2 : 1) + W_BYTES * NW;
   static constexpr uint32_t TMA_BYTES = WRES ? A_BYTES : A_BYTES + W_BYTES * NW;
   static constexpr uint32_t WBUF = WRES ? (uint32_t)WCH * NW * W_BYTES : 0;
   static constexpr int ALO = (WRES && TF32) ? 2 : 0;      // separate lo slots (weight-resident)
@@ -153,14 +169,17 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
   // accumulator (measured ~2e-8 per MMA); splitting keeps the main chain at K/8 MMAs and the
   // corr chain's error is 2^-11 smaller. The epilogue sums main + corr with round-to-nearest.
   constexpr int ACOLS = TF32 ? 2 * BN : BN;
-  static_assert(2 * ACOLS <= 512, "TMEM holds 512 columns");
-  constexpr int TCOLS = 2 * ACOLS < 32 ? 32 : 2 * ACOLS;
+  constexpr bool TSA = C::TSA;
+  constexpr uint32_t AU0 = 2 * ACOLS;                        // TSA: two A units (hi | lo) of 64 columns
+  constexpr int TUSED = 2 * ACOLS + (TSA ? 128 : 0);
+  static_assert(TUSED <= 512, "TMEM holds 512 columns");
+  constexpr int TCOLS = TUSED <= 32 ? 32 : TUSED <= 64 ? 64 : TUSED <= 128 ? 128 : TUSED <= 256 ? 256 : 512;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared state space (STS/LDS, not generic ST/LD)
   uint8_t* sWres = smem + STAGES * C::STAGE_BYTES;           // [WCH][hi, lo] (weight-resident)
   uint8_t* sAlo = sWres + C::WBUF;                           // [ALO] (weight-resident 3xTF32)
   uint8_t* sR = sAlo + C::ALO * C::A_BYTES;                  // [RS][R_BYTES]
-  constexpr int NLO = WRES ? 2 : STAGES;                     // lo_ready barriers
+  constexpr int NLO = (WRES || TSA) ? 2 : STAGES;            // lo_ready barriers
   __shared__ uint64_t full[STAGES], empty[STAGES], lo_ready[NLO], alo_free[2], tfull[2], tempty[2],
       rfull[RS], rempty[RS], w_full;
   __shared__ uint32_t tmem_base;
@@ -280,12 +299,28 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
           const int nk = a.K[src] / BK;
           for (int kc = 0; kc < nk; ++kc, ++ci, ++j) {
             if (TF32) {
-              if (WRES) mbar_wait(&lo_ready[j & 1], (uint32_t)((j >> 1) & 1));
+              if (WRES || TSA) mbar_wait(&lo_ready[j & 1], (uint32_t)((j >> 1) & 1));
               else mbar_wait(&lo_ready[s], ph);
             } else {
               mbar_wait(&full[s], ph);
             }
             tc_fence_after();
+            if constexpr (TSA) {                        // A from TMEM unit (j & 1): hi | lo
+              const uint32_t ah = tbase + AU0 + (uint32_t)(j & 1) * 64, al = ah + 32;
+              const uint64_t wd0 = make_sdesc(smem_u32(stW(s)), 16, 1024, LAYOUT_SW128);
+              const uint64_t wld0 = sdesc_add(wd0, C::W_BYTES);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                mma_tf32_ts_w(d, ah + k * 8, sdesc_add(wd0, k * 32), idesc, first ? 0u : 1u);   // main: hi.hi
+                mma_tf32_ts_w(dc, al + k * 8, sdesc_add(wd0, k * 32), idesc, first ? 0u : 1u);  // corr: lo.hi
+                mma_tf32_ts_w(dc, ah + k * 8, sdesc_add(wld0, k * 32), idesc, 1u);             //     + hi.lo
+                first = false;
+              }
+              mma_commit_w(&empty[s]);
+              mma_commit_w(&alo_free[j & 1]);
+              if (++s == STAGES) { s = 0; ph ^= 1; }
+              continue;
+            }
             const uint32_t a0 = smem_u32(stA(s));
             const uint32_t w0 = WRES ? smem_u32(sWres + ci * C::NW * C::W_BYTES) : smem_u32(stW(s));
             const uint32_t al0 = WRES ? smem_u32(sAlo + (j & 1) * C::A_BYTES) : smem_u32(stAlo(s));
@@ -323,6 +358,30 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
           const int nk = a.K[src] / BK;
           for (int kc = 0; kc < nk; ++kc, ++j) {
             mbar_wait(&full[s], ph);
+            if constexpr (TSA) {                        // this thread's row -> tf32 hi | lo -> TMEM
+              const int row = (warp & 3) * 32 + lane;
+              const uint8_t* rr = stA(s) + row * 128;   // SW128: chunk c at (c ^ (row % 8)) * 16
+              uint32_t hv[32], lv[32];
+#pragma unroll
+              for (int cc = 0; cc < 8; ++cc) {
+                const float4 v = *reinterpret_cast<const float4*>(rr + ((cc ^ (row & 7)) * 16));
+                const float4 h = tf32_hi4(v), l = tf32_lo4(v, h);
+                hv[4 * cc] = __float_as_uint(h.x); hv[4 * cc + 1] = __float_as_uint(h.y);
+                hv[4 * cc + 2] = __float_as_uint(h.z); hv[4 * cc + 3] = __float_as_uint(h.w);
+                lv[4 * cc] = __float_as_uint(l.x); lv[4 * cc + 1] = __float_as_uint(l.y);
+                lv[4 * cc + 2] = __float_as_uint(l.z); lv[4 * cc + 3] = __float_as_uint(l.w);
+              }
+              mbar_wait(&alo_free[j & 1], (uint32_t)(((j >> 1) & 1) ^ 1));
+              tc_fence_after();
+              const uint32_t ta = tbase + ((uint32_t)((warp & 3) * 32) << 16) + AU0 + (uint32_t)(j & 1) * 64;
+              tmem_st32(ta, hv);
+              tmem_st32(ta + 32, lv);
+              tmem_wait_st();
+              tc_fence_before();
+              mbar_arrive(&lo_ready[j & 1]);
+              if (++s == STAGES) { s = 0; ph ^= 1; }
+              continue;
+            }
             if (WRES && j >= 2) mbar_wait(&alo_free[j & 1], (uint32_t)(((j - 2) >> 1) & 1));
             float4* hi = reinterpret_cast<float4*>(stA(s));
             float4* out = reinterpret_cast<float4*>(WRES ? sAlo + (j & 1) * C::A_BYTES : stAlo(s));
