@@ -61,6 +61,7 @@ struct BankWs {
   float *w32, *c32, *d32;
   double* Q64;    // [n][m][m] scratch for one pair weight
   float* Q32;     // [n][qslots][2][m][m] pair weights, tf32 hi/lo planes
+  float* ab;      // [n][batch][L][2] fused-output parts (C v, C P_Ne v) of the last state
   void *Va, *Vb;
   size_t bytes;
 };
@@ -77,6 +78,7 @@ static BankWs carve_bank(void* ws, int n, int m, int64_t L, int batch, int qslot
   w.d32 = c.take<float>((size_t)n);
   w.Q64 = c.take<double>(qslots ? (size_t)n * m * m : 0);
   w.Q32 = c.take<float>((size_t)n * qslots * 2 * m * m);
+  w.ab = c.take<float>(m == 64 ? (size_t)n * batch * (size_t)L * 2 : 0);
   const size_t vbytes = (size_t)n * batch * (size_t)L * m * sizeof(float);
   w.Va = c.take<char>(vbytes);
   w.Vb = c.take<char>(vbytes);
@@ -347,6 +349,13 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
                      const double* Bbar, const double* C, const double* D, const float* u, float* y, void* ws,
                      size_t ws_bytes, cudaStream_t st) {
   const char variant = stage_variant(m);
+  // output fusion: the producer of each channel's last state writes (C v, C P_Ne v) instead of
+  // v (R24); taken with the m = 64 TMA stage GEMM and warp-specialized head
+  static const bool ab_off = [] {
+    const char* e = getenv("CASC_BANK_AB");
+    return e && e[0] == '0';
+  }();
+  const bool use_ab = m == 64 && variant == 's' && !ab_off && !(getenv("CASC_BANK_HEAD") && getenv("CASC_BANK_HEAD")[0] == 'o');
   std::vector<int> meta((size_t)4 * n);
   int *Neff = meta.data(), *Kc = Neff + n, *par = Neff + 2 * n, *order = Neff + 3 * n;
   int maxNe = 0;
@@ -403,6 +412,7 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     BankHeadArg a{};
     a.u = static_cast<const float*>(u); a.krT = w.krT; a.V = static_cast<float*>(w.Va);
     a.sys_list = dorder; a.n_list = n; a.L = L; a.batch = batch;
+    if (use_ab) { a.Neff = dNeff; a.Kc = dKc; a.cvec = w.c32; a.wvec = w.w32; a.ab = w.ab; }
     a.tiles_per_cta = pick_group(ntiles, (int64_t)n * batch, 16);
     ProfScope ps(st, K_BANK_HEAD, (double)n * batch * L * (1 + m) * 4.0,
                  (double)n * batch * L * 2.0 * m * 128);
@@ -436,6 +446,11 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       g.sys_list = dorder; g.n_list = cnt; g.n_sys_total = n;
       g.t_first = pass == 0 ? 0 : (int)(((int64_t)1 << (k - 1)) / 128);
       g.w_resident = resident_weights();
+      if (use_ab) {                                 // channels whose last streaming stage this is
+        g.ab_neff = dNeff; g.ab_level = k + 1; g.ab_c = w.c32; g.ab_w = w.w32; g.ab = w.ab;
+        // their (C v, C P_Ne v) parts are needed on every row: no skipped leading tiles
+        if (count_ge(k + 1) > count_ge(k + 2)) g.t_first = 0;
+      }
       ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt * batch * L * m * 4.0, 2.0 * cnt * batch * L * (double)mm);
       if ((rc = launch_mimo_gemm(g, true, st))) return rc;
       continue;
@@ -482,6 +497,13 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     }
   }
   // ---- tail: stage Ne + y = C v + D u
+  if (use_ab) {                                     // from the fused (C v, C P_Ne v) parts
+    BankAbTailArg a{};
+    a.ab = w.ab; a.u = static_cast<const float*>(u); a.y = static_cast<float*>(y);
+    a.d = w.d32; a.Neff = dNeff; a.n_ch = n; a.L = L; a.batch = batch;
+    ProfScope ps(st, K_BANK_TAIL, (double)n * batch * L * (8 + 8 + 4 + 4), (double)n * batch * L * 3);
+    return launch_bank_ab_tail(a, st);
+  }
   {
     BankTailArg a{};
     a.Va = static_cast<const float*>(w.Va); a.Vb = static_cast<const float*>(w.Vb); a.parity = dpar;

@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
     // ---------------------------------------------------------------- epilogue (warps 2..5)
     const int q = warp & 3, row = q * 32 + lane;
     const bool leader = (warp == 2 && lane == 0);
+    const bool to_ab = a.ab != nullptr && a.Neff[c] == a.Kc[c];   // the cascade ends at the head
     for (int i = 0; i < nt; ++i) {
       const int slot = i & 1;
       mbar_wait(&tfull[slot], (uint32_t)((i >> 1) & 1));
@@ -153,6 +154,17 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
       for (int c0 = 0; c0 < MS; c0 += 16) tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + slot * MS + c0, v + c0);
       tc_fence_before();
       mbar_arrive(&tempty[slot]);
+      if (to_ab) {                                // y parts c . v, w . v instead of storing v
+        float pa = 0.f, pb = 0.f;
+#pragma unroll
+        for (int n = 0; n < MS; ++n) {
+          pa = fmaf(__ldg(a.cvec + (int64_t)c * MS + n), v[n], pa);
+          pb = fmaf(__ldg(a.wvec + (int64_t)c * MS + n), v[n], pb);
+        }
+        const int64_t l = (tile_begin + i) * TM + row;
+        if (l < a.L) *reinterpret_cast<float2*>(a.ab + ((int64_t)seq * a.L + l) * 2) = make_float2(pa, pb);
+        continue;
+      }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {               // two SW128 halves of 32 fp32 columns
         if (leader) bulk_wait_read0();            // the previous store has read the staging

@@ -309,6 +309,29 @@ int launch_bank_derived(const double* p64, int slots, const double* Bbar, const 
   return CASC_OK;
 }
 
+// ============================================================================ fused-output tail
+// y_l = a_l + b_{l - 2^Ne} + d u_l with (a, b) = (C v, C P_Ne v) of the last state, written by
+// the stage (or head) that produced v^(Ne): stage Ne and y = C v + D u in
+// the regrouped form of R21/R24, without storing or re-reading v^(Ne).
+__global__ void bank_ab_tail_kernel(BankAbTailArg a) {
+  const int64_t n = (int64_t)a.n_ch * a.batch * a.L;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t seq = e / a.L, l = e % a.L;
+    const int c = (int)(seq / a.batch);
+    const int64_t sh = (int64_t)1 << a.Neff[c];
+    const float2 ab = *reinterpret_cast<const float2*>(a.ab + e * 2);
+    const float b = l >= sh ? a.ab[(e - sh) * 2 + 1] : 0.f;
+    a.y[e] = fmaf(a.d[c], a.u[e], ab.x + b);
+  }
+}
+int launch_bank_ab_tail(const BankAbTailArg& a, cudaStream_t st) {
+  const int64_t n = (int64_t)a.n_ch * a.batch * a.L;
+  if (n <= 0) return CASC_OK;
+  bank_ab_tail_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 148 * 16), 256, 0, st>>>(a);
+  CASC_LAUNCHED();
+  return CASC_OK;
+}
+
 // ============================================================================ launchers
 template <int MS>
 static int head_launch(const BankHeadArg& a, cudaStream_t st) {

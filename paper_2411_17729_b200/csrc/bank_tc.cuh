@@ -10,6 +10,14 @@ struct BankHeadArg {
   float* V;                // [n_ch][batch][L][MS]
   const int* sys_list; int n_list;
   int64_t L; int batch; int tiles_per_cta;
+  // output fusion (ws head): channels with Neff == Kc end at the head; their epilogue writes
+  // ab[seq][l] = (c . v_l, w . v_l) instead of v (null: always write v)
+  const int* Neff; const int* Kc; const float* cvec; const float* wvec; float* ab;
+};
+struct BankAbTailArg {     // y_l = a_l + b_{l - 2^Ne} + d u_l  (b = 0 before l = 2^Ne)
+  const float* ab; const float* u; float* y;   // ab [n_ch][batch][L][2]; u, y [n_ch][batch][L]
+  const float* d; const int* Neff;
+  int n_ch; int64_t L; int batch;
 };
 struct BankStageArg {
   const float* Vs; float* Vd;   // [n_ch][batch][L][MS]
@@ -49,6 +57,7 @@ int launch_bank_head_ws(int m, const BankHeadArg& a, int64_t n_seq_total, cudaSt
 int launch_bank_stage_ws(int m, const BankStageArg& a, cudaStream_t st);
 int launch_bank_stage_rp(int m, const BankStageArg& a, cudaStream_t st);
 int launch_bank_tail(int m, const BankTailArg& a, cudaStream_t st);
+int launch_bank_ab_tail(const BankAbTailArg& a, cudaStream_t st);
 int launch_kr_init(const double* Bbar, double* Kr, int n, int ms, cudaStream_t st);
 int launch_bank_derived(const double* p64, int slots, const double* Bbar, const double* C, const double* D,
                         const int* Neff, const int* Kc, double* Kr64, float* krT, double* w64, float* w32,

@@ -409,6 +409,8 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
     for (Walk<C::GT> w(n_tiles); w.valid(); w.next(), ++t_local) {
       const TileCoord tc = decode(w.tile(), a, n_nblk, nt_eff);
       const int acc = (int)(t_local & 1);
+      const bool to_ab = TF32 && a.ab != nullptr && a.ab_neff[tc.sys] == a.ab_level;
+      float pa = 0.f, pb = 0.f;
       mbar_wait(&tfull[acc], (uint32_t)((t_local >> 1) & 1));
       tc_fence_after();
       for (int j = 0; j < NCH; ++j) {
@@ -435,7 +437,15 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
               const float4 r = *reinterpret_cast<const float4*>(p);
               f[0] += r.x; f[1] += r.y; f[2] += r.z; f[3] += r.w;
             }
-            *reinterpret_cast<float4*>(p) = make_float4(f[0], f[1], f[2], f[3]);
+            if (to_ab) {                            // y parts: c . v and w . v of this row
+              const int col = tc.nb * BN + j * C::CW + c * 4;
+              const float4 cc4 = __ldg(reinterpret_cast<const float4*>(a.ab_c + (int64_t)tc.sys * 64 + col));
+              const float4 ww4 = __ldg(reinterpret_cast<const float4*>(a.ab_w + (int64_t)tc.sys * 64 + col));
+              pa = fmaf(cc4.x, f[0], pa); pa = fmaf(cc4.y, f[1], pa); pa = fmaf(cc4.z, f[2], pa); pa = fmaf(cc4.w, f[3], pa);
+              pb = fmaf(ww4.x, f[0], pb); pb = fmaf(ww4.y, f[1], pb); pb = fmaf(ww4.z, f[2], pb); pb = fmaf(ww4.w, f[3], pb);
+            } else {
+              *reinterpret_cast<float4*>(p) = make_float4(f[0], f[1], f[2], f[3]);
+            }
           } else {
             float f[8];
 #pragma unroll
@@ -455,16 +465,31 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
         }
         fence_async_smem();
         named_sync(1, 128);
-        if (leader) {
-          tma_store_3d(&maps.out, rbuf, tc.nb * BN + j * C::CW, a.out_row0 + tc.l0, tc.seq);
-          bulk_commit();
-          if (prev_rs >= 0) {                       // the previous chunk's store has read its slot
-            bulk_wait_read<1>();
-            mbar_arrive(&rempty[prev_rs]);
+        if (to_ab) {                                // nothing stored: the slot is free now
+          if (leader) {
+            if (prev_rs >= 0) {
+              bulk_wait_read<0>();
+              mbar_arrive(&rempty[prev_rs]);
+            }
+            mbar_arrive(&rempty[rs]);
           }
+          prev_rs = -1;
+        } else {
+          if (leader) {
+            tma_store_3d(&maps.out, rbuf, tc.nb * BN + j * C::CW, a.out_row0 + tc.l0, tc.seq);
+            bulk_commit();
+            if (prev_rs >= 0) {                     // the previous chunk's store has read its slot
+              bulk_wait_read<1>();
+              mbar_arrive(&rempty[prev_rs]);
+            }
+          }
+          prev_rs = rs;
         }
-        prev_rs = rs;
         if (++rs == RS) { rs = 0; rph ^= 1; }
+      }
+      if (to_ab) {
+        const int64_t l = (int64_t)tc.l0 + row;
+        if (l < a.L) *reinterpret_cast<float2*>(a.ab + ((int64_t)tc.seq * a.L + l) * 2) = make_float2(pa, pb);
       }
     }
     if (leader) bulk_wait<0>();
@@ -515,6 +540,8 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
   a.sys_list = g.sys_list;
   a.n_list = g.sys_list ? g.n_list : 1;
   a.t_first = g.t_first;
+  a.ab_neff = g.ab_neff; a.ab_level = g.ab_level; a.ab_c = g.ab_c; a.ab_w = g.ab_w; a.ab = g.ab;
+  if (g.ab && (!TF32 || g.n_out != 64)) return CASC_ERR_UNSUPPORTED;
   const int64_t nseq_total = (int64_t)(g.n_sys_total > 0 ? g.n_sys_total : 1) * g.batch;
   for (int s = 0; s < g.n_src; ++s) {
     if (g.src[s].K % C::BK) return CASC_ERR_UNSUPPORTED;

@@ -18,6 +18,10 @@ struct MimoArg {
   const int* sys_list; int n_list;   // systems processed (bank channels); null: one system
   int t_first;                       // first 128-step time tile processed in each sequence
   int a_row0[3], r_row0, out_row0;   // rows in front of local row 0 (sequence-shard halo)
+  // Bank output fusion (fp32 n_out = 64): for systems with ab_neff[sys] == ab_level this stage
+  // is their last streaming stage; instead of storing v^(Ne) the epilogue writes
+  // ab[seq][l] = (c . v_l, w . v_l) with c = C, w = C P_Ne (R24)
+  const int* ab_neff; int ab_level; const float* ab_c; const float* ab_w; float* ab;
 };
 struct MimoSrc {
   const void* A; const void* W; int K; int64_t shift;
@@ -34,6 +38,8 @@ struct MimoGemm {
   int t_first = 0;
   int64_t R_row0 = 0, out_row0 = 0;  // halo rows in front of local row 0 of R / out
   int w_resident = 0;                // keep the weights in shared memory across tiles
+  const int* ab_neff = nullptr; int ab_level = -1;    // see MimoArg
+  const float* ab_c = nullptr; const float* ab_w = nullptr; float* ab = nullptr;
 };
 
 bool mimo_tc_supported(int m, int p, int q);
