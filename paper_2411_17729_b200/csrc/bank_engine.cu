@@ -53,6 +53,16 @@ static int resident_weights() {
   return on;
 }
 
+// Weight-resident GEMM for stage pairs (three weight pairs per tile, 96 KB): on by default,
+// CASC_BANK_PAIR_WRES=0 reloads the weights per tile through the ring.
+static int pair_wres() {
+  static const int on = [] {
+    const char* e = getenv("CASC_BANK_PAIR_WRES");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  return on;
+}
+
 struct BankWs {
   int* meta;      // Neff | Kc | parity | order   (4 n ints)
   double* Kr64;   // [n][m][128]
@@ -355,7 +365,7 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     const char* e = getenv("CASC_BANK_AB");
     return e && e[0] == '0';
   }();
-  const bool use_ab = m == 64 && variant == 's' && !ab_off && !(getenv("CASC_BANK_HEAD") && getenv("CASC_BANK_HEAD")[0] == 'o');
+  const bool use_ab = m == 64 && (variant == 's' || variant == 't') && !ab_off && !(getenv("CASC_BANK_HEAD") && getenv("CASC_BANK_HEAD")[0] == 'o');
   std::vector<int> meta((size_t)4 * n);
   int *Neff = meta.data(), *Kc = Neff + n, *par = Neff + 2 * n, *order = Neff + 3 * n;
   int maxNe = 0;
@@ -482,7 +492,11 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       g.src[2].w_plane_off = 2 * pass; g.src[2].w_planes = (int64_t)n * qslots * 2;
       g.src[2].w_plane_stride = 2 * qslots;
       g.n_src = 3; g.R = Vs; g.out = Vd; g.n_out = m; g.L = L; g.batch = batch;
-      g.sys_list = dorder; g.n_list = cnt2; g.n_sys_total = n; g.t_first = t_first; g.w_resident = resident_weights();
+      g.sys_list = dorder; g.n_list = cnt2; g.n_sys_total = n; g.t_first = t_first; g.w_resident = pair_wres();
+      if (use_ab) {                                 // channels ending with this pair (Ne == k + 2)
+        g.ab_neff = dNeff; g.ab_level = k + 2; g.ab_c = w.c32; g.ab_w = w.w32; g.ab = w.ab;
+        if (count_ge(k + 2) > count_ge(k + 3)) g.t_first = 0;
+      }
       ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt2 * batch * L * m * 4.0, 4.0 * cnt2 * batch * L * (double)mm);
       if ((rc = launch_mimo_gemm(g, true, st))) return rc;
     }
@@ -492,6 +506,10 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       g.src[0].w_plane_off = 2 * k; g.src[0].w_planes = planes; g.src[0].w_plane_stride = 2 * (N_max + 1);
       g.n_src = 1; g.R = Vs; g.out = Vd; g.n_out = m; g.L = L; g.batch = batch;
       g.sys_list = dorder + cnt2; g.n_list = cnt1; g.n_sys_total = n; g.t_first = t_first; g.w_resident = resident_weights();
+      if (use_ab) {                                 // every channel here ends with stage k
+        g.ab_neff = dNeff; g.ab_level = k + 1; g.ab_c = w.c32; g.ab_w = w.w32; g.ab = w.ab;
+        g.t_first = 0;
+      }
       ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt1 * batch * L * m * 4.0, 2.0 * cnt1 * batch * L * (double)mm);
       if ((rc = launch_mimo_gemm(g, true, st))) return rc;
     }

@@ -76,10 +76,12 @@ inline PackLayout pack_layout(void* pack, int n_sys, int m, int N_max, int mode)
 __device__ __forceinline__ float to_f32(float x) { return x; }
 __device__ __forceinline__ float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }
 
+// Round to tf32 (10 explicit mantissa bits), nearest with ties away from zero: add half a tf32
+// ulp to the magnitude bits and clear the 13 dropped bits. Bitwise equal to cvt.rna.tf32.f32
+// for every finite input (checked exhaustively on B200, tools/ubench/cvt_check.cu) but on the
+// integer pipe: cvt runs on the XU pipe, which bounded the split warps of the 3xTF32 kernels.
 __device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 // 3xTF32 split of a streaming fp32 operand (R17): hi = rna_tf32(x), lo = rna_tf32(x - hi)
 // (x - hi is exact in fp32), so x = hi + lo to ~2^-23 relative with an unbiased rounding.

@@ -81,6 +81,8 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// fp32 pair -> bf16x2, round to nearest even (F2FP). An integer-pipe version (bitwise equal,
+// tools/ubench/cvt_check.cu) was measured slower here: 2.19 vs 2.09 ms per E4 stage launch.
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -107,12 +109,12 @@ struct Cfg {
   // (N = 64 tiles: the two accumulator buffers leave room for two A units of 64 columns).
   // An SS tf32 MMA at N = 64 reads 6 KB of shared memory (48 cycles at 128 B/cycle vs the
   // 32-cycle floor); with A in TMEM only W is read from shared memory.
-  static constexpr bool TSA = TF32 && BN == 64 && !WRES;
+  static constexpr bool TSA = TF32 && BN == 64;
   static constexpr uint32_t STAGE_BYTES =                 // ring slot: A[, A lo][, W hi[, W lo]]
       WRES ? A_BYTES : A_BYTES * ((TF32 && !TSA) ? 2 : 1) + W_BYTES * NW;
   static constexpr uint32_t TMA_BYTES = WRES ? A_BYTES : A_BYTES + W_BYTES * NW;
   static constexpr uint32_t WBUF = WRES ? (uint32_t)WCH * NW * W_BYTES : 0;
-  static constexpr int ALO = (WRES && TF32) ? 2 : 0;      // separate lo slots (weight-resident)
+  static constexpr int ALO = (WRES && TF32 && !TSA) ? 2 : 0;   // separate lo slots (weight-resident SS)
   static constexpr int RS = RSO ? RSO : ((TF32 && BN == 64) ? 4 : 2);   // residual / staging chunks
   static constexpr uint32_t R_BYTES = BM * 128;           // 16 KB
   static constexpr int STAGES_FIT =
@@ -307,7 +309,8 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
             tc_fence_after();
             if constexpr (TSA) {                        // A from TMEM unit (j & 1): hi | lo
               const uint32_t ah = tbase + AU0 + (uint32_t)(j & 1) * 64, al = ah + 32;
-              const uint64_t wd0 = make_sdesc(smem_u32(stW(s)), 16, 1024, LAYOUT_SW128);
+              const uint64_t wd0 = make_sdesc(WRES ? smem_u32(sWres + ci * C::NW * C::W_BYTES) : smem_u32(stW(s)), 16, 1024,
+                                              LAYOUT_SW128);
               const uint64_t wld0 = sdesc_add(wd0, C::W_BYTES);
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
