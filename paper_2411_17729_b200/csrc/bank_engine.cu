@@ -8,6 +8,8 @@
 //             = (I + P_{k+1} z^-2s)(I + P_k z^-s) v, the product of two adjacent factors of
 //             PAPER.md Eq. 5; a last odd stage runs alone.                 Va <-> Vb
 //   tail    : stage Ne + y = C v + D u                                 -> y
+//             (m = 64: the producer of each channel's last state writes (C v, C P_Ne v) per row
+//             instead of v, and the tail adds the shifted parts and D u, R24)
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -25,19 +27,20 @@ namespace casc {
 
 static constexpr int kHeadK = 7;      // Krylov head covers stages 0..6 (128 lags)
 
-// stage-kernel variant (CASC_BANK_STAGE, for A/B measurements): 't' TMA-pipelined shifted GEMM
-// with stage pairing (default, m % 64 == 0), 'r' register-prefetch kernel, 'w' warp-specialized.
+// stage-kernel variant (CASC_BANK_STAGE, for A/B measurements), m % 64 == 0:
+//   't' (default) stage pairs (R23): one pass applies two adjacent factors of Eq. 5 through a
+//       3-source TMA GEMM with the A operands in TMEM and the three weight pairs resident in
+//       shared memory; half the HBM passes of 's' (E2: 3.97 vs 4.30 ms for the streaming stages)
+//   's' one stage per pass (HBM-bound, ~84% of the measured copy bandwidth)
+//   'r' register-prefetch kernel, 'w' warp-specialized CUDA-core variant (m = 16, 32 use 'r')
 static char stage_variant(int m) {
   static const char env = [] {
     const char* e = getenv("CASC_BANK_STAGE");
-    return e ? e[0] : 's';
+    return e ? e[0] : 't';
   }();
   if (env == 'w' || env == 'r') return env;
   if (m % 64 != 0) return 'r';
-  // 's' (default): TMA GEMM, one stage per pass (DRAM 64% of peak under ncu, L2 40%);
-  // 't': stage pairs (half the DRAM bytes, but a 3-slot ring cannot cover the six chunks a
-  // pair tile needs: latency-bound at DRAM 26% / L2 28%; kept for the next round's work)
-  return env == 't' ? 't' : 's';
+  return env == 's' ? 's' : 't';
 }
 
 static int pair_slots(int n_max) { return n_max > kHeadK ? (n_max - kHeadK + 1) / 2 : 0; }
@@ -497,7 +500,8 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
         g.ab_neff = dNeff; g.ab_level = k + 2; g.ab_c = w.c32; g.ab_w = w.w32; g.ab = w.ab;
         if (count_ge(k + 2) > count_ge(k + 3)) g.t_first = 0;
       }
-      ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt2 * batch * L * m * 4.0, 4.0 * cnt2 * batch * L * (double)mm);
+      // algorithmic (unfused streaming) bytes and flops of the two stages this pass applies
+      ProfScope ps(st, K_BANK_STAGE, 4.0 * cnt2 * batch * L * m * 4.0, 4.0 * cnt2 * batch * L * (double)mm);
       if ((rc = launch_mimo_gemm(g, true, st))) return rc;
     }
     if (cnt1 > 0) {

@@ -27,6 +27,7 @@
 //   warps 6-9   (3xTF32 only) hi/lo split of each landed A tile.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -123,7 +124,6 @@ struct Cfg {
   static constexpr int CW = 128 / ES;                     // epilogue chunk width (columns)
   static constexpr int R_WARP = TF32 ? 10 : 6;            // residual / staging producer warp
   static constexpr int THREADS = 32 * (R_WARP + 1);
-  static constexpr int GT = WRES ? 16 : 1;                // tiles per block of the tile walk
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + WBUF + ALO * A_BYTES + RS * R_BYTES;
 };
 
@@ -144,16 +144,17 @@ __device__ __forceinline__ TileCoord decode(int64_t tile, const MimoArg& a, int 
   return t;
 }
 
-// The CTA's walk over tiles: blocks of GT consecutive tiles dealt round-robin over the grid
-// (GT = 1: plain round-robin). Every role runs its own copy of the same walk.
-template <int GT>
+// The CTA's walk over tiles: blocks of gt consecutive tiles dealt round-robin over the grid
+// (gt = 1: plain round-robin; weight-resident mode: one contiguous range per CTA, so a CTA
+// reloads its resident weights only where its range crosses a system boundary). Every role
+// runs its own copy of the same walk.
 struct Walk {
-  int64_t blk, i, n_tiles;
-  __device__ Walk(int64_t n) : blk(blockIdx.x), i(0), n_tiles(n) {}
-  __device__ bool valid() const { return blk * GT + i < n_tiles; }
-  __device__ int64_t tile() const { return blk * GT + i; }
+  int64_t blk, i, n_tiles, gt;
+  __device__ Walk(int64_t n, int64_t g) : blk(blockIdx.x), i(0), n_tiles(n), gt(g) {}
+  __device__ bool valid() const { return blk * gt + i < n_tiles; }
+  __device__ int64_t tile() const { return blk * gt + i; }
   __device__ void next() {
-    if (++i == GT || blk * GT + i >= n_tiles) { i = 0; blk += gridDim.x; }
+    if (++i == gt || blk * gt + i >= n_tiles) { i = 0; blk += gridDim.x; }
   }
 };
 }  // namespace
@@ -191,6 +192,21 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
   auto stAlo = [&](int s) { return smem + s * C::STAGE_BYTES + C::A_BYTES + C::NW * C::W_BYTES; };
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // optional wait-cycle accounting (a.dbg != null, CASC_GEMM_DBG=1): slots per role, see launcher
+  unsigned long long dacc[24];
+#pragma unroll
+  for (int i = 0; i < 24; ++i) dacc[i] = 0;
+  const long long t_start = clock64();
+#define TWM(slot, stmt)                                      \
+  do {                                                       \
+    if (a.dbg) {                                             \
+      const long long t0_ = clock64();                       \
+      stmt;                                                  \
+      dacc[slot] += (unsigned long long)(clock64() - t0_);   \
+    } else {                                                 \
+      stmt;                                                  \
+    }                                                        \
+  } while (0)
   const int64_t mt_per_b = (a.L + BM - 1) / BM;
   const int64_t nt_eff = mt_per_b - a.t_first;
   const int n_nblk = (a.n_out + BN - 1) / BN;
@@ -221,11 +237,11 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
     if (lane == 0) {
       int s = 0, s_last = -1, cur_sys = -1;
       uint32_t ph = 0, ph_last = 0;
-      for (Walk<C::GT> w(n_tiles); w.valid(); w.next()) {
+      for (Walk w(n_tiles, a.gt); w.valid(); w.next()) {
         const TileCoord tc = decode(w.tile(), a, n_nblk, nt_eff);
         if (WRES && tc.sys != cur_sys) {
           // every MMA issued so far must be done with the resident weights (MMAs complete in order)
-          if (s_last >= 0) mbar_wait(&empty[s_last], ph_last);
+          if (s_last >= 0) TWM(0, mbar_wait(&empty[s_last], ph_last));
           uint32_t bytes = 0;
           for (int src = 0; src < a.n_src; ++src) bytes += (uint32_t)(a.K[src] / BK) * C::NW * C::W_BYTES;
           mbar_arrive_expect_tx(&w_full, bytes);
@@ -244,7 +260,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
           const int nk = a.K[src] / BK;
           const int plane = tc.sys * a.w_plane_stride[src] + a.w_plane_off[src];
           for (int kc = 0; kc < nk; ++kc) {
-            mbar_wait(&empty[s], ph ^ 1);
+            TWM(1, mbar_wait(&empty[s], ph ^ 1));
             mbar_arrive_expect_tx(&full[s], C::TMA_BYTES);
             tma_load_3d(stA(s), &maps.A[src], &full[s], kc * BK, a.a_row0[src] + tc.l0 - (int)a.shift[src], tc.seq);
             if (!WRES) {
@@ -263,10 +279,10 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
     if (lane == 0) {
       int rs = 0;
       uint32_t rph = 0;
-      for (Walk<C::GT> w(n_tiles); w.valid(); w.next()) {
+      for (Walk w(n_tiles, a.gt); w.valid(); w.next()) {
         const TileCoord tc = decode(w.tile(), a, n_nblk, nt_eff);
         for (int j = 0; j < NCH; ++j) {
-          mbar_wait(&rempty[rs], rph ^ 1);
+          TWM(20, mbar_wait(&rempty[rs], rph ^ 1));
           if (a.has_residual) {
             mbar_arrive_expect_tx(&rfull[rs], C::R_BYTES);
             tma_load_3d(sR + rs * C::R_BYTES, &maps.R, &rfull[rs], tc.nb * BN + j * C::CW, a.r_row0 + tc.l0, tc.seq);
@@ -284,12 +300,12 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
       int s = 0, cur_sys = -1;
       uint32_t ph = 0, wph = 0;
       int64_t t_local = 0, j = 0;                 // tiles / chunks consumed by this CTA
-      for (Walk<C::GT> w(n_tiles); w.valid(); w.next(), ++t_local) {
+      for (Walk w(n_tiles, a.gt); w.valid(); w.next(), ++t_local) {
         const TileCoord tc = decode(w.tile(), a, n_nblk, nt_eff);
         const int acc = (int)(t_local & 1);
-        mbar_wait(&tempty[acc], (uint32_t)((t_local >> 1) & 1) ^ 1);
+        TWM(4, mbar_wait(&tempty[acc], (uint32_t)((t_local >> 1) & 1) ^ 1));
         if (WRES && tc.sys != cur_sys) {
-          mbar_wait(&w_full, wph);
+          TWM(5, mbar_wait(&w_full, wph));
           wph ^= 1;
           cur_sys = tc.sys;
         }
@@ -301,10 +317,10 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
           const int nk = a.K[src] / BK;
           for (int kc = 0; kc < nk; ++kc, ++ci, ++j) {
             if (TF32) {
-              if (WRES || TSA) mbar_wait(&lo_ready[j & 1], (uint32_t)((j >> 1) & 1));
-              else mbar_wait(&lo_ready[s], ph);
+              if (WRES || TSA) TWM(6, mbar_wait(&lo_ready[j & 1], (uint32_t)((j >> 1) & 1)));
+              else TWM(6, mbar_wait(&lo_ready[s], ph));
             } else {
-              mbar_wait(&full[s], ph);
+              TWM(6, mbar_wait(&full[s], ph));
             }
             tc_fence_after();
             if constexpr (TSA) {                        // A from TMEM unit (j & 1): hi | lo
@@ -356,11 +372,11 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       int64_t j = 0;
-      for (Walk<C::GT> w(n_tiles); w.valid(); w.next()) {
+      for (Walk w(n_tiles, a.gt); w.valid(); w.next()) {
         for (int src = 0; src < a.n_src; ++src) {
           const int nk = a.K[src] / BK;
           for (int kc = 0; kc < nk; ++kc, ++j) {
-            mbar_wait(&full[s], ph);
+            TWM(8, mbar_wait(&full[s], ph));
             if constexpr (TSA) {                        // this thread's row -> tf32 hi | lo -> TMEM
               const int row = (warp & 3) * 32 + lane;
               const uint8_t* rr = stA(s) + row * 128;   // SW128: chunk c at (c ^ (row % 8)) * 16
@@ -374,7 +390,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
                 lv[4 * cc] = __float_as_uint(l.x); lv[4 * cc + 1] = __float_as_uint(l.y);
                 lv[4 * cc + 2] = __float_as_uint(l.z); lv[4 * cc + 3] = __float_as_uint(l.w);
               }
-              mbar_wait(&alo_free[j & 1], (uint32_t)(((j >> 1) & 1) ^ 1));
+              TWM(9, mbar_wait(&alo_free[j & 1], (uint32_t)(((j >> 1) & 1) ^ 1)));
               tc_fence_after();
               const uint32_t ta = tbase + ((uint32_t)((warp & 3) * 32) << 16) + AU0 + (uint32_t)(j & 1) * 64;
               tmem_st32(ta, hv);
@@ -409,12 +425,12 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
     int64_t t_local = 0;
     int rs = 0, prev_rs = -1;
     uint32_t rph = 0;
-    for (Walk<C::GT> w(n_tiles); w.valid(); w.next(), ++t_local) {
+    for (Walk w(n_tiles, a.gt); w.valid(); w.next(), ++t_local) {
       const TileCoord tc = decode(w.tile(), a, n_nblk, nt_eff);
       const int acc = (int)(t_local & 1);
       const bool to_ab = TF32 && a.ab != nullptr && a.ab_neff[tc.sys] == a.ab_level;
       float pa = 0.f, pb = 0.f;
-      mbar_wait(&tfull[acc], (uint32_t)((t_local >> 1) & 1));
+      TWM(12, mbar_wait(&tfull[acc], (uint32_t)((t_local >> 1) & 1)));
       tc_fence_after();
       for (int j = 0; j < NCH; ++j) {
         uint8_t* rbuf = sR + rs * C::R_BYTES;
@@ -427,7 +443,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) + __uint_as_float(v[32 + e]));
         }
-        mbar_wait(&rfull[rs], rph);
+        TWM(13, mbar_wait(&rfull[rs], rph));
         uint8_t* rrow = rbuf + row * 128;          // SW128: 16-B chunk c at ((c ^ (row % 8)) * 16)
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
@@ -497,6 +513,13 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
     }
     if (leader) bulk_wait<0>();
   }
+  if (a.dbg) {
+    if (lane == 0)
+      for (int i = 0; i < 24; ++i)
+        if (dacc[i]) atomicAdd(a.dbg + i, dacc[i]);
+    if (threadIdx.x == 0) atomicAdd(a.dbg + 23, (unsigned long long)(clock64() - t_start));
+  }
+#undef TWM
   __syncthreads();
   if (warp == 1) tmem_dealloc<TCOLS>(tbase);
 }
@@ -568,9 +591,32 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
     return CASC_ERR_CUDA;
   const int64_t tiles = (int64_t)a.n_list * g.batch * (ceil_div(g.L, BM) - g.t_first) * ceil_div(g.n_out, BN);
   if (tiles <= 0) return CASC_OK;
-  const int grid = (int)std::min<int64_t>(ceil_div(tiles, C::GT), 148);
+  // weight-resident: contiguous ranges; otherwise round-robin single tiles
+  a.gt = WCH > 0 ? ceil_div(tiles, std::min<int64_t>(tiles, 148)) : 1;
+  const int grid = (int)std::min<int64_t>(ceil_div(tiles, a.gt), 148);
+  static unsigned long long* dbg = nullptr;
+  const bool want_dbg = getenv("CASC_GEMM_DBG") != nullptr;
+  if (want_dbg) {
+    if (!dbg) CASC_TRY(cudaMalloc(&dbg, 24 * sizeof(unsigned long long)));
+    CASC_TRY(cudaMemsetAsync(dbg, 0, 24 * sizeof(unsigned long long), st));
+    a.dbg = dbg;
+  }
   mimo_gemm_kernel<BN, TF32, RSO, WCH><<<grid, C::THREADS, C::SMEM, st>>>(maps, a);
   CASC_LAUNCHED();
+  if (want_dbg) {                               // diagnostics only: synchronises and prints
+    unsigned long long h[24];
+    CASC_TRY(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CASC_TRY(cudaStreamSynchronize(st));
+    static const char* nm[24] = {"prod.drain", "prod.empty", "", "", "mma.tempty", "mma.w_full", "mma.a_ready", "",
+                                 "xf.full", "xf.alo_free", "", "", "epi.tfull", "epi.rfull", "", "", "", "", "", "",
+                                 "res.rempty", "", "", "total"};
+    const double tot = (double)h[23] / grid;
+    fprintf(stderr, "casc gemm dbg BN=%d tf32=%d wch=%d n_src=%d grid=%d tiles=%lld: cycles/CTA %.0f |", BN, (int)TF32, WCH,
+            g.n_src, grid, (long long)tiles, tot);
+    for (int i = 0; i < 23; ++i)
+      if (h[i]) fprintf(stderr, " %s %.0f%%", nm[i], 100.0 * h[i] / grid / tot / ((i >= 8 && i < 16) ? 4.0 : 1.0));
+    fprintf(stderr, "\n");
+  }
   return CASC_OK;
 }
 
@@ -595,7 +641,18 @@ int launch_mimo_gemm(const MimoGemm& g, bool tf32, cudaStream_t st) {
       return launch_cfg<64, true>(g, st);
     }
   } else {
-    if (g.n_out % 256 == 0) return launch_cfg<256, false>(g, st);
+    if (g.n_out % 256 == 0) {
+      // residual / staging chunks for the 256-wide bf16 tiles (CASC_GEMM_RS256 = 2 | 3 | 4):
+      // with 2 the epilogue waited on residual loads ~50% of the time (the slot doubles as the
+      // store staging); 4 chunks (ring 3 x 48 KB) measured 11% faster on the E4 stage GEMM
+      static const int rs = [] {
+        const char* e = getenv("CASC_GEMM_RS256");
+        return e ? atoi(e) : 4;
+      }();
+      if (rs == 3) return launch_cfg<256, false, 3>(g, st);
+      if (rs == 4) return launch_cfg<256, false, 4>(g, st);
+      return launch_cfg<256, false>(g, st);
+    }
     if (g.n_out % 128 == 0) return launch_cfg<128, false>(g, st);
     if (g.n_out % 64 == 0) return launch_cfg<64, false>(g, st);
   }

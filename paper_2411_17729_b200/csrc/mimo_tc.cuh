@@ -22,6 +22,8 @@ struct MimoArg {
   // is their last streaming stage; instead of storing v^(Ne) the epilogue writes
   // ab[seq][l] = (c . v_l, w . v_l) with c = C, w = C P_Ne (R24)
   const int* ab_neff; int ab_level; const float* ab_c; const float* ab_w; float* ab;
+  int64_t gt;                        // tiles per block of the CTA tile walk
+  unsigned long long* dbg;           // optional wait-cycle counters (CASC_GEMM_DBG=1)
 };
 struct MimoSrc {
   const void* A; const void* W; int K; int64_t shift;
