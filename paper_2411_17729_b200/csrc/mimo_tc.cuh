@@ -49,5 +49,8 @@ bool mimo_tc_supported(int m, int p, int q);
 bool map3d(CUtensorMap* m, const void* base, bool f32, int64_t d0, int64_t d1, int64_t d2, int rows);
 // tf32 = true: 3xTF32 (fp32 signals, weights as tf32 hi/lo planes); else bf16.
 int launch_mimo_gemm(const MimoGemm& g, bool tf32, cudaStream_t st);
+// bf16, n_out % 256 == 0, one system: 256 x 256 tiles on CTA pairs (mimo_tc2.cu)
+bool mimo_pair_ok(const MimoGemm& g, bool tf32);
+int launch_mimo_gemm_pair(const MimoGemm& g, cudaStream_t st);
 
 }  // namespace casc
