@@ -230,7 +230,11 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = tmem_base;
+  // A CTA that allocates all 512 columns owns the whole TMEM, so its base is column 0, lane 0.
+  // Using the constant keeps every TMEM operand address a compile-time value: loaded from shared
+  // memory it lives in per-thread registers and each MMA issue pays R2UR conversions.
+  if (TCOLS == 512 && tmem_base != 0) __trap();
+  const uint32_t tbase = TCOLS == 512 ? 0u : tmem_base;
 
   if (warp == 0) {
     // =========================================================== TMA producer
@@ -327,14 +331,9 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
               const uint32_t ah = tbase + AU0 + (uint32_t)(j & 1) * 64, al = ah + 32;
               const uint64_t wd0 = make_sdesc(WRES ? smem_u32(sWres + ci * C::NW * C::W_BYTES) : smem_u32(stW(s)), 16, 1024,
                                               LAYOUT_SW128);
-              const uint64_t wld0 = sdesc_add(wd0, C::W_BYTES);
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                mma_tf32_ts_w(d, ah + k * 8, sdesc_add(wd0, k * 32), idesc, first ? 0u : 1u);   // main: hi.hi
-                mma_tf32_ts_w(dc, al + k * 8, sdesc_add(wd0, k * 32), idesc, first ? 0u : 1u);  // corr: lo.hi
-                mma_tf32_ts_w(dc, ah + k * 8, sdesc_add(wld0, k * 32), idesc, 1u);             //     + hi.lo
-                first = false;
-              }
+              // main: hi.hi; corr: lo.hi + hi.lo (four K-steps, one asm block)
+              mma_3xtf32_ts_chunk_w(d, dc, ah, al, wd0, sdesc_add(wd0, C::W_BYTES), idesc, first ? 0u : 1u);
+              first = false;
               mma_commit_w(&empty[s]);
               mma_commit_w(&alo_free[j & 1]);
               if (++s == STAGES) { s = 0; ph ^= 1; }

@@ -157,7 +157,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   tc_fence_before();
   cluster_sync();                                          // both CTAs' barriers and TMEM ready
   tc_fence_after();
-  const uint32_t tbase = tmem_base;
+  if (tmem_base != 0) __trap();                            // 512 columns: the whole TMEM
+  constexpr uint32_t tbase = 0;
 
   if (warp == 0) {
     // =========================================================== TMA producer (both CTAs)
