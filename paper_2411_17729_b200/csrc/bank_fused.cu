@@ -175,7 +175,9 @@ __global__ void __launch_bounds__(THREADS, 1) bank_fused_kernel(const __grid_con
       accfull[2], accempty[2], stg_full[2], stg_empty[2], tready[NA];
   __shared__ uint32_t tmem_base;
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // warp index broadcast from lane 0: provably warp-uniform, so role branches are uniform control
+  // flow and ptxas keeps role-local uniform values (descriptors, TMEM addresses) in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
   // optional wait-time accounting (a.dbg != null): 4 counters per role, clock64 cycles
   unsigned long long dacc[4] = {0, 0, 0, 0};
   const long long t_start = clock64();
@@ -671,8 +673,22 @@ int launch_bank_fused(const BankFusedArg& a, const float* pack_f32, int n_planes
   if (cudaFuncSetAttribute(bank_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES) !=
       cudaSuccess)
     return CASC_ERR_CUDA;
-  bank_fused_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(maps, a);
-  CASC_LAUNCHED();
+  // CTAs wait on one another (publication flags, sequence-slot counters): a cooperative launch
+  // guarantees that every CTA of the grid is resident at once (one per SM here)
+  int dev = 0, coop = 0, per_sm = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bank_fused_kernel, THREADS, SMEM_BYTES) != cudaSuccess)
+    return CASC_ERR_CUDA;
+  if (!coop || grid > per_sm * sms) return CASC_ERR_UNSUPPORTED;
+  BankFusedArg arg = a;
+  void* params[] = {(void*)&maps, (void*)&arg};
+  if (cudaLaunchCooperativeKernel((const void*)bank_fused_kernel, dim3(grid), dim3(THREADS), params, SMEM_BYTES, st) !=
+      cudaSuccess) {
+    (void)cudaGetLastError();
+    return CASC_ERR_CUDA;
+  }
+  count_launch();
   return CASC_OK;
 }
 

@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
   __shared__ uint64_t z_full[2], z_empty[2], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
 
-  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid / 32, 0), lane = tid % 32;
   const int li = blockIdx.y / a.batch, b = blockIdx.y % a.batch;
   const int c = a.sys_list[li];
   const int seq = c * a.batch + b;

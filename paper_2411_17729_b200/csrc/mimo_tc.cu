@@ -191,7 +191,9 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
   auto stWlo = [&](int s) { return smem + s * C::STAGE_BYTES + C::A_BYTES + C::W_BYTES; };
   auto stAlo = [&](int s) { return smem + s * C::STAGE_BYTES + C::A_BYTES + C::NW * C::W_BYTES; };
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // warp index broadcast from lane 0: provably warp-uniform, so role branches are uniform control
+  // flow and ptxas keeps role-local uniform values (descriptors, TMEM addresses) in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
   // optional wait-cycle accounting (a.dbg != null, CASC_GEMM_DBG=1): slots per role, see launcher
   unsigned long long dacc[24];
 #pragma unroll

@@ -133,7 +133,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   auto stA = [&](int s) { return smem + s * STAGE_BYTES; };
   auto stW = [&](int s) { return smem + s * STAGE_BYTES + A_BYTES; };
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // warp index broadcast from lane 0: provably warp-uniform, so role branches are uniform control
+  // flow and ptxas keeps role-local uniform values (descriptors, TMEM addresses) in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
   const uint32_t rank = cta_rank();
   const bool is_leader = rank == 0;
   const int64_t blocks_per_b = (a.L + 2 * HM - 1) / (2 * HM);

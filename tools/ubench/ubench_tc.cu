@@ -121,6 +121,212 @@ __global__ void k_mma_mw(int N, int iters, unsigned long long* out, int nw) {
   if (threadIdx.x < 32) tmem_dealloc<512>(tb);
 }
 
+// pattern of the 3xTF32 GEMM: per K-step mma(d, A_hi, W_hi), mma(dc, A_lo, W_hi), mma(dc, A_hi, W_lo)
+// mode 0: d != dc (two accumulators), mode 1: d == dc (one accumulator); A in TMEM
+template <int MODE>
+__global__ void k_mma_3x(int iters, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t tb;
+  __shared__ uint64_t bar;
+  for (int i = threadIdx.x; i < (16384 + 32768) / 4; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.f;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+  if (threadIdx.x < 32) tmem_alloc<512>(&tb);
+  fence_async_smem();
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  const long long t0 = clock64();
+  if (threadIdx.x < 32) {
+    const uint32_t idesc = make_idesc(FMT_TF32, 128, 64);
+    const uint64_t bd0 = make_sdesc(smem_u32(sm) + 16384, 16, 1024, LAYOUT_SW128);
+    const uint32_t d = tb, dc = MODE == 0 ? tb + 64 : tb, ah = tb + 256, al = tb + 288;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        mma_ts_w(d, ah + k * 8, bd0 + 2 * k, idesc, 1);
+        mma_ts_w(dc, al + k * 8, bd0 + 2 * k, idesc, 1);
+        mma_ts_w(dc, ah + k * 8, bd0 + 512 + 2 * k, idesc, 1);
+      }
+    }
+    if (threadIdx.x == 0) mma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) out[0] = (unsigned long long)(t1 - t0);
+  tc_fence_before(); __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc<512>(tb);
+}
+
+// TMEM contention: warp 0 issues the 3xTF32 TS pattern (N = 64) while warps 2-5 load and/or
+// warps 6-9 store TMEM (epilogue / transform traffic); cycles per MMA
+__global__ void k_contend(int iters, int ld_on, int st_on, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t tb;
+  __shared__ uint64_t bar;
+  __shared__ volatile int stop;
+  for (int i = threadIdx.x; i < (16384 + 32768) / 4; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.f;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); stop = 0; }
+  if (threadIdx.x < 32) tmem_alloc<512>(&tb);
+  fence_async_smem();
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  const int warp = threadIdx.x / 32;
+  float acc = 0.f;
+  if (warp == 0) {
+    const uint32_t idesc = make_idesc(FMT_TF32, 128, 64);
+    const uint64_t bd0 = make_sdesc(smem_u32(sm) + 16384, 16, 1024, LAYOUT_SW128);
+    const uint32_t d = tb, dc = tb + 64, ah = tb + 256, al = tb + 288;
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        mma_ts_w(d, ah + k * 8, bd0 + 2 * k, idesc, 1);
+        mma_ts_w(dc, al + k * 8, bd0 + 2 * k, idesc, 1);
+        mma_ts_w(dc, ah + k * 8, bd0 + 512 + 2 * k, idesc, 1);
+      }
+    }
+    if (threadIdx.x == 0) mma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) { out[0] = (unsigned long long)(t1 - t0); stop = 1; }
+  } else if (warp >= 2 && warp <= 5 && ld_on) {
+    const uint32_t base = tb + ((uint32_t)((warp & 3) * 32) << 16) + 128;
+    int i = 0;
+    while (!stop) {
+      uint32_t r[32];
+      ld32(base + ((i++ * 32) & 63), r);
+      acc += __uint_as_float(r[i & 31]);
+    }
+  } else if (warp >= 6 && warp <= 9 && st_on) {
+    const uint32_t base = tb + ((uint32_t)((warp & 3) * 32) << 16) + 320;
+    uint32_t r[32];
+    for (int e = 0; e < 32; ++e) r[e] = e;
+    int i = 0;
+    while (!stop) {
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+          "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+          ::"r"(base + ((i++ * 32) & 127)), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+            "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+            "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),
+            "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]) : "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+  }
+  if (acc == 1234.5f) out[1] = 1;
+  tc_fence_before(); __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc<512>(tb);
+}
+
+// shared-memory contention: warp 0 issues the 3xTF32 TS pattern while `nw` other warps stream
+// 16-byte loads (mode 1) or stores (mode 2) through a separate 64 KB region
+__global__ void k_smem_contend(int iters, int nw, int mode, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t tb;
+  __shared__ uint64_t bar;
+  __shared__ volatile int stop;
+  for (int i = threadIdx.x; i < (16384 + 32768) / 4; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.f;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); stop = 0; }
+  if (threadIdx.x < 32) tmem_alloc<512>(&tb);
+  fence_async_smem();
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  const int warp = threadIdx.x / 32;
+  float acc = 0.f;
+  float4* buf = reinterpret_cast<float4*>(sm + 65536);
+  if (warp == 0) {
+    const uint32_t idesc = make_idesc(FMT_TF32, 128, 64);
+    const uint64_t bd0 = make_sdesc(smem_u32(sm) + 16384, 16, 1024, LAYOUT_SW128);
+    const uint32_t d = tb, dc = tb + 64, ah = tb + 256, al = tb + 288;
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        mma_ts_w(d, ah + k * 8, bd0 + 2 * k, idesc, 1);
+        mma_ts_w(dc, al + k * 8, bd0 + 2 * k, idesc, 1);
+        mma_ts_w(dc, ah + k * 8, bd0 + 512 + 2 * k, idesc, 1);
+      }
+    }
+    if (threadIdx.x == 0) mma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) { out[0] = (unsigned long long)(t1 - t0); stop = 1; }
+  } else if (warp >= 1 && warp <= nw) {
+    int i = threadIdx.x;
+    while (!stop) {
+      if (mode == 1) { const float4 v = buf[i & 4095]; acc += v.x; }
+      else buf[i & 4095] = make_float4(acc, 1.f, 2.f, 3.f);
+      i += 32 * nw;
+    }
+  }
+  if (acc == 1234.5f) out[1] = 1;
+  tc_fence_before(); __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc<512>(tb);
+}
+
+// commits between chunks: a tcgen05.commit to an mbarrier after every `per` chunks of 12 MMAs
+__global__ void k_mma_commit(int iters, int per, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t tb;
+  __shared__ uint64_t bar, cb[4];
+  for (int i = threadIdx.x; i < (16384 + 32768) / 4; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.f;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); for (int i = 0; i < 4; ++i) mbar_init(&cb[i], 1); fence_mbar_init(); }
+  if (threadIdx.x < 32) tmem_alloc<512>(&tb);
+  fence_async_smem();
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  const long long t0 = clock64();
+  if (threadIdx.x < 32) {
+    const uint32_t idesc = make_idesc(FMT_TF32, 128, 64);
+    const uint64_t wd = make_sdesc(smem_u32(sm) + 16384, 16, 1024, LAYOUT_SW128);
+    for (int i = 0; i < iters; ++i) {
+      mma_3xtf32_ts_chunk_w(tb, tb + 64, tb + 256 + (i & 1) * 64, tb + 288 + (i & 1) * 64, wd, wd + 512, idesc, 1);
+      if (per > 0 && (i % per) == per - 1) { mma_commit_w(&cb[i & 3]); mma_commit_w(&cb[(i + 1) & 3]); }
+      if (per < 0) tc_fence_after();              // fence::after_thread_sync between chunks
+      if (per < -1) tc_fence_before();
+    }
+    if (threadIdx.x == 0) mma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) out[0] = (unsigned long long)(t1 - t0);
+  tc_fence_before(); __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc<512>(tb);
+}
+
+// MMA issue with operands that are runtime values (kernel parameters offset by a loop counter
+// and a value loaded from shared memory), as in the real kernels
+__global__ void k_mma_rt(int iters, uint32_t doff, uint32_t aoff, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t tb;
+  __shared__ uint64_t bar;
+  for (int i = threadIdx.x; i < (16384 + 32768) / 4; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.f;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+  if (threadIdx.x < 32) tmem_alloc<512>(&tb);
+  fence_async_smem();
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  const long long t0 = clock64();
+  if (threadIdx.x < 32) {
+    const uint32_t idesc = make_idesc(FMT_TF32, 128, 64);
+    const uint32_t base = tb;
+    for (int i = 0; i < iters; ++i) {
+      const uint32_t j = (uint32_t)i & 1;
+      const uint64_t wd = make_sdesc(smem_u32(sm) + 16384 + j * 8192, 16, 1024, LAYOUT_SW128);
+      const uint32_t d = base + doff + j * 64, dc = d + 128, ah = base + aoff + j * 64, al = ah + 32;
+      mma_3xtf32_ts_chunk_w(d, dc, ah, al, wd, wd + 512, idesc, 1);
+    }
+    if (threadIdx.x == 0) mma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) out[0] = (unsigned long long)(t1 - t0);
+  tc_fence_before(); __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc<512>(tb);
+}
+
 __global__ void k_tmem_ld64(int nwarps, int iters, unsigned long long* out, float* sink) {
   __shared__ uint32_t tb;
   const int warp = threadIdx.x / 32;
@@ -283,6 +489,47 @@ int main() {
         printf("mma tf32 %s N=%d issuers=%d: %.1f cyc per mma (all issuers) %s\n", ts ? "TS" : "SS", N, nw,
                (double)h / (4.0 * it * nw), cudaGetErrorString(e));
       }
+  cudaFuncSetAttribute(k_mma_3x<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  cudaFuncSetAttribute(k_mma_3x<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  for (int mode = 0; mode < 2; ++mode) {
+    const int it = 2048;
+    if (mode == 0) k_mma_3x<0><<<1, 128, 64 * 1024>>>(it, d);
+    else k_mma_3x<1><<<1, 128, 64 * 1024>>>(it, d);
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("3xTF32 TS pattern, %s: %.1f cyc per mma\n", mode == 0 ? "main + corr accumulators" : "one accumulator",
+           (double)h / (12.0 * it));
+  }
+  cudaFuncSetAttribute(k_contend, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  for (int cfg = 0; cfg < 4; ++cfg) {
+    const int it = 4096;
+    k_contend<<<1, 320, 64 * 1024>>>(it, cfg & 1, cfg >> 1, d);
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("3xTF32 TS MMA with TMEM ld %s, st %s: %.1f cyc per mma\n", (cfg & 1) ? "on " : "off", (cfg >> 1) ? "on " : "off",
+           (double)h / (12.0 * it));
+  }
+  cudaFuncSetAttribute(k_smem_contend, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024);
+  for (int mode = 1; mode <= 2; ++mode)
+    for (int nw : {2, 4, 8}) {
+      const int it = 4096;
+      k_smem_contend<<<1, 320, 128 * 1024>>>(it, nw, mode, d);
+      cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+      printf("3xTF32 TS MMA with %d warps of smem %s: %.1f cyc per mma\n", nw, mode == 1 ? "loads" : "stores",
+             (double)h / (12.0 * it));
+    }
+  cudaFuncSetAttribute(k_mma_commit, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  for (int per : {0, 1, 2, 4, -1, -2}) {
+    const int it = 4096;
+    k_mma_commit<<<1, 128, 64 * 1024>>>(it, per, d);
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("3xTF32 TS chunks with 2 commits every %d chunks: %.1f cyc per mma\n", per, (double)h / (12.0 * it));
+  }
+  cudaFuncSetAttribute(k_mma_rt, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  {
+    const int it = 4096;
+    k_mma_rt<<<1, 128, 64 * 1024>>>(it, 0, 384, d);
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("3xTF32 TS chunk, runtime operands: %.1f cyc per mma\n", (double)h / (12.0 * it));
+  }
   for (int nw : {1, 4, 8}) {
     const int it = 4096;
     k_tmem_ld64<<<1, 256>>>(nw, it, d, sink);
