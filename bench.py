@@ -187,6 +187,10 @@ def roofline(prof: dict, mode: str, cfg: str):
         ach = by / t / 1e9
         peak = pk["hbm_gbs"]
         note = "HBM copy bandwidth (%s)" % pk["source"]
+        if cls == "bank_stage":
+            note += ("; algorithmic bytes = one read + one write of the m x (L batch) state per stage "
+                     "(SURVEY 8d); a bank_stage pass applies two stages (R23), so its DRAM traffic "
+                     "(ncu, 'traffic') is about half of them")
         out = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak}
     out.update({"traffic": ncu_traffic(cls, cfg), "kernel": cls, "launches_timed": r["launches"],
                 "avg_launch_ms": t * 1e3, "algorithmic_bytes_per_launch": by,

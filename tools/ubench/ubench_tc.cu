@@ -7,6 +7,7 @@
 #include "../../paper_2411_17729_b200/csrc/sm100.cuh"
 using namespace casc::sm100;
 
+__device__ __forceinline__ int lane_id() { return threadIdx.x % 32; }
 __device__ __forceinline__ void ld32(uint32_t taddr, uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -295,6 +296,66 @@ __global__ void k_mma_commit(int iters, int per, unsigned long long* out) {
   if (threadIdx.x < 32) tmem_dealloc<512>(tb);
 }
 
+// ALU issue contention: warp 1 issues 3xTF32 TS chunks while `nw` other warps run dense
+// independent integer/float work (no memory), like the transform and epilogue warps
+__global__ void k_mma_alu(int iters, int nw, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t tb;
+  __shared__ uint64_t bar;
+  __shared__ volatile int stop;
+  for (int i = threadIdx.x; i < (16384 + 32768) / 4; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.f;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); stop = 0; }
+  if (threadIdx.x < 32) tmem_alloc<512>(&tb);
+  fence_async_smem();
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0);
+  if (nw < 0) {                 // non-zero operands: random-ish smem B and TMEM A
+    for (int i = threadIdx.x; i < (16384 + 32768) / 4; i += blockDim.x)
+      reinterpret_cast<float*>(sm)[i] = __uint_as_float(0x3f800000u | ((i * 2654435761u) >> 9));
+    fence_async_smem();
+    if (warp < 4) {
+      uint32_t v[32];
+      for (int e = 0; e < 32; ++e) v[e] = 0x3f800000u | (((threadIdx.x * 37 + e) * 2654435761u) >> 9);
+      const uint32_t ta = tb + ((uint32_t)((warp & 3) * 32) << 16);
+      for (int c = 0; c < 512; c += 32)
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+                     "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+                     ::"r"(ta + c), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+                       "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+                       "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+                       "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]) : "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before(); __syncthreads(); tc_fence_after();
+  }
+  uint32_t x[8];
+  for (int e = 0; e < 8; ++e) x[e] = threadIdx.x * 7 + e;
+  if (warp == 1) {
+    const uint32_t idesc = make_idesc(FMT_TF32, 128, 64);
+    const uint64_t wd = make_sdesc(smem_u32(sm) + 16384, 16, 1024, LAYOUT_SW128);
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i)
+      mma_3xtf32_ts_chunk_w(tb, tb + 64, tb + 256 + (i & 1) * 64, tb + 288 + (i & 1) * 64, wd, wd + 512, idesc, 1);
+    if (lane_id() == 0) mma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    if (lane_id() == 0) { out[0] = (unsigned long long)(t1 - t0); stop = 1; }
+  } else if (warp >= 2 && warp < 2 + (nw < 0 ? 0 : nw)) {
+    while (!stop) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] = ((x[e] + 0x1000u) & 0xFFFFE000u) ^ (x[(e + 1) & 7] >> 3);
+    }
+  }
+  uint32_t acc = 0;
+  for (int e = 0; e < 8; ++e) acc ^= x[e];
+  if (acc == 0x12345u) out[1] = 1;
+  tc_fence_before(); __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc<512>(tb);
+}
+
 // MMA issue with operands that are runtime values (kernel parameters offset by a loop counter
 // and a value loaded from shared memory), as in the real kernels
 __global__ void k_mma_rt(int iters, uint32_t doff, uint32_t aoff, unsigned long long* out) {
@@ -522,6 +583,13 @@ int main() {
     k_mma_commit<<<1, 128, 64 * 1024>>>(it, per, d);
     cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
     printf("3xTF32 TS chunks with 2 commits every %d chunks: %.1f cyc per mma\n", per, (double)h / (12.0 * it));
+  }
+  cudaFuncSetAttribute(k_mma_alu, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  for (int nw : {0, 8, -1}) {
+    const int it = 4096;
+    k_mma_alu<<<1, 320, 64 * 1024>>>(it, nw, d);
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("3xTF32 TS chunks with %d dense-ALU warps (-1: nonzero operands): %.1f cyc per mma\n", nw, (double)h / (12.0 * it));
   }
   cudaFuncSetAttribute(k_mma_rt, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   {
