@@ -356,6 +356,49 @@ __global__ void k_mma_alu(int iters, int nw, unsigned long long* out) {
   if (threadIdx.x < 32) tmem_dealloc<512>(tb);
 }
 
+// spin-wait contention: warp 1 issues 3xTF32 TS chunks with 2 commits per chunk (as the GEMM)
+// while `nw` other warps spin in mbarrier.try_wait on a barrier that never completes
+__global__ void k_mma_spin(int iters, int nw, int hint_ns, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint32_t tb;
+  __shared__ uint64_t bar, never, cb[4];
+  __shared__ volatile int stop;
+  for (int i = threadIdx.x; i < (16384 + 32768) / 4; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.f;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&never, 1); for (int i = 0; i < 4; ++i) mbar_init(&cb[i], 1); fence_mbar_init(); stop = 0; }
+  if (threadIdx.x < 32) tmem_alloc<512>(&tb);
+  fence_async_smem();
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0);
+  if (warp == 1) {
+    const uint32_t idesc = make_idesc(FMT_TF32, 128, 64);
+    const uint64_t wd = make_sdesc(smem_u32(sm) + 16384, 16, 1024, LAYOUT_SW128);
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      mma_3xtf32_ts_chunk_w(tb, tb + 64, tb + 256 + (i & 1) * 64, tb + 288 + (i & 1) * 64, wd, wd + 512, idesc, 1);
+      mma_commit_w(&cb[i & 3]);
+      mma_commit_w(&cb[(i + 1) & 3]);
+    }
+    if (lane_id() == 0) mma_commit(&bar);
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    const long long t1 = clock64();
+    if (lane_id() == 0) { out[0] = (unsigned long long)(t1 - t0); stop = 1; }
+  } else if (warp >= 2 && warp < 2 + nw) {
+    while (!stop) {
+      uint32_t ok;
+      if (hint_ns > 0)
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0, %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok) : "r"(smem_u32(&never)), "r"(hint_ns) : "memory");
+      else
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok) : "r"(smem_u32(&never)) : "memory");
+      if (ok) break;
+    }
+  }
+  tc_fence_before(); __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc<512>(tb);
+}
+
 // MMA issue with operands that are runtime values (kernel parameters offset by a loop counter
 // and a value loaded from shared memory), as in the real kernels
 __global__ void k_mma_rt(int iters, uint32_t doff, uint32_t aoff, unsigned long long* out) {
@@ -590,6 +633,15 @@ int main() {
     k_mma_alu<<<1, 320, 64 * 1024>>>(it, nw, d);
     cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
     printf("3xTF32 TS chunks with %d dense-ALU warps (-1: nonzero operands): %.1f cyc per mma\n", nw, (double)h / (12.0 * it));
+  }
+  cudaFuncSetAttribute(k_mma_spin, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  for (int cfg = 0; cfg < 5; ++cfg) {
+    const int nw = cfg == 0 ? 0 : (cfg < 3 ? 4 : 8), hint = (cfg == 2 || cfg == 4) ? 20000 : 0;
+    const int it = 4096;
+    k_mma_spin<<<1, 320, 64 * 1024>>>(it, nw, hint, d);
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("3xTF32 TS chunks + commits, %d warps spinning in try_wait (hint %d ns): %.1f cyc per mma\n", nw, hint,
+           (double)h / (12.0 * it));
   }
   cudaFuncSetAttribute(k_mma_rt, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   {
