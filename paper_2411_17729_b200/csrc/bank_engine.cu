@@ -67,7 +67,7 @@ static int pair_wres() {
 }
 
 struct BankWs {
-  int* meta;      // Neff | Kc | parity | order   (4 n ints)
+  int* meta;      // Neff | Kc | parity | order | iota | head-enders by input chunk   (6 n ints)
   double* Kr64;   // [n][m][128]
   float* krT;     // [n][2][m][128]
   double* w64;    // [n][m]
@@ -82,7 +82,7 @@ struct BankWs {
 static BankWs carve_bank(void* ws, int n, int m, int64_t L, int batch, int qslots) {
   Carver c(ws);
   BankWs w{};
-  w.meta = c.take<int>((size_t)4 * n);
+  w.meta = c.take<int>((size_t)6 * n);
   w.Kr64 = c.take<double>((size_t)n * m * 128);
   w.krT = c.take<float>((size_t)n * 2 * m * 128);
   w.w64 = c.take<double>((size_t)n * m);
@@ -316,9 +316,18 @@ __global__ void pair_split_kernel(const double* Q64, float* Q32, const int* Neff
 }
 
 // One wave of n channels; Pw points at the wave's first channel inside the full pack.
+struct BankStream {        // host-buffer run: output channels copied out as soon as they are final
+  void* y_host = nullptr;           // pinned [n][batch][L] (null: no streaming)
+  cudaStream_t cout = nullptr;      // copy-out stream
+  cudaEvent_t u_ready = nullptr;    // input copy completion (the head waits for it)
+  std::vector<cudaEvent_t>* events = nullptr;   // created here, destroyed by the caller
+  // input arriving in chunks of channels [bounds[i], bounds[i+1]) (memory order), chunk i complete
+  // at u_events[i]: the head runs per chunk as its input lands
+  int n_chunks = 0; const int* bounds = nullptr; const cudaEvent_t* u_events = nullptr;
+};
 static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int N_max, const PackLayout& Pw,
                      const double* Bbar, const double* C, const double* D, const float* u, float* y, void* ws,
-                     size_t ws_bytes, cudaStream_t st);
+                     size_t ws_bytes, cudaStream_t st, int* pinned_meta = nullptr, const BankStream* bs = nullptr);
 
 // Bounded-memory bank: with a workspace smaller than the whole bank needs, the channels are
 // processed in consecutive waves of as many channels as fit (each wave is an independent bank).
@@ -358,9 +367,74 @@ int engine_bank_tc(int n, int m, int64_t L, int batch, const int* N_host, int N_
   return CASC_OK;
 }
 
+// End to end from host buffers with the transfers overlapped (casc_run_host, one wave): the input
+// copy (copy-in stream) overlaps the parameter upload, the powers and the derived data, and each
+// group of channels whose cascade is complete (the head for Ne <= 7, then every stage pass) gets
+// its tail and its output copy (copy-out stream) while the remaining passes run. u_h / y_h should
+// be pinned. CASC_ERR_WORKSPACE if the whole bank does not fit the workspace (caller falls back).
+int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host, int N_max, const void* pack,
+                          const double* Bbar, const double* C, const double* D, float* u_dev, float* y_dev,
+                          const void* u_h, const void* y_h, void* ws, size_t ws_bytes, cudaStream_t st) {
+  int maxNe = 0;
+  for (int s = 0; s < n; ++s) maxNe = std::max(maxNe, eff_order_b(N_host[s], L));
+  const int qslots = stage_variant(m) == 't' ? pair_slots(maxNe) : 0;
+  if (m != 64 || carve_bank(nullptr, n, m, L, batch, qslots).bytes > ws_bytes) return CASC_ERR_WORKSPACE;
+  static cudaStream_t out_streams[16] = {};        // per device copy-out stream (created once)
+  static int* pinned[16] = {};                     // per device pinned staging of the channel table
+  static size_t pinned_n[16] = {};
+  int dev = 0;
+  CASC_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 16) return CASC_ERR_UNSUPPORTED;
+  static cudaStream_t in_streams[16] = {};
+  if (!out_streams[dev]) CASC_TRY(cudaStreamCreateWithFlags(&out_streams[dev], cudaStreamNonBlocking));
+  if (!in_streams[dev]) CASC_TRY(cudaStreamCreateWithFlags(&in_streams[dev], cudaStreamNonBlocking));
+  if (pinned_n[dev] < (size_t)6 * n) {
+    if (pinned[dev]) cudaFreeHost(pinned[dev]);
+    pinned[dev] = nullptr;
+    pinned_n[dev] = 0;
+    CASC_TRY(cudaHostAlloc(&pinned[dev], sizeof(int) * 6 * (size_t)n, cudaHostAllocDefault));
+    pinned_n[dev] = (size_t)6 * n;
+  }
+  std::vector<cudaEvent_t> events;
+  // input in ~8 chunks of channels: chunk i's head starts as soon as chunk i has landed
+  const int n_chunks = std::min(n, 8);
+  std::vector<int> bounds(n_chunks + 1);
+  for (int i = 0; i <= n_chunks; ++i) bounds[i] = (int)((int64_t)n * i / n_chunks);
+  std::vector<cudaEvent_t> u_ev(n_chunks);
+  cudaEvent_t ev_start;
+  CASC_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+  events.push_back(ev_start);
+  CASC_TRY(cudaEventRecord(ev_start, st));                   // u may be reused only after earlier work
+  CASC_TRY(cudaStreamWaitEvent(in_streams[dev], ev_start, 0));
+  const size_t row = (size_t)batch * L * sizeof(float);
+  for (int i = 0; i < n_chunks; ++i) {
+    CASC_TRY(cudaEventCreateWithFlags(&u_ev[i], cudaEventDisableTiming));
+    events.push_back(u_ev[i]);
+    CASC_TRY(cudaMemcpyAsync((char*)u_dev + bounds[i] * row, (const char*)u_h + bounds[i] * row,
+                             (size_t)(bounds[i + 1] - bounds[i]) * row, cudaMemcpyHostToDevice, in_streams[dev]));
+    CASC_TRY(cudaEventRecord(u_ev[i], in_streams[dev]));
+  }
+  BankStream bs;
+  bs.y_host = const_cast<void*>(y_h);
+  bs.cout = out_streams[dev];
+  bs.events = &events;
+  bs.n_chunks = n_chunks;
+  bs.bounds = bounds.data();
+  bs.u_events = u_ev.data();
+  PackLayout P = pack_layout(const_cast<void*>(pack), n, m, N_max, CASC_FP32);
+  int rc = bank_wave(n, m, L, batch, N_host, N_max, P, Bbar, C, D, u_dev, y_dev, ws, ws_bytes, st, pinned[dev], &bs);
+  cudaError_t e1 = cudaStreamSynchronize(bs.cout), e2 = cudaStreamSynchronize(st);
+  cudaStreamSynchronize(in_streams[dev]);
+  for (auto& e : events) cudaEventDestroy(e);
+  if (rc) return rc;
+  return (e1 != cudaSuccess || e2 != cudaSuccess) ? CASC_ERR_CUDA : CASC_OK;
+}
+
+// pinned_meta: optional pinned host staging for the channel table (4n ints, untouched until the
+// stream has consumed it), so the upload is a true asynchronous copy
 static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int N_max, const PackLayout& Pw,
                      const double* Bbar, const double* C, const double* D, const float* u, float* y, void* ws,
-                     size_t ws_bytes, cudaStream_t st) {
+                     size_t ws_bytes, cudaStream_t st, int* pinned_meta, const BankStream* bs) {
   const char variant = stage_variant(m);
   // output fusion: the producer of each channel's last state writes (C v, C P_Ne v) instead of
   // v (R24); taken with the m = 64 TMA stage GEMM and warp-specialized head
@@ -369,8 +443,10 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     return e && e[0] == '0';
   }();
   const bool use_ab = m == 64 && (variant == 's' || variant == 't') && !ab_off && !(getenv("CASC_BANK_HEAD") && getenv("CASC_BANK_HEAD")[0] == 'o');
-  std::vector<int> meta((size_t)4 * n);
-  int *Neff = meta.data(), *Kc = Neff + n, *par = Neff + 2 * n, *order = Neff + 3 * n;
+  std::vector<int> meta_v(pinned_meta ? 0 : (size_t)6 * n);
+  int* meta = pinned_meta ? pinned_meta : meta_v.data();
+  int *Neff = meta, *Kc = Neff + n, *par = Neff + 2 * n, *order = Neff + 3 * n, *iota = Neff + 4 * n,
+      *hend = Neff + 5 * n;
   int maxNe = 0;
   for (int s = 0; s < n; ++s) {
     Neff[s] = eff_order_b(N_host[s], L);
@@ -390,8 +466,21 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
   int rc;
   std::iota(order, order + n, 0);
   std::stable_sort(order, order + n, [&](int a, int b) { return Neff[a] > Neff[b]; });
-  CASC_TRY(cudaMemcpyAsync(w.meta, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-  const int *dNeff = w.meta, *dKc = w.meta + n, *dpar = w.meta + 2 * n, *dorder = w.meta + 3 * n;
+  std::iota(iota, iota + n, 0);
+  const bool chunked = bs && bs->n_chunks > 1;
+  std::vector<int> hend_off(chunked ? bs->n_chunks + 1 : 1, 0);
+  if (chunked) {                                   // head-ending channels (Ne == Kc), grouped by chunk
+    int o = 0;
+    for (int ci = 0; ci < bs->n_chunks; ++ci) {
+      hend_off[ci] = o;
+      for (int c = bs->bounds[ci]; c < bs->bounds[ci + 1]; ++c)
+        if (Neff[c] == Kc[c]) hend[o++] = c;
+    }
+    hend_off[bs->n_chunks] = o;
+  }
+  CASC_TRY(cudaMemcpyAsync(w.meta, meta, (size_t)6 * n * sizeof(int), cudaMemcpyHostToDevice, st));
+  const int *dNeff = w.meta, *dKc = w.meta + n, *dpar = w.meta + 2 * n, *dorder = w.meta + 3 * n,
+            *diota = w.meta + 4 * n, *dhend = w.meta + 5 * n;
   auto count_ge = [&](int need) {                    // channels with Neff >= need: a prefix of order
     int c = 0;
     while (c < n && Neff[order[c]] >= need) ++c;
@@ -420,18 +509,50 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     }
   }
   const int64_t ntiles = ceil_div(L, 128);
-  // ---- head: stages 0..Kc-1 (+ Bbar u), all channels
-  {
+  // streaming outputs (host-buffer run): channels order[a, b) are final -> tail + copy out
+  const bool streaming = bs && bs->y_host && use_ab;
+  auto emit_ids = [&](const int* dlist, const int* hlist, int cnt) -> int {
+    if (!streaming || cnt <= 0) return CASC_OK;
+    BankAbTailArg t{};
+    t.ab = w.ab; t.u = static_cast<const float*>(u); t.y = static_cast<float*>(y);
+    t.d = w.d32; t.Neff = dNeff; t.n_ch = n; t.L = L; t.batch = batch;
+    t.list = dlist; t.n_list = cnt;
+    int rc2;
+    {
+      ProfScope ps(st, K_BANK_TAIL, (double)cnt * batch * L * 24.0, (double)cnt * batch * L * 3);
+      if ((rc2 = launch_bank_ab_tail(t, st))) return rc2;
+    }
+    cudaEvent_t ev;
+    CASC_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    bs->events->push_back(ev);
+    CASC_TRY(cudaEventRecord(ev, st));
+    CASC_TRY(cudaStreamWaitEvent(bs->cout, ev, 0));
+    const size_t row = (size_t)batch * L * sizeof(float);
+    for (int i = 0; i < cnt;) {                   // merge runs of consecutive channel ids
+      int j = i + 1;
+      while (j < cnt && hlist[j] == hlist[j - 1] + 1) ++j;
+      CASC_TRY(cudaMemcpyAsync((char*)bs->y_host + (size_t)hlist[i] * row, (const char*)y + (size_t)hlist[i] * row,
+                               (size_t)(j - i) * row, cudaMemcpyDeviceToHost, bs->cout));
+      i = j;
+    }
+    return CASC_OK;
+  };
+  auto emit = [&](int a, int b) -> int { return emit_ids(dorder + a, order + a, b - a); };
+  // ---- head: stages 0..Kc-1 (+ Bbar u), all channels (per input chunk when the input is streamed)
+  if (bs && bs->u_ready) CASC_TRY(cudaStreamWaitEvent(st, bs->u_ready, 0));
+  for (int ci = 0; ci < (chunked ? bs->n_chunks : 1); ++ci) {
+    if (chunked) CASC_TRY(cudaStreamWaitEvent(st, bs->u_events[ci], 0));
+    const int hc0 = chunked ? bs->bounds[ci] : 0, hcn = chunked ? bs->bounds[ci + 1] - hc0 : n;
     BankHeadArg a{};
     a.u = static_cast<const float*>(u); a.krT = w.krT; a.V = static_cast<float*>(w.Va);
-    a.sys_list = dorder; a.n_list = n; a.L = L; a.batch = batch;
+    a.sys_list = chunked ? diota + hc0 : dorder; a.n_list = hcn; a.L = L; a.batch = batch;
     if (use_ab) { a.Neff = dNeff; a.Kc = dKc; a.cvec = w.c32; a.wvec = w.w32; a.ab = w.ab; }
     a.tiles_per_cta = pick_group(ntiles, (int64_t)n * batch, 16);
     ProfScope ps(st, K_BANK_HEAD, (double)n * batch * L * (1 + m) * 4.0,
                  (double)n * batch * L * 2.0 * m * 128);
     // warp-specialized TMA-store head for m = 64 (CASC_BANK_HEAD=old selects the previous kernel).
-    // A TMEM-operand (TS) variant was measured slower (2.0 vs 1.3 ms on E2): tcgen05 reads a
-    // TMEM A operand at ~64 B/cycle, below shared memory's 128 B/cycle.
+    // A TMEM-operand (TS) variant was measured slower (1.67 vs 1.30 ms on E2, same box): its four
+    // builder warps write 128 KB of hi/lo per tile to TMEM.
     static const bool old_head = [] {
       const char* e = getenv("CASC_BANK_HEAD");
       return e && e[0] == 'o';
@@ -440,10 +561,13 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       const char* e = getenv("CASC_HEAD_GROUP");
       return e ? atoi(e) : 64;
     }();
-    if (m == 64 && !old_head) a.tiles_per_cta = pick_group(ntiles, (int64_t)n * batch, head_group);
+    if (m == 64 && !old_head) a.tiles_per_cta = pick_group(ntiles, (int64_t)hcn * batch, head_group);
     rc = (m == 64 && !old_head) ? launch_bank_head_ws(m, a, (int64_t)n * batch, st) : launch_bank_head(m, a, st);
     if (rc) return rc;
+    if (chunked && (rc = emit_ids(dhend + hend_off[ci], hend + hend_off[ci], hend_off[ci + 1] - hend_off[ci])))
+      return rc;
   }
+  if (!chunked && (rc = emit(count_ge(kHeadK + 1), n))) return rc;   // cascades that end at the head (Ne <= 7)
   // ---- streaming stages k >= kHeadK over the channels with Neff > k (prefixes of `order`)
   int pass = 0;
   for (int k = kHeadK; k < maxNe; k += (variant == 't' ? 2 : 1), ++pass) {
@@ -464,8 +588,11 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
         // their (C v, C P_Ne v) parts are needed on every row: no skipped leading tiles
         if (count_ge(k + 1) > count_ge(k + 2)) g.t_first = 0;
       }
-      ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt * batch * L * m * 4.0, 2.0 * cnt * batch * L * (double)mm);
-      if ((rc = launch_mimo_gemm(g, true, st))) return rc;
+      {
+        ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt * batch * L * m * 4.0, 2.0 * cnt * batch * L * (double)mm);
+        if ((rc = launch_mimo_gemm(g, true, st))) return rc;
+      }
+      if ((rc = emit(count_ge(k + 2), count_ge(k + 1)))) return rc;   // channels with Ne == k + 1
       continue;
     }
     if (variant != 't') {
@@ -517,7 +644,9 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt1 * batch * L * m * 4.0, 2.0 * cnt1 * batch * L * (double)mm);
       if ((rc = launch_mimo_gemm(g, true, st))) return rc;
     }
+    if ((rc = emit(count_ge(k + 3), count_ge(k + 1)))) return rc;     // channels with Ne in {k + 1, k + 2}
   }
+  if (streaming) return CASC_OK;                      // every channel was emitted
   // ---- tail: stage Ne + y = C v + D u
   if (use_ab) {                                     // from the fused (C v, C P_Ne v) parts
     BankAbTailArg a{};

@@ -314,10 +314,11 @@ int launch_bank_derived(const double* p64, int slots, const double* Bbar, const 
 // the stage (or head) that produced v^(Ne): stage Ne and y = C v + D u in
 // the regrouped form of R21/R24, without storing or re-reading v^(Ne).
 __global__ void bank_ab_tail_kernel(BankAbTailArg a) {
-  const int64_t n = (int64_t)a.n_ch * a.batch * a.L;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t seq = e / a.L, l = e % a.L;
-    const int c = (int)(seq / a.batch);
+  const int64_t per = (int64_t)a.batch * a.L;
+  const int64_t n = (a.list ? (int64_t)a.n_list : (int64_t)a.n_ch) * per;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = a.list ? a.list[i / per] : (int)(i / per);
+    const int64_t e = (int64_t)c * per + i % per, l = e % a.L;
     const int64_t sh = (int64_t)1 << a.Neff[c];
     const float2 ab = *reinterpret_cast<const float2*>(a.ab + e * 2);
     const float b = l >= sh ? a.ab[(e - sh) * 2 + 1] : 0.f;
@@ -325,7 +326,7 @@ __global__ void bank_ab_tail_kernel(BankAbTailArg a) {
   }
 }
 int launch_bank_ab_tail(const BankAbTailArg& a, cudaStream_t st) {
-  const int64_t n = (int64_t)a.n_ch * a.batch * a.L;
+  const int64_t n = (a.list ? (int64_t)a.n_list : (int64_t)a.n_ch) * a.batch * a.L;
   if (n <= 0) return CASC_OK;
   bank_ab_tail_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 148 * 16), 256, 0, st>>>(a);
   CASC_LAUNCHED();

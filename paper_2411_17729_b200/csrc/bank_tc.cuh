@@ -18,6 +18,7 @@ struct BankAbTailArg {     // y_l = a_l + b_{l - 2^Ne} + d u_l  (b = 0 before l 
   const float* ab; const float* u; float* y;   // ab [n_ch][batch][L][2]; u, y [n_ch][batch][L]
   const float* d; const int* Neff;
   int n_ch; int64_t L; int batch;
+  const int* list; int n_list;                 // optional: only channels list[0..n_list)
 };
 struct BankStageArg {
   const float* Vs; float* Vd;   // [n_ch][batch][L][MS]

@@ -407,6 +407,22 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
   h.apply_bytes = std::min(h.apply_bytes, dev_ws_bytes - fixed);
   cudaStream_t st = (cudaStream_t)stream;
   const size_t es = (mode == CASC_BF16) ? 2 : 4;
+  if (n_sys > 1 && m == 64 && bank_tc_path(m, p, q, mode) && !getenv("CASC_RUN_HOST_SERIAL")) {
+    // banks: parameters and powers on `st`; u arrives in chunks on a copy stream (the head runs per
+    // chunk as it lands) and finished channels' outputs go back while later stage passes run
+    for (int s = 0; s < n_sys; ++s)
+      if (N_host[s] < 0 || N_host[s] > N_max) return CASC_ERR_DIM;
+    CASC_TRY(cudaMemcpyAsync(h.Abar, Abar_h, sizeof(double) * n_sys * m * m, cudaMemcpyHostToDevice, st));
+    CASC_TRY(cudaMemcpyAsync(h.Bbar, Bbar_h, sizeof(double) * n_sys * m, cudaMemcpyHostToDevice, st));
+    CASC_TRY(cudaMemcpyAsync(h.C, C_h, sizeof(double) * n_sys * m, cudaMemcpyHostToDevice, st));
+    if (D_h) CASC_TRY(cudaMemcpyAsync(h.D, D_h, sizeof(double) * n_sys, cudaMemcpyHostToDevice, st));
+    rc = engine_powers(n_sys, m, N_host, N_max, h.Abar, mode, h.pack, st);
+    if (rc) return rc;
+    rc = engine_bank_pipelined(n_sys, m, L, batch, N_host, N_max, h.pack, h.Bbar, h.C, D_h ? h.D : nullptr,
+                               static_cast<float*>(h.u), static_cast<float*>(h.y), u_h, y_h, h.apply_ws,
+                               h.apply_bytes, st);
+    if (rc != CASC_ERR_WORKSPACE) return rc;            // else: the serial path below (channel waves)
+  }
   CASC_TRY(cudaMemcpyAsync(h.Abar, Abar_h, sizeof(double) * n_sys * m * m, cudaMemcpyHostToDevice, st));
   CASC_TRY(cudaMemcpyAsync(h.Bbar, Bbar_h, sizeof(double) * n_sys * m * p, cudaMemcpyHostToDevice, st));
   CASC_TRY(cudaMemcpyAsync(h.C, C_h, sizeof(double) * n_sys * q * m, cudaMemcpyHostToDevice, st));
