@@ -378,14 +378,21 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
   int maxNe = 0;
   for (int s = 0; s < n; ++s) maxNe = std::max(maxNe, eff_order_b(N_host[s], L));
   const int qslots = stage_variant(m) == 't' ? pair_slots(maxNe) : 0;
-  if (m != 64 || carve_bank(nullptr, n, m, L, batch, qslots).bytes > ws_bytes) return CASC_ERR_WORKSPACE;
-  static cudaStream_t out_streams[16] = {};        // per device copy-out stream (created once)
-  static int* pinned[16] = {};                     // per device pinned staging of the channel table
+  if (m != 64) return CASC_ERR_UNSUPPORTED;
+  // channels per wave (bounded memory, as engine_bank_tc); every wave streams its own input chunks
+  // and outputs, and wave w+1's input copy overlaps wave w's compute
+  int nw = n;
+  while (nw > 0 && carve_bank(nullptr, nw, m, L, batch, qslots).bytes > ws_bytes) {
+    const size_t per = carve_bank(nullptr, 1, m, L, batch, qslots).bytes;
+    nw = (int)std::min<size_t>((size_t)nw - 1, ws_bytes / std::max<size_t>(per, 1));
+  }
+  if (nw < 1) return CASC_ERR_WORKSPACE;
+  static cudaStream_t out_streams[16] = {}, in_streams[16] = {};   // per device (created once)
+  static int* pinned[16] = {};                     // per device pinned staging of the channel tables
   static size_t pinned_n[16] = {};
   int dev = 0;
   CASC_TRY(cudaGetDevice(&dev));
   if (dev < 0 || dev >= 16) return CASC_ERR_UNSUPPORTED;
-  static cudaStream_t in_streams[16] = {};
   if (!out_streams[dev]) CASC_TRY(cudaStreamCreateWithFlags(&out_streams[dev], cudaStreamNonBlocking));
   if (!in_streams[dev]) CASC_TRY(cudaStreamCreateWithFlags(&in_streams[dev], cudaStreamNonBlocking));
   if (pinned_n[dev] < (size_t)6 * n) {
@@ -396,41 +403,59 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
     pinned_n[dev] = (size_t)6 * n;
   }
   std::vector<cudaEvent_t> events;
-  // input in ~8 chunks of channels: chunk i's head starts as soon as chunk i has landed
-  const int n_chunks = std::min(n, 8);
-  std::vector<int> bounds(n_chunks + 1);
-  for (int i = 0; i <= n_chunks; ++i) bounds[i] = (int)((int64_t)n * i / n_chunks);
-  std::vector<cudaEvent_t> u_ev(n_chunks);
+  auto new_event = [&](cudaEvent_t* e) -> int {
+    CASC_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    events.push_back(*e);
+    return CASC_OK;
+  };
   cudaEvent_t ev_start;
-  CASC_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
-  events.push_back(ev_start);
+  int rc = new_event(&ev_start);
+  if (rc) return rc;
   CASC_TRY(cudaEventRecord(ev_start, st));                   // u may be reused only after earlier work
   CASC_TRY(cudaStreamWaitEvent(in_streams[dev], ev_start, 0));
   const size_t row = (size_t)batch * L * sizeof(float);
-  for (int i = 0; i < n_chunks; ++i) {
-    CASC_TRY(cudaEventCreateWithFlags(&u_ev[i], cudaEventDisableTiming));
-    events.push_back(u_ev[i]);
-    CASC_TRY(cudaMemcpyAsync((char*)u_dev + bounds[i] * row, (const char*)u_h + bounds[i] * row,
-                             (size_t)(bounds[i + 1] - bounds[i]) * row, cudaMemcpyHostToDevice, in_streams[dev]));
-    CASC_TRY(cudaEventRecord(u_ev[i], in_streams[dev]));
+  const int waves = (n + nw - 1) / nw;
+  std::vector<std::vector<int>> bounds(waves);
+  std::vector<std::vector<cudaEvent_t>> u_ev(waves);
+  for (int w = 0; w < waves; ++w) {                          // input copies of every wave, in ~8 chunks each
+    const int c0 = w * nw, cn = std::min(nw, n - c0), nc = std::min(cn, 8);
+    bounds[w].resize(nc + 1);
+    u_ev[w].resize(nc);
+    for (int i = 0; i <= nc; ++i) bounds[w][i] = (int)((int64_t)cn * i / nc);
+    for (int i = 0; i < nc; ++i) {
+      if ((rc = new_event(&u_ev[w][i]))) return rc;
+      const size_t off = (size_t)(c0 + bounds[w][i]) * row;
+      CASC_TRY(cudaMemcpyAsync((char*)u_dev + off, (const char*)u_h + off, (size_t)(bounds[w][i + 1] - bounds[w][i]) * row,
+                               cudaMemcpyHostToDevice, in_streams[dev]));
+      CASC_TRY(cudaEventRecord(u_ev[w][i], in_streams[dev]));
+    }
   }
-  BankStream bs;
-  bs.y_host = const_cast<void*>(y_h);
-  bs.cout = out_streams[dev];
-  bs.events = &events;
-  bs.n_chunks = n_chunks;
-  bs.bounds = bounds.data();
-  bs.u_events = u_ev.data();
   PackLayout P = pack_layout(const_cast<void*>(pack), n, m, N_max, CASC_FP32);
-  int rc = bank_wave(n, m, L, batch, N_host, N_max, P, Bbar, C, D, u_dev, y_dev, ws, ws_bytes, st, pinned[dev], &bs);
-  cudaError_t e1 = cudaStreamSynchronize(bs.cout), e2 = cudaStreamSynchronize(st);
-  cudaStreamSynchronize(in_streams[dev]);
+  const int64_t slot_mm = (int64_t)(N_max + 1) * m * m;
+  for (int w = 0; w < waves && rc == CASC_OK; ++w) {
+    const int c0 = w * nw, cn = std::min(nw, n - c0);
+    BankStream bs;
+    bs.y_host = (char*)const_cast<void*>(y_h) + (size_t)c0 * row;
+    bs.cout = out_streams[dev];
+    bs.events = &events;
+    bs.n_chunks = (int)u_ev[w].size();
+    bs.bounds = bounds[w].data();
+    bs.u_events = u_ev[w].data();
+    PackLayout Pw = P;
+    Pw.p64 += c0 * slot_mm;
+    Pw.f32 += c0 * slot_mm * 2;
+    const int64_t sig = (int64_t)c0 * batch * L;
+    rc = bank_wave(cn, m, L, batch, N_host + c0, N_max, Pw, Bbar + (int64_t)c0 * m, C + (int64_t)c0 * m,
+                   D ? D + c0 : nullptr, u_dev + sig, y_dev + sig, ws, ws_bytes, st, pinned[dev] + 6 * (size_t)c0, &bs);
+  }
+  cudaError_t e1 = cudaStreamSynchronize(out_streams[dev]), e2 = cudaStreamSynchronize(st);
+  cudaError_t e3 = cudaStreamSynchronize(in_streams[dev]);
   for (auto& e : events) cudaEventDestroy(e);
   if (rc) return rc;
-  return (e1 != cudaSuccess || e2 != cudaSuccess) ? CASC_ERR_CUDA : CASC_OK;
+  return (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) ? CASC_ERR_CUDA : CASC_OK;
 }
 
-// pinned_meta: optional pinned host staging for the channel table (4n ints, untouched until the
+// pinned_meta: optional pinned host staging for the channel table (6n ints, untouched until the
 // stream has consumed it), so the upload is a true asynchronous copy
 static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int N_max, const PackLayout& Pw,
                      const double* Bbar, const double* C, const double* D, const float* u, float* y, void* ws,
