@@ -427,6 +427,48 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
   CASC_TRY(cudaMemcpyAsync(h.Bbar, Bbar_h, sizeof(double) * n_sys * m * p, cudaMemcpyHostToDevice, st));
   CASC_TRY(cudaMemcpyAsync(h.C, C_h, sizeof(double) * n_sys * q * m, cudaMemcpyHostToDevice, st));
   if (D_h) CASC_TRY(cudaMemcpyAsync(h.D, D_h, sizeof(double) * n_sys * q * p, cudaMemcpyHostToDevice, st));
+  if (n_sys == 1 && batch > 1 && mimo_tc_path(1, m, p, q, mode) && !getenv("CASC_RUN_HOST_SERIAL")) {
+    // one MIMO system: the batch's sequences are independent, so they run in chunks whose input
+    // copy (copy-in stream) overlaps the previous chunk's compute and whose output copy (copy-out
+    // stream) overlaps the next chunk's
+    rc = engine_powers(1, m, N_host, N_max, h.Abar, mode, h.pack, st);
+    if (rc) return rc;
+    static cudaStream_t in_s[16] = {}, out_s[16] = {};
+    int dev = 0;
+    CASC_TRY(cudaGetDevice(&dev));
+    if (dev >= 0 && dev < 16) {
+      if (!in_s[dev]) CASC_TRY(cudaStreamCreateWithFlags(&in_s[dev], cudaStreamNonBlocking));
+      if (!out_s[dev]) CASC_TRY(cudaStreamCreateWithFlags(&out_s[dev], cudaStreamNonBlocking));
+      const int nc = std::min(batch, 8);
+      std::vector<cudaEvent_t> ev((size_t)2 * nc + 1);
+      for (auto& e : ev) CASC_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CASC_TRY(cudaEventRecord(ev[2 * nc], st));
+      CASC_TRY(cudaStreamWaitEvent(in_s[dev], ev[2 * nc], 0));
+      const size_t in_row = es * (size_t)L * p, out_row = es * (size_t)L * q;
+      std::vector<int> b0(nc + 1);
+      for (int i = 0; i <= nc; ++i) b0[i] = (int)((int64_t)batch * i / nc);
+      for (int i = 0; i < nc; ++i) {
+        CASC_TRY(cudaMemcpyAsync((char*)h.u + b0[i] * in_row, (const char*)u_h + b0[i] * in_row,
+                                 (size_t)(b0[i + 1] - b0[i]) * in_row, cudaMemcpyHostToDevice, in_s[dev]));
+        CASC_TRY(cudaEventRecord(ev[2 * i], in_s[dev]));
+      }
+      for (int i = 0; i < nc && rc == CASC_OK; ++i) {
+        CASC_TRY(cudaStreamWaitEvent(st, ev[2 * i], 0));
+        rc = engine_apply(1, m, p, q, L, b0[i + 1] - b0[i], N_host, N_max, mode, h.pack, h.Bbar, h.C,
+                          D_h ? h.D : nullptr, (const char*)h.u + b0[i] * in_row, (char*)h.y + b0[i] * out_row,
+                          h.apply_ws, h.apply_bytes, st);
+        CASC_TRY(cudaEventRecord(ev[2 * i + 1], st));
+        CASC_TRY(cudaStreamWaitEvent(out_s[dev], ev[2 * i + 1], 0));
+        CASC_TRY(cudaMemcpyAsync((char*)y_h + b0[i] * out_row, (const char*)h.y + b0[i] * out_row,
+                                 (size_t)(b0[i + 1] - b0[i]) * out_row, cudaMemcpyDeviceToHost, out_s[dev]));
+      }
+      cudaError_t e1 = cudaStreamSynchronize(out_s[dev]), e2 = cudaStreamSynchronize(st);
+      cudaStreamSynchronize(in_s[dev]);
+      for (auto& e : ev) cudaEventDestroy(e);
+      if (rc) return rc;
+      return (e1 != cudaSuccess || e2 != cudaSuccess) ? CASC_ERR_CUDA : CASC_OK;
+    }
+  }
   CASC_TRY(cudaMemcpyAsync(h.u, u_h, es * n_sys * batch * L * p, cudaMemcpyHostToDevice, st));
   rc = engine_powers(n_sys, m, N_host, N_max, h.Abar, mode, h.pack, st);
   if (rc) return rc;

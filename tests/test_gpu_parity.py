@@ -218,3 +218,20 @@ def test_determinism_bitwise():
     a, _ = run_gpu(wl)
     b, _ = run_gpu(wl)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("mode", ["bf16", "fp32"])
+def test_run_host_mimo_batch_chunks_bitwise(mode):
+    """casc_run_host for one MIMO system runs the batch in chunks with the copies overlapped; each
+    sequence's arithmetic is unchanged, so y is bitwise the device-resident path's."""
+    import paper_2411_17729_b200 as pk
+    from paper_2411_17729_b200.runner import storage_to_torch
+    wl = S.make_random_mimo(128, 64, 64, L=1000, batch=5, N=8, rho=0.97, mode=mode)
+    y_dev, _ = run_gpu(wl)
+    u_h = storage_to_torch(wl.u_storage(), mode).reshape(1, wl.batch, wl.L, wl.p).pin_memory()
+    y_h = torch.empty((1, wl.batch, wl.L, wl.q), dtype=u_h.dtype).pin_memory()
+    f = lambda a: torch.from_numpy(np.ascontiguousarray(a))  # noqa: E731
+    ws = torch.empty(pk.run_host_bytes(1, wl.m, wl.p, wl.q, wl.L, wl.batch, int(wl.N.max()), mode),
+                     dtype=torch.uint8, device="cuda")
+    pk.run_host(f(wl.Abar), f(wl.Bbar), f(wl.C), f(wl.D), u_h, y_h, list(wl.N), mode, ws)
+    assert np.array_equal(y_h.float().double().numpy(), y_dev)
