@@ -238,9 +238,13 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
   if (TCOLS == 512 && tmem_base != 0) __trap();
   const uint32_t tbase = TCOLS == 512 ? 0u : tmem_base;
 
+  // Producer loops run on the whole warp and only lane 0 issues: a loop inside a lane-divergent
+  // region makes ptxas keep every role's loop-carried values in per-thread registers, and the MMA
+  // warp then pays R2UR conversions for each MMA operand (measured: 49 per 12-MMA chunk, 0 this way).
   if (warp == 0) {
     // =========================================================== TMA producer
-    if (lane == 0) {
+    {
+      const bool issue = lane == 0;
       int s = 0, s_last = -1, cur_sys = -1;
       uint32_t ph = 0, ph_last = 0;
       for (Walk w(n_tiles, a.gt); w.valid(); w.next()) {
@@ -250,14 +254,16 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
           if (s_last >= 0) TWM(0, mbar_wait(&empty[s_last], ph_last));
           uint32_t bytes = 0;
           for (int src = 0; src < a.n_src; ++src) bytes += (uint32_t)(a.K[src] / BK) * C::NW * C::W_BYTES;
-          mbar_arrive_expect_tx(&w_full, bytes);
+          if (issue) mbar_arrive_expect_tx(&w_full, bytes);
           int ci = 0;
           for (int src = 0; src < a.n_src; ++src) {
             const int plane = tc.sys * a.w_plane_stride[src] + a.w_plane_off[src];
             for (int kc = 0; kc < a.K[src] / BK; ++kc, ++ci) {
               uint8_t* wdst = sWres + ci * C::NW * C::W_BYTES;
-              tma_load_3d(wdst, &maps.W[src], &w_full, kc * BK, tc.nb * BN, plane);
-              if (TF32) tma_load_3d(wdst + C::W_BYTES, &maps.W[src], &w_full, kc * BK, tc.nb * BN, plane + 1);
+              if (issue) {
+                tma_load_3d(wdst, &maps.W[src], &w_full, kc * BK, tc.nb * BN, plane);
+                if (TF32) tma_load_3d(wdst + C::W_BYTES, &maps.W[src], &w_full, kc * BK, tc.nb * BN, plane + 1);
+              }
             }
           }
           cur_sys = tc.sys;
@@ -267,11 +273,13 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
           const int plane = tc.sys * a.w_plane_stride[src] + a.w_plane_off[src];
           for (int kc = 0; kc < nk; ++kc) {
             TWM(1, mbar_wait(&empty[s], ph ^ 1));
-            mbar_arrive_expect_tx(&full[s], C::TMA_BYTES);
-            tma_load_3d(stA(s), &maps.A[src], &full[s], kc * BK, a.a_row0[src] + tc.l0 - (int)a.shift[src], tc.seq);
-            if (!WRES) {
-              tma_load_3d(stW(s), &maps.W[src], &full[s], kc * BK, tc.nb * BN, plane);
-              if (TF32) tma_load_3d(stWlo(s), &maps.W[src], &full[s], kc * BK, tc.nb * BN, plane + 1);
+            if (issue) {
+              mbar_arrive_expect_tx(&full[s], C::TMA_BYTES);
+              tma_load_3d(stA(s), &maps.A[src], &full[s], kc * BK, a.a_row0[src] + tc.l0 - (int)a.shift[src], tc.seq);
+              if (!WRES) {
+                tma_load_3d(stW(s), &maps.W[src], &full[s], kc * BK, tc.nb * BN, plane);
+                if (TF32) tma_load_3d(stWlo(s), &maps.W[src], &full[s], kc * BK, tc.nb * BN, plane + 1);
+              }
             }
             s_last = s;
             ph_last = ph;
@@ -282,18 +290,21 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
     }
   } else if (warp == C::R_WARP) {
     // =========================================================== residual / staging producer
-    if (lane == 0) {
+    {
+      const bool issue = lane == 0;
       int rs = 0;
       uint32_t rph = 0;
       for (Walk w(n_tiles, a.gt); w.valid(); w.next()) {
         const TileCoord tc = decode(w.tile(), a, n_nblk, nt_eff);
         for (int j = 0; j < NCH; ++j) {
           TWM(20, mbar_wait(&rempty[rs], rph ^ 1));
-          if (a.has_residual) {
-            mbar_arrive_expect_tx(&rfull[rs], C::R_BYTES);
-            tma_load_3d(sR + rs * C::R_BYTES, &maps.R, &rfull[rs], tc.nb * BN + j * C::CW, a.r_row0 + tc.l0, tc.seq);
-          } else {
-            mbar_arrive(&rfull[rs]);
+          if (issue) {
+            if (a.has_residual) {
+              mbar_arrive_expect_tx(&rfull[rs], C::R_BYTES);
+              tma_load_3d(sR + rs * C::R_BYTES, &maps.R, &rfull[rs], tc.nb * BN + j * C::CW, a.r_row0 + tc.l0, tc.seq);
+            } else {
+              mbar_arrive(&rfull[rs]);
+            }
           }
           if (++rs == RS) { rs = 0; rph ^= 1; }
         }
@@ -306,10 +317,13 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
       int s = 0, cur_sys = -1;
       uint32_t ph = 0, wph = 0;
       int64_t t_local = 0, j = 0;                 // tiles / chunks consumed by this CTA
+      int nch_tile = 0;                           // K chunks per tile, all sources in order
+#pragma unroll
+      for (int q = 0; q < 3; ++q) if (q < a.n_src) nch_tile += a.K[q] / BK;
       for (Walk w(n_tiles, a.gt); w.valid(); w.next(), ++t_local) {
         const TileCoord tc = decode(w.tile(), a, n_nblk, nt_eff);
         const int acc = (int)(t_local & 1);
-        TWM(4, mbar_wait(&tempty[acc], (uint32_t)((t_local >> 1) & 1) ^ 1));
+        TWM(4, mbar_wait_u(&tempty[acc], (uint32_t)((t_local >> 1) & 1) ^ 1));
         if (WRES && tc.sys != cur_sys) {
           TWM(5, mbar_wait(&w_full, wph));
           wph ^= 1;
@@ -318,12 +332,10 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
         tc_fence_after();
         const uint32_t d = tbase + acc * ACOLS, dc = d + BN;
         bool first = true;
-        int ci = 0;
-        for (int src = 0; src < a.n_src; ++src) {
-          const int nk = a.K[src] / BK;
-          for (int kc = 0; kc < nk; ++kc, ++ci, ++j) {
+        for (int ci = 0; ci < nch_tile; ++ci, ++j) {
+          {
             if (TF32) {
-              if (WRES || TSA) TWM(6, mbar_wait(&lo_ready[j & 1], (uint32_t)((j >> 1) & 1)));
+              if (WRES || TSA) TWM(6, mbar_wait_u(&lo_ready[j & 1], (uint32_t)((j >> 1) & 1)));
               else TWM(6, mbar_wait(&lo_ready[s], ph));
             } else {
               TWM(6, mbar_wait(&full[s], ph));

@@ -35,6 +35,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
+// Whole-warp wait with a warp-uniform exit (vote): code after it stays uniform control flow, so
+// ptxas can keep loop-carried MMA operands in uniform registers.
+__device__ __forceinline__ void mbar_wait_u(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "vote.sync.all.pred p, p, 0xffffffff;\n\t"
+      "@!p bra.uni WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
 // ------------------------------------------------------------------ proxies / fences
 __device__ __forceinline__ void fence_async_smem() {       // generic-proxy smem writes -> async proxy
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
