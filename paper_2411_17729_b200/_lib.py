@@ -6,6 +6,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcascade_b200.so")
+# diagnostics only: A/B two builds of the library within one process launch environment
+if os.environ.get("CASC_LIB_OVERRIDE"):
+    LIB_PATH = os.path.abspath(os.environ["CASC_LIB_OVERRIDE"])
 
 c_int, c_size_t, c_int64, c_void_p, c_char_p = ctypes.c_int, ctypes.c_size_t, ctypes.c_int64, ctypes.c_void_p, ctypes.c_char_p
 P_int = ctypes.POINTER(ctypes.c_int)

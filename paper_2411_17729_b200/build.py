@@ -52,6 +52,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     flags = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
              "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
+    flags += os.environ.get("CASC_NVCC_FLAGS", "").split()          # diagnostics builds only
     if verbose:
         flags += ["-Xptxas", "-v"]
     from concurrent.futures import ThreadPoolExecutor

@@ -654,7 +654,9 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       }
       // algorithmic (unfused streaming) bytes and flops of the two stages this pass applies
       ProfScope ps(st, K_BANK_STAGE, 4.0 * cnt2 * batch * L * m * 4.0, 4.0 * cnt2 * batch * L * (double)mm);
-      if ((rc = launch_mimo_gemm(g, true, st))) return rc;
+      rc = launch_bank_hist(g, st);
+      if (rc == CASC_ERR_UNSUPPORTED) rc = launch_mimo_gemm(g, true, st);
+      if (rc) return rc;
     }
     if (cnt1 > 0) {
       MimoGemm g{};
@@ -667,7 +669,9 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
         g.t_first = 0;
       }
       ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt1 * batch * L * m * 4.0, 2.0 * cnt1 * batch * L * (double)mm);
-      if ((rc = launch_mimo_gemm(g, true, st))) return rc;
+      rc = launch_bank_hist(g, st);
+      if (rc == CASC_ERR_UNSUPPORTED) rc = launch_mimo_gemm(g, true, st);
+      if (rc) return rc;
     }
     if ((rc = emit(count_ge(k + 3), count_ge(k + 1)))) return rc;     // channels with Ne in {k + 1, k + 2}
   }

@@ -135,7 +135,12 @@ __device__ __forceinline__ TileCoord decode(int64_t tile, const MimoArg& a, int 
   TileCoord t;
   t.nb = (int)(tile % n_nblk);
   const int64_t r = tile / n_nblk;
-  t.l0 = (int)((a.t_first + r % nt_eff) * BM);
+  // Time tiles in residue-class order: with S = nt_eff / perm_j (the smallest shift in tiles),
+  // position q holds tile (q % perm_j) * S + q / perm_j, so the tiles reading a row (as the
+  // residual and at shifts S, 2S, 3S) follow each other and the row is fetched from DRAM once.
+  int64_t q = r % nt_eff;
+  if (a.perm_j) q = (q % a.perm_j) * (nt_eff / a.perm_j) + q / a.perm_j;
+  t.l0 = (int)((a.t_first + q) * BM);
   const int64_t sidx = r / nt_eff;
   const int li = (int)(sidx / a.batch), b = (int)(sidx % a.batch);
   const int sys = a.sys_list ? a.sys_list[li] : 0;
@@ -173,8 +178,11 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
   // corr chain's error is 2^-11 smaller. The epilogue sums main + corr with round-to-nearest.
   constexpr int ACOLS = TF32 ? 2 * BN : BN;
   constexpr bool TSA = C::TSA;
-  constexpr uint32_t AU0 = 2 * ACOLS;                        // TSA: two A units (hi | lo) of 64 columns
-  constexpr int TUSED = 2 * ACOLS + (TSA ? 128 : 0);
+  constexpr uint32_t AU0 = 2 * ACOLS;                        // TSA: first A unit (hi | lo, 64 columns)
+  // A units (TSA: TMEM, 64 columns each; weight-resident SS: shared-memory lo slots): with four
+  // units the transform of chunk j + 2 no longer waits for the MMAs of chunk j to complete
+  constexpr int NAU_SH = TSA ? 2 : 1, NAU = 1 << NAU_SH;
+  constexpr int TUSED = 2 * ACOLS + (TSA ? 64 * NAU : 0);
   static_assert(TUSED <= 512, "TMEM holds 512 columns");
   constexpr int TCOLS = TUSED <= 32 ? 32 : TUSED <= 64 ? 64 : TUSED <= 128 ? 128 : TUSED <= 256 ? 256 : 512;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -182,9 +190,9 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
   uint8_t* sWres = smem + STAGES * C::STAGE_BYTES;           // [WCH][hi, lo] (weight-resident)
   uint8_t* sAlo = sWres + C::WBUF;                           // [ALO] (weight-resident 3xTF32)
   uint8_t* sR = sAlo + C::ALO * C::A_BYTES;                  // [RS][R_BYTES]
-  constexpr int NLO = (WRES || TSA) ? 2 : STAGES;            // lo_ready barriers
-  __shared__ uint64_t full[STAGES], empty[STAGES], lo_ready[NLO], alo_free[2], tfull[2], tempty[2],
-      rfull[RS], rempty[RS], w_full;
+  constexpr int NLO = (WRES || TSA) ? NAU : STAGES;            // lo_ready barriers
+  __shared__ uint64_t full[STAGES], empty[STAGES], lo_ready[NLO], alo_free[NAU], tfull[2], tempty[2],
+      rfull[RS], rempty[RS], w_full, wfree;
   __shared__ uint32_t tmem_base;
   auto stA = [&](int s) { return smem + s * C::STAGE_BYTES; };
   auto stW = [&](int s) { return smem + s * C::STAGE_BYTES + C::A_BYTES; };
@@ -216,11 +224,14 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
   constexpr int NCH = BN / C::CW;                   // epilogue chunks per tile
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    // TSA + resident weights: a ring slot (A only) is free once the transform warps have read it
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], (TSA && WRES) ? 128 : 1); }
     for (int s = 0; s < NLO; ++s) mbar_init(&lo_ready[s], 128);
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); mbar_init(&alo_free[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
+    for (int s = 0; s < NAU; ++s) mbar_init(&alo_free[s], 1);
     for (int s = 0; s < RS; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 1); }
     mbar_init(&w_full, 1);
+    mbar_init(&wfree, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<TCOLS>(&tmem_base);
@@ -245,13 +256,15 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
     // =========================================================== TMA producer
     {
       const bool issue = lane == 0;
-      int s = 0, s_last = -1, cur_sys = -1;
-      uint32_t ph = 0, ph_last = 0;
+      int s = 0, cur_sys = -1, n_reload = 0;
+      uint32_t ph = 0;
       for (Walk w(n_tiles, a.gt); w.valid(); w.next()) {
         const TileCoord tc = decode(w.tile(), a, n_nblk, nt_eff);
         if (WRES && tc.sys != cur_sys) {
-          // every MMA issued so far must be done with the resident weights (MMAs complete in order)
-          if (s_last >= 0) TWM(0, mbar_wait(&empty[s_last], ph_last));
+          // every MMA with the previous weights must be complete (the MMA warp commits wfree when it
+          // meets the system change)
+          if (n_reload > 0) TWM(0, mbar_wait(&wfree, (uint32_t)((n_reload - 1) & 1)));
+          ++n_reload;
           uint32_t bytes = 0;
           for (int src = 0; src < a.n_src; ++src) bytes += (uint32_t)(a.K[src] / BK) * C::NW * C::W_BYTES;
           if (issue) mbar_arrive_expect_tx(&w_full, bytes);
@@ -281,8 +294,6 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
                 if (TF32) tma_load_3d(stWlo(s), &maps.W[src], &full[s], kc * BK, tc.nb * BN, plane + 1);
               }
             }
-            s_last = s;
-            ph_last = ph;
             if (++s == STAGES) { s = 0; ph ^= 1; }
           }
         }
@@ -314,6 +325,8 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
     // =========================================================== MMA issuer (whole warp, elected lane issues)
     {
       const uint32_t idesc = make_idesc(TF32 ? FMT_TF32 : FMT_BF16, BM, BN);
+      const uint32_t idesc128 = make_idesc(FMT_TF32, BM, 2 * BN);   // TSA: A hi x [W hi | W lo]
+      const bool mma8 = a.mma8 != 0;
       int s = 0, cur_sys = -1;
       uint32_t ph = 0, wph = 0;
       int64_t t_local = 0, j = 0;                 // tiles / chunks consumed by this CTA
@@ -325,6 +338,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
         const int acc = (int)(t_local & 1);
         TWM(4, mbar_wait_u(&tempty[acc], (uint32_t)((t_local >> 1) & 1) ^ 1));
         if (WRES && tc.sys != cur_sys) {
+          if (cur_sys >= 0) mma_commit_w(&wfree);   // all MMAs issued so far used the old weights
           TWM(5, mbar_wait(&w_full, wph));
           wph ^= 1;
           cur_sys = tc.sys;
@@ -335,27 +349,28 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
         for (int ci = 0; ci < nch_tile; ++ci, ++j) {
           {
             if (TF32) {
-              if (WRES || TSA) TWM(6, mbar_wait_u(&lo_ready[j & 1], (uint32_t)((j >> 1) & 1)));
+              if (WRES || TSA) TWM(6, mbar_wait_u(&lo_ready[j & (NAU - 1)], (uint32_t)((j >> NAU_SH) & 1)));
               else TWM(6, mbar_wait(&lo_ready[s], ph));
             } else {
               TWM(6, mbar_wait(&full[s], ph));
             }
             tc_fence_after();
-            if constexpr (TSA) {                        // A from TMEM unit (j & 1): hi | lo
-              const uint32_t ah = tbase + AU0 + (uint32_t)(j & 1) * 64, al = ah + 32;
+            if constexpr (TSA) {                        // A from TMEM unit (j & (NAU - 1)): hi | lo
+              const uint32_t ah = tbase + AU0 + (uint32_t)(j & (NAU - 1)) * 64, al = ah + 32;
               const uint64_t wd0 = make_sdesc(WRES ? smem_u32(sWres + ci * C::NW * C::W_BYTES) : smem_u32(stW(s)), 16, 1024,
                                               LAYOUT_SW128);
               // main: hi.hi; corr: lo.hi + hi.lo (four K-steps, one asm block)
-              mma_3xtf32_ts_chunk_w(d, dc, ah, al, wd0, sdesc_add(wd0, C::W_BYTES), idesc, first ? 0u : 1u);
+              if (mma8) mma_3xtf32_ts_chunk8_w(d, dc, ah, al, wd0, idesc128, idesc, first ? 0u : 1u);
+              else mma_3xtf32_ts_chunk_w(d, dc, ah, al, wd0, sdesc_add(wd0, C::W_BYTES), idesc, first ? 0u : 1u);
               first = false;
-              mma_commit_w(&empty[s]);
-              mma_commit_w(&alo_free[j & 1]);
+              if (!WRES) mma_commit_w(&empty[s]);         // the slot also holds W
+              mma_commit_w(&alo_free[j & (NAU - 1)]);
               if (++s == STAGES) { s = 0; ph ^= 1; }
               continue;
             }
             const uint32_t a0 = smem_u32(stA(s));
             const uint32_t w0 = WRES ? smem_u32(sWres + ci * C::NW * C::W_BYTES) : smem_u32(stW(s));
-            const uint32_t al0 = WRES ? smem_u32(sAlo + (j & 1) * C::A_BYTES) : smem_u32(stAlo(s));
+            const uint32_t al0 = WRES ? smem_u32(sAlo + (j & (NAU - 1)) * C::A_BYTES) : smem_u32(stAlo(s));
             const uint64_t ad0 = make_sdesc(a0, 16, 1024, LAYOUT_SW128), wd0 = make_sdesc(w0, 16, 1024, LAYOUT_SW128);
             const uint64_t ald0 = make_sdesc(al0, 16, 1024, LAYOUT_SW128), wld0 = sdesc_add(wd0, C::W_BYTES);
 #pragma unroll
@@ -371,7 +386,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
               first = false;
             }
             mma_commit_w(&empty[s]);
-            if (WRES && TF32) mma_commit_w(&alo_free[j & 1]);
+            if (WRES && TF32) mma_commit_w(&alo_free[j & (NAU - 1)]);
             if (++s == STAGES) { s = 0; ph ^= 1; }
           }
         }
@@ -403,20 +418,21 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
                 lv[4 * cc] = __float_as_uint(l.x); lv[4 * cc + 1] = __float_as_uint(l.y);
                 lv[4 * cc + 2] = __float_as_uint(l.z); lv[4 * cc + 3] = __float_as_uint(l.w);
               }
-              TWM(9, mbar_wait(&alo_free[j & 1], (uint32_t)(((j >> 1) & 1) ^ 1)));
+              if (WRES) mbar_arrive(&empty[s]);         // slot read: the producer may refill it
+              TWM(9, mbar_wait(&alo_free[j & (NAU - 1)], (uint32_t)(((j >> NAU_SH) & 1) ^ 1)));
               tc_fence_after();
-              const uint32_t ta = tbase + ((uint32_t)((warp & 3) * 32) << 16) + AU0 + (uint32_t)(j & 1) * 64;
+              const uint32_t ta = tbase + ((uint32_t)((warp & 3) * 32) << 16) + AU0 + (uint32_t)(j & (NAU - 1)) * 64;
               tmem_st32(ta, hv);
               tmem_st32(ta + 32, lv);
               tmem_wait_st();
               tc_fence_before();
-              mbar_arrive(&lo_ready[j & 1]);
+              mbar_arrive(&lo_ready[j & (NAU - 1)]);
               if (++s == STAGES) { s = 0; ph ^= 1; }
               continue;
             }
-            if (WRES && j >= 2) mbar_wait(&alo_free[j & 1], (uint32_t)(((j - 2) >> 1) & 1));
+            if (WRES && j >= NAU) mbar_wait(&alo_free[j & (NAU - 1)], (uint32_t)(((j - NAU) >> NAU_SH) & 1));
             float4* hi = reinterpret_cast<float4*>(stA(s));
-            float4* out = reinterpret_cast<float4*>(WRES ? sAlo + (j & 1) * C::A_BYTES : stAlo(s));
+            float4* out = reinterpret_cast<float4*>(WRES ? sAlo + (j & (NAU - 1)) * C::A_BYTES : stAlo(s));
 #pragma unroll
             for (int e = t; e < (int)(C::A_BYTES / 16); e += 128) {
               const float4 v = hi[e], h = tf32_hi4(v);
@@ -424,7 +440,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
               out[e] = tf32_lo4(v, h);
             }
             fence_async_smem();
-            mbar_arrive(&lo_ready[WRES ? (int)(j & 1) : s]);
+            mbar_arrive(&lo_ready[WRES ? (int)(j & (NAU - 1)) : s]);
             if (++s == STAGES) { s = 0; ph ^= 1; }
           }
         }
@@ -594,6 +610,18 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
     const int64_t planes = g.src[s].w_planes > 0 ? g.src[s].w_planes : (TF32 ? 2 : 1);
     if (!map3d(&maps.W[s], g.src[s].W, TF32, g.src[s].K, g.n_out, planes, BN)) return CASC_ERR_CUDA;
   }
+  {
+    // stride of the shifts in time tiles -> tile order (decode); CASC_GEMM_PERM=0 keeps the natural order
+    static const bool perm_on = [] {
+      const char* e = getenv("CASC_GEMM_PERM");
+      return !(e && e[0] == '0');
+    }();
+    int64_t S = 0;
+    for (int s = 0; s < g.n_src; ++s)
+      if (g.src[s].shift > 0 && g.src[s].shift % BM == 0) S = S ? std::min<int64_t>(S, g.src[s].shift / BM) : g.src[s].shift / BM;
+    const int64_t nt_eff = (g.L + BM - 1) / BM - g.t_first;
+    a.perm_j = (perm_on && S > 1 && nt_eff % S == 0) ? nt_eff / S : 0;
+  }
   a.has_residual = g.R != nullptr;
   a.r_row0 = (int)g.R_row0;
   a.out_row0 = (int)g.out_row0;
@@ -607,6 +635,10 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
   // weight-resident: contiguous ranges; otherwise round-robin single tiles
   a.gt = WCH > 0 ? ceil_div(tiles, std::min<int64_t>(tiles, 148)) : 1;
   const int grid = (int)std::min<int64_t>(ceil_div(tiles, a.gt), 148);
+  {
+    const char* e8 = getenv("CASC_GEMM_MMA8");
+    a.mma8 = (e8 && e8[0] == '0') ? 0 : 1;
+  }
   static unsigned long long* dbg = nullptr;
   const bool want_dbg = getenv("CASC_GEMM_DBG") != nullptr;
   if (want_dbg) {
@@ -627,7 +659,7 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
     fprintf(stderr, "casc gemm dbg BN=%d tf32=%d wch=%d n_src=%d grid=%d tiles=%lld: cycles/CTA %.0f |", BN, (int)TF32, WCH,
             g.n_src, grid, (long long)tiles, tot);
     for (int i = 0; i < 23; ++i)
-      if (h[i]) fprintf(stderr, " %s %.0f%%", nm[i], 100.0 * h[i] / grid / tot / ((i >= 8 && i < 16) ? 4.0 : 1.0));
+      if (h[i]) fprintf(stderr, " %s %.0f%%", nm[i], 100.0 * h[i] / grid / tot / ((i == 8 || i == 9 || (i >= 12 && i < 16)) ? 4.0 : 1.0));
     fprintf(stderr, "\n");
   }
   return CASC_OK;
@@ -648,7 +680,16 @@ int launch_mimo_gemm(const MimoGemm& g, bool tf32, cudaStream_t st) {
         int chunks = 0;
         for (int s = 0; s < g.n_src; ++s) chunks += g.src[s].K / 32;
         if (chunks <= 2) return launch_cfg<64, true, 4, 2>(g, st);
-        if (chunks <= 6) return launch_cfg<64, true, 2, 6>(g, st);
+        if (chunks <= 6) {
+          // stage pairs: residual chunks vs A ring slots (CASC_GEMM_PAIR_RS = 2 | 3 | 4)
+          static const int prs = [] {
+            const char* e = getenv("CASC_GEMM_PAIR_RS");
+            return e ? atoi(e) : 2;
+          }();
+          if (prs == 3) return launch_cfg<64, true, 3, 6>(g, st);
+          if (prs == 4) return launch_cfg<64, true, 4, 6>(g, st);
+          return launch_cfg<64, true, 2, 6>(g, st);
+        }
       }
       if (rs == 2) return launch_cfg<64, true, 2>(g, st);
       if (rs == 6) return launch_cfg<64, true, 6>(g, st);

@@ -24,6 +24,8 @@ struct MimoArg {
   const int* ab_neff; int ab_level; const float* ab_c; const float* ab_w; float* ab;
   int64_t gt;                        // tiles per block of the CTA tile walk
   unsigned long long* dbg;           // optional wait-cycle counters (CASC_GEMM_DBG=1)
+  int mma8;                          // TSA 3xTF32: 8 MMAs per chunk (N = 128 hi.[hi|lo]) instead of 12
+  int64_t perm_j;                    // time-tile order within a sequence (0: natural), see decode()
 };
 struct MimoSrc {
   const void* A; const void* W; int K; int64_t shift;
@@ -49,6 +51,9 @@ bool mimo_tc_supported(int m, int p, int q);
 bool map3d(CUtensorMap* m, const void* base, bool f32, int64_t d0, int64_t d1, int64_t d2, int rows);
 // tf32 = true: 3xTF32 (fp32 signals, weights as tf32 hi/lo planes); else bf16.
 int launch_mimo_gemm(const MimoGemm& g, bool tf32, cudaStream_t st);
+// Bank stage pass with the state history resident in shared memory (bank_hist.cu): m = 64 fp32,
+// 1 or 3 sources v at shifts c * s (s a multiple of 128); CASC_ERR_UNSUPPORTED otherwise.
+int launch_bank_hist(const MimoGemm& g, cudaStream_t st);
 // bf16, n_out % 256 == 0, one system: 256 x 256 tiles on CTA pairs (mimo_tc2.cu)
 bool mimo_pair_ok(const MimoGemm& g, bool tf32);
 int launch_mimo_gemm_pair(const MimoGemm& g, cudaStream_t st);

@@ -164,7 +164,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 
   if (warp == 0) {
     // =========================================================== TMA producer (both CTAs)
-    if (lane == 0) {
+    {                                         // whole warp loops, lane 0 issues (uniform MMA operands, mimo_tc.cu)
+      const bool issue = lane == 0;
       int s = 0;
       uint32_t ph = 0;
       for (int64_t t = pair; t < n_tiles; t += n_pairs) {
@@ -174,11 +175,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const int plane = a.w_plane_off[src];
           for (int kc = 0; kc < nk; ++kc) {
             mbar_wait(&empty[s], ph ^ 1);
-            if (is_leader) mbar_arrive_expect_tx(&full[s], 2 * STAGE_BYTES);
-            uint32_t fb;                            // the leader CTA's full[s] (shared::cluster)
-            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(fb) : "r"(smem_u32(&full[s])));
-            tma_load_2sm(stA(s), &maps.A[src], fb, kc * BK, a.a_row0[src] + tc.l0 - (int)a.shift[src], tc.seq);
-            tma_load_2sm(stW(s), &maps.W[src], fb, kc * BK, tc.nb * BN + (int)rank * 128, plane);
+            if (issue) {
+              if (is_leader) mbar_arrive_expect_tx(&full[s], 2 * STAGE_BYTES);
+              uint32_t fb;                          // the leader CTA's full[s] (shared::cluster)
+              asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(fb) : "r"(smem_u32(&full[s])));
+              tma_load_2sm(stA(s), &maps.A[src], fb, kc * BK, a.a_row0[src] + tc.l0 - (int)a.shift[src], tc.seq);
+              tma_load_2sm(stW(s), &maps.W[src], fb, kc * BK, tc.nb * BN + (int)rank * 128, plane);
+            }
             if (++s == STAGES) { s = 0; ph ^= 1; }
           }
         }
@@ -186,14 +189,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
   } else if (warp == R_WARP) {
     // =========================================================== residual / staging producer (per CTA)
-    if (lane == 0) {
+    {
+      const bool issue = lane == 0;
       int rs = 0;
       uint32_t rph = 0;
       for (int64_t t = pair; t < n_tiles; t += n_pairs) {
         const PairCoord tc = decode2(t, a, n_nblk, nb_eff, t0_blk, rank);
         for (int j = 0; j < NCH; ++j) {
           mbar_wait(&rempty[rs], rph ^ 1);
-          if (a.has_residual) {
+          if (!issue) {
+          } else if (a.has_residual) {
             mbar_arrive_expect_tx(&rfull[rs], R_BYTES);
             tma_load_1(sR + rs * R_BYTES, &maps.R, &rfull[rs], tc.nb * BN + j * CW, a.r_row0 + tc.l0, tc.seq);
           } else {

@@ -164,6 +164,29 @@ __device__ __forceinline__ void mma_3xtf32_ts_chunk_w(uint32_t d, uint32_t dc, u
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [a3], v3, %6, 1;\n\t}"
       ::"r"(d), "r"(dc), "r"(ah), "r"(al), "l"(wd), "l"(wl), "r"(idesc), "r"(acc));
 }
+// The same chunk with 8 MMAs: the hi.hi and hi.lo products share A = a_hi, so one N = 2*64 MMA
+// against [W hi | W lo] (lo stored right after hi: one K-major SW128 operand of 128 rows) writes
+// hi.hi to d and hi.lo to d + 64 = dc; lo.hi then accumulates into dc. Fewer MMA instructions and
+// operands per chunk (the issuing warp's instruction stream bounds the N = 64 bank stage).
+__device__ __forceinline__ void mma_3xtf32_ts_chunk8_w(uint32_t d, uint32_t dc, uint32_t ah, uint32_t al,
+                                                       uint64_t wd, uint32_t idesc128, uint32_t idesc64,
+                                                       uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 a1, a2, a3, l1, l2, l3;\n\t.reg .b64 w1, w2, w3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %6, 0;\n\t"
+      "add.u32 a1, %2, 8;\n\tadd.u32 a2, %2, 16;\n\tadd.u32 a3, %2, 24;\n\t"
+      "add.u32 l1, %3, 8;\n\tadd.u32 l2, %3, 16;\n\tadd.u32 l3, %3, 24;\n\t"
+      "add.u64 w1, %4, 2;\n\tadd.u64 w2, %4, 4;\n\tadd.u64 w3, %4, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %4, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%3], %4, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a1], w1, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [l1], w1, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a2], w2, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [l2], w2, %7, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a3], w3, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [l3], w3, %7, 1;\n\t}"
+      ::"r"(d), "r"(dc), "r"(ah), "r"(al), "l"(wd), "r"(idesc128), "r"(acc), "r"(idesc64));
+}
 __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
   asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
                "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
