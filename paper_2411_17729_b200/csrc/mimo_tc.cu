@@ -684,7 +684,7 @@ int launch_mimo_gemm(const MimoGemm& g, bool tf32, cudaStream_t st) {
           // stage pairs: residual chunks vs A ring slots (CASC_GEMM_PAIR_RS = 2 | 3 | 4)
           static const int prs = [] {
             const char* e = getenv("CASC_GEMM_PAIR_RS");
-            return e ? atoi(e) : 2;
+            return e ? atoi(e) : 3;
           }();
           if (prs == 3) return launch_cfg<64, true, 3, 6>(g, st);
           if (prs == 4) return launch_cfg<64, true, 4, 6>(g, st);

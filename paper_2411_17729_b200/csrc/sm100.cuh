@@ -27,12 +27,17 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}"
                ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+// The lanes that entered together leave together: lanes spinning independently can exit the
+// loop in different iterations, and a .sync.aligned tcgen05.ld / st right after a diverged exit
+// corrupted one 32-lane quadrant of a tile in bank_hist.cu (found under load, tools/hist_diag.py).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const unsigned lanes = __activemask();
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+  __syncwarp(lanes);
 }
 
 // Whole-warp wait with a warp-uniform exit (vote): code after it stays uniform control flow, so
