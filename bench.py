@@ -187,11 +187,15 @@ def roofline(prof: dict, mode: str, cfg: str):
         ach = by / t / 1e9
         peak = pk["hbm_gbs"]
         note = "HBM copy bandwidth (%s)" % pk["source"]
-        if cls == "bank_stage":
-            note += ("; algorithmic bytes = one read + one write of the m x (L batch) state per stage "
-                     "(SURVEY 8d); a bank_stage pass applies two stages (R23), so its DRAM traffic "
-                     "(ncu, 'traffic') is about half of them")
         out = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak}
+        if cls == "bank_stage":
+            # B_fused = the bytes of the schedule run (one read + one write of the m x L
+            # state per pass; a pair pass applies two stages, R23); B_ns = one read + one write per
+            # stage = flops * 4 / m (8m B and 2m^2 flop per row and stage, m = 64)
+            note += ("; achieved/frac: B_fused = one read + one write of the state per pass (a pair "
+                     "pass applies two stages); frac_ns: B_ns = one read + one write per stage")
+            ach_ns = fl * 4.0 / 64.0 / t / 1e9
+            out.update({"achieved_ns": ach_ns, "frac_ns": ach_ns / peak})
     out.update({"traffic": ncu_traffic(cls, cfg), "kernel": cls, "launches_timed": r["launches"],
                 "avg_launch_ms": t * 1e3, "algorithmic_bytes_per_launch": by,
                 "algorithmic_flops_per_launch": fl, "peak_note": note})

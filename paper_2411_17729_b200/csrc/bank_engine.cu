@@ -652,8 +652,9 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
         g.ab_neff = dNeff; g.ab_level = k + 2; g.ab_c = w.c32; g.ab_w = w.w32; g.ab = w.ab;
         if (count_ge(k + 2) > count_ge(k + 3)) g.t_first = 0;
       }
-      // algorithmic (unfused streaming) bytes and flops of the two stages this pass applies
-      ProfScope ps(st, K_BANK_STAGE, 4.0 * cnt2 * batch * L * m * 4.0, 4.0 * cnt2 * batch * L * (double)mm);
+      // bytes of the schedule run (SURVEY 8d B_fused): one read + one write of the state for the two
+      // stages this pass applies; flops of both stages (bench.py derives the unfused B_ns from them)
+      ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt2 * batch * L * m * 4.0, 4.0 * cnt2 * batch * L * (double)mm);
       rc = launch_bank_hist(g, st);
       if (rc == CASC_ERR_UNSUPPORTED) rc = launch_mimo_gemm(g, true, st);
       if (rc) return rc;
