@@ -4,9 +4,13 @@
 //
 // per 128-step tile one K = 128 GEMM (3xTF32: hi.hi + lo.hi + hi.lo) whose A operand, the
 // Toeplitz matrix u_{l-j}, is a 4 KB shared-memory buffer Z read with LBO = 64 B (row r, K chunk
-// c' = Z-row r + 4c'). Roles (192 threads, two CTAs per SM):
+// c' = Z-row r + 4c'). The Krylov weights are stored hi and lo stacked along N ([K chunk][hi 64 |
+// lo 64 rows]), so Z_hi x [B_hi | B_lo] is one N = 128 MMA writing hi.hi to the main and hi.lo to
+// the correction accumulator, and Z_lo x B_hi (N = 64) adds to the correction: the MMAs read 14 KB
+// of shared memory per K step instead of 18 KB (shared-memory bandwidth bounds this kernel).
+// Roles (192 threads, two CTAs per SM):
 //   warp 0     builds Z for the next tiles into a 2-slot ring (u staged through shared memory)
-//   warp 1     issues the 48 MMAs of a tile into one of two TMEM accumulators
+//   warp 1     issues the 32 MMAs of a tile into one of two TMEM accumulators (main | corr)
 //   warps 2-5  drain TMEM (lane = time row) into a SWIZZLE_128B staging tile and TMA-store it
 // Each CTA walks `tiles_per_cta` consecutive tiles of one sequence, so the Krylov weights
 // (64 KB of hi/lo) are loaded once per CTA.
@@ -39,9 +43,8 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared state space (STS/LDS, not generic ST/LD)
   float* Stg = reinterpret_cast<float*>(smem);                 // [128 rows][32] SW128 half tile, 16 KB
-  float* Bhi = Stg + TM * 32;                                  // [BCH][MS][4]
-  float* Blo = Bhi + KL * MS;
-  float* Zb = Blo + KL * MS;                                   // [2 slots][hi|lo][ZR][4]
+  float* Bc = Stg + TM * 32;                                   // [BCH][hi MS | lo MS][4]
+  float* Zb = Bc + 2 * KL * MS;                                // [2 slots][hi|lo][ZR][4]
   float* Us = Zb + 2 * 2 * ZR * 4;                             // [2 slots][264] u window
   __shared__ uint64_t z_full[2], z_empty[2], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
@@ -56,8 +59,8 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
   const float* kl = kh + MS * KL;
   for (int e = tid; e < MS * BCH; e += 192) {
     const int ch = e / MS, n = e % MS;
-    *reinterpret_cast<float4*>(Bhi + (ch * MS + n) * 4) = __ldg(reinterpret_cast<const float4*>(kh + n * KL + ch * 4));
-    *reinterpret_cast<float4*>(Blo + (ch * MS + n) * 4) = __ldg(reinterpret_cast<const float4*>(kl + n * KL + ch * 4));
+    *reinterpret_cast<float4*>(Bc + (ch * 2 * MS + n) * 4) = __ldg(reinterpret_cast<const float4*>(kh + n * KL + ch * 4));
+    *reinterpret_cast<float4*>(Bc + (ch * 2 * MS + MS + n) * 4) = __ldg(reinterpret_cast<const float4*>(kl + n * KL + ch * 4));
   }
   fence_async_smem();
   if (tid == 0) {
@@ -69,7 +72,7 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<2 * MS>(&tmem_base);
+  if (warp == 1) tmem_alloc<4 * MS>(&tmem_base);         // 2 slots x (main | corr)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -116,28 +119,26 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc(FMT_TF32, TM, MS);
-      const uint32_t bh = smem_u32(Bhi), bl = smem_u32(Blo);
+    {                                             // whole warp: operands stay in uniform registers
+      const uint32_t idesc = make_idesc(FMT_TF32, TM, MS), idesc2 = make_idesc(FMT_TF32, TM, 2 * MS);
+      const uint32_t bc = smem_u32(Bc);
       for (int i = 0; i < nt; ++i) {
         const int slot = i & 1;
-        mbar_wait(&z_full[slot], (uint32_t)((i >> 1) & 1));
-        mbar_wait(&tempty[slot], (uint32_t)(((i >> 1) & 1) ^ 1));
+        mbar_wait_u(&z_full[slot], (uint32_t)((i >> 1) & 1));
+        mbar_wait_u(&tempty[slot], (uint32_t)(((i >> 1) & 1) ^ 1));
         tc_fence_after();
         const uint32_t zh = smem_u32(Zb + slot * 2 * ZR * 4), zl = zh + ZR * 16;
-        const uint32_t acc = tbase + slot * MS;
+        const uint32_t acc = tbase + slot * 2 * MS;
 #pragma unroll 4
         for (int ks = 0; ks < KL / 8; ++ks) {
           const uint64_t azh = make_sdesc(zh + ks * 128, 64, 128, LAYOUT_NONE);
           const uint64_t azl = make_sdesc(zl + ks * 128, 64, 128, LAYOUT_NONE);
-          const uint64_t bdh = make_sdesc(bh + ks * 2 * MS * 16, MS * 16, 128, LAYOUT_NONE);
-          const uint64_t bdl = make_sdesc(bl + ks * 2 * MS * 16, MS * 16, 128, LAYOUT_NONE);
-          mma_tf32(acc, azh, bdh, idesc, ks > 0);
-          mma_tf32(acc, azl, bdh, idesc, 1);
-          mma_tf32(acc, azh, bdl, idesc, 1);
+          const uint64_t bd = make_sdesc(bc + ks * 2 * 2 * MS * 16, 2 * MS * 16, 128, LAYOUT_NONE);
+          mma_tf32_w(acc, azh, bd, idesc2, ks > 0);          // [hi.hi | hi.lo]
+          mma_tf32_w(acc + MS, azl, bd, idesc, 1);          // corr += lo.hi
         }
-        mma_commit(&z_empty[slot]);
-        mma_commit(&tfull[slot]);
+        mma_commit_w(&z_empty[slot]);
+        mma_commit_w(&tfull[slot]);
       }
     }
   } else {
@@ -147,11 +148,16 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
     const bool to_ab = a.ab != nullptr && a.Neff[c] == a.Kc[c];   // the cascade ends at the head
     for (int i = 0; i < nt; ++i) {
       const int slot = i & 1;
-      mbar_wait(&tfull[slot], (uint32_t)((i >> 1) & 1));
+      mbar_wait_u(&tfull[slot], (uint32_t)((i >> 1) & 1));
       tc_fence_after();
-      float v[MS];
+      float v[MS], vc[MS];
+      const uint32_t tacc = tbase + ((uint32_t)(q * 32) << 16) + slot * 2 * MS;
 #pragma unroll
-      for (int c0 = 0; c0 < MS; c0 += 16) tmem_ld16(tbase + ((uint32_t)(q * 32) << 16) + slot * MS + c0, v + c0);
+      for (int c0 = 0; c0 < MS; c0 += 16) tmem_ld16(tacc + c0, v + c0);
+#pragma unroll
+      for (int c0 = 0; c0 < MS; c0 += 16) tmem_ld16(tacc + MS + c0, vc + c0);
+#pragma unroll
+      for (int n = 0; n < MS; ++n) v[n] += vc[n];             // main + corr (round to nearest)
       tc_fence_before();
       mbar_arrive(&tempty[slot]);
       if (to_ab) {                                // y parts c . v, w . v instead of storing v
@@ -185,7 +191,7 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
     if (leader) bulk_wait0();
   }
   __syncthreads();
-  if (warp == 1) tmem_dealloc<2 * MS>(tbase);
+  if (warp == 1) tmem_dealloc<4 * MS>(tbase);
 }
 
 int launch_bank_head_ws(int m, const BankHeadArg& a, int64_t n_seq_total, cudaStream_t st) {
