@@ -133,6 +133,33 @@ __global__ void __launch_bounds__(256) powers_small_kernel(const double* Abar, c
       }
     }
     if (k == Ns) break;
+    if (m == 64) {
+      // P_{k+1} = P_k P_k on the fp64 tensor path (mma.sync m8n8k4 f64; per-element fused
+      // multiply-adds in float64 like the FMA loop below, in a different summation order): warp w
+      // owns rows 8w..8w+7, eight 8 x 8 column tiles, K = 64 in 16 steps of 4
+      const int w = tid / 32, lane = tid % 32, g = lane >> 2, t4 = lane & 3;
+      double d[8][2];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) d[n][0] = d[n][1] = 0.0;
+#pragma unroll 4
+      for (int ks = 0; ks < 16; ++ks) {
+        const double av = Pk[(8 * w + g) * LD + 4 * ks + t4];
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+          const double bv = Pk[(4 * ks + t4) * LD + 8 * n + g];
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(d[n][0]), "+d"(d[n][1]) : "d"(av), "d"(bv));
+        }
+      }
+      __syncthreads();                                  // all reads of P_k done
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        S[(8 * w + g) * LD + 8 * n + 2 * t4] = d[n][0];
+        S[(8 * w + g) * LD + 8 * n + 2 * t4 + 1] = d[n][1];
+      }
+      __syncthreads();
+      continue;
+    }
     double acc[4][4] = {};                              // P_{k+1} = P_k P_k
     for (int kk = 0; kk < m; ++kk) {
       double av[4], bv[4];
