@@ -269,6 +269,36 @@ __global__ void __launch_bounds__(256) bank_derived_kernel(const double* p64, in
     for (int e = tid; e < ms * ms; e += 256) Ps[(e / ms) * (ms + 1) + e % ms] = Ps0[i * mm + e];
     __syncthreads();
     const int cols = 1 << i;
+    if (ms == 64 && cols >= 8) {
+      // Kr[:, cols + j] = P_i Kr[:, j] on the fp64 tensor path (mma.sync m8n8k4 f64): warp w owns
+      // rows 8w..8w+7 and cols / 8 column tiles, K = 64 in 16 steps of 4
+      const int w = tid / 32, lane = tid % 32, g = lane >> 2, t4 = lane & 3;
+      for (int n0 = 0; n0 < cols; n0 += 64) {       // up to 8 column tiles per pass
+        double d[8][2];
+#pragma unroll
+        for (int n = 0; n < 8; ++n) d[n][0] = d[n][1] = 0.0;
+        const int ntile = (cols - n0) / 8 < 8 ? (cols - n0) / 8 : 8;
+        for (int ks = 0; ks < 16; ++ks) {
+          const double av = Ps[(8 * w + g) * (ms + 1) + 4 * ks + t4];
+#pragma unroll
+          for (int n = 0; n < 8; ++n) {
+            if (n < ntile) {
+              const double bv = Kr[(4 * ks + t4) * 129 + n0 + 8 * n + g];
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                           : "+d"(d[n][0]), "+d"(d[n][1]) : "d"(av), "d"(bv));
+            }
+          }
+        }
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+          if (n < ntile) {
+            Kr[(8 * w + g) * 129 + cols + n0 + 8 * n + 2 * t4] = d[n][0];
+            Kr[(8 * w + g) * 129 + cols + n0 + 8 * n + 2 * t4 + 1] = d[n][1];
+          }
+        }
+      }
+      continue;
+    }
     for (int e = tid; e < ms * cols; e += 256) {   // Kr[r][cols + j] = sum_k P_i[r][k] Kr[k][j]
       const int r = e / cols, j = e % cols;
       double acc = 0.0;
@@ -286,11 +316,14 @@ __global__ void __launch_bounds__(256) bank_derived_kernel(const double* p64, in
     krT[(int64_t)s * 2 * ms * 128 + r * 128 + kp] = hi;
     krT[(int64_t)s * 2 * ms * 128 + ms * 128 + r * 128 + kp] = tf32_rna((float)(v - (double)hi));
   }
-  // w = C P_Ne (row vector times matrix), and fp32 copies
+  // w = C P_Ne (row vector times matrix), and fp32 copies; P_Ne staged through shared memory
   const double* PN = Ps0 + (int64_t)Neff[s] * mm;
+  __syncthreads();                                 // Ps (the last P_i) and Kr reads done
+  for (int e = tid; e < ms * ms; e += 256) Ps[(e / ms) * (ms + 1) + e % ms] = PN[e];
+  __syncthreads();
   for (int j = tid; j < ms; j += 256) {
     double acc = 0.0;
-    for (int k = 0; k < ms; ++k) acc = fma(C[(int64_t)s * ms + k], PN[(int64_t)k * ms + j], acc);
+    for (int k = 0; k < ms; ++k) acc = fma(C[(int64_t)s * ms + k], Ps[k * (ms + 1) + j], acc);
     w64[(int64_t)s * ms + j] = acc;
     w32[(int64_t)s * ms + j] = (float)acc;
     c32[(int64_t)s * ms + j] = (float)C[(int64_t)s * ms + j];
