@@ -145,7 +145,9 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
     // ---------------------------------------------------------------- epilogue (warps 2..5)
     const int q = warp & 3, row = q * 32 + lane;
     const bool leader = (warp == 2 && lane == 0);
-    const bool to_ab = a.ab != nullptr && a.Neff[c] == a.Kc[c];   // the cascade ends at the head
+    // the cascade ends at the head (R24), or one stage after it with that stage folded into y (R25)
+    const bool to_ab4 = a.ab != nullptr && a.fold && a.Neff[c] == a.Kc[c] + 1;
+    const bool to_ab = (a.ab != nullptr && a.Neff[c] == a.Kc[c]) || to_ab4;
     for (int i = 0; i < nt; ++i) {
       const int slot = i & 1;
       mbar_wait_u(&tfull[slot], (uint32_t)((i >> 1) & 1));
@@ -160,15 +162,31 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
       for (int n = 0; n < MS; ++n) v[n] += vc[n];             // main + corr (round to nearest)
       tc_fence_before();
       mbar_arrive(&tempty[slot]);
-      if (to_ab) {                                // y parts c . v, w . v instead of storing v
-        float pa = 0.f, pb = 0.f;
-#pragma unroll
-        for (int n = 0; n < MS; ++n) {
-          pa = fmaf(__ldg(a.cvec + (int64_t)c * MS + n), v[n], pa);
-          pb = fmaf(__ldg(a.wvec + (int64_t)c * MS + n), v[n], pb);
-        }
+      if (to_ab) {                                // y parts c . v, w . v instead of storing v (R24)
         const int64_t l = (tile_begin + i) * TM + row;
-        if (l < a.L) *reinterpret_cast<float2*>(a.ab + ((int64_t)seq * a.L + l) * 2) = make_float2(pa, pb);
+        if (to_ab4) {                             // R25: (C v, C P_{Ne-1} v | C P_Ne v, C P_Ne P_{Ne-1} v)
+          float pa = 0.f, pb = 0.f, p1 = 0.f, p3 = 0.f;
+#pragma unroll
+          for (int n = 0; n < MS; ++n) {
+            pa = fmaf(__ldg(a.cvec + (int64_t)c * MS + n), v[n], pa);
+            pb = fmaf(__ldg(a.wvec + (int64_t)c * MS + n), v[n], pb);
+            p1 = fmaf(__ldg(a.c1vec + (int64_t)c * MS + n), v[n], p1);
+            p3 = fmaf(__ldg(a.c3vec + (int64_t)c * MS + n), v[n], p3);
+          }
+          if (l < a.L) {
+            const int64_t r = (int64_t)seq * a.L + l;
+            *reinterpret_cast<float2*>(a.ab + r * 2) = make_float2(pa, p1);
+            *reinterpret_cast<float2*>(a.abx + r * 2) = make_float2(pb, p3);
+          }
+        } else {
+          float pa = 0.f, pb = 0.f;
+#pragma unroll
+          for (int n = 0; n < MS; ++n) {
+            pa = fmaf(__ldg(a.cvec + (int64_t)c * MS + n), v[n], pa);
+            pb = fmaf(__ldg(a.wvec + (int64_t)c * MS + n), v[n], pb);
+          }
+          if (l < a.L) *reinterpret_cast<float2*>(a.ab + ((int64_t)seq * a.L + l) * 2) = make_float2(pa, pb);
+        }
         continue;
       }
 #pragma unroll

@@ -92,6 +92,7 @@ struct HistArg {
   int w_plane_off[3], w_plane_stride[3];
   int64_t n_pos, gt;                    // positions in all, per CTA
   const int* ab_neff; int ab_level; const float* ab_c; const float* ab_w; float* ab;
+  int ab_fold; const float* ab_c1; const float* ab_c3; float* abx;   // R25: Neff == level + 1 -> four parts
   float* out;                           // destination state [nseq][L][64]
 };
 
@@ -320,7 +321,9 @@ __global__ void __launch_bounds__(THREADS, 1) bank_hist_kernel(const __grid_cons
         continue;
       }
       const int acc = (int)(tl % NACC);
-      const bool to_ab = a.ab != nullptr && a.ab_neff[it.sys] == a.ab_level;
+      const int ne = a.ab != nullptr ? a.ab_neff[it.sys] : -2;    // -2: never a level
+      const bool to_ab4 = a.ab != nullptr && a.ab_fold && ne == a.ab_level + 1;   // R25: the last stage folds into y
+      const bool to_ab = a.ab != nullptr && (ne == a.ab_level || to_ab4);
       const bool any_src = it.t >= S;
       // warp-uniform waits before the .sync.aligned tcgen05.ld / st: a per-lane spin loop can
       // leave the warp diverged there (measured: one 32-row quadrant of a tile corrupted)
@@ -359,7 +362,27 @@ __global__ void __launch_bounds__(THREADS, 1) bank_hist_kernel(const __grid_cons
       mbar_arrive(&tempty[acc]);                      // accumulator drained (every loaded value used)
       mbar_arrive(&slot_free[sr]);                    // residual rows read
       const int64_t l = (int64_t)it.t * HBM + row;
-      if (to_ab) {                                    // y parts: c . v and w . v of this row
+      if (to_ab4) {                                   // R25: four parts (C v, C P_{Ne-1} v | C P_Ne v, C P_Ne P_{Ne-1} v)
+        float pa = 0.f, pb = 0.f, p1 = 0.f, p3 = 0.f;
+#pragma unroll
+        for (int col = 0; col < HM; col += 4) {
+          const float4 c4 = __ldg(reinterpret_cast<const float4*>(a.ab_c + (int64_t)it.sys * HM + col));
+          const float4 w4 = __ldg(reinterpret_cast<const float4*>(a.ab_w + (int64_t)it.sys * HM + col));
+          const float4 e4 = __ldg(reinterpret_cast<const float4*>(a.ab_c1 + (int64_t)it.sys * HM + col));
+          const float4 g4 = __ldg(reinterpret_cast<const float4*>(a.ab_c3 + (int64_t)it.sys * HM + col));
+          const float f0 = __uint_as_float(vm[col]), f1 = __uint_as_float(vm[col + 1]);
+          const float f2 = __uint_as_float(vm[col + 2]), f3 = __uint_as_float(vm[col + 3]);
+          pa = fmaf(c4.x, f0, pa); pa = fmaf(c4.y, f1, pa); pa = fmaf(c4.z, f2, pa); pa = fmaf(c4.w, f3, pa);
+          pb = fmaf(w4.x, f0, pb); pb = fmaf(w4.y, f1, pb); pb = fmaf(w4.z, f2, pb); pb = fmaf(w4.w, f3, pb);
+          p1 = fmaf(e4.x, f0, p1); p1 = fmaf(e4.y, f1, p1); p1 = fmaf(e4.z, f2, p1); p1 = fmaf(e4.w, f3, p1);
+          p3 = fmaf(g4.x, f0, p3); p3 = fmaf(g4.y, f1, p3); p3 = fmaf(g4.z, f2, p3); p3 = fmaf(g4.w, f3, p3);
+        }
+        if (l < a.L) {
+          const int64_t r = (int64_t)it.seq * a.L + l;
+          *reinterpret_cast<float2*>(a.ab + r * 2) = make_float2(pa, p1);
+          *reinterpret_cast<float2*>(a.abx + r * 2) = make_float2(pb, p3);
+        }
+      } else if (to_ab) {                             // y parts: c . v and w . v of this row (R24)
         float pa = 0.f, pb = 0.f;
 #pragma unroll
         for (int col = 0; col < HM; col += 4) {
@@ -387,12 +410,23 @@ __global__ void __launch_bounds__(THREADS, 1) bank_hist_kernel(const __grid_cons
 
 // Applicable to the bank stage passes: fp32, m = 64, 1 or 3 sources A = R = v at shifts c * s,
 // s a multiple of 128 with the tile count a multiple of s / 128, no halo rows.
-int launch_bank_hist(const MimoGemm& g, cudaStream_t st) {
-  // CASC_BANK_HIST = 0 (off) | p (stage pairs only) | s (single stages only); default both
+static char hist_mode() {     // CASC_BANK_HIST = 0 (off) | p (stage pairs only) | s (single stages only)
   static const char mode = [] {
     const char* e = getenv("CASC_BANK_HIST");
     return e ? e[0] : '1';
   }();
+  return mode;
+}
+bool bank_hist_ok(int64_t L, int64_t shift, int n_src, int t_first) {
+  const char mode = hist_mode();
+  if (mode == '0' || (mode == 'p' && n_src != 3) || (mode == 's' && n_src != 1)) return false;
+  if (!(n_src == 1 || n_src == 3) || shift <= 0 || shift % HBM) return false;
+  const int nt = (int)((L + HBM - 1) / HBM), S = (int)(shift / HBM);
+  if (S > nt || nt % S || (t_first >= S && t_first > 0)) return false;
+  return !(nt / S == 1 && t_first > 0);
+}
+int launch_bank_hist(const MimoGemm& g, cudaStream_t st) {
+  const char mode = hist_mode();
   if (mode == '0' || (mode == 'p' && g.n_src != 3) || (mode == 's' && g.n_src != 1)) return CASC_ERR_UNSUPPORTED;
   if (g.n_out != HM || !(g.n_src == 1 || g.n_src == 3) || g.R_row0 || g.out_row0) return CASC_ERR_UNSUPPORTED;
   const int64_t s = g.src[0].shift;
@@ -408,6 +442,7 @@ int launch_bank_hist(const MimoGemm& g, cudaStream_t st) {
   a.ns = g.n_src; a.S = S; a.nt = nt; a.t_first = g.t_first; a.nt_eff = nt - g.t_first;
   a.L = g.L; a.batch = g.batch; a.sys_list = g.sys_list; a.n_list = g.sys_list ? g.n_list : 1;
   a.ab_neff = g.ab_neff; a.ab_level = g.ab_level; a.ab_c = g.ab_c; a.ab_w = g.ab_w; a.ab = g.ab;
+  a.ab_fold = g.ab_fold; a.ab_c1 = g.ab_c1; a.ab_c3 = g.ab_c3; a.abx = g.abx;
   const int64_t nseq_total = (int64_t)(g.n_sys_total > 0 ? g.n_sys_total : 1) * g.batch;
   if (!map3d(&maps.V, g.R, true, HM, g.L, nseq_total, HBM)) return CASC_ERR_CUDA;
   a.out = static_cast<float*>(g.out);

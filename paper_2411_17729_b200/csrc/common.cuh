@@ -1,5 +1,7 @@
 // Shared device/host helpers of libcascade_b200 (internal; not part of the C ABI).
 #pragma once
+#include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -19,9 +21,19 @@ inline void count_launch(int n = 1) { g_launches += n; }
     if (e__ != cudaSuccess) return CASC_ERR_CUDA;           \
   } while (0)
 
+// diagnostics (CASC_SYNC_DEBUG=1): synchronise after every launch and name the failing one
+inline bool sync_debug() {
+  static const bool on = getenv("CASC_SYNC_DEBUG") != nullptr;
+  return on;
+}
+inline void sync_check(const char* file, int line) {
+  const cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) fprintf(stderr, "casc: launch at %s:%d failed: %s\n", file, line, cudaGetErrorString(e));
+}
 #define CASC_LAUNCHED()                                     \
   do {                                                      \
     ::casc::count_launch();                                 \
+    if (::casc::sync_debug()) ::casc::sync_check(__FILE__, __LINE__); \
     if (cudaPeekAtLastError() != cudaSuccess) {             \
       (void)cudaGetLastError();                             \
       return CASC_ERR_CUDA;                                 \

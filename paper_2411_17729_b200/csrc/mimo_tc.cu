@@ -596,7 +596,7 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
   a.n_list = g.sys_list ? g.n_list : 1;
   a.t_first = g.t_first;
   a.ab_neff = g.ab_neff; a.ab_level = g.ab_level; a.ab_c = g.ab_c; a.ab_w = g.ab_w; a.ab = g.ab;
-  if (g.ab && (!TF32 || g.n_out != 64)) return CASC_ERR_UNSUPPORTED;
+  if (g.ab && (!TF32 || g.n_out != 64 || g.ab_fold)) return CASC_ERR_UNSUPPORTED;
   const int64_t nseq_total = (int64_t)(g.n_sys_total > 0 ? g.n_sys_total : 1) * g.batch;
   for (int s = 0; s < g.n_src; ++s) {
     if (g.src[s].K % C::BK) return CASC_ERR_UNSUPPORTED;

@@ -44,6 +44,9 @@ struct MimoGemm {
   int w_resident = 0;                // keep the weights in shared memory across tiles
   const int* ab_neff = nullptr; int ab_level = -1;    // see MimoArg
   const float* ab_c = nullptr; const float* ab_w = nullptr; float* ab = nullptr;
+  // folded last stage (R25): channels with ab_neff == ab_level + 1 write the four parts
+  // ab = (C v, C P_{Ne-1} v), abx = (C P_Ne v, C P_Ne P_{Ne-1} v) (bank_hist.cu only)
+  int ab_fold = 0; const float* ab_c1 = nullptr; const float* ab_c3 = nullptr; float* abx = nullptr;
 };
 
 bool mimo_tc_supported(int m, int p, int q);
@@ -54,6 +57,8 @@ int launch_mimo_gemm(const MimoGemm& g, bool tf32, cudaStream_t st);
 // Bank stage pass with the state history resident in shared memory (bank_hist.cu): m = 64 fp32,
 // 1 or 3 sources v at shifts c * s (s a multiple of 128); CASC_ERR_UNSUPPORTED otherwise.
 int launch_bank_hist(const MimoGemm& g, cudaStream_t st);
+// whether launch_bank_hist takes a pass with these parameters (the engine plans R25 with it)
+bool bank_hist_ok(int64_t L, int64_t shift, int n_src, int t_first);
 // bf16, n_out % 256 == 0, one system: 256 x 256 tiles on CTA pairs (mimo_tc2.cu)
 bool mimo_pair_ok(const MimoGemm& g, bool tf32);
 int launch_mimo_gemm_pair(const MimoGemm& g, cudaStream_t st);
