@@ -106,3 +106,13 @@ def test_hist_many_short_ranges():
     """One channel over 148 CTAs: most CTA ranges start inside a chain (up to three warm-up tiles)."""
     wl = _bank(1, 128 * 48, 4, [13])
     _check(wl, _gpu_y(wl))
+
+
+def test_fold_matches_single_stage_pass():
+    """R25 (the last stage of odd channels folded into y, orders 8/10/12 here) against the same
+    bank with the single-stage passes run (CASC_BANK_FOLD=0): same sums regrouped."""
+    wl = _bank(8, 128 * 48, 2, [8, 9, 10, 11, 12, 13, 10, 8])
+    y_fold = _gpu_y(wl)
+    _check(wl, y_fold)
+    y_single = _gpu_y(wl, {"CASC_BANK_FOLD": "0"})
+    assert rel(y_fold, y_single) < 2e-6
