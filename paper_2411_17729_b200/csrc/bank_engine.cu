@@ -72,11 +72,10 @@ struct BankWs {
   float* krT;     // [n][2][m][128]
   double* w64;    // [n][m]
   float *w32, *c32, *d32;
-  float *c1_32, *c3_32;  // [n][m] C P_{Ne-1}, C P_Ne P_{Ne-1} (R25)
+  float* pvec;   // [n][kMaxParts][m] output-part row vectors (R24-R26)
   double* Q64;    // [n][m][m] scratch for one pair weight
   float* Q32;     // [n][qslots][2][m][m] pair weights, tf32 hi/lo planes
-  float* ab;      // [n][batch][L][2] fused-output parts of the last state (R24; R25: first two)
-  float* abx;     // [n][batch][L][2] the other two R25 parts
+  float* parts;   // [kMaxParts][n * batch * L] fused output parts of the last stages (R24-R26)
   void *Va, *Vb;
   size_t bytes;
 };
@@ -91,12 +90,10 @@ static BankWs carve_bank(void* ws, int n, int m, int64_t L, int batch, int qslot
   w.w32 = c.take<float>((size_t)n * m);
   w.c32 = c.take<float>((size_t)n * m);
   w.d32 = c.take<float>((size_t)n);
-  w.c1_32 = c.take<float>((size_t)n * m);
-  w.c3_32 = c.take<float>((size_t)n * m);
+  w.pvec = c.take<float>((size_t)n * kMaxParts * m);
   w.Q64 = c.take<double>(qslots ? (size_t)n * m * m : 0);
   w.Q32 = c.take<float>((size_t)n * qslots * 2 * m * m);
-  w.ab = c.take<float>(m == 64 ? (size_t)n * batch * (size_t)L * 2 : 0);
-  w.abx = c.take<float>(m == 64 ? (size_t)n * batch * (size_t)L * 2 : 0);
+  w.parts = c.take<float>(m == 64 ? (size_t)kMaxParts * n * batch * (size_t)L : 0);
   const size_t vbytes = (size_t)n * batch * (size_t)L * m * sizeof(float);
   w.Va = c.take<char>(vbytes);
   w.Vb = c.take<char>(vbytes);
@@ -497,16 +494,24 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
   std::iota(order, order + n, 0);
   std::stable_sort(order, order + n, [&](int a, int b) { return Neff[a] > Neff[b]; });
   std::iota(iota, iota + n, 0);
-  // R25: channels with an odd number of streaming stages skip their last (single) stage pass: the
-  // pass that produces v^(Ne-1) writes four parts per row and the tail applies stage Ne-1 with y.
-  // Planned only where every such producing pass runs on the history-resident kernel (or the head).
-  bool fold = use_ab && variant == 't' && !(getenv("CASC_BANK_FOLD") && getenv("CASC_BANK_FOLD")[0] == '0');
-  for (int k = kHeadK; fold && k + 3 <= maxNe; k += 2) {
-    bool ends4 = false;                            // a channel with Ne == k + 3 ends at the pass at k
-    for (int s = 0; s < n; ++s) ends4 |= Neff[s] == k + 3;
-    if (ends4 && !bank_hist_ok(L, (int64_t)1 << k, 3, 0)) fold = false;
+  // R24-R26 (common.cuh OutParts): y is formed from parts written by the kernel producing
+  // v^(Ne-d); with fold, d = 1 for an odd number of streaming stages (no single-stage pass) and
+  // d = 2 for an even number >= 2 (the last stage-pair pass is skipped). Planned only where every
+  // pass producing d > 0 parts runs on the history-resident kernel (or is the head).
+  // CASC_BANK_FOLD = 0 | 1 (R25, default) | 2 (R25 + R26: measured slower, E2 3.90 vs 3.75 ms and
+  // E5 807 vs 768 ms, the eight-part epilogues cost more than the skipped pair passes save)
+  static const int fold_mode = [] {
+    const char* e = getenv("CASC_BANK_FOLD");
+    return e ? atoi(e) : 1;
+  }();
+  int fold = (use_ab && variant == 't') ? fold_mode : 0;
+  for (int c = 0; fold && c < n; ++c) {
+    const int d = fold_depth(Neff[c], Kc[c], fold), lp = Neff[c] - d;
+    if (d > 0 && lp > Kc[c] && !bank_hist_ok(L, (int64_t)1 << (lp - 2), 3, 0)) fold = 0;
   }
-  auto ends_at_head = [&](int c) { return Neff[c] == Kc[c] || (fold && Neff[c] == Kc[c] + 1); };
+  std::vector<int> Lp(n);                          // the state level each channel's parts come from
+  for (int c = 0; c < n; ++c) Lp[c] = Neff[c] - fold_depth(Neff[c], Kc[c], fold);
+  auto ends_at_head = [&](int c) { return Lp[c] == Kc[c]; };
   const bool chunked = bs && bs->n_chunks > 1;
   std::vector<int> hend_off(chunked ? bs->n_chunks + 1 : 1, 0);
   if (chunked) {                                   // head-ending channels (Ne == Kc), grouped by chunk
@@ -526,16 +531,26 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     while (c < n && Neff[order[c]] >= need) ++c;
     return c;
   };
+  auto count_lp_ge = [&](int need) {                 // channels with Lp >= need: a prefix of order too
+    int c = 0;
+    while (c < n && Lp[order[c]] >= need) ++c;
+    return c;
+  };
+  const int64_t plane = (int64_t)n * batch * L;
+  OutParts op;
+  if (use_ab) {
+    op.planes = w.parts; op.plane = plane; op.vec = w.pvec; op.neff = dNeff; op.kc = dKc; op.fold = fold;
+  }
 
   // ---- derived: Krylov columns, w = C P_Ne, fp32 copies, pair weights
   {
     ProfScope ps(st, K_DERIVED, 0.0, 2.0 * n * (double)m * m * 128);
     if ((rc = launch_bank_derived(P.p64, N_max + 1, Bbar, C, D, dNeff, dKc, w.Kr64, w.krT, w.w64, w.w32, w.c32,
-                                  w.d32, w.c1_32, w.c3_32, n, m, st)))
+                                  w.d32, use_ab ? w.pvec : nullptr, fold, n, m, st)))
       return rc;
     for (int j = 0; j < qslots; ++j) {          // Q_k = P_{k+1} P_k for pass j (k = 7 + 2j)
       const int k = kHeadK + 2 * j;
-      if (count_ge(k + 2) == 0) continue;
+      if (count_lp_ge(k + 2) == 0) continue;
       DgemmArg q{};
       q.M = m; q.N = m; q.K = m;
       q.A = P.p64 + (k + 1) * mm; q.lda = m; q.sA = (int64_t)(N_max + 1) * mm;
@@ -554,8 +569,8 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
   auto emit_ids = [&](const int* dlist, const int* hlist, int cnt) -> int {
     if (!streaming || cnt <= 0) return CASC_OK;
     BankAbTailArg t{};
-    t.ab = w.ab; t.u = static_cast<const float*>(u); t.y = static_cast<float*>(y);
-    t.abx = w.abx; t.d = w.d32; t.Neff = dNeff; t.Kc = dKc; t.fold = fold; t.n_ch = n; t.L = L; t.batch = batch;
+    t.op = op; t.u = static_cast<const float*>(u); t.y = static_cast<float*>(y);
+    t.d = w.d32; t.n_ch = n; t.L = L; t.batch = batch;
     t.list = dlist; t.n_list = cnt;
     int rc2;
     {
@@ -586,10 +601,7 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     BankHeadArg a{};
     a.u = static_cast<const float*>(u); a.krT = w.krT; a.V = static_cast<float*>(w.Va);
     a.sys_list = chunked ? diota + hc0 : dorder; a.n_list = hcn; a.L = L; a.batch = batch;
-    if (use_ab) {
-      a.Neff = dNeff; a.Kc = dKc; a.cvec = w.c32; a.wvec = w.w32; a.ab = w.ab;
-      a.fold = fold; a.c1vec = w.c1_32; a.c3vec = w.c3_32; a.abx = w.abx;
-    }
+    if (use_ab) a.op = op;
     a.tiles_per_cta = pick_group(ntiles, (int64_t)n * batch, 16);
     ProfScope ps(st, K_BANK_HEAD, (double)n * batch * L * (1 + m) * 4.0,
                  (double)n * batch * L * 2.0 * m * 128);
@@ -610,8 +622,8 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     if (chunked && (rc = emit_ids(dhend + hend_off[ci], hend + hend_off[ci], hend_off[ci + 1] - hend_off[ci])))
       return rc;
   }
-  // cascades that end at the head (Ne <= 7; with R25 also Ne == 8)
-  if (!chunked && (rc = emit(count_ge(kHeadK + 1 + (fold ? 1 : 0)), n))) return rc;
+  // cascades whose output parts come from the head (Ne <= 7; with fold also Ne = 8, 9)
+  if (!chunked && (rc = emit(count_lp_ge(kHeadK + 1), n))) return rc;
   // ---- streaming stages k >= kHeadK over the channels with Neff > k (prefixes of `order`)
   int pass = 0;
   for (int k = kHeadK; k < maxNe; k += (variant == 't' ? 2 : 1), ++pass) {
@@ -628,7 +640,7 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       g.t_first = pass == 0 ? 0 : (int)(((int64_t)1 << (k - 1)) / 128);
       g.w_resident = resident_weights();
       if (use_ab) {                                 // channels whose last streaming stage this is
-        g.ab_neff = dNeff; g.ab_level = k + 1; g.ab_c = w.c32; g.ab_w = w.w32; g.ab = w.ab;
+        g.ab_neff = dNeff; g.ab_level = k + 1; g.ab_c = w.c32; g.ab_w = w.w32; g.ab = w.parts; g.ab_plane = plane;
         // their (C v, C P_Ne v) parts are needed on every row: no skipped leading tiles
         if (count_ge(k + 1) > count_ge(k + 2)) g.t_first = 0;
       }
@@ -653,7 +665,7 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     }
     // pass: stages k and k+1 for channels with Neff >= k+2; stage k alone for Neff == k+1.
     // The destination holds v^(k-2) (two passes ago), equal to v^(k+2) on rows < 2^(k-2).
-    const int cnt2 = count_ge(k + 2), cnt1 = count_ge(k + 1) - cnt2;
+    const int cnt2 = count_lp_ge(k + 2), cnt1 = count_lp_ge(k + 1) - cnt2;   // cnt1 = 0 with fold
     const int t_first = pass == 0 ? 0 : (int)(((int64_t)1 << (k - 2)) / 128);
     const int64_t planes = (int64_t)n * (N_max + 1) * 2;
     if (cnt2 > 0) {
@@ -667,13 +679,11 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       g.src[2].w_plane_stride = 2 * qslots;
       g.n_src = 3; g.R = Vs; g.out = Vd; g.n_out = m; g.L = L; g.batch = batch;
       g.sys_list = dorder; g.n_list = cnt2; g.n_sys_total = n; g.t_first = t_first; g.w_resident = pair_wres();
-      if (use_ab) {                                 // channels ending with this pair (Ne == k + 2)
-        g.ab_neff = dNeff; g.ab_level = k + 2; g.ab_c = w.c32; g.ab_w = w.w32; g.ab = w.ab;
-        if (count_ge(k + 2) > count_ge(k + 3)) g.t_first = 0;
-        if (fold && count_ge(k + 3) > count_ge(k + 4)) {   // and, with R25, channels with Ne == k + 3
-          g.ab_fold = 1; g.ab_c1 = w.c1_32; g.ab_c3 = w.c3_32; g.abx = w.abx;   // (planning checked this pass)
-          g.t_first = 0;
-        }
+      if (use_ab) {                                 // channels whose parts come from this pass (Lp == k + 2)
+        g.ab_neff = dNeff; g.ab_level = k + 2; g.ab_c = w.c32; g.ab_w = w.w32; g.ab = w.parts; g.ab_plane = plane;
+        g.parts = op; g.parts.level = k + 2;
+        for (int c = 0; c < n; ++c) g.parts_deep |= (Lp[c] == k + 2 && Lp[c] != Neff[c]);
+        if (count_lp_ge(k + 2) > count_lp_ge(k + 3)) g.t_first = 0;   // their parts need every row
       }
       // bytes of the schedule run (SURVEY 8d B_fused): one read + one write of the state for the two
       // stages this pass applies; flops of both stages (bench.py derives the unfused B_ns from them)
@@ -682,14 +692,15 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       if (rc == CASC_ERR_UNSUPPORTED) rc = launch_mimo_gemm(g, true, st);
       if (rc) return rc;
     }
-    if (cnt1 > 0 && !fold) {                       // single stage k for Ne == k + 1 (folded with R25)
+    if (cnt1 > 0) {                                // single stage k for Ne == k + 1 (none with fold)
       MimoGemm g{};
       g.src[0].A = Vs; g.src[0].W = P.f32; g.src[0].K = m; g.src[0].shift = (int64_t)1 << k;
       g.src[0].w_plane_off = 2 * k; g.src[0].w_planes = planes; g.src[0].w_plane_stride = 2 * (N_max + 1);
       g.n_src = 1; g.R = Vs; g.out = Vd; g.n_out = m; g.L = L; g.batch = batch;
       g.sys_list = dorder + cnt2; g.n_list = cnt1; g.n_sys_total = n; g.t_first = t_first; g.w_resident = resident_weights();
       if (use_ab) {                                 // every channel here ends with stage k
-        g.ab_neff = dNeff; g.ab_level = k + 1; g.ab_c = w.c32; g.ab_w = w.w32; g.ab = w.ab;
+        g.ab_neff = dNeff; g.ab_level = k + 1; g.ab_c = w.c32; g.ab_w = w.w32; g.ab = w.parts; g.ab_plane = plane;
+        g.parts = op; g.parts.level = k + 1;
         g.t_first = 0;
       }
       ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt1 * batch * L * m * 4.0, 2.0 * cnt1 * batch * L * (double)mm);
@@ -697,15 +708,14 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       if (rc == CASC_ERR_UNSUPPORTED) rc = launch_mimo_gemm(g, true, st);
       if (rc) return rc;
     }
-    // channels now final: Ne in {k + 1, k + 2}, or with R25 in {k + 2, k + 3}
-    if ((rc = fold ? emit(count_ge(k + 4), count_ge(k + 2)) : emit(count_ge(k + 3), count_ge(k + 1)))) return rc;
+    if ((rc = emit(count_lp_ge(k + 3), count_lp_ge(k + 1)))) return rc;   // channels with Lp in {k + 1, k + 2}
   }
   if (streaming) return CASC_OK;                      // every channel was emitted
   // ---- tail: stage Ne + y = C v + D u
   if (use_ab) {                                     // from the fused (C v, C P_Ne v) parts
     BankAbTailArg a{};
-    a.ab = w.ab; a.u = static_cast<const float*>(u); a.y = static_cast<float*>(y);
-    a.abx = w.abx; a.d = w.d32; a.Neff = dNeff; a.Kc = dKc; a.fold = fold; a.n_ch = n; a.L = L; a.batch = batch;
+    a.op = op; a.u = static_cast<const float*>(u); a.y = static_cast<float*>(y);
+    a.d = w.d32; a.n_ch = n; a.L = L; a.batch = batch;
     ProfScope ps(st, K_BANK_TAIL, (double)n * batch * L * (8 + 8 + 4 + 4), (double)n * batch * L * 3);
     return launch_bank_ab_tail(a, st);
   }

@@ -145,9 +145,14 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
     // ---------------------------------------------------------------- epilogue (warps 2..5)
     const int q = warp & 3, row = q * 32 + lane;
     const bool leader = (warp == 2 && lane == 0);
-    // the cascade ends at the head (R24), or one stage after it with that stage folded into y (R25)
-    const bool to_ab4 = a.ab != nullptr && a.fold && a.Neff[c] == a.Kc[c] + 1;
-    const bool to_ab = (a.ab != nullptr && a.Neff[c] == a.Kc[c]) || to_ab4;
+    // channels whose output parts are produced at the head (Ne - d == Kc, R24-R26) write them
+    int depth = 0;
+    bool to_parts = false;
+    if (a.op.planes != nullptr) {
+      const int ne = a.op.neff[c], kc = a.op.kc[c];
+      depth = fold_depth(ne, kc, a.op.fold);
+      to_parts = ne - depth == kc;
+    }
     for (int i = 0; i < nt; ++i) {
       const int slot = i & 1;
       mbar_wait_u(&tfull[slot], (uint32_t)((i >> 1) & 1));
@@ -162,30 +167,18 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
       for (int n = 0; n < MS; ++n) v[n] += vc[n];             // main + corr (round to nearest)
       tc_fence_before();
       mbar_arrive(&tempty[slot]);
-      if (to_ab) {                                // y parts c . v, w . v instead of storing v (R24)
+      if (to_parts) {                             // the 2^(depth+1) output parts instead of v
         const int64_t l = (tile_begin + i) * TM + row;
-        if (to_ab4) {                             // R25: (C v, C P_{Ne-1} v | C P_Ne v, C P_Ne P_{Ne-1} v)
-          float pa = 0.f, pb = 0.f, p1 = 0.f, p3 = 0.f;
+        const float* vb = a.op.vec + (int64_t)c * kMaxParts * MS;
+        const int np = 2 << depth;
+        for (int bp = 0; bp < np; ++bp) {
+          float p = 0.f;
 #pragma unroll
-          for (int n = 0; n < MS; ++n) {
-            pa = fmaf(__ldg(a.cvec + (int64_t)c * MS + n), v[n], pa);
-            pb = fmaf(__ldg(a.wvec + (int64_t)c * MS + n), v[n], pb);
-            p1 = fmaf(__ldg(a.c1vec + (int64_t)c * MS + n), v[n], p1);
-            p3 = fmaf(__ldg(a.c3vec + (int64_t)c * MS + n), v[n], p3);
+          for (int n = 0; n < MS; n += 4) {
+            const float4 c4 = __ldg(reinterpret_cast<const float4*>(vb + bp * MS + n));
+            p = fmaf(c4.x, v[n], p); p = fmaf(c4.y, v[n + 1], p); p = fmaf(c4.z, v[n + 2], p); p = fmaf(c4.w, v[n + 3], p);
           }
-          if (l < a.L) {
-            const int64_t r = (int64_t)seq * a.L + l;
-            *reinterpret_cast<float2*>(a.ab + r * 2) = make_float2(pa, p1);
-            *reinterpret_cast<float2*>(a.abx + r * 2) = make_float2(pb, p3);
-          }
-        } else {
-          float pa = 0.f, pb = 0.f;
-#pragma unroll
-          for (int n = 0; n < MS; ++n) {
-            pa = fmaf(__ldg(a.cvec + (int64_t)c * MS + n), v[n], pa);
-            pb = fmaf(__ldg(a.wvec + (int64_t)c * MS + n), v[n], pb);
-          }
-          if (l < a.L) *reinterpret_cast<float2*>(a.ab + ((int64_t)seq * a.L + l) * 2) = make_float2(pa, pb);
+          if (l < a.L) a.op.planes[bp * a.op.plane + (int64_t)seq * a.L + l] = p;
         }
         continue;
       }

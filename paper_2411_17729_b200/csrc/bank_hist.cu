@@ -91,8 +91,7 @@ struct HistArg {
   const int* sys_list; int n_list;
   int w_plane_off[3], w_plane_stride[3];
   int64_t n_pos, gt;                    // positions in all, per CTA
-  const int* ab_neff; int ab_level; const float* ab_c; const float* ab_w; float* ab;
-  int ab_fold; const float* ab_c1; const float* ab_c3; float* abx;   // R25: Neff == level + 1 -> four parts
+  OutParts op;                          // fused output parts (R24-R26); planes == null: always store v
   float* out;                           // destination state [nseq][L][64]
 };
 
@@ -321,9 +320,13 @@ __global__ void __launch_bounds__(THREADS, 1) bank_hist_kernel(const __grid_cons
         continue;
       }
       const int acc = (int)(tl % NACC);
-      const int ne = a.ab != nullptr ? a.ab_neff[it.sys] : -2;    // -2: never a level
-      const bool to_ab4 = a.ab != nullptr && a.ab_fold && ne == a.ab_level + 1;   // R25: the last stage folds into y
-      const bool to_ab = a.ab != nullptr && (ne == a.ab_level || to_ab4);
+      int depth = 0;                                  // this channel's parts at this level, if any
+      bool to_parts = false;
+      if (a.op.planes != nullptr) {
+        const int ne = a.op.neff[it.sys];
+        depth = fold_depth(ne, a.op.kc[it.sys], a.op.fold);
+        to_parts = ne - depth == a.op.level;
+      }
       const bool any_src = it.t >= S;
       // warp-uniform waits before the .sync.aligned tcgen05.ld / st: a per-lane spin loop can
       // leave the warp diverged there (measured: one 32-row quadrant of a tile corrupted)
@@ -362,38 +365,20 @@ __global__ void __launch_bounds__(THREADS, 1) bank_hist_kernel(const __grid_cons
       mbar_arrive(&tempty[acc]);                      // accumulator drained (every loaded value used)
       mbar_arrive(&slot_free[sr]);                    // residual rows read
       const int64_t l = (int64_t)it.t * HBM + row;
-      if (to_ab4) {                                   // R25: four parts (C v, C P_{Ne-1} v | C P_Ne v, C P_Ne P_{Ne-1} v)
-        float pa = 0.f, pb = 0.f, p1 = 0.f, p3 = 0.f;
+      if (to_parts) {                                 // the 2^(depth+1) output parts of this row
+        const float* vb = a.op.vec + (int64_t)it.sys * kMaxParts * HM;
+        const int np = 2 << depth;
+        const int64_t r = (int64_t)it.seq * a.L + l;
+        for (int b = 0; b < np; ++b) {
+          float p = 0.f;
 #pragma unroll
-        for (int col = 0; col < HM; col += 4) {
-          const float4 c4 = __ldg(reinterpret_cast<const float4*>(a.ab_c + (int64_t)it.sys * HM + col));
-          const float4 w4 = __ldg(reinterpret_cast<const float4*>(a.ab_w + (int64_t)it.sys * HM + col));
-          const float4 e4 = __ldg(reinterpret_cast<const float4*>(a.ab_c1 + (int64_t)it.sys * HM + col));
-          const float4 g4 = __ldg(reinterpret_cast<const float4*>(a.ab_c3 + (int64_t)it.sys * HM + col));
-          const float f0 = __uint_as_float(vm[col]), f1 = __uint_as_float(vm[col + 1]);
-          const float f2 = __uint_as_float(vm[col + 2]), f3 = __uint_as_float(vm[col + 3]);
-          pa = fmaf(c4.x, f0, pa); pa = fmaf(c4.y, f1, pa); pa = fmaf(c4.z, f2, pa); pa = fmaf(c4.w, f3, pa);
-          pb = fmaf(w4.x, f0, pb); pb = fmaf(w4.y, f1, pb); pb = fmaf(w4.z, f2, pb); pb = fmaf(w4.w, f3, pb);
-          p1 = fmaf(e4.x, f0, p1); p1 = fmaf(e4.y, f1, p1); p1 = fmaf(e4.z, f2, p1); p1 = fmaf(e4.w, f3, p1);
-          p3 = fmaf(g4.x, f0, p3); p3 = fmaf(g4.y, f1, p3); p3 = fmaf(g4.z, f2, p3); p3 = fmaf(g4.w, f3, p3);
+          for (int col = 0; col < HM; col += 4) {
+            const float4 c4 = __ldg(reinterpret_cast<const float4*>(vb + b * HM + col));
+            p = fmaf(c4.x, __uint_as_float(vm[col]), p); p = fmaf(c4.y, __uint_as_float(vm[col + 1]), p);
+            p = fmaf(c4.z, __uint_as_float(vm[col + 2]), p); p = fmaf(c4.w, __uint_as_float(vm[col + 3]), p);
+          }
+          if (l < a.L) a.op.planes[b * a.op.plane + r] = p;
         }
-        if (l < a.L) {
-          const int64_t r = (int64_t)it.seq * a.L + l;
-          *reinterpret_cast<float2*>(a.ab + r * 2) = make_float2(pa, p1);
-          *reinterpret_cast<float2*>(a.abx + r * 2) = make_float2(pb, p3);
-        }
-      } else if (to_ab) {                             // y parts: c . v and w . v of this row (R24)
-        float pa = 0.f, pb = 0.f;
-#pragma unroll
-        for (int col = 0; col < HM; col += 4) {
-          const float4 c4 = __ldg(reinterpret_cast<const float4*>(a.ab_c + (int64_t)it.sys * HM + col));
-          const float4 w4 = __ldg(reinterpret_cast<const float4*>(a.ab_w + (int64_t)it.sys * HM + col));
-          const float f0 = __uint_as_float(vm[col]), f1 = __uint_as_float(vm[col + 1]);
-          const float f2 = __uint_as_float(vm[col + 2]), f3 = __uint_as_float(vm[col + 3]);
-          pa = fmaf(c4.x, f0, pa); pa = fmaf(c4.y, f1, pa); pa = fmaf(c4.z, f2, pa); pa = fmaf(c4.w, f3, pa);
-          pb = fmaf(w4.x, f0, pb); pb = fmaf(w4.y, f1, pb); pb = fmaf(w4.z, f2, pb); pb = fmaf(w4.w, f3, pb);
-        }
-        if (l < a.L) *reinterpret_cast<float2*>(a.ab + ((int64_t)it.seq * a.L + l) * 2) = make_float2(pa, pb);
       } else if (l < a.L) {
         float* orow = a.out + ((int64_t)it.seq * a.L + l) * HM;
 #pragma unroll
@@ -441,8 +426,7 @@ int launch_bank_hist(const MimoGemm& g, cudaStream_t st) {
   HistArg a{};
   a.ns = g.n_src; a.S = S; a.nt = nt; a.t_first = g.t_first; a.nt_eff = nt - g.t_first;
   a.L = g.L; a.batch = g.batch; a.sys_list = g.sys_list; a.n_list = g.sys_list ? g.n_list : 1;
-  a.ab_neff = g.ab_neff; a.ab_level = g.ab_level; a.ab_c = g.ab_c; a.ab_w = g.ab_w; a.ab = g.ab;
-  a.ab_fold = g.ab_fold; a.ab_c1 = g.ab_c1; a.ab_c3 = g.ab_c3; a.abx = g.abx;
+  a.op = g.parts;
   const int64_t nseq_total = (int64_t)(g.n_sys_total > 0 ? g.n_sys_total : 1) * g.batch;
   if (!map3d(&maps.V, g.R, true, HM, g.L, nseq_total, HBM)) return CASC_ERR_CUDA;
   a.out = static_cast<float*>(g.out);

@@ -255,8 +255,8 @@ int launch_kr_split(const double* Kr, const int* Kc, float* krT, int n, int ms, 
 __global__ void __launch_bounds__(256) bank_derived_kernel(const double* p64, int slots, const double* Bbar,
                                                            const double* C, const double* D, const int* Neff,
                                                            const int* Kc, double* Kr64, float* krT, double* w64,
-                                                           float* w32, float* c32, float* d32, float* c1_32,
-                                                           float* c3_32, int ms) {
+                                                           float* w32, float* c32, float* d32, float* pvec,
+                                                           int fold, int ms) {
   extern __shared__ double dsm[];
   double* Ps = dsm;                         // [ms][ms+1]
   double* Kr = Ps + ms * (ms + 1);          // [ms][129]
@@ -322,42 +322,46 @@ __global__ void __launch_bounds__(256) bank_derived_kernel(const double* p64, in
   __syncthreads();                                 // Ps (the last P_i) and Kr reads done
   for (int e = tid; e < ms * ms; e += 256) Ps[(e / ms) * (ms + 1) + e % ms] = PN[e];
   __syncthreads();
-  double* wsm = Kr;                                // w in shared memory (Kr is no longer read)
   for (int j = tid; j < ms; j += 256) {
     double acc = 0.0;
     for (int k = 0; k < ms; ++k) acc = fma(C[(int64_t)s * ms + k], Ps[k * (ms + 1) + j], acc);
     w64[(int64_t)s * ms + j] = acc;
     w32[(int64_t)s * ms + j] = (float)acc;
-    wsm[j] = acc;
     c32[(int64_t)s * ms + j] = (float)C[(int64_t)s * ms + j];
   }
   if (tid == 0) d32[s] = D ? (float)D[s] : 0.f;
-  // R25 (the last stage folded into the output): C P_{Ne-1} and (C P_Ne) P_{Ne-1}, float64 -> fp32
-  if (c1_32 && Neff[s] >= 1) {
-    const double* PM = Ps0 + (int64_t)(Neff[s] - 1) * mm;
-    __syncthreads();                               // Ps (P_Ne) and wsm complete
-    for (int e = tid; e < ms * ms; e += 256) Ps[(e / ms) * (ms + 1) + e % ms] = PM[e];
+  // output-part row vectors (common.cuh OutParts): v_b = C prod_{i in b} P_{j0+i}, j0 = Ne - d, built
+  // in float64 by multiplying in one stage at a time (the P's are powers of Abar and commute)
+  if (pvec) {
+    const int ne = Neff[s], d = fold_depth(ne, Kc[s], fold), j0 = ne - d;
+    double* vs = Kr;                               // [kMaxParts][ms] float64 vectors (Kr no longer read)
     __syncthreads();
-    for (int j = tid; j < ms; j += 256) {
-      double a1 = 0.0, a3 = 0.0;
-      for (int k = 0; k < ms; ++k) {
-        a1 = fma(C[(int64_t)s * ms + k], Ps[k * (ms + 1) + j], a1);
-        a3 = fma(wsm[k], Ps[k * (ms + 1) + j], a3);
+    for (int j = tid; j < ms; j += 256) vs[j] = C[(int64_t)s * ms + j];
+    for (int q = 0; q <= d; ++q) {                 // vectors with bit q set from those without
+      const double* Pq = Ps0 + (int64_t)(j0 + q) * mm;
+      __syncthreads();
+      for (int e = tid; e < ms * ms; e += 256) Ps[(e / ms) * (ms + 1) + e % ms] = Pq[e];
+      __syncthreads();
+      for (int e = tid; e < (1 << q) * ms; e += 256) {
+        const int b = e / ms, j = e % ms;
+        double acc = 0.0;
+        for (int k = 0; k < ms; ++k) acc = fma(vs[b * ms + k], Ps[k * (ms + 1) + j], acc);
+        vs[(b | (1 << q)) * ms + j] = acc;
       }
-      c1_32[(int64_t)s * ms + j] = (float)a1;
-      c3_32[(int64_t)s * ms + j] = (float)a3;
     }
+    __syncthreads();
+    for (int e = tid; e < (2 << d) * ms; e += 256) pvec[(int64_t)s * kMaxParts * ms + e] = (float)vs[e];
   }
 }
 
 int launch_bank_derived(const double* p64, int slots, const double* Bbar, const double* C, const double* D,
                         const int* Neff, const int* Kc, double* Kr64, float* krT, double* w64, float* w32,
-                        float* c32, float* d32, float* c1_32, float* c3_32, int n, int ms, cudaStream_t st) {
+                        float* c32, float* d32, float* pvec, int fold, int n, int ms, cudaStream_t st) {
   const size_t smem = (size_t)(ms * (ms + 1) + ms * 129) * sizeof(double);
   if (cudaFuncSetAttribute(bank_derived_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return CASC_ERR_CUDA;
-  bank_derived_kernel<<<n, 256, smem, st>>>(p64, slots, Bbar, C, D, Neff, Kc, Kr64, krT, w64, w32, c32, d32, c1_32,
-                                            c3_32, ms);
+  bank_derived_kernel<<<n, 256, smem, st>>>(p64, slots, Bbar, C, D, Neff, Kc, Kr64, krT, w64, w32, c32, d32, pvec,
+                                            fold, ms);
   CASC_LAUNCHED();
   return CASC_OK;
 }
@@ -372,20 +376,24 @@ __global__ void bank_ab_tail_kernel(BankAbTailArg a) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = a.list ? a.list[i / per] : (int)(i / per);
     const int64_t e = (int64_t)c * per + i % per, l = e % a.L;
-    const int ne = a.Neff[c];
-    if (a.fold && ((ne - a.Kc[c]) & 1)) {          // R25: stage Ne-1 folded into the output
-      const int64_t h = (int64_t)1 << (ne - 1);
-      float s = a.ab[e * 2];
-      if (l >= h) s += a.ab[(e - h) * 2 + 1];
-      if (l >= 2 * h) s += a.abx[(e - 2 * h) * 2];
-      if (l >= 3 * h) s += a.abx[(e - 3 * h) * 2 + 1];
-      a.y[e] = fmaf(a.d[c], a.u[e], s);
-    } else {
-      const int64_t sh = (int64_t)1 << ne;
-      const float2 ab = *reinterpret_cast<const float2*>(a.ab + e * 2);
-      const float b = l >= sh ? a.ab[(e - sh) * 2 + 1] : 0.f;
-      a.y[e] = fmaf(a.d[c], a.u[e], ab.x + b);
+    const int ne = a.op.neff[c];
+    const int d = fold_depth(ne, a.op.kc[c], a.op.fold);
+    const int64_t h = (int64_t)1 << (ne - d);      // stages ne-d .. ne are applied here: shifts h, 2h, 4h
+    const float* pl = a.op.planes + e;
+    const int64_t P = a.op.plane;
+    float s = pl[0];
+    if (l >= h) s += pl[P - h];
+    if (d >= 1) {
+      if (l >= 2 * h) s += pl[2 * P - 2 * h];
+      if (l >= 3 * h) s += pl[3 * P - 3 * h];
     }
+    if (d >= 2) {
+      if (l >= 4 * h) s += pl[4 * P - 4 * h];
+      if (l >= 5 * h) s += pl[5 * P - 5 * h];
+      if (l >= 6 * h) s += pl[6 * P - 6 * h];
+      if (l >= 7 * h) s += pl[7 * P - 7 * h];
+    }
+    a.y[e] = fmaf(a.d[c], a.u[e], s);
   }
 }
 int launch_bank_ab_tail(const BankAbTailArg& a, cudaStream_t st) {

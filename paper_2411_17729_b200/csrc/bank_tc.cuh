@@ -10,19 +10,14 @@ struct BankHeadArg {
   float* V;                // [n_ch][batch][L][MS]
   const int* sys_list; int n_list;
   int64_t L; int batch; int tiles_per_cta;
-  // output fusion (ws head): channels with Neff == Kc end at the head; their epilogue writes
-  // ab[seq][l] = (c . v_l, w . v_l) instead of v (null: always write v)
-  const int* Neff; const int* Kc; const float* cvec; const float* wvec; float* ab;
-  // R25: with fold, channels with Neff == Kc + 1 write (C v, C P_{Ne-1} v, C P_Ne v, C P_Ne P_{Ne-1} v)
-  int fold = 0; const float* c1vec = nullptr; const float* c3vec = nullptr; float* abx = nullptr;
+  // fused output (ws head, R24-R26): channels whose parts level is Kc write their parts, not v
+  OutParts op;
 };
-// y_l = a_l + b_{l - 2^Ne} + d u_l (R24; ab = (a, b)), or with the last stage folded (R25, channels
-// with Neff - Kc odd when fold): y_l = a0_l + a1_{l-h} + a2_{l-2h} + a3_{l-3h} + d u_l, h = 2^(Ne-1),
-// ab = (a0, a1), abx = (a2, a3); parts before l = 0 are zero
+// y_l = sum_b p_b(l - o_b) + d u_l from the fused output parts (common.cuh OutParts, R24-R26)
 struct BankAbTailArg {
-  const float* ab; const float* u; float* y;   // ab, abx [n_ch][batch][L][2]; u, y [n_ch][batch][L]
-  const float* abx = nullptr;
-  const float* d; const int* Neff; const int* Kc; int fold;
+  OutParts op;
+  const float* u; float* y;                    // u, y [n_ch][batch][L]
+  const float* d;
   int n_ch; int64_t L; int batch;
   const int* list; int n_list;                 // optional: only channels list[0..n_list)
 };
@@ -68,7 +63,7 @@ int launch_bank_ab_tail(const BankAbTailArg& a, cudaStream_t st);
 int launch_kr_init(const double* Bbar, double* Kr, int n, int ms, cudaStream_t st);
 int launch_bank_derived(const double* p64, int slots, const double* Bbar, const double* C, const double* D,
                         const int* Neff, const int* Kc, double* Kr64, float* krT, double* w64, float* w32,
-                        float* c32, float* d32, float* c1_32, float* c3_32, int n, int ms, cudaStream_t st);
+                        float* c32, float* d32, float* pvec, int fold, int n, int ms, cudaStream_t st);
 int launch_kr_split(const double* Kr, const int* Kc, float* krT, int n, int ms, cudaStream_t st);
 
 }  // namespace casc

@@ -41,6 +41,26 @@ inline void sync_check(const char* file, int line) {
   } while (0)
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+// Fused output of a bank channel's last stages (R24-R26). y is linear in the state, so
+// the kernel producing v' = v^(Ne-d) writes the 2^(d+1) row scalars p_b = (C prod_{i in b} P_{j_i}) . v'
+// over the subsets b of the stages j_i = Ne-d+i (i = 0..d; stage Ne is the tail's, R21), and the
+// tail forms y_l = sum_b p_b(l - o_b) + D u_l with o_b = sum_{i in b} 2^{j_i}.
+//   d = 0 (R24): the pass producing v^(Ne); d = 1 (R25): Ne - Kc odd, the single-stage pass is
+//   skipped; d = 2 (R26): Ne - Kc even >= 2, the channel's last stage-pair pass is skipped.
+constexpr int kMaxParts = 8;
+__host__ __device__ inline int fold_depth(int ne, int kc, int fold) {   // fold: 0 (R24) | 1 (R25) | 2 (R26)
+  return (!fold || ne == kc) ? 0 : (((ne - kc) & 1) ? 1 : (fold >= 2 ? 2 : 0));
+}
+struct OutParts {
+  float* planes = nullptr;          // [kMaxParts][plane]: part b of row r at planes[b * plane + r]
+  int64_t plane = 0;                // rows per plane (channels x batch x L)
+  const float* vec = nullptr;       // [n_ch][kMaxParts][64] fp32 row vectors
+  const int* neff = nullptr;        // per channel Ne and head stages Kc (device)
+  const int* kc = nullptr;
+  int fold = 0;                     // d = fold_depth(Ne, Kc, fold)
+  int level = -1;                   // state level this launch produces: channels with Ne - d == level write
+};
+
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Bump allocator used both to size (base == nullptr) and to carve a workspace.

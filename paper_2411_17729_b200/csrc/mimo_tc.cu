@@ -537,7 +537,11 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
       }
       if (to_ab) {
         const int64_t l = (int64_t)tc.l0 + row;
-        if (l < a.L) *reinterpret_cast<float2*>(a.ab + ((int64_t)tc.seq * a.L + l) * 2) = make_float2(pa, pb);
+        if (l < a.L) {
+          const int64_t r = (int64_t)tc.seq * a.L + l;
+          a.ab[r] = pa;
+          a.ab[a.ab_plane + r] = pb;
+        }
       }
     }
     if (leader) bulk_wait<0>();
@@ -596,7 +600,8 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
   a.n_list = g.sys_list ? g.n_list : 1;
   a.t_first = g.t_first;
   a.ab_neff = g.ab_neff; a.ab_level = g.ab_level; a.ab_c = g.ab_c; a.ab_w = g.ab_w; a.ab = g.ab;
-  if (g.ab && (!TF32 || g.n_out != 64 || g.ab_fold)) return CASC_ERR_UNSUPPORTED;
+  a.ab_plane = g.ab_plane;
+  if (g.parts_deep || (g.ab && (!TF32 || g.n_out != 64))) return CASC_ERR_UNSUPPORTED;
   const int64_t nseq_total = (int64_t)(g.n_sys_total > 0 ? g.n_sys_total : 1) * g.batch;
   for (int s = 0; s < g.n_src; ++s) {
     if (g.src[s].K % C::BK) return CASC_ERR_UNSUPPORTED;

@@ -20,8 +20,8 @@ struct MimoArg {
   int a_row0[3], r_row0, out_row0;   // rows in front of local row 0 (sequence-shard halo)
   // Bank output fusion (fp32 n_out = 64): for systems with ab_neff[sys] == ab_level this stage
   // is their last streaming stage; instead of storing v^(Ne) the epilogue writes
-  // ab[seq][l] = (c . v_l, w . v_l) with c = C, w = C P_Ne (R24)
-  const int* ab_neff; int ab_level; const float* ab_c; const float* ab_w; float* ab;
+  // ab planes (c . v_l, w . v_l) with c = C, w = C P_Ne (R24)
+  const int* ab_neff; int ab_level; const float* ab_c; const float* ab_w; float* ab; int64_t ab_plane;
   int64_t gt;                        // tiles per block of the CTA tile walk
   unsigned long long* dbg;           // optional wait-cycle counters (CASC_GEMM_DBG=1)
   int mma8;                          // TSA 3xTF32: 8 MMAs per chunk (N = 128 hi.[hi|lo]) instead of 12
@@ -44,9 +44,10 @@ struct MimoGemm {
   int w_resident = 0;                // keep the weights in shared memory across tiles
   const int* ab_neff = nullptr; int ab_level = -1;    // see MimoArg
   const float* ab_c = nullptr; const float* ab_w = nullptr; float* ab = nullptr;
-  // folded last stage (R25): channels with ab_neff == ab_level + 1 write the four parts
-  // ab = (C v, C P_{Ne-1} v), abx = (C P_Ne v, C P_Ne P_{Ne-1} v) (bank_hist.cu only)
-  int ab_fold = 0; const float* ab_c1 = nullptr; const float* ab_c3 = nullptr; float* abx = nullptr;
+  int64_t ab_plane = 0;              // ab holds two planes: (c . v) at ab[r], (w . v) at ab[ab_plane + r]
+  // general fused output (R24-R26, common.cuh) for the history-resident stage kernel; parts_deep:
+  // some channel of this pass writes more than the two R24 parts (the multi-source GEMM cannot)
+  OutParts parts; int parts_deep = 0;
 };
 
 bool mimo_tc_supported(int m, int p, int q);

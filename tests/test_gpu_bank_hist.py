@@ -116,3 +116,13 @@ def test_fold_matches_single_stage_pass():
     _check(wl, y_fold)
     y_single = _gpu_y(wl, {"CASC_BANK_FOLD": "0"})
     assert rel(y_fold, y_single) < 2e-6
+
+
+def test_fold_two_stages_matches():
+    """R26 (opt-in, CASC_BANK_FOLD=2): even channels skip their last stage-pair pass and the head or
+    the previous pass writes eight parts; same y as the unfolded bank."""
+    wl = _bank(8, 128 * 48, 2, [8, 9, 10, 11, 12, 13, 11, 9])
+    y2 = _gpu_y(wl, {"CASC_BANK_FOLD": "2"})
+    _check(wl, y2)
+    y0 = _gpu_y(wl, {"CASC_BANK_FOLD": "0"})
+    assert rel(y2, y0) < 2e-6
