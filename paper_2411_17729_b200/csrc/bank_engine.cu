@@ -24,6 +24,7 @@
 #include "mimo_tc.cuh"
 
 namespace casc {
+cudaEvent_t g_timing_t0 = nullptr;   // CASC_TIMING diagnostics: origin recorded by casc_run_host
 
 static constexpr int kHeadK = 7;      // Krylov head covers stages 0..6 (128 lags)
 
@@ -420,7 +421,11 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
   std::vector<std::vector<int>> bounds(waves);
   std::vector<std::vector<cudaEvent_t>> u_ev(waves);
   for (int w = 0; w < waves; ++w) {                          // input copies of every wave, in ~8 chunks each
-    const int c0 = w * nw, cn = std::min(nw, n - c0), nc = std::min(cn, 8);
+    static const int chunks = [] {                  // input chunks per wave (CASC_E2E_CHUNKS)
+      const char* e = getenv("CASC_E2E_CHUNKS");
+      return e ? std::max(1, atoi(e)) : 1;   // measured: 1 chunk 4.48 ms e2e on E2, 8 chunks 4.80
+    }();
+    const int c0 = w * nw, cn = std::min(nw, n - c0), nc = std::min(cn, chunks);
     bounds[w].resize(nc + 1);
     u_ev[w].resize(nc);
     for (int i = 0; i <= nc; ++i) bounds[w][i] = (int)((int64_t)cn * i / nc);
@@ -449,6 +454,16 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
     const int64_t sig = (int64_t)c0 * batch * L;
     rc = bank_wave(cn, m, L, batch, N_host + c0, N_max, Pw, Bbar + (int64_t)c0 * m, C + (int64_t)c0 * m,
                    D ? D + c0 : nullptr, u_dev + sig, y_dev + sig, ws, ws_bytes, st, pinned[dev] + 6 * (size_t)c0, &bs);
+  }
+  if (getenv("CASC_TIMING") && g_timing_t0) {       // diagnostics: when each stream finishes
+    cudaEvent_t a, b, c;
+    cudaEventCreate(&a); cudaEventCreate(&b); cudaEventCreate(&c);
+    cudaEventRecord(a, in_streams[dev]); cudaEventRecord(b, st); cudaEventRecord(c, out_streams[dev]);
+    cudaDeviceSynchronize();
+    float ta, tb, tc;
+    cudaEventElapsedTime(&ta, g_timing_t0, a); cudaEventElapsedTime(&tb, g_timing_t0, b); cudaEventElapsedTime(&tc, g_timing_t0, c);
+    fprintf(stderr, "casc timing: input copies done %.3f, compute done %.3f, output copies done %.3f ms\n", ta, tb, tc);
+    cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c);
   }
   cudaError_t e1 = cudaStreamSynchronize(out_streams[dev]), e2 = cudaStreamSynchronize(st);
   cudaError_t e3 = cudaStreamSynchronize(in_streams[dev]);
@@ -624,6 +639,18 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
   }
   // cascades whose output parts come from the head (Ne <= 7; with fold also Ne = 8, 9)
   if (!chunked && (rc = emit(count_lp_ge(kHeadK + 1), n))) return rc;
+  auto tmark = [&](const char* what) {              // CASC_TIMING diagnostics
+    if (!getenv("CASC_TIMING") || !g_timing_t0) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    cudaEventSynchronize(e);
+    float t;
+    cudaEventElapsedTime(&t, g_timing_t0, e);
+    fprintf(stderr, "casc timing: %s %.3f ms\n", what, t);
+    cudaEventDestroy(e);
+  };
+  tmark("head done");
   // ---- streaming stages k >= kHeadK over the channels with Neff > k (prefixes of `order`)
   int pass = 0;
   for (int k = kHeadK; k < maxNe; k += (variant == 't' ? 2 : 1), ++pass) {
@@ -710,6 +737,7 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     }
     if ((rc = emit(count_lp_ge(k + 3), count_lp_ge(k + 1)))) return rc;   // channels with Lp in {k + 1, k + 2}
   }
+  tmark("passes done");
   if (streaming) return CASC_OK;                      // every channel was emitted
   // ---- tail: stage Ne + y = C v + D u
   if (use_ab) {                                     // from the fused (C v, C P_Ne v) parts

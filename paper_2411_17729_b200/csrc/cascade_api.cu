@@ -23,6 +23,7 @@
 #include "profile.cuh"
 
 namespace casc {
+extern cudaEvent_t g_timing_t0;   // bank_engine.cu (diagnostics)
 thread_local int g_launches = 0;
 
 static int eff_order(int N, int64_t L) {
@@ -412,6 +413,10 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
     // chunk as it lands) and finished channels' outputs go back while later stage passes run
     for (int s = 0; s < n_sys; ++s)
       if (N_host[s] < 0 || N_host[s] > N_max) return CASC_ERR_DIM;
+    if (getenv("CASC_TIMING")) {                        // diagnostics: timeline origin (bank_engine.cu)
+      if (!casc::g_timing_t0) cudaEventCreate(&casc::g_timing_t0);
+      cudaEventRecord(casc::g_timing_t0, st);
+    }
     CASC_TRY(cudaMemcpyAsync(h.Abar, Abar_h, sizeof(double) * n_sys * m * m, cudaMemcpyHostToDevice, st));
     CASC_TRY(cudaMemcpyAsync(h.Bbar, Bbar_h, sizeof(double) * n_sys * m, cudaMemcpyHostToDevice, st));
     CASC_TRY(cudaMemcpyAsync(h.C, C_h, sizeof(double) * n_sys * m, cudaMemcpyHostToDevice, st));

@@ -52,4 +52,5 @@ if os.environ.get("E2E_TRACE"):
     evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
     t0 = min(e.time_range.start for e in evs)
     for e in sorted(evs, key=lambda e: e.time_range.start):
-        print(f"{(e.time_range.start - t0) / 1e3:8.3f} {(e.time_range.end - t0) / 1e3:8.3f}  {e.name[:60]}")
+        sid = getattr(e, "device_resource_id", None)
+        print(f"{(e.time_range.start - t0) / 1e3:8.3f} {(e.time_range.end - t0) / 1e3:8.3f}  s{sid}  {e.name[:60]}")
