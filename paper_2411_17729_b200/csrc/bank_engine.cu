@@ -557,8 +557,25 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     op.planes = w.parts; op.plane = plane; op.vec = w.pvec; op.neff = dNeff; op.kc = dKc; op.fold = fold;
   }
 
+  cudaStream_t qs = st;                            // pair weights' stream (side stream below)
+  cudaEvent_t q_start = nullptr, q_done = nullptr;
+  struct EvGuard {                                 // destroyed once the waits are enqueued
+    cudaEvent_t* a; cudaEvent_t* b;
+    ~EvGuard() { if (*a) cudaEventDestroy(*a); if (*b) cudaEventDestroy(*b); }
+  } ev_guard{&q_start, &q_done};
   // ---- derived: Krylov columns, w = C P_Ne, fp32 copies, pair weights
   {
+    // the pair weights Q_k need only the powers: they run on a side stream under derived + head
+    static cudaStream_t q_streams[16] = {};
+    int qdev = 0;
+    CASC_TRY(cudaGetDevice(&qdev));
+    if (qdev < 0 || qdev >= 16) return CASC_ERR_UNSUPPORTED;
+    if (!q_streams[qdev]) CASC_TRY(cudaStreamCreateWithFlags(&q_streams[qdev], cudaStreamNonBlocking));
+    qs = q_streams[qdev];
+    CASC_TRY(cudaEventCreateWithFlags(&q_start, cudaEventDisableTiming));
+    CASC_TRY(cudaEventCreateWithFlags(&q_done, cudaEventDisableTiming));
+    CASC_TRY(cudaEventRecord(q_start, st));
+    CASC_TRY(cudaStreamWaitEvent(qs, q_start, 0));
     ProfScope ps(st, K_DERIVED, 0.0, 2.0 * n * (double)m * m * 128);
     if ((rc = launch_bank_derived(P.p64, N_max + 1, Bbar, C, D, dNeff, dKc, w.Kr64, w.krT, w.w64, w.w32, w.c32,
                                   w.d32, use_ab ? w.pvec : nullptr, fold, n, m, st)))
@@ -572,11 +589,12 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       q.B = P.p64 + k * mm; q.ldb = m; q.sB = (int64_t)(N_max + 1) * mm;
       q.C = w.Q64; q.ldc = m; q.sC = mm;
       q.skip_below = dNeff; q.level = k + 2;
-      if ((rc = launch_dgemm(q, n, st))) return rc;
-      pair_split_kernel<<<(int)std::min<int64_t>(ceil_div((int64_t)n * mm, 256), 148 * 8), 256, 0, st>>>(
+      if ((rc = launch_dgemm(q, n, qs))) return rc;
+      pair_split_kernel<<<(int)std::min<int64_t>(ceil_div((int64_t)n * mm, 256), 148 * 8), 256, 0, qs>>>(
           w.Q64, w.Q32, dNeff, k + 2, n, m, qslots, j);
       CASC_LAUNCHED();
     }
+    CASC_TRY(cudaEventRecord(q_done, qs));
   }
   const int64_t ntiles = ceil_div(L, 128);
   // streaming outputs (host-buffer run): channels order[a, b) are final -> tail + copy out
@@ -651,6 +669,7 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     cudaEventDestroy(e);
   };
   tmark("head done");
+  if (q_done) CASC_TRY(cudaStreamWaitEvent(st, q_done, 0));   // the pair weights
   // ---- streaming stages k >= kHeadK over the channels with Neff > k (prefixes of `order`)
   int pass = 0;
   for (int k = kHeadK; k < maxNe; k += (variant == 't' ? 2 : 1), ++pass) {
