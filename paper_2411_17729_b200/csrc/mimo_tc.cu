@@ -672,6 +672,7 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
 
 int launch_mimo_gemm(const MimoGemm& g, bool tf32, cudaStream_t st) {
   if (mimo_pair_ok(g, tf32)) return launch_mimo_gemm_pair(g, st);
+  if (tf32 && mimo_pair_tf32_ok(g)) return launch_mimo_gemm_pair_tf32(g, st);
   if (tf32) {
     if (g.n_out % 128 == 0) return launch_cfg<128, true>(g, st);   // main + corr accumulators
     if (g.n_out % 64 == 0) {
