@@ -31,18 +31,23 @@ using namespace sm100;
 
 namespace {
 constexpr int HM = 128;                   // rows per CTA
-constexpr int BN = 128;                   // output columns per pair tile
 constexpr int BK = 32;                    // fp32 K per chunk (128-byte rows)
 constexpr uint32_t A_BYTES = HM * 128;    // 16 KB (hi in place; lo in its own 16 KB)
-constexpr uint32_t W_BYTES = 64 * 128;    // 8 KB: this CTA's 64 weight rows, one of hi / lo
-constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * W_BYTES;   // A hi | A lo | W hi | W lo
-constexpr int STAGES = 4;
 constexpr int RS = 2;                     // residual / staging chunks (128 rows x 32 fp32)
 constexpr uint32_t R_BYTES = HM * 128;
 constexpr int CW = 32;                    // epilogue chunk width (fp32 columns = 128 bytes)
-constexpr int NCH = BN / CW;
 constexpr int THREADS = 11 * 32;          // 0 TMA, 1 MMA, 2-5 epilogue, 6-9 transform, 10 residual
-constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + RS * R_BYTES;
+// BN output columns per pair tile: 128 (two TMEM accumulators, 4 ring slots) or 256 (the state
+// chunk is staged and split once for all 256 columns; one accumulator, 3 ring slots)
+template <int BN>
+struct PCfg {
+  static constexpr uint32_t W_BYTES = (BN / 2) * 128;             // this CTA's BN/2 weight rows, hi or lo
+  static constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * W_BYTES;   // A hi | A lo | W hi | W lo
+  static constexpr int STAGES = BN == 128 ? 4 : 3;
+  static constexpr int NACC = BN == 128 ? 2 : 1;
+  static constexpr int NCH = BN / CW;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + RS * R_BYTES;
+};
 
 __device__ __forceinline__ uint32_t cta_rank3() {
   uint32_t r;
@@ -98,6 +103,7 @@ __device__ __forceinline__ void tmem_ld32_3(uint32_t taddr, uint32_t* r) {
 struct PairCoord3 {
   int seq, l0, nb;     // l0: first row of this CTA's half
 };
+template <int BN>
 __device__ __forceinline__ PairCoord3 decode3(int64_t tile, const MimoArg& a, int n_nblk, int64_t nb_eff, int t0_blk,
                                               uint32_t rank) {
   PairCoord3 t;
@@ -109,12 +115,16 @@ __device__ __forceinline__ PairCoord3 decode3(int64_t tile, const MimoArg& a, in
 }
 }  // namespace
 
+template <int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     mimo_gemm_pair_tf32_kernel(const __grid_constant__ MimoMaps maps, MimoArg a) {
+  using C = PCfg<BN>;
+  constexpr int STAGES = C::STAGES, NACC = C::NACC, NCH = C::NCH;
+  constexpr uint32_t STAGE_BYTES = C::STAGE_BYTES, W_BYTES = C::W_BYTES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sR = smem + STAGES * STAGE_BYTES;
-  __shared__ uint64_t full_a[STAGES], full_w[STAGES], lo_ready[STAGES], empty[STAGES], tfull[2], tempty[2], rfull[RS],
+  __shared__ uint64_t full_a[STAGES], full_w[STAGES], lo_ready[STAGES], empty[STAGES], tfull[NACC], tempty[NACC], rfull[RS],
       rempty[RS];
   __shared__ uint32_t tmem_base;
   auto stA = [&](int s) { return smem + s * STAGE_BYTES; };
@@ -135,7 +145,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_a[s], 1); mbar_init(&full_w[s], 1); mbar_init(&lo_ready[s], 2 * 128); mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * 128); }
+    for (int s = 0; s < NACC; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * 128); }
     for (int s = 0; s < RS; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 1); }
     fence_mbar_init();
   }
@@ -156,7 +166,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     int s = 0;
     uint32_t ph = 0;
     for (int64_t t = pair; t < n_tiles; t += n_pairs) {
-      const PairCoord3 tc = decode3(t, a, n_nblk, nb_eff, t0_blk, rank);
+      const PairCoord3 tc = decode3<BN>(t, a, n_nblk, nb_eff, t0_blk, rank);
       for (int src = 0; src < a.n_src; ++src) {
         const int nk = a.K[src] / BK;
         const int plane = a.w_plane_off[src];
@@ -168,8 +178,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             if (is_leader) mbar_arrive_expect_tx(&full_w[s], 2 * 2 * W_BYTES);   // both CTAs' W hi + lo
             uint32_t fw;                          // the leader CTA's full_w[s] (shared::cluster)
             asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(fw) : "r"(smem_u32(&full_w[s])));
-            tma_load_2sm3(stW(s), &maps.W[src], fw, kc * BK, tc.nb * BN + (int)rank * 64, plane);
-            tma_load_2sm3(stW(s) + W_BYTES, &maps.W[src], fw, kc * BK, tc.nb * BN + (int)rank * 64, plane + 1);
+            tma_load_2sm3(stW(s), &maps.W[src], fw, kc * BK, tc.nb * BN + (int)rank * (BN / 2), plane);
+            tma_load_2sm3(stW(s) + W_BYTES, &maps.W[src], fw, kc * BK, tc.nb * BN + (int)rank * (BN / 2), plane + 1);
           }
           if (++s == STAGES) { s = 0; ph ^= 1; }
         }
@@ -181,7 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     int rs = 0;
     uint32_t rph = 0;
     for (int64_t t = pair; t < n_tiles; t += n_pairs) {
-      const PairCoord3 tc = decode3(t, a, n_nblk, nb_eff, t0_blk, rank);
+      const PairCoord3 tc = decode3<BN>(t, a, n_nblk, nb_eff, t0_blk, rank);
       for (int j = 0; j < NCH; ++j) {
         mbar_wait(&rempty[rs], rph ^ 1);
         if (!issue) {
@@ -202,8 +212,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       uint32_t ph = 0;
       int64_t t_local = 0;
       for (int64_t t = pair; t < n_tiles; t += n_pairs, ++t_local) {
-        const int acc = (int)(t_local & 1);
-        mbar_wait_u(&tempty[acc], (uint32_t)((t_local >> 1) & 1) ^ 1);
+        const int acc = (int)(t_local % NACC);
+        mbar_wait_u(&tempty[acc], (uint32_t)((t_local / NACC) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tbase + acc * 2 * BN, dc = d + BN;
         bool first = true;
@@ -266,9 +276,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     int rs = 0, prev_rs = -1;
     uint32_t rph = 0;
     for (int64_t t = pair; t < n_tiles; t += n_pairs, ++t_local) {
-      const PairCoord3 tc = decode3(t, a, n_nblk, nb_eff, t0_blk, rank);
-      const int acc = (int)(t_local & 1);
-      mbar_wait_u(&tfull[acc], (uint32_t)((t_local >> 1) & 1));
+      const PairCoord3 tc = decode3<BN>(t, a, n_nblk, nb_eff, t0_blk, rank);
+      const int acc = (int)(t_local % NACC);
+      mbar_wait_u(&tfull[acc], (uint32_t)((t_local / NACC) & 1));
       tc_fence_after();
       for (int j = 0; j < NCH; ++j) {
         uint8_t* rbuf = sR + rs * R_BYTES;
@@ -323,13 +333,15 @@ bool mimo_pair_tf32_ok(const MimoGemm& g) {
     const char* e = getenv("CASC_GEMM_PAIR_TF32");
     return e && e[0] == '0';
   }();
-  if (off || g.n_out % BN != 0 || g.w_resident || g.ab || g.parts_deep || g.sys_list != nullptr) return false;
+  if (off || g.n_out % 128 != 0 || g.w_resident || g.ab || g.parts_deep || g.sys_list != nullptr) return false;
   for (int s = 0; s < g.n_src; ++s)
     if (g.src[s].K % BK || g.src[s].w_plane_stride != 0) return false;   // one weight plane pair per source
   return true;
 }
 
-int launch_mimo_gemm_pair_tf32(const MimoGemm& g, cudaStream_t st) {
+template <int BN>
+static int launch_pt(const MimoGemm& g, cudaStream_t st) {
+  using C = PCfg<BN>;
   MimoMaps maps;
   memset(&maps, 0, sizeof(maps));
   MimoArg a{};
@@ -349,23 +361,34 @@ int launch_mimo_gemm_pair_tf32(const MimoGemm& g, cudaStream_t st) {
     a.a_row0[s] = (int)g.src[s].row0;
     if (!map3d(&maps.A[s], g.src[s].A, true, g.src[s].K, g.src[s].row0 + g.L, nseq_total, HM)) return CASC_ERR_CUDA;
     const int64_t planes = g.src[s].w_planes > 0 ? g.src[s].w_planes : 2;
-    if (!map3d(&maps.W[s], g.src[s].W, true, g.src[s].K, g.n_out, planes, 64)) return CASC_ERR_CUDA;
+    if (!map3d(&maps.W[s], g.src[s].W, true, g.src[s].K, g.n_out, planes, BN / 2)) return CASC_ERR_CUDA;
   }
   a.has_residual = g.R != nullptr;
   a.r_row0 = (int)g.R_row0;
   a.out_row0 = (int)g.out_row0;
   if (g.R && !map3d(&maps.R, g.R, true, g.n_out, g.R_row0 + g.L, nseq_total, HM)) return CASC_ERR_CUDA;
   if (!map3d(&maps.out, g.out, true, g.n_out, g.out_row0 + g.L, nseq_total, HM)) return CASC_ERR_CUDA;
-  if (cudaFuncSetAttribute(mimo_gemm_pair_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) !=
-      cudaSuccess)
+  if (cudaFuncSetAttribute(mimo_gemm_pair_tf32_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)C::SMEM) != cudaSuccess)
     return CASC_ERR_CUDA;
   const int64_t blocks = (g.L + 2 * HM - 1) / (2 * HM) - g.t_first / 2;
   const int64_t tiles = (int64_t)g.batch * blocks * (g.n_out / BN);
   if (tiles <= 0) return CASC_OK;
   const int pairs = (int)std::min<int64_t>(tiles, 74);
-  mimo_gemm_pair_tf32_kernel<<<2 * pairs, THREADS, SMEM, st>>>(maps, a);
+  mimo_gemm_pair_tf32_kernel<BN><<<2 * pairs, THREADS, C::SMEM, st>>>(maps, a);
   CASC_LAUNCHED();
   return CASC_OK;
+}
+
+int launch_mimo_gemm_pair_tf32(const MimoGemm& g, cudaStream_t st) {
+  // CASC_GEMM_PAIR_TF32_BN = 128 | 256 (default 128: E3 stage 0.81 ms vs 0.87 ms with 256, whose
+  // single accumulator leaves the epilogue exposed)
+  static const int bn = [] {
+    const char* e = getenv("CASC_GEMM_PAIR_TF32_BN");
+    return e ? atoi(e) : 128;
+  }();
+  if (bn == 256 && g.n_out % 256 == 0) return launch_pt<256>(g, st);
+  return launch_pt<128>(g, st);
 }
 
 }  // namespace casc

@@ -84,3 +84,13 @@ def test_pair_tf32_matches_single_cta_gemm(case):
     y_pair = _gpu_y(case)
     y_one = _gpu_y(case, {"CASC_GEMM_PAIR_TF32": "0"})
     assert rel(y_pair, y_one) < 2e-6
+
+
+def test_pair_tf32_bn128_matches_bn256():
+    """m = 256 stages on 256 x 128 pair tiles (two accumulators) and on 256 x 256 tiles (state
+    chunk split once for both column halves): the same products, the same summation order per
+    output element."""
+    case = CASES[1]
+    y256 = _gpu_y(case)
+    y128 = _gpu_y(case, {"CASC_GEMM_PAIR_TF32_BN": "128"})
+    assert rel(y256, y128) < 1e-7
