@@ -85,7 +85,8 @@ __device__ __forceinline__ void mma_commit_pair_w(uint64_t* bar) {
 __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {   // arrive on the leader CTA's copy
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+  // default semantics (release, CTA scope): a cluster-scope release compiles to MEMBAR.ALL.GPU
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 __device__ __forceinline__ void tmem_ld32_2(uint32_t taddr, uint32_t* r) {
   asm volatile(
