@@ -370,36 +370,51 @@ int launch_bank_derived(const double* p64, int slots, const double* Bbar, const 
 // y_l = a_l + b_{l - 2^Ne} + d u_l with (a, b) = (C v, C P_Ne v) of the last state, written by
 // the stage (or head) that produced v^(Ne): stage Ne and y = C v + D u in
 // the regrouped form of R21/R24, without storing or re-reading v^(Ne).
+__device__ __forceinline__ float4 f4add(float4 x, float4 y) { return make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w); }
+// One (channel, sequence) per blockIdx.y, time rows along x; 4 rows per thread when every row
+// offset is a multiple of 4 (L, the plane stride, the part shift h), so a shifted part is either
+// wholly inside or wholly before the sequence for the 4 rows.
 __global__ void bank_ab_tail_kernel(BankAbTailArg a) {
-  const int64_t per = (int64_t)a.batch * a.L;
-  const int64_t n = (a.list ? (int64_t)a.n_list : (int64_t)a.n_ch) * per;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = a.list ? a.list[i / per] : (int)(i / per);
-    const int64_t e = (int64_t)c * per + i % per, l = e % a.L;
+  const int64_t nseq = (a.list ? (int64_t)a.n_list : (int64_t)a.n_ch) * a.batch;
+  const int64_t P = a.op.plane;
+  const bool vec = (a.L % 4 == 0) && (P % 4 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(a.u) | reinterpret_cast<uintptr_t>(a.y) |
+                     reinterpret_cast<uintptr_t>(a.op.planes)) % 16 == 0);
+  for (int64_t sq = blockIdx.y; sq < nseq; sq += gridDim.y) {
+    const int ci = (int)(sq / a.batch), b = (int)(sq % a.batch);
+    const int c = a.list ? a.list[ci] : ci;
+    const int64_t base = ((int64_t)c * a.batch + b) * a.L;
     const int ne = a.op.neff[c];
     const int d = fold_depth(ne, a.op.kc[c], a.op.fold);
-    const int64_t h = (int64_t)1 << (ne - d);      // stages ne-d .. ne are applied here: shifts h, 2h, 4h
-    const float* pl = a.op.planes + e;
-    const int64_t P = a.op.plane;
-    float s = pl[0];
-    if (l >= h) s += pl[P - h];
-    if (d >= 1) {
-      if (l >= 2 * h) s += pl[2 * P - 2 * h];
-      if (l >= 3 * h) s += pl[3 * P - 3 * h];
+    const int np = 2 << d;                         // parts: stages ne-d .. ne applied here, shifts k*h
+    const int64_t h = (int64_t)1 << (ne - d);
+    const float dc = a.d[c];
+    const float* pl = a.op.planes + base;
+    if (vec && h % 4 == 0) {
+      for (int64_t l = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); l < a.L; l += 4 * (int64_t)gridDim.x * blockDim.x) {
+        float4 s = __ldcs(reinterpret_cast<const float4*>(pl + l));
+        for (int k = 1; k < np; ++k)
+          if (l >= k * h) s = f4add(s, __ldcs(reinterpret_cast<const float4*>(pl + k * P + l - k * h)));
+        const float4 u4 = __ldcs(reinterpret_cast<const float4*>(a.u + base + l));
+        __stcs(reinterpret_cast<float4*>(a.y + base + l),
+               make_float4(fmaf(dc, u4.x, s.x), fmaf(dc, u4.y, s.y), fmaf(dc, u4.z, s.z), fmaf(dc, u4.w, s.w)));
+      }
+    } else {
+      for (int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; l < a.L; l += (int64_t)gridDim.x * blockDim.x) {
+        float s = pl[l];
+        for (int k = 1; k < np; ++k)
+          if (l >= k * h) s += pl[k * P + l - k * h];
+        a.y[base + l] = fmaf(dc, a.u[base + l], s);
+      }
     }
-    if (d >= 2) {
-      if (l >= 4 * h) s += pl[4 * P - 4 * h];
-      if (l >= 5 * h) s += pl[5 * P - 5 * h];
-      if (l >= 6 * h) s += pl[6 * P - 6 * h];
-      if (l >= 7 * h) s += pl[7 * P - 7 * h];
-    }
-    a.y[e] = fmaf(a.d[c], a.u[e], s);
   }
 }
 int launch_bank_ab_tail(const BankAbTailArg& a, cudaStream_t st) {
-  const int64_t n = (a.list ? (int64_t)a.n_list : (int64_t)a.n_ch) * a.batch * a.L;
-  if (n <= 0) return CASC_OK;
-  bank_ab_tail_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 148 * 16), 256, 0, st>>>(a);
+  const int64_t nseq = (a.list ? (int64_t)a.n_list : (int64_t)a.n_ch) * a.batch;
+  if (nseq <= 0 || a.L <= 0) return CASC_OK;
+  const int64_t per_block = (a.L % 4 == 0 && a.op.plane % 4 == 0) ? 4 * 256 : 256;
+  dim3 grid((unsigned)std::min<int64_t>(ceil_div(a.L, per_block), 64), (unsigned)std::min<int64_t>(nseq, 65535));
+  bank_ab_tail_kernel<<<grid, 256, 0, st>>>(a);
   CASC_LAUNCHED();
   return CASC_OK;
 }
