@@ -110,7 +110,9 @@ int launch_pack(const PackLayout& P, int n_sys, int N_max, int m, cudaStream_t s
 // as soon as it is formed -- one launch instead of N_max + 1.
 __global__ void __launch_bounds__(256) powers_small_kernel(const double* Abar, const int* hdr, double* p64,
                                                            float* f32, __nv_bfloat16* b16, int N_max, int m) {
-  constexpr int LD = 65;
+  // row stride 72 doubles: the B-fragment loads (lanes g = 0..7 along a row, t4 = 0..3 down four
+  // rows) fall in two disjoint halves of the banks, 2 wavefronts per load (stride 65: 4)
+  constexpr int LD = 72;
   __shared__ double S[64 * LD];                          // P_k; P_{k+1} overwrites it in place
   const int s = blockIdx.x, tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
   const int64_t mm = (int64_t)m * m;
