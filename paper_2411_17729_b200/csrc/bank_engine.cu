@@ -641,16 +641,23 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     // warp-specialized TMA-store head for m = 64 (CASC_BANK_HEAD=old selects the previous kernel).
     // A TMEM-operand (TS) variant was measured slower (1.67 vs 1.30 ms on E2, same box): its four
     // builder warps write 128 KB of hi/lo per tile to TMEM.
-    static const bool old_head = [] {
+    // CASC_BANK_HEAD = ws (default: one CTA per tile) | pair (CTA pairs, M = 256: measured the same
+    // 1.16 ms on E2 -- the head is bound by the tensor pipe, 69% active, not by operand reads) | old
+    static const char head_kind = [] {
       const char* e = getenv("CASC_BANK_HEAD");
-      return e && e[0] == 'o';
+      return e ? e[0] : 'w';
     }();
+    const bool old_head = head_kind == 'o';
     static const int head_group = [] {
       const char* e = getenv("CASC_HEAD_GROUP");
       return e ? atoi(e) : 64;
     }();
     if (m == 64 && !old_head) a.tiles_per_cta = pick_group(ntiles, (int64_t)hcn * batch, head_group);
-    rc = (m == 64 && !old_head) ? launch_bank_head_ws(m, a, (int64_t)n * batch, st) : launch_bank_head(m, a, st);
+    if (m == 64 && !old_head)
+      rc = head_kind == 'p' ? launch_bank_head_pair(m, a, (int64_t)n * batch, st)
+                            : launch_bank_head_ws(m, a, (int64_t)n * batch, st);
+    else
+      rc = launch_bank_head(m, a, st);
     if (rc) return rc;
     if (chunked && (rc = emit_ids(dhend + hend_off[ci], hend + hend_off[ci], hend_off[ci + 1] - hend_off[ci])))
       return rc;

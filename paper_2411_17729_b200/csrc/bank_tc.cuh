@@ -56,6 +56,8 @@ int launch_bank_fused(const BankFusedArg& a, const float* pack_f32, int n_planes
 bool bank_tc_supported(int m);
 int launch_bank_head(int m, const BankHeadArg& a, cudaStream_t st);
 int launch_bank_head_ws(int m, const BankHeadArg& a, int64_t n_seq_total, cudaStream_t st);
+// the same head on CTA pairs (M = 256 per MMA, the Krylov operand split between the pair)
+int launch_bank_head_pair(int m, const BankHeadArg& a, int64_t n_seq_total, cudaStream_t st);
 int launch_bank_stage_ws(int m, const BankStageArg& a, cudaStream_t st);
 int launch_bank_stage_rp(int m, const BankStageArg& a, cudaStream_t st);
 int launch_bank_tail(int m, const BankTailArg& a, cudaStream_t st);

@@ -126,3 +126,14 @@ def test_fold_two_stages_matches():
     _check(wl, y2)
     y0 = _gpu_y(wl, {"CASC_BANK_FOLD": "0"})
     assert rel(y2, y0) < 2e-6
+
+
+def test_head_pair_matches_one_cta_head():
+    """The bank head on CTA pairs (bank_head_pair.cu, CASC_BANK_HEAD=pair) against the one-CTA
+    head (the default): the same K = 128 Toeplitz products; an odd tile count (the last pair's
+    second tile past the sequence end) and channels ending at the head (Ne <= 7, output parts)."""
+    wl = _bank(6, 128 * 47 - 5, 3, [5, 7, 9, 12, 8, 13])
+    y_pair = _gpu_y(wl, {"CASC_BANK_HEAD": "pair"})
+    _check(wl, y_pair)
+    y_ws = _gpu_y(wl)
+    assert rel(y_pair, y_ws) < 1e-6
