@@ -416,11 +416,21 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
   if (rc) return rc;
   CASC_TRY(cudaEventRecord(ev_start, st));                   // u may be reused only after earlier work
   CASC_TRY(cudaStreamWaitEvent(in_streams[dev], ev_start, 0));
+  const bool timing = getenv("CASC_TIMING") && g_timing_t0;  // diagnostics: copy-in timeline
+  cudaEvent_t t_start = nullptr, t_in0 = nullptr;
+  if (timing) {
+    cudaEventCreate(&t_start); cudaEventCreate(&t_in0);
+    cudaEventRecord(t_start, in_streams[dev]);
+  }
   const size_t row = (size_t)batch * L * sizeof(float);
   const int waves = (n + nw - 1) / nw;
   std::vector<std::vector<int>> bounds(waves);
   std::vector<std::vector<cudaEvent_t>> u_ev(waves);
-  for (int w = 0; w < waves; ++w) {                          // input copies of every wave, in ~8 chunks each
+  // input copies of wave w, submitted just before the wave's own work: a small host->device copy
+  // the wave enqueues (its channel table) queues behind every copy submitted before it on the
+  // copy engine, so submitting all waves' inputs up front delayed wave 0 by the whole input (E5:
+  // 140 ms); wave w+1's copy still runs during wave w's compute
+  for (int w = 0; w < waves; ++w) {                // chunk bounds and completion events of every wave
     static const int chunks = [] {                  // input chunks per wave (CASC_E2E_CHUNKS)
       const char* e = getenv("CASC_E2E_CHUNKS");
       return e ? std::max(1, atoi(e)) : 1;   // measured: 1 chunk 4.48 ms e2e on E2, 8 chunks 4.80
@@ -429,17 +439,24 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
     bounds[w].resize(nc + 1);
     u_ev[w].resize(nc);
     for (int i = 0; i <= nc; ++i) bounds[w][i] = (int)((int64_t)cn * i / nc);
-    for (int i = 0; i < nc; ++i) {
+    for (int i = 0; i < nc; ++i)
       if ((rc = new_event(&u_ev[w][i]))) return rc;
+  }
+  auto submit_inputs = [&](int w) -> int {
+    const int c0 = w * nw, nc = (int)u_ev[w].size();
+    for (int i = 0; i < nc; ++i) {
       const size_t off = (size_t)(c0 + bounds[w][i]) * row;
       CASC_TRY(cudaMemcpyAsync((char*)u_dev + off, (const char*)u_h + off, (size_t)(bounds[w][i + 1] - bounds[w][i]) * row,
                                cudaMemcpyHostToDevice, in_streams[dev]));
       CASC_TRY(cudaEventRecord(u_ev[w][i], in_streams[dev]));
+      if (timing && w == 0 && i == nc - 1) cudaEventRecord(t_in0, in_streams[dev]);
     }
-  }
+    return CASC_OK;
+  };
   PackLayout P = pack_layout(const_cast<void*>(pack), n, m, N_max, CASC_FP32);
   const int64_t slot_mm = (int64_t)(N_max + 1) * m * m;
   for (int w = 0; w < waves && rc == CASC_OK; ++w) {
+    if ((rc = submit_inputs(w))) break;
     const int c0 = w * nw, cn = std::min(nw, n - c0);
     BankStream bs;
     bs.y_host = (char*)const_cast<void*>(y_h) + (size_t)c0 * row;
@@ -463,6 +480,12 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
     float ta, tb, tc;
     cudaEventElapsedTime(&ta, g_timing_t0, a); cudaEventElapsedTime(&tb, g_timing_t0, b); cudaEventElapsedTime(&tc, g_timing_t0, c);
     fprintf(stderr, "casc timing: input copies done %.3f, compute done %.3f, output copies done %.3f ms\n", ta, tb, tc);
+    if (t_start && t_in0) {
+      float t0s, t0i;
+      cudaEventElapsedTime(&t0s, g_timing_t0, t_start); cudaEventElapsedTime(&t0i, g_timing_t0, t_in0);
+      fprintf(stderr, "casc timing: copy-in starts %.3f, wave 0 input landed %.3f ms\n", t0s, t0i);
+      cudaEventDestroy(t_start); cudaEventDestroy(t_in0);
+    }
     cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c);
   }
   cudaError_t e1 = cudaStreamSynchronize(out_streams[dev]), e2 = cudaStreamSynchronize(st);
