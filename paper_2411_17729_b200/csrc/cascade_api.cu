@@ -444,7 +444,16 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
     if (dev >= 0 && dev < 16) {
       if (!in_s[dev]) CASC_TRY(cudaStreamCreateWithFlags(&in_s[dev], cudaStreamNonBlocking));
       if (!out_s[dev]) CASC_TRY(cudaStreamCreateWithFlags(&out_s[dev], cudaStreamNonBlocking));
-      const int nc = std::min(batch, 8);
+      // batch chunks (CASC_MIMO_CHUNKS): by default one per 64 MiB of input, 1..8 -- each chunk adds
+      // its launches' fill/drain; the first input and last output chunk are exposed (E3 e2e: 4
+      // chunks 14.8 ms, 8: 15.0, 16: 17.5; E4 with 4.3 GB of input takes 8)
+      static const int chunks_env = [] {
+        const char* e = getenv("CASC_MIMO_CHUNKS");
+        return e ? std::max(1, atoi(e)) : 0;
+      }();
+      const int64_t in_bytes = (int64_t)es * batch * L * p;
+      const int chunks = chunks_env ? chunks_env : (int)std::min<int64_t>(8, std::max<int64_t>(1, ceil_div(in_bytes, (int64_t)64 << 20)));
+      const int nc = std::min(batch, chunks);
       std::vector<cudaEvent_t> ev((size_t)2 * nc + 1);
       for (auto& e : ev) CASC_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       CASC_TRY(cudaEventRecord(ev[2 * nc], st));
@@ -452,11 +461,15 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
       const size_t in_row = es * (size_t)L * p, out_row = es * (size_t)L * q;
       std::vector<int> b0(nc + 1);
       for (int i = 0; i <= nc; ++i) b0[i] = (int)((int64_t)batch * i / nc);
-      for (int i = 0; i < nc; ++i) {
+      // chunk i+1's input is submitted after chunk i's work is queued: the small table upload inside
+      // each chunk's apply queues behind every copy submitted before it on the copy engine
+      auto submit = [&](int i) -> int {
         CASC_TRY(cudaMemcpyAsync((char*)h.u + b0[i] * in_row, (const char*)u_h + b0[i] * in_row,
                                  (size_t)(b0[i + 1] - b0[i]) * in_row, cudaMemcpyHostToDevice, in_s[dev]));
         CASC_TRY(cudaEventRecord(ev[2 * i], in_s[dev]));
-      }
+        return CASC_OK;
+      };
+      if ((rc = submit(0))) return rc;
       for (int i = 0; i < nc && rc == CASC_OK; ++i) {
         CASC_TRY(cudaStreamWaitEvent(st, ev[2 * i], 0));
         rc = engine_apply(1, m, p, q, L, b0[i + 1] - b0[i], N_host, N_max, mode, h.pack, h.Bbar, h.C,
@@ -466,6 +479,7 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
         CASC_TRY(cudaStreamWaitEvent(out_s[dev], ev[2 * i + 1], 0));
         CASC_TRY(cudaMemcpyAsync((char*)y_h + b0[i] * out_row, (const char*)h.y + b0[i] * out_row,
                                  (size_t)(b0[i + 1] - b0[i]) * out_row, cudaMemcpyDeviceToHost, out_s[dev]));
+        if (i + 1 < nc && (rc = submit(i + 1))) break;
       }
       cudaError_t e1 = cudaStreamSynchronize(out_s[dev]), e2 = cudaStreamSynchronize(st);
       cudaStreamSynchronize(in_s[dev]);
