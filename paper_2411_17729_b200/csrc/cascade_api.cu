@@ -417,8 +417,6 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
       if (!casc::g_timing_t0) cudaEventCreate(&casc::g_timing_t0);
       cudaEventRecord(casc::g_timing_t0, st);
     }
-    // (the input copy waits for the parameters and powers: started before them, under the
-    // parameter copies, E2 e2e measured 5.48 vs 4.26 ms)
     CASC_TRY(cudaMemcpyAsync(h.Abar, Abar_h, sizeof(double) * n_sys * m * m, cudaMemcpyHostToDevice, st));
     CASC_TRY(cudaMemcpyAsync(h.Bbar, Bbar_h, sizeof(double) * n_sys * m, cudaMemcpyHostToDevice, st));
     CASC_TRY(cudaMemcpyAsync(h.C, C_h, sizeof(double) * n_sys * m, cudaMemcpyHostToDevice, st));

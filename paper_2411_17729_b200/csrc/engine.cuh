@@ -15,8 +15,7 @@ int engine_bank_tc(int n, int m, int64_t L, int batch, const int* N_host, int N_
                    size_t ws_bytes, cudaStream_t st);
 int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host, int N_max, const void* pack,
                           const double* Bbar, const double* C, const double* D, float* u_dev, float* y_dev,
-                          const void* u_h, const void* y_h, void* ws, size_t ws_bytes, cudaStream_t st,
-                          cudaEvent_t inputs_free = nullptr);
+                          const void* u_h, const void* y_h, void* ws, size_t ws_bytes, cudaStream_t st);
 bool mimo_tc_path(int n, int m, int p, int q, int mode);
 size_t mimo_ws_bytes(int m, int p, int q, int64_t L, int batch, int mode);
 int engine_mimo_tc(int m, int p, int q, int64_t L, int batch, int N, int N_max, int mode, const void* pack,
