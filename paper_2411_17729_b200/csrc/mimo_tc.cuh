@@ -63,7 +63,7 @@ bool bank_hist_ok(int64_t L, int64_t shift, int n_src, int t_first);
 // bf16, n_out % 256 == 0, one system: 256 x 256 tiles on CTA pairs (mimo_tc2.cu)
 bool mimo_pair_ok(const MimoGemm& g, bool tf32);
 int launch_mimo_gemm_pair(const MimoGemm& g, cudaStream_t st);
-// 3xTF32, n_out % 128 == 0, one system: 256 x 128 tiles on CTA pairs (mimo_tc3.cu)
+// 3xTF32, n_out % 64 == 0, one system: 256 x 64|128 tiles on CTA pairs (mimo_tc3.cu)
 bool mimo_pair_tf32_ok(const MimoGemm& g);
 int launch_mimo_gemm_pair_tf32(const MimoGemm& g, cudaStream_t st);
 

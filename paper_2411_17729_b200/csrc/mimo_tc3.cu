@@ -37,14 +37,14 @@ constexpr int RS = 2;                     // residual / staging chunks (128 rows
 constexpr uint32_t R_BYTES = HM * 128;
 constexpr int CW = 32;                    // epilogue chunk width (fp32 columns = 128 bytes)
 constexpr int THREADS = 11 * 32;          // 0 TMA, 1 MMA, 2-5 epilogue, 6-9 transform, 10 residual
-// BN output columns per pair tile: 128 (two TMEM accumulators, 4 ring slots) or 256 (the state
-// chunk is staged and split once for all 256 columns; one accumulator, 3 ring slots)
+// BN output columns per pair tile: 64 or 128 (two TMEM accumulators, 4 ring slots) or 256 (the
+// state chunk is staged and split once for all 256 columns; one accumulator, 3 ring slots)
 template <int BN>
 struct PCfg {
   static constexpr uint32_t W_BYTES = (BN / 2) * 128;             // this CTA's BN/2 weight rows, hi or lo
   static constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * W_BYTES;   // A hi | A lo | W hi | W lo
-  static constexpr int STAGES = BN == 128 ? 4 : 3;
-  static constexpr int NACC = BN == 128 ? 2 : 1;
+  static constexpr int STAGES = BN == 256 ? 3 : 4;
+  static constexpr int NACC = BN == 256 ? 1 : 2;
   static constexpr int NCH = BN / CW;
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + RS * R_BYTES;
 };
@@ -328,12 +328,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512) : "memory");
 }
 
+// CASC_GEMM_PAIR_TF32_BN = 128 | 256 | 64 (default 128: E3 stage 0.81 ms vs 0.87 ms with 256, whose
+// single accumulator leaves the epilogue exposed; 64-wide outputs stay on the one-CTA kernel unless
+// 64 is asked for: the E3 output stage measured 0.59 ms on pairs vs 0.47 ms)
+static int pair_bn() {
+  static const int bn = [] {
+    const char* e = getenv("CASC_GEMM_PAIR_TF32_BN");
+    return e ? atoi(e) : 128;
+  }();
+  return bn;
+}
+static bool bn64() { return pair_bn() == 64; }
+
 bool mimo_pair_tf32_ok(const MimoGemm& g) {
   static const bool off = [] {
     const char* e = getenv("CASC_GEMM_PAIR_TF32");
     return e && e[0] == '0';
   }();
-  if (off || g.n_out % 128 != 0 || g.w_resident || g.ab || g.parts_deep || g.sys_list != nullptr) return false;
+  if (off || g.n_out % (bn64() ? 64 : 128) != 0 || g.w_resident || g.ab || g.parts_deep || g.sys_list != nullptr) return false;
   for (int s = 0; s < g.n_src; ++s)
     if (g.src[s].K % BK || g.src[s].w_plane_stride != 0) return false;   // one weight plane pair per source
   return true;
@@ -381,14 +393,10 @@ static int launch_pt(const MimoGemm& g, cudaStream_t st) {
 }
 
 int launch_mimo_gemm_pair_tf32(const MimoGemm& g, cudaStream_t st) {
-  // CASC_GEMM_PAIR_TF32_BN = 128 | 256 (default 128: E3 stage 0.81 ms vs 0.87 ms with 256, whose
-  // single accumulator leaves the epilogue exposed)
-  static const int bn = [] {
-    const char* e = getenv("CASC_GEMM_PAIR_TF32_BN");
-    return e ? atoi(e) : 128;
-  }();
+  const int bn = pair_bn();
   if (bn == 256 && g.n_out % 256 == 0) return launch_pt<256>(g, st);
-  return launch_pt<128>(g, st);
+  if (g.n_out % 128 == 0) return launch_pt<128>(g, st);
+  return launch_pt<64>(g, st);                    // 64-wide outputs (the MIMO output stage, q = 64)
 }
 
 }  // namespace casc

@@ -94,3 +94,16 @@ def test_pair_tf32_bn128_matches_bn256():
     y256 = _gpu_y(case)
     y128 = _gpu_y(case, {"CASC_GEMM_PAIR_TF32_BN": "128"})
     assert rel(y256, y128) < 1e-7
+
+
+@pytest.mark.parametrize("case", [(64, 64, 64, 1000, 3, 9), (192, 64, 64, 700, 2, 8)])
+def test_pair_tf32_64_wide_outputs(case):
+    """64-column outputs (m = 64 stages, q = 64 output stages) on 256 x 64 pair tiles (opt-in,
+    CASC_GEMM_PAIR_TF32_BN=64) against the oracle and the default kernels."""
+    wl = _wl(*case)
+    y = _gpu_y(case, {"CASC_GEMM_PAIR_TF32_BN": "64"})
+    u = wl.u_all()
+    y_ref = oracle.apply_workload(wl, u=u, channels=range(wl.n_ch))
+    assert rel(y, y_ref) <= 1e-5
+    y_one = _gpu_y(case)
+    assert rel(y, y_one) < 2e-6
