@@ -5,10 +5,13 @@
 
 A step is one pass of the whole hot path over one batch of synthetic input: powers by repeated
 squaring (a1) + apply (first stage, stages, last stage with y = Cv + Du),
-inputs resident in HBM. The default workload is BASELINE.json configs[1] (E2: 256 HiPPO-LegS
-SISO channels, m=64, L=16384, batch 4, fp32). With N GPUs (torchrun) every rank runs its own
-E2-sized share of a 256*N-channel bank (channel sharding: no collective; weak scaling); the time
-is the max over ranks of the device-timed steps.
+inputs resident in HBM. The default workload is BASELINE.json configs[3] (E4: one MIMO system,
+m=1024, p=q=256, L=2^20, batch 8, bf16 storage / fp32 accumulate), the configuration the
+metric's "1/2/4/8 B200" scaling is quoted on: with N GPUs (torchrun) the sequence is sharded
+across the ranks (rank r owns rows [r L/N, (r+1) L/N); per-stage halo exchange over NCCL inside
+the library; strong scaling). E5 (4096 HiPPO channels) shards channels round-robin by N_c (no
+collective). E1-E3 are selectable with --config. The time is the max over ranks of the
+device-timed steps.
 
 `--impl reference` times the float64 oracle (oracle/) on this host's cores on a bounded sample
 of the same workload (rank 0 only). The oracle is test infrastructure; this flag and the
@@ -39,7 +42,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="E2", choices=list(CONFIG_INDEX))
+    ap.add_argument("--config", default="E4", choices=list(CONFIG_INDEX))
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle CPU baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -76,14 +79,22 @@ def make_workload(cfg: str, world: int, rank: int):
                                          "2^k rows from rank r-1 (NCCL P2P)") if world > 1 else "single"}
     if cfg == "E5":
         wl = S.make_E5()
-        per = wl.n_ch // world
-        chans = list(range(per * rank, per * (rank + 1)))
+        chans = e5_channels(wl.N, world, rank)
         Ns = wl.N[chans]
-        return wl, chans, {"workload": "E5", "n_ch_total": wl.n_ch, "n_ch_per_gpu": per, "m": 64, "p": 1,
+        return wl, chans, {"workload": "E5", "n_ch_total": wl.n_ch, "n_ch_this_gpu": len(chans), "m": 64, "p": 1,
                            "q": 1, "L": wl.L, "batch": wl.batch, "N_c_range": [int(Ns.min()), int(Ns.max())],
-                           "stages_per_gpu": int((Ns + 1).sum()),
-                           "parallelism": f"channel-sharded x{world} (no collective), channel waves in HBM"}
+                           "stages_this_gpu": int((Ns + 1).sum()),
+                           "parallelism": (f"channel-sharded x{world}: channels sorted by N_c and dealt round-robin "
+                                           "(SURVEY §8e), no collective; channel waves in HBM")}
     raise SystemExit(f"unknown config {cfg}")
+
+
+def e5_channels(N, world: int, rank: int) -> list:
+    """balance sum(N_c + 1) across ranks by sorting the channels by N_c (descending,
+    stable) and dealing them round-robin; each rank's list is returned in channel order."""
+    import numpy as np
+    order = np.argsort(-np.asarray(N), kind="stable")
+    return sorted(int(c) for c in order[rank::world])
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -148,12 +159,25 @@ def gpu_smi_id(torch, dev: int) -> str:
 
 # ----------------------------------------------------------------------------- peaks
 def peaks():
+    """Roofline denominators: MEASURED_PEAKS.json (driver-written: HBM copy, cuBLAS bf16 burst and
+    sustained) and profiles/r02_tf32_peak.json (this repo's measurement of the tf32 tensor peak the
+    same way: torch.matmul fp32 inputs with TF32 enabled, 8192^3, burst and sustained)."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         d = json.load(open(path))
-        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
-                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+        out = {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+               "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
+    else:
+        out = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+    tf = os.path.join(ROOT, "profiles", "r02_tf32_peak.json")
+    if os.path.exists(tf):
+        d = json.load(open(tf))
+        out.update({"tf32_tflops": d["tf32_tflops"], "tf32_tflops_sustained": d["tf32_tflops_sustained"],
+                    "tf32_source": "measured (profiles/r02_tf32_peak.json)"})
+    else:
+        out.update({"tf32_tflops": 0.5 * out["bf16_tflops"], "tf32_tflops_sustained": 0.5 * out["bf16_tflops_sustained"],
+                    "tf32_source": "assumed: 1/2 of bf16 (nominal ratio)"})
+    return out
 
 
 def ncu_traffic(kernel_class: str, cfg: str):
@@ -167,42 +191,63 @@ def ncu_traffic(kernel_class: str, cfg: str):
 
 
 def roofline(prof: dict, mode: str, cfg: str):
-    """Roofline of the dominant kernel class (largest total device time in the timed region)."""
+    """Roofline of the dominant kernel class (largest total device time in the timed region).
+
+    The bound is the binding roof of the EXECUTED work (the schedule actually run): t_roof =
+    max(exec_bytes / HBM, exec_flops / peak of the pipe the flops run on), sustained peaks (kernels
+    timed inside a long step). `achieved` / `frac` are that roof's units per second and the ratio to
+    its peak; the algorithmic figures (SURVEY §8d per-unit bytes and flops x units) are reported
+    beside them, with frac_ns against B_ns for the bank stage (one read + one write per stage)."""
     if not prof:
         return None
     cls, r = max(prof.items(), key=lambda kv: kv[1]["ms"])
     pk = peaks()
     t = r["ms"] / r["launches"] / 1e3                      # average launch duration, s
     by, fl = r["bytes"] / r["launches"], r["flops"] / r["launches"]
-    tensor_classes = ("mimo_tc_stage", "mimo_tc_first", "mimo_tc_last")
-    if cls in tensor_classes:
-        if mode == "bf16":
-            peak, note = pk["bf16_tflops_sustained"], "bf16 sustained (%s)" % pk["source"]
-        else:
-            peak = pk["bf16_tflops_sustained"] * 0.5 / 3.0
-            note = "3xTF32 useful-flop peak = sustained bf16 x 0.5 (tf32/bf16 nominal) / 3 (%s)" % pk["source"]
-        ach = fl / t / 1e12
-        out = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak}
+    xby, xfl = r.get("exec_bytes", r["bytes"]) / r["launches"], r.get("exec_flops", r["flops"]) / r["launches"]
+    pipe = r.get("pipe", "none")
+    pipe_peak = {"bf16": pk["bf16_tflops_sustained"], "tf32": pk["tf32_tflops_sustained"]}.get(pipe)
+    t_hbm = xby / (pk["hbm_gbs"] * 1e9)
+    t_ten = xfl / (pipe_peak * 1e12) if pipe_peak else 0.0
+    if pipe_peak and t_ten >= t_hbm:
+        ach = xfl / t / 1e12
+        out = {"bound": "tensor", "achieved": ach, "peak": pipe_peak, "unit": "TFLOP/s", "frac": ach / pipe_peak}
+        note = f"{pipe} tensor pipe, sustained ({pk['tf32_source'] if pipe == 'tf32' else pk['source']})"
     else:
-        ach = by / t / 1e9
-        peak = pk["hbm_gbs"]
-        note = "HBM copy bandwidth (%s)" % pk["source"]
-        out = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak}
-        if cls == "bank_stage":
-            # SURVEY 8d: B_fused = the bytes of the schedule run (one read + one write of the m x L
-            # state per pass; a pair pass applies two stages, R23); B_ns = one read + one write per
-            # stage = flops * 4 / m (8m B and 2m^2 flop per row and stage, m = 64)
-            note += ("; achieved/frac: B_fused = one read + one write of the state per pass (a pair "
-                     "pass applies two stages); frac_ns: B_ns = one read + one write per stage")
-            ach_ns = fl * 4.0 / 64.0 / t / 1e9
-            out.update({"achieved_ns": ach_ns, "frac_ns": ach_ns / peak})
-    out.update({"traffic": ncu_traffic(cls, cfg), "kernel": cls, "launches_timed": r["launches"],
-                "avg_launch_ms": t * 1e3, "algorithmic_bytes_per_launch": by,
-                "algorithmic_flops_per_launch": fl, "peak_note": note})
+        ach = xby / t / 1e9
+        out = {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach / pk["hbm_gbs"]}
+        note = f"HBM copy bandwidth ({pk['source']})"
+    out.update({
+        "traffic": ncu_traffic(cls, cfg), "kernel": cls, "launches_timed": r["launches"],
+        "avg_launch_ms": t * 1e3, "peak_note": note,
+        "executed": {"bytes_per_launch": xby, "flops_per_launch": xfl, "pipe": pipe,
+                     "t_roof_hbm_ms": t_hbm * 1e3, "t_roof_tensor_ms": t_ten * 1e3,
+                     "frac_of_binding_roof": max(t_hbm, t_ten) / t},
+        "algorithmic": {"bytes_per_launch": by, "flops_per_launch": fl,
+                        "gbs": by / t / 1e9, "frac_hbm": by / t / 1e9 / pk["hbm_gbs"],
+                        "tflops": fl / t / 1e12}})
+    if cls == "bank_stage":
+        # B_ns = one read + one write of the m-wide state per stage = flops x 4 / m (m = 64)
+        ach_ns = fl * 4.0 / 64.0 / t / 1e9
+        out.update({"achieved_ns": ach_ns, "frac_ns": ach_ns / pk["hbm_gbs"]})
     return out
 
 
 # ----------------------------------------------------------------------------- oracle (CPU)
+def cpu_info() -> dict:
+    """Host CPU: model name (/proc/cpuinfo), logical cores (nproc) and the BLAS threads numpy uses."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    nproc = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    return {"cpu_model": model, "nproc": nproc, "blas_threads": oracle_threads()}
+
+
 def oracle_threads() -> int:
     try:
         from threadpoolctl import threadpool_info
@@ -268,13 +313,14 @@ def run_reference(args, world, rank):
         f, s, t, desc = oracle_sample(wl, chans[off:] + chans[:off], per_step)
         tot_f, tot_s, tot_t = tot_f + f, tot_s + s, tot_t + t
     value = tot_f / tot_t / 1e9
-    cores = oracle_threads()
+    ci = cpu_info()
+    cores = ci["blas_threads"]
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
             "samples_per_s": tot_s / tot_t, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE recipe)", "config": cfgd,
             "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
-                             "sample": desc + f"; each step a bounded sample (~{per_step:.0f}s)"},
+                             "sample": desc + f"; each step a bounded sample (~{per_step:.0f}s)", **ci},
             "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -405,8 +451,10 @@ def run_ours(args, world, rank, local_rank):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         f_s, s_s, t_s, desc = oracle_sample(wl, chans, args.cpu_seconds)
+        ci = cpu_info()
         cpu = {"value": f_s / t_s / 1e9, "unit": "GFLOP/s", "samples_per_s": s_s / t_s,
-               "cores": oracle_threads(), "kind": "oracle", "sample": desc, "seconds": t_s}
+               "cores": ci["blas_threads"], "kind": "oracle", "sample": desc, "seconds": t_s, **ci,
+               "note": "float64 numpy oracle (BLAS-threaded matmuls), not tuned; cores = BLAS threads used"}
     cfgd = dict(cfgd)
     cfgd["l2"] = "512 MiB buffer written between timed steps (flush); state buffers also exceed L2"
     cfgd["timed_step"] = "powers (fp64 squaring + pack) + apply (all stages, y = Cv + Du)"

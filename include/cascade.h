@@ -196,6 +196,10 @@ int casc_profile_reset(void);
 int casc_profile_num_classes(void);
 const char* casc_profile_class_name(int cls);
 int casc_profile_read(int cls, int* launches, double* ms, double* bytes, double* flops);
+/* The EXECUTED work of the same records (summed): the HBM bytes the schedule run moves and the
+ * math-pipe flops it issues (3xTF32 counts three tf32 products; skipped zero blocks are not
+ * counted); pipe: 0 none, 1 tf32, 2 bf16, 3 fp64, 4 fp32 (CUDA cores) -- the peak to judge them by. */
+int casc_profile_read_exec(int cls, double* exec_bytes, double* exec_flops, int* pipe);
 
 /* ----------------------------------------------------------------------------------------
  * Hardware self-test of the tensor-core building block (diagnostics; used by tests/):

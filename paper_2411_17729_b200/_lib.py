@@ -49,6 +49,8 @@ SIGNATURES = {
     "casc_profile_class_name": (c_char_p, [c_int]),
     "casc_profile_read": (c_int, [c_int, P_int, ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+    "casc_profile_read_exec": (c_int, [c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                       P_int]),
 }
 
 _lib = None

@@ -14,6 +14,7 @@ import torch
 from ._lib import check, int_array, lib
 
 MODES = {"fp32": 0, "bf16": 1}
+PIPES = {0: "none", 1: "tf32", 2: "bf16", 3: "fp64", 4: "fp32"}
 STORAGE = {0: torch.float32, 1: torch.bfloat16}
 
 
@@ -170,6 +171,10 @@ def profile_read() -> dict:
         check(L.casc_profile_read(c, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(by), ctypes.byref(fl)),
               "casc_profile_read")
         if n.value:
-            out[L.casc_profile_class_name(c).decode()] = {"launches": n.value, "ms": ms.value,
-                                                          "bytes": by.value, "flops": fl.value}
+            xb, xf, pipe = ctypes.c_double(0), ctypes.c_double(0), ctypes.c_int(0)
+            check(L.casc_profile_read_exec(c, ctypes.byref(xb), ctypes.byref(xf), ctypes.byref(pipe)),
+                  "casc_profile_read_exec")
+            out[L.casc_profile_class_name(c).decode()] = {
+                "launches": n.value, "ms": ms.value, "bytes": by.value, "flops": fl.value,
+                "exec_bytes": xb.value, "exec_flops": xf.value, "pipe": PIPES.get(pipe.value, "none")}
     return out

@@ -27,48 +27,27 @@ namespace casc {
 cudaEvent_t g_timing_t0 = nullptr;   // CASC_TIMING diagnostics: origin recorded by casc_run_host
 
 static constexpr int kHeadK = 7;      // Krylov head covers stages 0..6 (128 lags)
+static constexpr int kMetaInts = 4;   // per-channel host table: Neff | Kc | parity | order
 
-// stage-kernel variant (CASC_BANK_STAGE, for A/B measurements), m % 64 == 0:
-//   't' (default) stage pairs (R23): one pass applies two adjacent factors of Eq. 5 through a
-//       3-source TMA GEMM with the A operands in TMEM and the three weight pairs resident in
-//       shared memory; half the HBM passes of 's' (E2: 3.97 vs 4.30 ms for the streaming stages)
-//   's' one stage per pass (HBM-bound, ~84% of the measured copy bandwidth)
-//   'r' register-prefetch kernel, 'w' warp-specialized CUDA-core variant (m = 16, 32 use 'r')
-static char stage_variant(int m) {
-  static const char env = [] {
-    const char* e = getenv("CASC_BANK_STAGE");
-    return e ? e[0] : 't';
+// the fused output parts (R24-R26) for m = 64; CASC_BANK_AB=0 stores v and runs the separate tail
+// (tests compare the two)
+static bool bank_ab_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CASC_BANK_AB");
+    return !(e && e[0] == '0');
   }();
-  if (env == 'w' || env == 'r') return env;
-  if (m % 64 != 0) return 'r';
-  return env == 's' ? 's' : 't';
+  return on;
 }
+
+// stage kernels: m % 64 == 0 runs stage pairs (R23) on the history-resident tensor-core
+// kernel (bank_hist.cu; the multi-source TMA GEMM of mimo_tc.cu where it does not apply); m = 16, 32
+// run one stage per pass on the CUDA-core register-prefetch kernel (bank_stage_rp.cu: HBM-bound)
+static char stage_variant(int m) { return m % 64 == 0 ? 't' : 'r'; }
 
 static int pair_slots(int n_max) { return n_max > kHeadK ? (n_max - kHeadK + 1) / 2 : 0; }
 
-// Weight-resident GEMM mode for the stage (CASC_BANK_WRES=1). Measured slower on E2 (5.2 ms vs
-// 4.5 ms per step for the stages): the single weight buffer needs a pipeline drain at every
-// channel change, which costs more than the ring traffic it saves. Off by default.
-static int resident_weights() {
-  static const int on = [] {
-    const char* e = getenv("CASC_BANK_WRES");
-    return e && e[0] == '1' ? 1 : 0;
-  }();
-  return on;
-}
-
-// Weight-resident GEMM for stage pairs (three weight pairs per tile, 96 KB): on by default,
-// CASC_BANK_PAIR_WRES=0 reloads the weights per tile through the ring.
-static int pair_wres() {
-  static const int on = [] {
-    const char* e = getenv("CASC_BANK_PAIR_WRES");
-    return e && e[0] == '0' ? 0 : 1;
-  }();
-  return on;
-}
-
 struct BankWs {
-  int* meta;      // Neff | Kc | parity | order | iota | head-enders by input chunk   (6 n ints)
+  int* meta;      // Neff | Kc | parity | order   (kMetaInts n ints)
   double* Kr64;   // [n][m][128]
   float* krT;     // [n][2][m][128]
   double* w64;    // [n][m]
@@ -84,7 +63,7 @@ struct BankWs {
 static BankWs carve_bank(void* ws, int n, int m, int64_t L, int batch, int qslots) {
   Carver c(ws);
   BankWs w{};
-  w.meta = c.take<int>((size_t)6 * n);
+  w.meta = c.take<int>((size_t)kMetaInts * n);
   w.Kr64 = c.take<double>((size_t)n * m * 128);
   w.krT = c.take<float>((size_t)n * 2 * m * 128);
   w.w64 = c.take<double>((size_t)n * m);
@@ -117,184 +96,8 @@ static int eff_order_b(int N, int64_t L) {
   return N < kstar ? N : kstar;
 }
 
-// ---------------------------------------------------------------- fused persistent path
-// bank_fused.cu: one launch for the whole bank, states in TMEM, levels exchanged through L2.
-// Opt-in (CASC_BANK_FUSED=1, read per call) for m = 64 when every channel has Ne >= 7: it is
-// correct (tests/test_gpu_bank_fused.py) but measured slower than the multi-kernel path on E2
-// (8.9 vs 6.4 ms for head + stages + tail): its tf32 N=64 MMAs are shared-memory-bound (48 cyc
-// each, 128 B/cyc) and the per-tile publication chain adds latency; see DESIGN.md.
-static bool fused_enabled() {
-  const char* e = getenv("CASC_BANK_FUSED");
-  return e && e[0] == '1';
-}
-static bool discard_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("CASC_DISCARD");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-static constexpr int kFusedT = 4;           // tiles per chunk (TMEM: 4 x 64 state columns)
-
-struct FusedWs {
-  int* meta;        // Neff | Kc | order
-  double* Kr64;     // [n][64][128]
-  float* krimg;     // [n][16384]
-  double* w64;      // [n][64]
-  float *w32, *c32, *d32;
-  unsigned* done;   // [n*batch]
-  unsigned* flags;  // [S][ntiles]
-  float* pub;       // [S][NL][ntiles*128][64]
-  size_t bytes;
-};
-static FusedWs carve_fused(void* ws, int n, int64_t L, int batch, int S, int NL) {
-  Carver c(ws);
-  FusedWs w{};
-  const int64_t ntiles = ceil_div(L, 128);
-  w.meta = c.take<int>((size_t)3 * n);
-  w.Kr64 = c.take<double>((size_t)n * 64 * 128);
-  w.krimg = c.take<float>((size_t)n * 16384);
-  w.w64 = c.take<double>((size_t)n * 64);
-  w.w32 = c.take<float>((size_t)n * 64);
-  w.c32 = c.take<float>((size_t)n * 64);
-  w.d32 = c.take<float>((size_t)n);
-  w.done = c.take<unsigned>((size_t)n * batch);
-  w.flags = c.take<unsigned>((size_t)S * ntiles);
-  w.pub = c.take<float>((size_t)S * NL * ntiles * 128 * 64);
-  w.bytes = c.bytes();
-  return w;
-}
-static int sm_count() {
-  static const int n = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v > 0 ? v : 148;
-  }();
-  return n;
-}
-// sequence slots: enough for every sequence a CTA can be working on while others lag behind
-static int fused_slots(int64_t nchunk, int64_t Q) {
-  const int64_t s = 2 * ceil_div(148, nchunk) + 4;
-  return (int)std::min<int64_t>(Q, s);
-}
-static size_t fused_ws_bytes(int n, int m, int64_t L, int batch, int n_max) {
-  if (m != 64 || !fused_enabled()) return 0;
-  const int NL = eff_order_b(n_max, L) - 6;
-  if (NL < 1) return 0;
-  const int64_t nchunk = ceil_div(ceil_div(L, 128), kFusedT);
-  return carve_fused(nullptr, n, L, batch, fused_slots(nchunk, (int64_t)n * batch), NL).bytes;
-}
-
 size_t bank_ws_bytes(int n, int m, int64_t L, int batch, int n_max) {
-  return std::max(carve_bank(nullptr, n, m, L, batch, stage_variant(m) == 't' ? pair_slots(n_max) : 0).bytes,
-                  fused_ws_bytes(n, m, L, batch, n_max));
-}
-
-// Returns CASC_ERR_UNSUPPORTED when the fused path does not apply (caller falls back to the
-// multi-kernel path), CASC_ERR_WORKSPACE when not even one sequence slot fits.
-static int bank_fused(int n, int64_t L, int batch, const int* N_host, int N_max, const void* pack,
-                      const double* Bbar, const double* C, const double* D, const void* u, void* y, void* ws,
-                      size_t ws_bytes, cudaStream_t st) {
-  constexpr int m = 64;
-  if (!fused_enabled()) return CASC_ERR_UNSUPPORTED;
-  const int64_t Q = (int64_t)n * batch;
-  const int64_t ntiles = ceil_div(L, 128);
-  if (Q >= (1 << 26) || ntiles >= (1 << 24)) return CASC_ERR_UNSUPPORTED;
-  std::vector<int> meta((size_t)3 * n);
-  int *Neff = meta.data(), *Kc = Neff + n, *order = Neff + 2 * n;
-  int maxNe = 0;
-  double flops = 0, bytes = 0;
-  for (int s = 0; s < n; ++s) {
-    Neff[s] = eff_order_b(N_host[s], L);
-    if (Neff[s] < kHeadK) return CASC_ERR_UNSUPPORTED;
-    Kc[s] = kHeadK;
-    maxNe = std::max(maxNe, Neff[s]);
-    flops += 2.0 * m * m * (N_host[s] + 1) * (double)L * batch;          // PAPER count, SURVEY 8d
-    bytes += ((N_host[s] + 1) * 2.0 * m * 4.0 + 8.0) * (double)L * batch;  // unfused streaming bytes
-  }
-  std::iota(order, order + n, 0);
-  std::stable_sort(order, order + n, [&](int a, int b) { return Neff[a] > Neff[b]; });
-  const int NL = maxNe - 6;
-  int T = kFusedT;
-  if (const char* e = getenv("CASC_FUSED_T")) T = std::max(1, std::min(kFusedT, atoi(e)));
-  const int64_t nchunk = ceil_div(ntiles, T);
-  int S = fused_slots(nchunk, Q);
-  if (const char* e = getenv("CASC_FUSED_SLOTS")) S = std::max(1, std::min(S, atoi(e)));   // tests: force reuse
-  while (S > 1 && carve_fused(nullptr, n, L, batch, S, NL).bytes > ws_bytes) --S;
-  FusedWs w = carve_fused(ws, n, L, batch, S, NL);
-  if (w.bytes > ws_bytes) return CASC_ERR_WORKSPACE;
-  PackLayout P = pack_layout(const_cast<void*>(pack), n, m, N_max, CASC_FP32);
-  const int64_t mm = (int64_t)m * m;
-  int rc;
-  CASC_TRY(cudaMemcpyAsync(w.meta, meta.data(), meta.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-  const int *dNeff = w.meta, *dKc = w.meta + n, *dorder = w.meta + 2 * n;
-  {
-    // derived: Krylov columns Kr[:, j] = Abar^j Bbar (j < 128) by doubling with the powers
-    // (Kr_{2^i + j} = P_i Kr_j), their tf32 hi/lo smem image; w = C P_Ne; fp32 copies of C, D
-    ProfScope ps(st, K_DERIVED, 0.0, 2.0 * n * (double)m * m * 128);
-    if ((rc = launch_kr_init(Bbar, w.Kr64, n, m, st))) return rc;
-    for (int i = 0; i < kHeadK; ++i) {
-      DgemmArg a{};
-      a.M = m; a.N = 1 << i; a.K = m;
-      a.A = P.p64 + i * mm; a.lda = m; a.sA = (int64_t)(N_max + 1) * mm;
-      a.B = w.Kr64; a.ldb = 128; a.sB = (int64_t)m * 128;
-      a.C = w.Kr64 + (1 << i); a.ldc = 128; a.sC = (int64_t)m * 128;
-      if ((rc = launch_dgemm(a, n, st))) return rc;
-    }
-    if ((rc = launch_kr_image(w.Kr64, dKc, w.krimg, n, st))) return rc;
-    DgemmArg a{};                                // w = C P_Ne  (1 x m)
-    a.M = 1; a.N = m; a.K = m;
-    a.A = C; a.lda = m; a.sA = m;
-    a.B = P.p64; a.ldb = m; a.sB = (int64_t)(N_max + 1) * mm; a.nB = mm; a.selB = dNeff;
-    a.C = w.w64; a.ldc = m; a.sC = m;
-    if ((rc = launch_dgemm(a, n, st))) return rc;
-    if ((rc = launch_f64_to_f32(w.w64, w.w32, (int64_t)n * m, st))) return rc;
-    if ((rc = launch_f64_to_f32(C, w.c32, (int64_t)n * m, st))) return rc;
-    if (D) {
-      if ((rc = launch_f64_to_f32(D, w.d32, n, st))) return rc;
-    } else {
-      CASC_TRY(cudaMemsetAsync(w.d32, 0, sizeof(float) * n, st));
-    }
-  }
-  CASC_TRY(cudaMemsetAsync(w.done, 0, sizeof(unsigned) * (size_t)Q, st));
-  CASC_TRY(cudaMemsetAsync(w.flags, 0, sizeof(unsigned) * (size_t)S * ntiles, st));
-  BankFusedArg a{};
-  a.u = static_cast<const float*>(u); a.y = static_cast<float*>(y); a.krimg = w.krimg;
-  a.cvec = w.c32; a.wvec = w.w32; a.dvec = w.d32; a.order = dorder; a.Neff = dNeff;
-  a.flags = w.flags; a.done = w.done; a.pub = w.pub;
-  a.L = L; a.batch = batch; a.ntiles = (int)ntiles; a.T = T; a.nchunk = (int)nchunk; a.S = S; a.NL = NL;
-  a.planes_per_ch = 2 * (N_max + 1); a.total_chunks = Q * nchunk; a.discard = discard_enabled() ? 1 : 0;
-  const int grid = (int)std::min<int64_t>(a.total_chunks, sm_count());
-  if (getenv("CASC_DEBUG"))
-    fprintf(stderr, "casc: bank_fused n=%d L=%lld batch=%d ntiles=%lld nchunk=%lld S=%d NL=%d grid=%d ws=%zu\n", n,
-            (long long)L, batch, (long long)ntiles, (long long)nchunk, S, NL, grid, w.bytes);
-  static unsigned long long* dbg = nullptr;
-  const bool want_dbg = getenv("CASC_FUSED_DBG") != nullptr;
-  if (want_dbg) {
-    if (!dbg) CASC_TRY(cudaMalloc(&dbg, 24 * sizeof(unsigned long long)));
-    CASC_TRY(cudaMemsetAsync(dbg, 0, 24 * sizeof(unsigned long long), st));
-    a.dbg = dbg;
-  }
-  {
-    ProfScope ps(st, K_BANK_FUSED, bytes, flops);
-    rc = launch_bank_fused(a, P.f32, (int)((int64_t)n * (N_max + 1) * 2), grid, st);
-  }
-  if (want_dbg && rc == CASC_OK) {          // diagnostics only: synchronises and prints
-    unsigned long long h[24];
-    CASC_TRY(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st));
-    CASC_TRY(cudaStreamSynchronize(st));
-    const double tot = (double)h[20] / grid;
-    static const char* nm[5][4] = {{"prod.wfree/done", "prod.flag", "prod.aempty", "-"},
-                                   {"mma.wfull", "mma.zfull", "mma.accempty", "mma.loready"},
-                                   {"xf.done", "xf.zempty", "xf.afull", "xf.lofree"},
-                                   {"epi.accfull", "epi.stg_empty", "epi.afull", "-"},
-                                   {"st.stg_full", "st.read", "st.release", "-"}};
-    fprintf(stderr, "casc fused dbg: grid %d, avg kernel cycles/CTA %.0f\n", grid, tot);
-    for (int r = 0; r < 5; ++r)
-      for (int i = 0; i < 4; ++i)
-        if (h[r * 4 + i]) fprintf(stderr, "  %-16s %6.1f%%\n", nm[r][i], 100.0 * h[r * 4 + i] / grid / tot);
-  }
-  return rc;
+  return carve_bank(nullptr, n, m, L, batch, stage_variant(m) == 't' ? pair_slots(n_max) : 0).bytes;
 }
 
 static int pick_group(int64_t ntiles, int64_t seqs, int want) {
@@ -322,11 +125,8 @@ __global__ void pair_split_kernel(const double* Q64, float* Q32, const int* Neff
 struct BankStream {        // host-buffer run: output channels copied out as soon as they are final
   void* y_host = nullptr;           // pinned [n][batch][L] (null: no streaming)
   cudaStream_t cout = nullptr;      // copy-out stream
-  cudaEvent_t u_ready = nullptr;    // input copy completion (the head waits for it)
   std::vector<cudaEvent_t>* events = nullptr;   // created here, destroyed by the caller
-  // input arriving in chunks of channels [bounds[i], bounds[i+1]) (memory order), chunk i complete
-  // at u_events[i]: the head runs per chunk as its input lands
-  int n_chunks = 0; const int* bounds = nullptr; const cudaEvent_t* u_events = nullptr;
+  cudaEvent_t u_event = nullptr;     // the wave's input copy has landed (the head waits for it)
 };
 static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int N_max, const PackLayout& Pw,
                      const double* Bbar, const double* C, const double* D, const float* u, float* y, void* ws,
@@ -337,10 +137,6 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
 int engine_bank_tc(int n, int m, int64_t L, int batch, const int* N_host, int N_max, const void* pack,
                    const double* Bbar, const double* C, const double* D, const void* u, void* y, void* ws,
                    size_t ws_bytes, cudaStream_t st) {
-  if (m == 64) {
-    const int rc = bank_fused(n, L, batch, N_host, N_max, pack, Bbar, C, D, u, y, ws, ws_bytes, st);
-    if (rc != CASC_ERR_UNSUPPORTED && rc != CASC_ERR_WORKSPACE) return rc;
-  }
   int maxNe = 0;
   for (int s = 0; s < n; ++s) maxNe = std::max(maxNe, eff_order_b(N_host[s], L));
   const int qslots = stage_variant(m) == 't' ? pair_slots(maxNe) : 0;
@@ -370,41 +166,30 @@ int engine_bank_tc(int n, int m, int64_t L, int batch, const int* N_host, int N_
   return CASC_OK;
 }
 
-// End to end from host buffers with the transfers overlapped (casc_run_host, one wave): the input
-// copy (copy-in stream) overlaps the parameter upload, the powers and the derived data, and each
-// group of channels whose cascade is complete (the head for Ne <= 7, then every stage pass) gets
-// its tail and its output copy (copy-out stream) while the remaining passes run. u_h / y_h should
-// be pinned. CASC_ERR_WORKSPACE if the whole bank does not fit the workspace (caller falls back).
+// End to end from host buffers with the transfers overlapped (casc_run_host): per wave, the input
+// copy (copy-in stream) overlaps the previous wave's compute, and each group of channels whose
+// cascade is complete (the head for Ne <= 7, then every stage pass) gets its tail and its output
+// copy (copy-out stream) while the remaining passes run. u_h / y_h should be pinned. The caller
+// holds the device context's lock (cascade_api.cu). CASC_ERR_WORKSPACE if not even one channel fits,
+// CASC_ERR_UNSUPPORTED for shapes without the fused output parts (the caller then runs the serial
+// path).
 int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host, int N_max, const void* pack,
                           const double* Bbar, const double* C, const double* D, float* u_dev, float* y_dev,
-                          const void* u_h, const void* y_h, void* ws, size_t ws_bytes, cudaStream_t st) {
+                          const void* u_h, const void* y_h, void* ws, size_t ws_bytes, cudaStream_t st,
+                          DevCtx* ctx) {
+  if (m != 64 || !bank_ab_enabled()) return CASC_ERR_UNSUPPORTED;
   int maxNe = 0;
   for (int s = 0; s < n; ++s) maxNe = std::max(maxNe, eff_order_b(N_host[s], L));
-  const int qslots = stage_variant(m) == 't' ? pair_slots(maxNe) : 0;
-  if (m != 64) return CASC_ERR_UNSUPPORTED;
-  // channels per wave (bounded memory, as engine_bank_tc); every wave streams its own input chunks
-  // and outputs, and wave w+1's input copy overlaps wave w's compute
+  const int qslots = pair_slots(maxNe);
+  // channels per wave (bounded memory, as engine_bank_tc)
   int nw = n;
   while (nw > 0 && carve_bank(nullptr, nw, m, L, batch, qslots).bytes > ws_bytes) {
     const size_t per = carve_bank(nullptr, 1, m, L, batch, qslots).bytes;
     nw = (int)std::min<size_t>((size_t)nw - 1, ws_bytes / std::max<size_t>(per, 1));
   }
   if (nw < 1) return CASC_ERR_WORKSPACE;
-  static cudaStream_t out_streams[16] = {}, in_streams[16] = {};   // per device (created once)
-  static int* pinned[16] = {};                     // per device pinned staging of the channel tables
-  static size_t pinned_n[16] = {};
-  int dev = 0;
-  CASC_TRY(cudaGetDevice(&dev));
-  if (dev < 0 || dev >= 16) return CASC_ERR_UNSUPPORTED;
-  if (!out_streams[dev]) CASC_TRY(cudaStreamCreateWithFlags(&out_streams[dev], cudaStreamNonBlocking));
-  if (!in_streams[dev]) CASC_TRY(cudaStreamCreateWithFlags(&in_streams[dev], cudaStreamNonBlocking));
-  if (pinned_n[dev] < (size_t)6 * n) {
-    if (pinned[dev]) cudaFreeHost(pinned[dev]);
-    pinned[dev] = nullptr;
-    pinned_n[dev] = 0;
-    CASC_TRY(cudaHostAlloc(&pinned[dev], sizeof(int) * 6 * (size_t)n, cudaHostAllocDefault));
-    pinned_n[dev] = (size_t)6 * n;
-  }
+  int rc;
+  if ((rc = ctx->ensure_pinned((size_t)kMetaInts * n))) return rc;
   std::vector<cudaEvent_t> events;
   auto new_event = [&](cudaEvent_t* e) -> int {
     CASC_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -412,86 +197,58 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
     return CASC_OK;
   };
   cudaEvent_t ev_start;
-  int rc = new_event(&ev_start);
-  if (rc) return rc;
+  if ((rc = new_event(&ev_start))) return rc;
   // u may be overwritten only after earlier work on st (starting the copy before the parameter
   // copies and powers measured slower on E2: 5.48 vs 4.26 ms e2e)
   CASC_TRY(cudaEventRecord(ev_start, st));
-  CASC_TRY(cudaStreamWaitEvent(in_streams[dev], ev_start, 0));
-  const bool timing = getenv("CASC_TIMING") && g_timing_t0;  // diagnostics: copy-in timeline
-  cudaEvent_t t_start = nullptr, t_in0 = nullptr;
-  if (timing) {
-    cudaEventCreate(&t_start); cudaEventCreate(&t_in0);
-    cudaEventRecord(t_start, in_streams[dev]);
-  }
+  CASC_TRY(cudaStreamWaitEvent(ctx->in, ev_start, 0));
   const size_t row = (size_t)batch * L * sizeof(float);
   const int waves = (n + nw - 1) / nw;
-  std::vector<std::vector<int>> bounds(waves);
-  std::vector<std::vector<cudaEvent_t>> u_ev(waves);
-  // input copies of wave w, submitted just before the wave's own work: a small host->device copy
-  // the wave enqueues (its channel table) queues behind every copy submitted before it on the
-  // copy engine, so submitting all waves' inputs up front delayed wave 0 by the whole input (E5:
-  // 140 ms); wave w+1's copy still runs during wave w's compute
-  for (int w = 0; w < waves; ++w) {                // chunk bounds and completion events of every wave
-    static const int chunks = [] {                  // input chunks per wave (CASC_E2E_CHUNKS)
-      const char* e = getenv("CASC_E2E_CHUNKS");
-      return e ? std::max(1, atoi(e)) : 1;   // measured: 1 chunk 4.48 ms e2e on E2, 8 chunks 4.80
-    }();
-    const int c0 = w * nw, cn = std::min(nw, n - c0), nc = std::min(cn, chunks);
-    bounds[w].resize(nc + 1);
-    u_ev[w].resize(nc);
-    for (int i = 0; i <= nc; ++i) bounds[w][i] = (int)((int64_t)cn * i / nc);
-    for (int i = 0; i < nc; ++i)
-      if ((rc = new_event(&u_ev[w][i]))) return rc;
-  }
-  auto submit_inputs = [&](int w) -> int {
-    const int c0 = w * nw, nc = (int)u_ev[w].size();
-    for (int i = 0; i < nc; ++i) {
-      const size_t off = (size_t)(c0 + bounds[w][i]) * row;
-      CASC_TRY(cudaMemcpyAsync((char*)u_dev + off, (const char*)u_h + off, (size_t)(bounds[w][i + 1] - bounds[w][i]) * row,
-                               cudaMemcpyHostToDevice, in_streams[dev]));
-      CASC_TRY(cudaEventRecord(u_ev[w][i], in_streams[dev]));
-      if (timing && w == 0 && i == nc - 1) cudaEventRecord(t_in0, in_streams[dev]);
-    }
-    return CASC_OK;
-  };
+  std::vector<cudaEvent_t> u_ev(waves);
+  for (int w = 0; w < waves; ++w)
+    if ((rc = new_event(&u_ev[w]))) return rc;
+  // the input copy of wave w is submitted just before the wave's own work: a small host->device copy
+  // the wave enqueues (its channel table) queues behind every copy submitted before it on the copy
+  // engine, so submitting all waves' inputs up front delayed wave 0 by the whole input (E5: 140 ms);
+  // wave w+1's copy still runs during wave w's compute
   PackLayout P = pack_layout(const_cast<void*>(pack), n, m, N_max, CASC_FP32);
   const int64_t slot_mm = (int64_t)(N_max + 1) * m * m;
   for (int w = 0; w < waves && rc == CASC_OK; ++w) {
-    if ((rc = submit_inputs(w))) break;
     const int c0 = w * nw, cn = std::min(nw, n - c0);
+    const size_t off = (size_t)c0 * row;
+    if (cudaMemcpyAsync((char*)u_dev + off, (const char*)u_h + off, (size_t)cn * row, cudaMemcpyHostToDevice,
+                        ctx->in) != cudaSuccess ||
+        cudaEventRecord(u_ev[w], ctx->in) != cudaSuccess) {
+      rc = CASC_ERR_CUDA;
+      break;
+    }
     BankStream bs;
-    bs.y_host = (char*)const_cast<void*>(y_h) + (size_t)c0 * row;
-    bs.cout = out_streams[dev];
+    bs.y_host = (char*)const_cast<void*>(y_h) + off;
+    bs.cout = ctx->out;
     bs.events = &events;
-    bs.n_chunks = (int)u_ev[w].size();
-    bs.bounds = bounds[w].data();
-    bs.u_events = u_ev[w].data();
+    bs.u_event = u_ev[w];
     PackLayout Pw = P;
     Pw.p64 += c0 * slot_mm;
     Pw.f32 += c0 * slot_mm * 2;
     const int64_t sig = (int64_t)c0 * batch * L;
     rc = bank_wave(cn, m, L, batch, N_host + c0, N_max, Pw, Bbar + (int64_t)c0 * m, C + (int64_t)c0 * m,
-                   D ? D + c0 : nullptr, u_dev + sig, y_dev + sig, ws, ws_bytes, st, pinned[dev] + 6 * (size_t)c0, &bs);
+                   D ? D + c0 : nullptr, u_dev + sig, y_dev + sig, ws, ws_bytes, st, ctx->pinned + kMetaInts * (size_t)c0,
+                   &bs);
   }
   if (getenv("CASC_TIMING") && g_timing_t0) {       // diagnostics: when each stream finishes
     cudaEvent_t a, b, c;
     cudaEventCreate(&a); cudaEventCreate(&b); cudaEventCreate(&c);
-    cudaEventRecord(a, in_streams[dev]); cudaEventRecord(b, st); cudaEventRecord(c, out_streams[dev]);
+    cudaEventRecord(a, ctx->in); cudaEventRecord(b, st); cudaEventRecord(c, ctx->out);
     cudaDeviceSynchronize();
     float ta, tb, tc;
     cudaEventElapsedTime(&ta, g_timing_t0, a); cudaEventElapsedTime(&tb, g_timing_t0, b); cudaEventElapsedTime(&tc, g_timing_t0, c);
     fprintf(stderr, "casc timing: input copies done %.3f, compute done %.3f, output copies done %.3f ms\n", ta, tb, tc);
-    if (t_start && t_in0) {
-      float t0s, t0i;
-      cudaEventElapsedTime(&t0s, g_timing_t0, t_start); cudaEventElapsedTime(&t0i, g_timing_t0, t_in0);
-      fprintf(stderr, "casc timing: copy-in starts %.3f, wave 0 input landed %.3f ms\n", t0s, t0i);
-      cudaEventDestroy(t_start); cudaEventDestroy(t_in0);
-    }
     cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c);
   }
-  cudaError_t e1 = cudaStreamSynchronize(out_streams[dev]), e2 = cudaStreamSynchronize(st);
-  cudaError_t e3 = cudaStreamSynchronize(in_streams[dev]);
+  // every stream is drained before returning, also on error: no copy into or out of the caller's
+  // host buffers is in flight after the call
+  cudaError_t e1 = cudaStreamSynchronize(ctx->out), e2 = cudaStreamSynchronize(st);
+  cudaError_t e3 = cudaStreamSynchronize(ctx->in);
   for (auto& e : events) cudaEventDestroy(e);
   if (rc) return rc;
   return (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) ? CASC_ERR_CUDA : CASC_OK;
@@ -504,16 +261,11 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
                      size_t ws_bytes, cudaStream_t st, int* pinned_meta, const BankStream* bs) {
   const char variant = stage_variant(m);
   // output fusion: the producer of each channel's last state writes (C v, C P_Ne v) instead of
-  // v (R24); taken with the m = 64 TMA stage GEMM and warp-specialized head
-  static const bool ab_off = [] {
-    const char* e = getenv("CASC_BANK_AB");
-    return e && e[0] == '0';
-  }();
-  const bool use_ab = m == 64 && (variant == 's' || variant == 't') && !ab_off && !(getenv("CASC_BANK_HEAD") && getenv("CASC_BANK_HEAD")[0] == 'o');
-  std::vector<int> meta_v(pinned_meta ? 0 : (size_t)6 * n);
+  // v (R24); taken with the m = 64 tensor-core stage kernels and head
+  const bool use_ab = m == 64 && bank_ab_enabled();
+  std::vector<int> meta_v(pinned_meta ? 0 : (size_t)kMetaInts * n);
   int* meta = pinned_meta ? pinned_meta : meta_v.data();
-  int *Neff = meta, *Kc = Neff + n, *par = Neff + 2 * n, *order = Neff + 3 * n, *iota = Neff + 4 * n,
-      *hend = Neff + 5 * n;
+  int *Neff = meta, *Kc = Neff + n, *par = Neff + 2 * n, *order = Neff + 3 * n;
   int maxNe = 0;
   for (int s = 0; s < n; ++s) {
     Neff[s] = eff_order_b(N_host[s], L);
@@ -533,16 +285,16 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
   int rc;
   std::iota(order, order + n, 0);
   std::stable_sort(order, order + n, [&](int a, int b) { return Neff[a] > Neff[b]; });
-  std::iota(iota, iota + n, 0);
   // R24-R26 (common.cuh OutParts): y is formed from parts written by the kernel producing
   // v^(Ne-d); with fold, d = 1 for an odd number of streaming stages (no single-stage pass) and
   // d = 2 for an even number >= 2 (the last stage-pair pass is skipped). Planned only where every
   // pass producing d > 0 parts runs on the history-resident kernel (or is the head).
-  // CASC_BANK_FOLD = 0 | 1 (R25, default) | 2 (R25 + R26: measured slower, E2 3.90 vs 3.75 ms and
-  // E5 807 vs 768 ms, the eight-part epilogues cost more than the skipped pair passes save)
+  // CASC_BANK_FOLD = 1 (R25, default) | 0 (R24 only: every streaming stage runs; the tests compare
+  // the two regroupings). R26 (fold 2: also skip the last stage-pair pass) measured slower (E2 3.90
+  // vs 3.75 ms, E5 807 vs 768 ms: eight-part epilogues cost more than the skipped passes save).
   static const int fold_mode = [] {
     const char* e = getenv("CASC_BANK_FOLD");
-    return e ? atoi(e) : 1;
+    return (e && e[0] == '0') ? 0 : 1;
   }();
   int fold = (use_ab && variant == 't') ? fold_mode : 0;
   for (int c = 0; fold && c < n; ++c) {
@@ -551,21 +303,8 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
   }
   std::vector<int> Lp(n);                          // the state level each channel's parts come from
   for (int c = 0; c < n; ++c) Lp[c] = Neff[c] - fold_depth(Neff[c], Kc[c], fold);
-  auto ends_at_head = [&](int c) { return Lp[c] == Kc[c]; };
-  const bool chunked = bs && bs->n_chunks > 1;
-  std::vector<int> hend_off(chunked ? bs->n_chunks + 1 : 1, 0);
-  if (chunked) {                                   // head-ending channels (Ne == Kc), grouped by chunk
-    int o = 0;
-    for (int ci = 0; ci < bs->n_chunks; ++ci) {
-      hend_off[ci] = o;
-      for (int c = bs->bounds[ci]; c < bs->bounds[ci + 1]; ++c)
-        if (ends_at_head(c)) hend[o++] = c;
-    }
-    hend_off[bs->n_chunks] = o;
-  }
-  CASC_TRY(cudaMemcpyAsync(w.meta, meta, (size_t)6 * n * sizeof(int), cudaMemcpyHostToDevice, st));
-  const int *dNeff = w.meta, *dKc = w.meta + n, *dpar = w.meta + 2 * n, *dorder = w.meta + 3 * n,
-            *diota = w.meta + 4 * n, *dhend = w.meta + 5 * n;
+  CASC_TRY(cudaMemcpyAsync(w.meta, meta, (size_t)kMetaInts * n * sizeof(int), cudaMemcpyHostToDevice, st));
+  const int *dNeff = w.meta, *dKc = w.meta + n, *dpar = w.meta + 2 * n, *dorder = w.meta + 3 * n;
   auto count_ge = [&](int need) {                    // channels with Neff >= need: a prefix of order
     int c = 0;
     while (c < n && Neff[order[c]] >= need) ++c;
@@ -591,12 +330,9 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
   // ---- derived: Krylov columns, w = C P_Ne, fp32 copies, pair weights
   {
     // the pair weights Q_k need only the powers: they run on a side stream under derived + head
-    static cudaStream_t q_streams[16] = {};
-    int qdev = 0;
-    CASC_TRY(cudaGetDevice(&qdev));
-    if (qdev < 0 || qdev >= 16) return CASC_ERR_UNSUPPORTED;
-    if (!q_streams[qdev]) CASC_TRY(cudaStreamCreateWithFlags(&q_streams[qdev], cudaStreamNonBlocking));
-    qs = q_streams[qdev];
+    DevCtx* ctx = dev_ctx();
+    if (!ctx) return CASC_ERR_CUDA;
+    qs = ctx->side;
     CASC_TRY(cudaEventCreateWithFlags(&q_start, cudaEventDisableTiming));
     CASC_TRY(cudaEventCreateWithFlags(&q_done, cudaEventDisableTiming));
     CASC_TRY(cudaEventRecord(q_start, st));
@@ -624,7 +360,10 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
   const int64_t ntiles = ceil_div(L, 128);
   // streaming outputs (host-buffer run): channels order[a, b) are final -> tail + copy out
   const bool streaming = bs && bs->y_host && use_ab;
-  auto emit_ids = [&](const int* dlist, const int* hlist, int cnt) -> int {
+  auto emit = [&](int a0, int b0) -> int {
+    const int* dlist = dorder + a0;
+    const int* hlist = order + a0;
+    const int cnt = b0 - a0;
     if (!streaming || cnt <= 0) return CASC_OK;
     BankAbTailArg t{};
     t.op = op; t.u = static_cast<const float*>(u); t.y = static_cast<float*>(y);
@@ -650,45 +389,33 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     }
     return CASC_OK;
   };
-  auto emit = [&](int a, int b) -> int { return emit_ids(dorder + a, order + a, b - a); };
-  // ---- head: stages 0..Kc-1 (+ Bbar u), all channels (per input chunk when the input is streamed)
-  if (bs && bs->u_ready) CASC_TRY(cudaStreamWaitEvent(st, bs->u_ready, 0));
-  for (int ci = 0; ci < (chunked ? bs->n_chunks : 1); ++ci) {
-    if (chunked) CASC_TRY(cudaStreamWaitEvent(st, bs->u_events[ci], 0));
-    const int hc0 = chunked ? bs->bounds[ci] : 0, hcn = chunked ? bs->bounds[ci + 1] - hc0 : n;
+  // ---- head: stages 0..Kc-1 (+ Bbar u), all channels
+  // the input copy of a host-buffer run is on a copy stream: the head (and the D u tail) may read u
+  // only after it landed
+  if (bs && bs->u_event) CASC_TRY(cudaStreamWaitEvent(st, bs->u_event, 0));
+  {
     BankHeadArg a{};
     a.u = static_cast<const float*>(u); a.krT = w.krT; a.V = static_cast<float*>(w.Va);
-    a.sys_list = chunked ? diota + hc0 : dorder; a.n_list = hcn; a.L = L; a.batch = batch;
+    a.sys_list = dorder; a.n_list = n; a.L = L; a.batch = batch;
     if (use_ab) a.op = op;
-    a.tiles_per_cta = pick_group(ntiles, (int64_t)n * batch, 16);
     ProfScope ps(st, K_BANK_HEAD, (double)n * batch * L * (1 + m) * 4.0,
                  (double)n * batch * L * 2.0 * m * 128);
-    // warp-specialized TMA-store head for m = 64 (CASC_BANK_HEAD=old selects the previous kernel).
-    // A TMEM-operand (TS) variant was measured slower (1.67 vs 1.30 ms on E2, same box): its four
-    // builder warps write 128 KB of hi/lo per tile to TMEM.
-    // CASC_BANK_HEAD = ws (default: one CTA per tile) | pair (CTA pairs, M = 256: measured the same
-    // 1.16 ms on E2 -- the head is bound by the tensor pipe, 69% active, not by operand reads) | old
-    static const char head_kind = [] {
-      const char* e = getenv("CASC_BANK_HEAD");
-      return e ? e[0] : 'w';
-    }();
-    const bool old_head = head_kind == 'o';
-    static const int head_group = [] {
-      const char* e = getenv("CASC_HEAD_GROUP");
-      return e ? atoi(e) : 64;
-    }();
-    if (m == 64 && !old_head) a.tiles_per_cta = pick_group(ntiles, (int64_t)hcn * batch, head_group);
-    if (m == 64 && !old_head)
-      rc = head_kind == 'p' ? launch_bank_head_pair(m, a, (int64_t)n * batch, st)
-                            : launch_bank_head_ws(m, a, (int64_t)n * batch, st);
-    else
+    // executed: m = 64 issues three tf32 products per K step (hi.[hi|lo] at N = 128, lo.hi)
+    if (m == 64) ps.exec((double)n * batch * L * (1 + m) * 4.0, 3.0 * n * batch * L * 2.0 * m * 128, PIPE_TF32);
+    // m = 64: warp-specialized TMA-store head (bank_head_ws.cu); m = 16, 32: CUDA-core head.
+    // Measured alternatives not kept: a TMEM-operand variant (1.67 vs 1.30 ms on E2),
+    // the head on CTA pairs (same 1.16 ms: the head is bound by the tensor pipe, 69% active)
+    if (m == 64) {
+      a.tiles_per_cta = pick_group(ntiles, (int64_t)n * batch, 64);
+      rc = launch_bank_head_ws(m, a, (int64_t)n * batch, st);
+    } else {
+      a.tiles_per_cta = pick_group(ntiles, (int64_t)n * batch, 16);
       rc = launch_bank_head(m, a, st);
+    }
     if (rc) return rc;
-    if (chunked && (rc = emit_ids(dhend + hend_off[ci], hend + hend_off[ci], hend_off[ci + 1] - hend_off[ci])))
-      return rc;
   }
-  // cascades whose output parts come from the head (Ne <= 7; with fold also Ne = 8, 9)
-  if (!chunked && (rc = emit(count_lp_ge(kHeadK + 1), n))) return rc;
+  // cascades whose output parts come from the head (Ne <= 7; with fold also Ne = 8)
+  if ((rc = emit(count_lp_ge(kHeadK + 1), n))) return rc;
   auto tmark = [&](const char* what) {              // CASC_TIMING diagnostics
     if (!getenv("CASC_TIMING") || !g_timing_t0) return;
     cudaEvent_t e;
@@ -703,32 +430,12 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
   tmark("head done");
   if (q_done) CASC_TRY(cudaStreamWaitEvent(st, q_done, 0));   // the pair weights
   // ---- streaming stages k >= kHeadK over the channels with Neff > k (prefixes of `order`)
+  // fraction of the dense MMA work a stage pass issues (1: every K block of the weights)
+  const double tri_frac = 1.0;
   int pass = 0;
   for (int k = kHeadK; k < maxNe; k += (variant == 't' ? 2 : 1), ++pass) {
     const float* Vs = static_cast<const float*>(pass % 2 == 0 ? w.Va : w.Vb);
     float* Vd = static_cast<float*>(pass % 2 == 0 ? w.Vb : w.Va);
-    if (variant == 's') {                           // TMA GEMM, one stage per pass
-      const int cnt = count_ge(k + 1);
-      MimoGemm g{};
-      g.src[0].A = Vs; g.src[0].W = P.f32; g.src[0].K = m; g.src[0].shift = (int64_t)1 << k;
-      g.src[0].w_plane_off = 2 * k; g.src[0].w_planes = (int64_t)n * (N_max + 1) * 2;
-      g.src[0].w_plane_stride = 2 * (N_max + 1);
-      g.n_src = 1; g.R = Vs; g.out = Vd; g.n_out = m; g.L = L; g.batch = batch;
-      g.sys_list = dorder; g.n_list = cnt; g.n_sys_total = n;
-      g.t_first = pass == 0 ? 0 : (int)(((int64_t)1 << (k - 1)) / 128);
-      g.w_resident = resident_weights();
-      if (use_ab) {                                 // channels whose last streaming stage this is
-        g.ab_neff = dNeff; g.ab_level = k + 1; g.ab_c = w.c32; g.ab_w = w.w32; g.ab = w.parts; g.ab_plane = plane;
-        // their (C v, C P_Ne v) parts are needed on every row: no skipped leading tiles
-        if (count_ge(k + 1) > count_ge(k + 2)) g.t_first = 0;
-      }
-      {
-        ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt * batch * L * m * 4.0, 2.0 * cnt * batch * L * (double)mm);
-        if ((rc = launch_mimo_gemm(g, true, st))) return rc;
-      }
-      if ((rc = emit(count_ge(k + 2), count_ge(k + 1)))) return rc;   // channels with Ne == k + 1
-      continue;
-    }
     if (variant != 't') {
       const int cnt = count_ge(k + 1);
       BankStageArg a{};
@@ -737,7 +444,7 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       a.sys_list = dorder; a.n_list = cnt; a.L = L; a.batch = batch;
       a.tiles_per_cta = pick_group(ntiles, (int64_t)cnt * batch, 8);
       ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt * batch * L * m * 4.0, 2.0 * cnt * batch * L * (double)mm);
-      rc = variant == 'w' ? launch_bank_stage_ws(m, a, st) : launch_bank_stage_rp(m, a, st);
+      rc = launch_bank_stage_rp(m, a, st);
       if (rc) return rc;
       continue;
     }
@@ -756,7 +463,7 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       g.src[2].w_plane_off = 2 * pass; g.src[2].w_planes = (int64_t)n * qslots * 2;
       g.src[2].w_plane_stride = 2 * qslots;
       g.n_src = 3; g.R = Vs; g.out = Vd; g.n_out = m; g.L = L; g.batch = batch;
-      g.sys_list = dorder; g.n_list = cnt2; g.n_sys_total = n; g.t_first = t_first; g.w_resident = pair_wres();
+      g.sys_list = dorder; g.n_list = cnt2; g.n_sys_total = n; g.t_first = t_first; g.w_resident = 1;
       if (use_ab) {                                 // channels whose parts come from this pass (Lp == k + 2)
         g.ab_neff = dNeff; g.ab_level = k + 2; g.ab_c = w.c32; g.ab_w = w.w32; g.ab = w.parts; g.ab_plane = plane;
         g.parts = op; g.parts.level = k + 2;
@@ -766,6 +473,8 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       // bytes of the schedule run (SURVEY 8d B_fused): one read + one write of the state for the two
       // stages this pass applies; flops of both stages (bench.py derives the unfused B_ns from them)
       ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt2 * batch * L * m * 4.0, 4.0 * cnt2 * batch * L * (double)mm);
+      // executed: three sources x three tf32 products (3xTF32) per row; triangular skips below
+      ps.exec(2.0 * cnt2 * batch * L * m * 4.0, 9.0 * 2.0 * cnt2 * batch * L * (double)mm * tri_frac, PIPE_TF32);
       rc = launch_bank_hist(g, st);
       if (rc == CASC_ERR_UNSUPPORTED) rc = launch_mimo_gemm(g, true, st);
       if (rc) return rc;
@@ -775,13 +484,14 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       g.src[0].A = Vs; g.src[0].W = P.f32; g.src[0].K = m; g.src[0].shift = (int64_t)1 << k;
       g.src[0].w_plane_off = 2 * k; g.src[0].w_planes = planes; g.src[0].w_plane_stride = 2 * (N_max + 1);
       g.n_src = 1; g.R = Vs; g.out = Vd; g.n_out = m; g.L = L; g.batch = batch;
-      g.sys_list = dorder + cnt2; g.n_list = cnt1; g.n_sys_total = n; g.t_first = t_first; g.w_resident = resident_weights();
+      g.sys_list = dorder + cnt2; g.n_list = cnt1; g.n_sys_total = n; g.t_first = t_first;
       if (use_ab) {                                 // every channel here ends with stage k
         g.ab_neff = dNeff; g.ab_level = k + 1; g.ab_c = w.c32; g.ab_w = w.w32; g.ab = w.parts; g.ab_plane = plane;
         g.parts = op; g.parts.level = k + 1;
         g.t_first = 0;
       }
       ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt1 * batch * L * m * 4.0, 2.0 * cnt1 * batch * L * (double)mm);
+      ps.exec(2.0 * cnt1 * batch * L * m * 4.0, 3.0 * 2.0 * cnt1 * batch * L * (double)mm * tri_frac, PIPE_TF32);
       rc = launch_bank_hist(g, st);
       if (rc == CASC_ERR_UNSUPPORTED) rc = launch_mimo_gemm(g, true, st);
       if (rc) return rc;

@@ -211,43 +211,6 @@ __global__ void __launch_bounds__(256) bank_tail_kernel(BankTailArg a) {
   if (l < a.L) a.y[seq * a.L + l] = fmaf(dc, a.u[seq * a.L + l], p[0]);
 }
 
-// ============================================================================ derived data
-// Kr64 [n][MS][128] float64 Krylov columns; column 0 = Bbar, the rest filled by dgemm levels.
-__global__ void kr_init_kernel(const double* Bbar, double* Kr, int n, int ms) {
-  const int64_t tot = (int64_t)n * ms * 128;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = e / (ms * 128), r = (e / 128) % ms, j = e % 128;
-    Kr[e] = (j == 0) ? Bbar[s * ms + r] : 0.0;
-  }
-}
-// krT32[s][0|1][n][k'] = hi | lo of Kr64[s][n][127 - k'], zero for lags >= 2^Kc[s]
-__global__ void kr_split_kernel(const double* Kr, const int* Kc, float* krT, int n, int ms) {
-  const int64_t tot = (int64_t)n * ms * 128;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = e / (ms * 128), r = (e / 128) % ms, kp = e % 128;
-    const int j = 127 - (int)kp;
-    const double v = (j < (1 << Kc[s])) ? Kr[(s * ms + r) * 128 + j] : 0.0;
-    const float hi = tf32_rna((float)v);
-    const float lo = tf32_rna((float)(v - (double)hi));
-    float* base = krT + s * 2 * ms * 128;
-    base[r * 128 + kp] = hi;
-    base[ms * 128 + r * 128 + kp] = lo;
-  }
-}
-
-int launch_kr_init(const double* Bbar, double* Kr, int n, int ms, cudaStream_t st) {
-  const int64_t tot = (int64_t)n * ms * 128;
-  kr_init_kernel<<<(int)std::min<int64_t>(ceil_div(tot, 256), 148 * 8), 256, 0, st>>>(Bbar, Kr, n, ms);
-  CASC_LAUNCHED();
-  return CASC_OK;
-}
-int launch_kr_split(const double* Kr, const int* Kc, float* krT, int n, int ms, cudaStream_t st) {
-  const int64_t tot = (int64_t)n * ms * 128;
-  kr_split_kernel<<<(int)std::min<int64_t>(ceil_div(tot, 256), 148 * 8), 256, 0, st>>>(Kr, Kc, krT, n, ms);
-  CASC_LAUNCHED();
-  return CASC_OK;
-}
-
 // ============================================================================ fused derived data
 // One CTA per channel: Krylov columns Kr[:, j] = Abar^j Bbar (j < 2^Kc) by doubling with the
 // powers (Kr_{2^i + j} = P_i Kr_j, float64 FMA in ascending k as dgemm_batched_kernel), their

@@ -36,36 +36,14 @@ struct BankTailArg {
   int n_ch; int64_t L; int batch;
 };
 
-// Fused persistent bank kernel (bank_fused.cu): m = 64, every channel with Ne >= 7.
-struct BankFusedArg {
-  const float* u; float* y;               // [n_ch][batch][L]
-  const float* krimg;                     // [n_ch][2][32][64][4] Krylov smem image (hi | lo)
-  const float* cvec; const float* wvec;   // [n_ch][64]: C and w = C P_Ne (fp32)
-  const float* dvec;                      // [n_ch]
-  const int* order; const int* Neff;      // processing order (Ne descending), effective orders
-  unsigned* flags;                        // [S][ntiles] publication flags (zeroed per launch)
-  unsigned* done;                         // [n_list*batch] completed chunks per sequence (zeroed)
-  const float* pub;                       // [S][NL][ntiles*128][64] publication planes
-  int64_t L; int batch; int ntiles; int T; int nchunk; int S; int NL; int planes_per_ch;
-  int64_t total_chunks; int discard;
-  unsigned long long* dbg;                // optional [24] wait-cycle counters (CASC_FUSED_DBG=1)
-};
-int launch_kr_image(const double* Kr, const int* Kc, float* img, int n, cudaStream_t st);
-int launch_bank_fused(const BankFusedArg& a, const float* pack_f32, int n_planes_total, int grid, cudaStream_t st);
-
 bool bank_tc_supported(int m);
 int launch_bank_head(int m, const BankHeadArg& a, cudaStream_t st);
 int launch_bank_head_ws(int m, const BankHeadArg& a, int64_t n_seq_total, cudaStream_t st);
-// the same head on CTA pairs (M = 256 per MMA, the Krylov operand split between the pair)
-int launch_bank_head_pair(int m, const BankHeadArg& a, int64_t n_seq_total, cudaStream_t st);
-int launch_bank_stage_ws(int m, const BankStageArg& a, cudaStream_t st);
 int launch_bank_stage_rp(int m, const BankStageArg& a, cudaStream_t st);
 int launch_bank_tail(int m, const BankTailArg& a, cudaStream_t st);
 int launch_bank_ab_tail(const BankAbTailArg& a, cudaStream_t st);
-int launch_kr_init(const double* Bbar, double* Kr, int n, int ms, cudaStream_t st);
 int launch_bank_derived(const double* p64, int slots, const double* Bbar, const double* C, const double* D,
                         const int* Neff, const int* Kc, double* Kr64, float* krT, double* w64, float* w32,
                         float* c32, float* d32, float* pvec, int fold, int n, int ms, cudaStream_t st);
-int launch_kr_split(const double* Kr, const int* Kc, float* krT, int n, int ms, cudaStream_t st);
 
 }  // namespace casc

@@ -249,6 +249,34 @@ int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_
   return CASC_OK;
 }
 
+int DevCtx::ensure_pinned(size_t n_ints) {
+  if (pinned_n >= n_ints) return CASC_OK;
+  if (pinned) cudaFreeHost(pinned);
+  pinned = nullptr;
+  pinned_n = 0;
+  CASC_TRY(cudaHostAlloc(&pinned, sizeof(int) * n_ints, cudaHostAllocDefault));
+  pinned_n = n_ints;
+  return CASC_OK;
+}
+
+DevCtx* dev_ctx() {
+  static std::mutex create_mu;
+  static DevCtx* ctx[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(create_mu);
+  if (!ctx[dev]) {
+    DevCtx* c = new DevCtx();
+    if (cudaStreamCreateWithFlags(&c->in, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->out, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->inputs_free, cudaEventDisableTiming) != cudaSuccess)
+      return nullptr;
+    ctx[dev] = c;
+  }
+  return ctx[dev];
+}
+
 int engine_powers(int n, int m, const int* N_host, int N_max, const double* Abar, int mode,
                   void* pack, cudaStream_t st) {
   if (n < 1 || m < 1 || N_max < 0 || !N_host || !Abar || !pack) return CASC_ERR_ARG;
@@ -263,6 +291,7 @@ int engine_powers(int n, int m, const int* N_host, int N_max, const double* Abar
   if (m <= 64) {                                  // banks: all squarings + packing in one launch
     int maxN = *std::max_element(N_host, N_host + n);
     ProfScope ps(st, K_POWERS, 16.0 * n * mm * (maxN + 1), 2.0 * n * (double)mm * m * maxN);
+    ps.exec(16.0 * n * mm * (maxN + 1), 2.0 * n * (double)mm * m * maxN, PIPE_FP64);
     return launch_powers_small(P, Abar, n, N_max, m, st);
   }
   // P_0 = Abar (strided copy into slot 0 of every system)
@@ -273,6 +302,7 @@ int engine_powers(int n, int m, const int* N_host, int N_max, const double* Abar
     int cnt = 0;
     for (int s = 0; s < n; ++s) cnt += N_host[s] >= k;
     ProfScope ps(st, K_POWERS, 16.0 * cnt * mm, 2.0 * cnt * (double)mm * m);
+    ps.exec(24.0 * cnt * mm, 2.0 * cnt * (double)mm * m, PIPE_FP64);
     DgemmArg a{};
     a.M = m; a.N = m; a.K = m;
     a.A = P.p64 + (k - 1) * mm; a.lda = m; a.sA = sys;
@@ -408,9 +438,13 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
   h.apply_bytes = std::min(h.apply_bytes, dev_ws_bytes - fixed);
   cudaStream_t st = (cudaStream_t)stream;
   const size_t es = (mode == CASC_BF16) ? 2 : 4;
-  if (n_sys > 1 && m == 64 && bank_tc_path(m, p, q, mode) && !getenv("CASC_RUN_HOST_SERIAL")) {
-    // banks: parameters and powers on `st`; u arrives in chunks on a copy stream (the head runs per
-    // chunk as it lands) and finished channels' outputs go back while later stage passes run
+  DevCtx* ctx = dev_ctx();
+  if (!ctx) return CASC_ERR_CUDA;
+  // calls on one device share the context's copy streams and pinned staging: serialise them
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  if (n_sys > 1 && m == 64 && bank_tc_path(m, p, q, mode)) {
+    // banks: parameters and powers on `st`; each wave's u arrives on the copy-in stream and
+    // finished channels' outputs go back while later stage passes run
     for (int s = 0; s < n_sys; ++s)
       if (N_host[s] < 0 || N_host[s] > N_max) return CASC_ERR_DIM;
     if (getenv("CASC_TIMING")) {                        // diagnostics: timeline origin (bank_engine.cu)
@@ -425,75 +459,68 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
     if (rc) return rc;
     rc = engine_bank_pipelined(n_sys, m, L, batch, N_host, N_max, h.pack, h.Bbar, h.C, D_h ? h.D : nullptr,
                                static_cast<float*>(h.u), static_cast<float*>(h.y), u_h, y_h, h.apply_ws,
-                               h.apply_bytes, st);
-    if (rc != CASC_ERR_WORKSPACE) return rc;            // else: the serial path below (channel waves)
+                               h.apply_bytes, st, ctx);
+    // else the serial path below (e.g. CASC_BANK_AB=0, which has no per-channel output streaming)
+    if (rc != CASC_ERR_WORKSPACE && rc != CASC_ERR_UNSUPPORTED) return rc;
   }
   CASC_TRY(cudaMemcpyAsync(h.Abar, Abar_h, sizeof(double) * n_sys * m * m, cudaMemcpyHostToDevice, st));
   CASC_TRY(cudaMemcpyAsync(h.Bbar, Bbar_h, sizeof(double) * n_sys * m * p, cudaMemcpyHostToDevice, st));
   CASC_TRY(cudaMemcpyAsync(h.C, C_h, sizeof(double) * n_sys * q * m, cudaMemcpyHostToDevice, st));
   if (D_h) CASC_TRY(cudaMemcpyAsync(h.D, D_h, sizeof(double) * n_sys * q * p, cudaMemcpyHostToDevice, st));
-  if (n_sys == 1 && batch > 1 && mimo_tc_path(1, m, p, q, mode) && !getenv("CASC_RUN_HOST_SERIAL")) {
+  if (n_sys == 1 && batch > 1 && mimo_tc_path(1, m, p, q, mode)) {
     // one MIMO system: the batch's sequences are independent, so they run in chunks whose input
     // copy (copy-in stream) overlaps the previous chunk's compute and whose output copy (copy-out
-    // stream) overlaps the next chunk's
-    // the input copy may start before the powers (they do not touch u; E3: 0.67 ms of squarings)
-    static cudaEvent_t inputs_free[16] = {};
-    int dev0 = 0;
-    CASC_TRY(cudaGetDevice(&dev0));
-    if (dev0 >= 0 && dev0 < 16) {
-      if (!inputs_free[dev0]) CASC_TRY(cudaEventCreateWithFlags(&inputs_free[dev0], cudaEventDisableTiming));
-      CASC_TRY(cudaEventRecord(inputs_free[dev0], st));
-    }
+    // stream) overlaps the next chunk's; the input copy may start before the powers (they do not
+    // touch u; E3: 0.67 ms of squarings)
+    CASC_TRY(cudaEventRecord(ctx->inputs_free, st));
     rc = engine_powers(1, m, N_host, N_max, h.Abar, mode, h.pack, st);
     if (rc) return rc;
-    static cudaStream_t in_s[16] = {}, out_s[16] = {};
-    int dev = 0;
-    CASC_TRY(cudaGetDevice(&dev));
-    if (dev >= 0 && dev < 16) {
-      if (!in_s[dev]) CASC_TRY(cudaStreamCreateWithFlags(&in_s[dev], cudaStreamNonBlocking));
-      if (!out_s[dev]) CASC_TRY(cudaStreamCreateWithFlags(&out_s[dev], cudaStreamNonBlocking));
-      // batch chunks (CASC_MIMO_CHUNKS): by default one per 64 MiB of input, 1..8 -- each chunk adds
-      // its launches' fill/drain; the first input and last output chunk are exposed (E3 e2e: 4
-      // chunks 14.8 ms, 8: 15.0, 16: 17.5; E4 with 4.3 GB of input takes 8)
-      static const int chunks_env = [] {
-        const char* e = getenv("CASC_MIMO_CHUNKS");
-        return e ? std::max(1, atoi(e)) : 0;
-      }();
-      const int64_t in_bytes = (int64_t)es * batch * L * p;
-      const int chunks = chunks_env ? chunks_env : (int)std::min<int64_t>(8, std::max<int64_t>(1, ceil_div(in_bytes, (int64_t)64 << 20)));
-      const int nc = std::min(batch, chunks);
-      std::vector<cudaEvent_t> ev((size_t)2 * nc + 1);
-      for (auto& e : ev) CASC_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      CASC_TRY(cudaStreamWaitEvent(in_s[dev], inputs_free[dev], 0));
-      const size_t in_row = es * (size_t)L * p, out_row = es * (size_t)L * q;
-      std::vector<int> b0(nc + 1);
-      for (int i = 0; i <= nc; ++i) b0[i] = (int)((int64_t)batch * i / nc);
-      // chunk i+1's input is submitted after chunk i's work is queued: the small table upload inside
-      // each chunk's apply queues behind every copy submitted before it on the copy engine
-      auto submit = [&](int i) -> int {
-        CASC_TRY(cudaMemcpyAsync((char*)h.u + b0[i] * in_row, (const char*)u_h + b0[i] * in_row,
-                                 (size_t)(b0[i + 1] - b0[i]) * in_row, cudaMemcpyHostToDevice, in_s[dev]));
-        CASC_TRY(cudaEventRecord(ev[2 * i], in_s[dev]));
-        return CASC_OK;
-      };
-      if ((rc = submit(0))) return rc;
-      for (int i = 0; i < nc && rc == CASC_OK; ++i) {
-        CASC_TRY(cudaStreamWaitEvent(st, ev[2 * i], 0));
+    // batch chunks (CASC_MIMO_CHUNKS, tests): by default one per 64 MiB of input, 1..8 -- each chunk
+    // adds its launches' fill/drain; the first input and last output chunk are exposed (E3 e2e: 4
+    // chunks 14.8 ms, 8: 15.0, 16: 17.5; E4 with 4.3 GB of input takes 8)
+    static const int chunks_env = [] {
+      const char* e = getenv("CASC_MIMO_CHUNKS");
+      return e ? std::max(1, atoi(e)) : 0;
+    }();
+    const int64_t in_bytes = (int64_t)es * batch * L * p;
+    const int chunks = chunks_env ? chunks_env : (int)std::min<int64_t>(8, std::max<int64_t>(1, ceil_div(in_bytes, (int64_t)64 << 20)));
+    const int nc = std::min(batch, chunks);
+    std::vector<cudaEvent_t> ev((size_t)2 * nc, nullptr);
+    for (auto& e : ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) { rc = CASC_ERR_CUDA; break; }
+    const size_t in_row = es * (size_t)L * p, out_row = es * (size_t)L * q;
+    std::vector<int> b0(nc + 1);
+    for (int i = 0; i <= nc; ++i) b0[i] = (int)((int64_t)batch * i / nc);
+    auto ok = [&](cudaError_t e) { if (e != cudaSuccess && rc == CASC_OK) rc = CASC_ERR_CUDA; return rc == CASC_OK; };
+    // chunk i+1's input is submitted after chunk i's work is queued: the small table upload inside
+    // each chunk's apply queues behind every copy submitted before it on the copy engine
+    auto submit = [&](int i) {
+      return ok(cudaMemcpyAsync((char*)h.u + b0[i] * in_row, (const char*)u_h + b0[i] * in_row,
+                                (size_t)(b0[i + 1] - b0[i]) * in_row, cudaMemcpyHostToDevice, ctx->in)) &&
+             ok(cudaEventRecord(ev[2 * i], ctx->in));
+    };
+    if (rc == CASC_OK && ok(cudaStreamWaitEvent(ctx->in, ctx->inputs_free, 0)) && submit(0)) {
+      for (int i = 0; i < nc; ++i) {
+        if (!ok(cudaStreamWaitEvent(st, ev[2 * i], 0))) break;
         rc = engine_apply(1, m, p, q, L, b0[i + 1] - b0[i], N_host, N_max, mode, h.pack, h.Bbar, h.C,
                           D_h ? h.D : nullptr, (const char*)h.u + b0[i] * in_row, (char*)h.y + b0[i] * out_row,
                           h.apply_ws, h.apply_bytes, st);
-        CASC_TRY(cudaEventRecord(ev[2 * i + 1], st));
-        CASC_TRY(cudaStreamWaitEvent(out_s[dev], ev[2 * i + 1], 0));
-        CASC_TRY(cudaMemcpyAsync((char*)y_h + b0[i] * out_row, (const char*)h.y + b0[i] * out_row,
-                                 (size_t)(b0[i + 1] - b0[i]) * out_row, cudaMemcpyDeviceToHost, out_s[dev]));
-        if (i + 1 < nc && (rc = submit(i + 1))) break;
+        if (rc) break;
+        if (!ok(cudaEventRecord(ev[2 * i + 1], st)) || !ok(cudaStreamWaitEvent(ctx->out, ev[2 * i + 1], 0)) ||
+            !ok(cudaMemcpyAsync((char*)y_h + b0[i] * out_row, (const char*)h.y + b0[i] * out_row,
+                                (size_t)(b0[i + 1] - b0[i]) * out_row, cudaMemcpyDeviceToHost, ctx->out)))
+          break;
+        if (i + 1 < nc && !submit(i + 1)) break;
       }
-      cudaError_t e1 = cudaStreamSynchronize(out_s[dev]), e2 = cudaStreamSynchronize(st);
-      cudaStreamSynchronize(in_s[dev]);
-      for (auto& e : ev) cudaEventDestroy(e);
-      if (rc) return rc;
-      return (e1 != cudaSuccess || e2 != cudaSuccess) ? CASC_ERR_CUDA : CASC_OK;
     }
+    // drain all three streams before returning, also on error: no copy into or out of the caller's
+    // host buffers may still be in flight, and the events are destroyed only once unused
+    const cudaError_t e1 = cudaStreamSynchronize(ctx->out), e2 = cudaStreamSynchronize(st);
+    const cudaError_t e3 = cudaStreamSynchronize(ctx->in);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (rc) return rc;
+    return (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) ? CASC_ERR_CUDA : CASC_OK;
   }
   CASC_TRY(cudaMemcpyAsync(h.u, u_h, es * n_sys * batch * L * p, cudaMemcpyHostToDevice, st));
   rc = engine_powers(n_sys, m, N_host, N_max, h.Abar, mode, h.pack, st);

@@ -1,8 +1,24 @@
 // Host engine entry points (internal).
 #pragma once
+#include <mutex>
 #include "common.cuh"
 
 namespace casc {
+// Per-device host context of the host-buffer entry (casc_run_host) and the side streams of the
+// engines: created once per device under a global lock, never freed (process lifetime).
+//   mu      serialises casc_run_host calls on one device (they share the copy streams and the
+//           pinned staging of the channel tables; the call is synchronous anyway)
+//   in/out  copy-in / copy-out streams; side: the bank's pair-weight stream (apply paths)
+struct DevCtx {
+  std::mutex mu;
+  cudaStream_t in = nullptr, out = nullptr, side = nullptr;
+  cudaEvent_t inputs_free = nullptr;
+  int* pinned = nullptr;
+  size_t pinned_n = 0;
+  int ensure_pinned(size_t n_ints);   // grow the pinned staging (caller holds mu)
+};
+DevCtx* dev_ctx();                    // the current device's context; nullptr on a CUDA error
+
 size_t apply_ws_bytes(int n, int m, int p, int q, int64_t L, int batch, int mode, int n_max);
 int validate_common(int n, int m, int p, int q, int64_t L, int batch, int N_max, int mode);
 int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_host, int N_max,
@@ -15,7 +31,8 @@ int engine_bank_tc(int n, int m, int64_t L, int batch, const int* N_host, int N_
                    size_t ws_bytes, cudaStream_t st);
 int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host, int N_max, const void* pack,
                           const double* Bbar, const double* C, const double* D, float* u_dev, float* y_dev,
-                          const void* u_h, const void* y_h, void* ws, size_t ws_bytes, cudaStream_t st);
+                          const void* u_h, const void* y_h, void* ws, size_t ws_bytes, cudaStream_t st,
+                          DevCtx* ctx);
 bool mimo_tc_path(int n, int m, int p, int q, int mode);
 size_t mimo_ws_bytes(int m, int p, int q, int64_t L, int batch, int mode);
 int engine_mimo_tc(int m, int p, int q, int64_t L, int batch, int N, int N_max, int mode, const void* pack,

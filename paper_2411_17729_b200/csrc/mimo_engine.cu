@@ -104,12 +104,15 @@ int engine_mimo_tc(int m, int p, int q, int64_t L, int batch, int N, int N_max, 
   int rc;
   if ((rc = mimo_derive(m, p, q, Ne, P, Bbar, C, D, w, tf32, st))) return rc;
   const double rows = (double)batch * L;
+  const double xf = tf32 ? 3.0 : 1.0;            // executed products per source: 3xTF32 or one bf16
+  const int pipe = tf32 ? PIPE_TF32 : PIPE_BF16;
   if (Ne == 0) {
     MimoGemm g{};
     g.src[0] = {u, w.CBD, p, 0};
     g.src[1] = {u, w.CAB, p, 1};
     g.n_src = 2; g.out = y; g.n_out = q; g.L = L; g.batch = batch;
     ProfScope ps(st, K_MIMO_LAST, rows * (p + q) * es, rows * 4.0 * q * p);
+    ps.exec(rows * (p + q) * es, rows * 4.0 * q * p * xf, pipe);
     return launch_mimo_gemm(g, tf32, st);
   }
   {
@@ -118,6 +121,7 @@ int engine_mimo_tc(int m, int p, int q, int64_t L, int batch, int N, int N_max, 
     g.src[1] = {u, w.AB, p, 1};
     g.n_src = 2; g.out = w.Va; g.n_out = m; g.L = L; g.batch = batch;
     ProfScope ps(st, K_MIMO_FIRST, rows * (p + m) * es, rows * 4.0 * m * p);
+    ps.exec(rows * (p + m) * es, rows * 4.0 * m * p * xf, pipe);
     if ((rc = launch_mimo_gemm(g, tf32, st))) return rc;
   }
   for (int k = 1; k <= Ne - 1; ++k) {
@@ -129,6 +133,7 @@ int engine_mimo_tc(int m, int p, int q, int64_t L, int batch, int N, int N_max, 
     g.src[0] = {Vs, Wk, m, (int64_t)1 << k};
     g.n_src = 1; g.R = Vs; g.out = Vd; g.n_out = m; g.L = L; g.batch = batch;
     ProfScope ps(st, K_MIMO_STAGE, rows * m * es * 2.0, rows * 2.0 * (double)mm);
+    ps.exec(rows * m * es * 2.0 + (double)mm * (tf32 ? 8.0 : 2.0), rows * 2.0 * (double)mm * xf, pipe);
     if ((rc = launch_mimo_gemm(g, tf32, st))) return rc;
   }
   {
@@ -140,6 +145,7 @@ int engine_mimo_tc(int m, int p, int q, int64_t L, int batch, int N, int N_max, 
     if (D) { g.src[2] = {u, w.D, p, 0}; g.n_src = 3; }
     g.out = y; g.n_out = q; g.L = L; g.batch = batch;
     ProfScope ps(st, K_MIMO_LAST, rows * (m + p + q) * es, rows * (4.0 * q * m + 2.0 * q * p));
+    ps.exec(rows * (m + p + q) * es, rows * (4.0 * q * m + (D ? 2.0 * q * p : 0.0)) * xf, pipe);
     if ((rc = launch_mimo_gemm(g, tf32, st))) return rc;
   }
   return CASC_OK;

@@ -326,7 +326,6 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
     {
       const uint32_t idesc = make_idesc(TF32 ? FMT_TF32 : FMT_BF16, BM, BN);
       const uint32_t idesc128 = make_idesc(FMT_TF32, BM, 2 * BN);   // TSA: A hi x [W hi | W lo]
-      const bool mma8 = a.mma8 != 0;
       int s = 0, cur_sys = -1;
       uint32_t ph = 0, wph = 0;
       int64_t t_local = 0, j = 0;                 // tiles / chunks consumed by this CTA
@@ -360,8 +359,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
               const uint64_t wd0 = make_sdesc(WRES ? smem_u32(sWres + ci * C::NW * C::W_BYTES) : smem_u32(stW(s)), 16, 1024,
                                               LAYOUT_SW128);
               // main: hi.hi; corr: lo.hi + hi.lo (four K-steps, one asm block)
-              if (mma8) mma_3xtf32_ts_chunk8_w(d, dc, ah, al, wd0, idesc128, idesc, first ? 0u : 1u);
-              else mma_3xtf32_ts_chunk_w(d, dc, ah, al, wd0, sdesc_add(wd0, C::W_BYTES), idesc, first ? 0u : 1u);
+              mma_3xtf32_ts_chunk8_w(d, dc, ah, al, wd0, idesc128, idesc, first ? 0u : 1u);
               first = false;
               if (!WRES) mma_commit_w(&empty[s]);         // the slot also holds W
               mma_commit_w(&alo_free[j & (NAU - 1)]);
@@ -616,16 +614,12 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
     if (!map3d(&maps.W[s], g.src[s].W, TF32, g.src[s].K, g.n_out, planes, BN)) return CASC_ERR_CUDA;
   }
   {
-    // stride of the shifts in time tiles -> tile order (decode); CASC_GEMM_PERM=0 keeps the natural order
-    static const bool perm_on = [] {
-      const char* e = getenv("CASC_GEMM_PERM");
-      return !(e && e[0] == '0');
-    }();
+    // stride of the shifts in time tiles -> tile order (decode)
     int64_t S = 0;
     for (int s = 0; s < g.n_src; ++s)
       if (g.src[s].shift > 0 && g.src[s].shift % BM == 0) S = S ? std::min<int64_t>(S, g.src[s].shift / BM) : g.src[s].shift / BM;
     const int64_t nt_eff = (g.L + BM - 1) / BM - g.t_first;
-    a.perm_j = (perm_on && S > 1 && nt_eff % S == 0) ? nt_eff / S : 0;
+    a.perm_j = (S > 1 && nt_eff % S == 0) ? nt_eff / S : 0;
   }
   a.has_residual = g.R != nullptr;
   a.r_row0 = (int)g.R_row0;
@@ -640,10 +634,6 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
   // weight-resident: contiguous ranges; otherwise round-robin single tiles
   a.gt = WCH > 0 ? ceil_div(tiles, std::min<int64_t>(tiles, 148)) : 1;
   const int grid = (int)std::min<int64_t>(ceil_div(tiles, a.gt), 148);
-  {
-    const char* e8 = getenv("CASC_GEMM_MMA8");
-    a.mma8 = (e8 && e8[0] == '0') ? 0 : 1;
-  }
   static unsigned long long* dbg = nullptr;
   const bool want_dbg = getenv("CASC_GEMM_DBG") != nullptr;
   if (want_dbg) {
@@ -673,47 +663,22 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
 int launch_mimo_gemm(const MimoGemm& g, bool tf32, cudaStream_t st) {
   if (mimo_pair_ok(g, tf32)) return launch_mimo_gemm_pair(g, st);
   if (tf32 && mimo_pair_tf32_ok(g)) return launch_mimo_gemm_pair_tf32(g, st);
+  // one-CTA kernel; template arguments <BN, TF32, residual/staging chunks, resident weight chunks>
+  // are the measured-best splits of shared memory: 3xTF32 N = 64 keeps 4 residual
+  // chunks (3 with the resident weights of a stage pair), bf16 N = 256 four (11% faster on E4 than 2)
   if (tf32) {
     if (g.n_out % 128 == 0) return launch_cfg<128, true>(g, st);   // main + corr accumulators
     if (g.n_out % 64 == 0) {
-      // bank streaming stage: split of shared memory between the A/W ring and the residual
-      // ring (CASC_GEMM_RS = 2 | 4 | 6 residual chunks; default 4)
-      static const int rs = [] {
-        const char* e = getenv("CASC_GEMM_RS");
-        return e ? atoi(e) : 4;
-      }();
       if (g.w_resident) {                         // weights resident across tiles (bank stage)
         int chunks = 0;
         for (int s = 0; s < g.n_src; ++s) chunks += g.src[s].K / 32;
         if (chunks <= 2) return launch_cfg<64, true, 4, 2>(g, st);
-        if (chunks <= 6) {
-          // stage pairs: residual chunks vs A ring slots (CASC_GEMM_PAIR_RS = 2 | 3 | 4)
-          static const int prs = [] {
-            const char* e = getenv("CASC_GEMM_PAIR_RS");
-            return e ? atoi(e) : 3;
-          }();
-          if (prs == 3) return launch_cfg<64, true, 3, 6>(g, st);
-          if (prs == 4) return launch_cfg<64, true, 4, 6>(g, st);
-          return launch_cfg<64, true, 2, 6>(g, st);
-        }
+        if (chunks <= 6) return launch_cfg<64, true, 3, 6>(g, st);
       }
-      if (rs == 2) return launch_cfg<64, true, 2>(g, st);
-      if (rs == 6) return launch_cfg<64, true, 6>(g, st);
       return launch_cfg<64, true>(g, st);
     }
   } else {
-    if (g.n_out % 256 == 0) {
-      // residual / staging chunks for the 256-wide bf16 tiles (CASC_GEMM_RS256 = 2 | 3 | 4):
-      // with 2 the epilogue waited on residual loads ~50% of the time (the slot doubles as the
-      // store staging); 4 chunks (ring 3 x 48 KB) measured 11% faster on the E4 stage GEMM
-      static const int rs = [] {
-        const char* e = getenv("CASC_GEMM_RS256");
-        return e ? atoi(e) : 4;
-      }();
-      if (rs == 3) return launch_cfg<256, false, 3>(g, st);
-      if (rs == 4) return launch_cfg<256, false, 4>(g, st);
-      return launch_cfg<256, false>(g, st);
-    }
+    if (g.n_out % 256 == 0) return launch_cfg<256, false, 4>(g, st);
     if (g.n_out % 128 == 0) return launch_cfg<128, false>(g, st);
     if (g.n_out % 64 == 0) return launch_cfg<64, false>(g, st);
   }

@@ -24,7 +24,6 @@ struct MimoArg {
   const int* ab_neff; int ab_level; const float* ab_c; const float* ab_w; float* ab; int64_t ab_plane;
   int64_t gt;                        // tiles per block of the CTA tile walk
   unsigned long long* dbg;           // optional wait-cycle counters (CASC_GEMM_DBG=1)
-  int mma8;                          // TSA 3xTF32: 8 MMAs per chunk (N = 128 hi.[hi|lo]) instead of 12
   int64_t perm_j;                    // time-tile order within a sequence (0: natural), see decode()
 };
 struct MimoSrc {

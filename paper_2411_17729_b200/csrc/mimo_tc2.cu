@@ -304,11 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 }
 
 bool mimo_pair_ok(const MimoGemm& g, bool tf32) {
-  static const bool off = [] {
-    const char* e = getenv("CASC_GEMM_PAIR");
-    return e && e[0] == '0';
-  }();
-  if (off || tf32 || g.n_out % 256 != 0 || g.w_resident || g.ab) return false;
+  if (tf32 || g.n_out % 256 != 0 || g.w_resident || g.ab) return false;
   for (int s = 0; s < g.n_src; ++s)
     if (g.src[s].K % BK || g.src[s].w_plane_stride != 0) return false;   // one weight plane per source
   return g.sys_list == nullptr;

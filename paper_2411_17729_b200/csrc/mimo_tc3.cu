@@ -328,24 +328,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512) : "memory");
 }
 
-// CASC_GEMM_PAIR_TF32_BN = 128 | 256 | 64 (default 128: E3 stage 0.81 ms vs 0.87 ms with 256, whose
-// single accumulator leaves the epilogue exposed; 64-wide outputs stay on the one-CTA kernel unless
-// 64 is asked for: the E3 output stage measured 0.59 ms on pairs vs 0.47 ms)
-static int pair_bn() {
-  static const int bn = [] {
-    const char* e = getenv("CASC_GEMM_PAIR_TF32_BN");
-    return e ? atoi(e) : 128;
-  }();
-  return bn;
-}
-static bool bn64() { return pair_bn() == 64; }
-
 bool mimo_pair_tf32_ok(const MimoGemm& g) {
   static const bool off = [] {
     const char* e = getenv("CASC_GEMM_PAIR_TF32");
     return e && e[0] == '0';
   }();
-  if (off || g.n_out % (bn64() ? 64 : 128) != 0 || g.w_resident || g.ab || g.parts_deep || g.sys_list != nullptr) return false;
+  // 128-wide tiles (64-wide outputs stay on the one-CTA kernel: the E3 output stage measured 0.47
+  // ms there vs 0.59 ms on pairs; a 256-wide tile with one accumulator measured 0.87 vs 0.81 ms)
+  if (off || g.n_out % 128 != 0 || g.w_resident || g.ab || g.parts_deep || g.sys_list != nullptr) return false;
   for (int s = 0; s < g.n_src; ++s)
     if (g.src[s].K % BK || g.src[s].w_plane_stride != 0) return false;   // one weight plane pair per source
   return true;
@@ -392,11 +382,6 @@ static int launch_pt(const MimoGemm& g, cudaStream_t st) {
   return CASC_OK;
 }
 
-int launch_mimo_gemm_pair_tf32(const MimoGemm& g, cudaStream_t st) {
-  const int bn = pair_bn();
-  if (bn == 256 && g.n_out % 256 == 0) return launch_pt<256>(g, st);
-  if (g.n_out % 128 == 0) return launch_pt<128>(g, st);
-  return launch_pt<64>(g, st);                    // 64-wide outputs (the MIMO output stage, q = 64)
-}
+int launch_mimo_gemm_pair_tf32(const MimoGemm& g, cudaStream_t st) { return launch_pt<128>(g, st); }
 
 }  // namespace casc

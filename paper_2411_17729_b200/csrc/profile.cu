@@ -12,6 +12,8 @@ struct ProfRec {
   cudaEvent_t a, b;
   int cls;
   double bytes, flops;
+  double xbytes, xflops;   // executed (ProfScope::exec); default = algorithmic
+  int pipe;
 };
 struct ProfState {
   bool on = false;
@@ -32,10 +34,17 @@ static thread_local ProfState g_prof;
 
 ProfScope::ProfScope(cudaStream_t st, int cls, double bytes, double flops) : st_(st), idx_(-1) {
   if (!g_prof.on) return;
-  ProfRec r{g_prof.get(), g_prof.get(), cls, bytes, flops};
+  ProfRec r{g_prof.get(), g_prof.get(), cls, bytes, flops, bytes, flops, PIPE_NONE};
   cudaEventRecord(r.a, st);
   g_prof.recs.push_back(r);
   idx_ = (int)g_prof.recs.size() - 1;
+}
+void ProfScope::exec(double bytes, double flops, int pipe) {
+  if (idx_ < 0) return;
+  ProfRec& r = g_prof.recs[idx_];
+  r.xbytes = bytes;
+  r.xflops = flops;
+  r.pipe = pipe;
 }
 ProfScope::~ProfScope() {
   if (idx_ >= 0) cudaEventRecord(g_prof.recs[idx_].b, st_);
@@ -44,7 +53,7 @@ ProfScope::~ProfScope() {
 static const char* kNames[K_NCLASS] = {"powers_square", "powers_pack", "derived", "first_stage",
                                        "stage", "last_stage", "direct", "convert",
                                        "bank_head", "bank_stage", "bank_tail", "mimo_tc_stage",
-                                       "mimo_tc_first", "mimo_tc_last", "bank_fused"};
+                                       "mimo_tc_first", "mimo_tc_last", "seq_halo"};
 
 }  // namespace casc
 
@@ -88,6 +97,21 @@ int casc_profile_read(int cls, int* launches, double* ms, double* bytes, double*
   if (ms) *ms = t;
   if (bytes) *bytes = by;
   if (flops) *flops = fl;
+  return CASC_OK;
+}
+
+int casc_profile_read_exec(int cls, double* exec_bytes, double* exec_flops, int* pipe) {
+  double by = 0, fl = 0;
+  int pp = PIPE_NONE;
+  for (auto& r : g_prof.recs) {
+    if (r.cls != cls) continue;
+    by += r.xbytes;
+    fl += r.xflops;
+    if (r.pipe != PIPE_NONE) pp = r.pipe;
+  }
+  if (exec_bytes) *exec_bytes = by;
+  if (exec_flops) *exec_flops = fl;
+  if (pipe) *pipe = pp;
   return CASC_OK;
 }
 

@@ -33,7 +33,7 @@ def effective_order(N: int, L: int) -> int:
     """Ne = min(N, floor(log2(L-1))): stages with 2^k >= L are identities (R20)."""
     if L <= 2:
         return 0
-    return min(N, int(math.floor(math.log2(L - 1))))
+    return min(N, (L - 1).bit_length() - 1)        # exact integer floor(log2(L - 1))
 
 
 @dataclass

@@ -116,24 +116,3 @@ def test_fold_matches_single_stage_pass():
     _check(wl, y_fold)
     y_single = _gpu_y(wl, {"CASC_BANK_FOLD": "0"})
     assert rel(y_fold, y_single) < 2e-6
-
-
-def test_fold_two_stages_matches():
-    """R26 (opt-in, CASC_BANK_FOLD=2): even channels skip their last stage-pair pass and the head or
-    the previous pass writes eight parts; same y as the unfolded bank."""
-    wl = _bank(8, 128 * 48, 2, [8, 9, 10, 11, 12, 13, 11, 9])
-    y2 = _gpu_y(wl, {"CASC_BANK_FOLD": "2"})
-    _check(wl, y2)
-    y0 = _gpu_y(wl, {"CASC_BANK_FOLD": "0"})
-    assert rel(y2, y0) < 2e-6
-
-
-def test_head_pair_matches_one_cta_head():
-    """The bank head on CTA pairs (bank_head_pair.cu, CASC_BANK_HEAD=pair) against the one-CTA
-    head (the default): the same K = 128 Toeplitz products; an odd tile count (the last pair's
-    second tile past the sequence end) and channels ending at the head (Ne <= 7, output parts)."""
-    wl = _bank(6, 128 * 47 - 5, 3, [5, 7, 9, 12, 8, 13])
-    y_pair = _gpu_y(wl, {"CASC_BANK_HEAD": "pair"})
-    _check(wl, y_pair)
-    y_ws = _gpu_y(wl)
-    assert rel(y_pair, y_ws) < 1e-6

@@ -221,9 +221,10 @@ def test_determinism_bitwise():
 
 
 @pytest.mark.parametrize("mode", ["bf16", "fp32"])
-def test_run_host_mimo_batch_chunks_bitwise(mode):
-    """casc_run_host for one MIMO system runs the batch in chunks with the copies overlapped; each
-    sequence's arithmetic is unchanged, so y is bitwise the device-resident path's."""
+def test_run_host_mimo_single_chunk_bitwise(mode):
+    """casc_run_host for one MIMO system with a small input (1.3 MB: one batch chunk, copies on the
+    copy streams): y is bitwise the device-resident path's. The multi-chunk runs are in
+    tests/test_gpu_e2e_paths.py."""
     import paper_2411_17729_b200 as pk
     from paper_2411_17729_b200.runner import storage_to_torch
     wl = S.make_random_mimo(128, 64, 64, L=1000, batch=5, N=8, rho=0.97, mode=mode)
