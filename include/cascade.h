@@ -19,7 +19,8 @@
  *   - Ownership: the caller allocates every buffer (device memory unless stated) including
  *     the workspace, sized by the matching *_bytes query. The library never allocates or
  *     frees device memory inside an apply call and keeps no state between calls
- *     (stateless; thread-safe for distinct workspaces).
+ *     (stateless; thread-safe for distinct workspaces). casc_run_host calls on one device are
+ *     serialised by the library (they share its per-device copy streams and pinned staging).
  *   - Asynchrony: all device work is enqueued on `stream`; no host synchronisation inside
  *     casc_powers / casc_apply / casc_apply_bank. casc_run_host synchronises `stream` once
  *     at its end (its output lives in host memory).
@@ -54,7 +55,7 @@ typedef enum casc_status {
   CASC_ERR_UNSUPPORTED = 4,  /* valid request the sm_100a kernels do not cover                */
   CASC_ERR_WORKSPACE = 5,    /* ws_bytes smaller than the *_bytes query                       */
   CASC_ERR_CUDA = 6,         /* a CUDA runtime call failed (launch, copy, device mismatch)    */
-  CASC_ERR_NCCL = 7          /* reserved for the sequence-sharded path                        */
+  CASC_ERR_NCCL = 7          /* NCCL missing or an NCCL call failed (sequence-sharded path)   */
 } casc_status;
 
 typedef enum casc_mode {
@@ -152,31 +153,50 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
                   void* dev_ws, size_t dev_ws_bytes, void* stream);
 
 /* ----------------------------------------------------------------------------------------
- * a7  Sequence-sharded steps (BASELINE configs[3] "per-stage NCCL halo exchange").
- *     Rank r owns time rows [r*L_loc, (r+1)*L_loc) of every sequence of ONE system
- *     (m, p, q multiples of 64). The cascade's stage k reads v_{l-2^k}, so
- *     before stage k each rank receives the last 2^k rows of v^(k) of rank r-1 (zeros on
- *     rank 0); the exchange itself is done by the caller (paper_2411_17729_b200/seqshard.py,
- *     NCCL through torch.distributed). Buffers carry the halo in front of the local rows:
- *       u_ext [batch][1 + L_loc][p]   (row 0 = u_{-1} of this shard)
- *       V     [batch][H + L_loc][m]   (rows [H - 2^k, H) = halo of stage k), H >= 2^Ne
- *       y     [batch][L_loc][q]
- *     Ne is the effective order for the GLOBAL length: min(N, floor(log2(L - 1))) (R20).
- *   casc_seq_prepare : derived weights (Abar Bbar, C P_Ne, C Bbar + D, C Abar Bbar) into ws
- *   casc_seq_first   : v^(1) = Bbar u_l + Abar Bbar u_{l-1} on the local rows
- *   casc_seq_stage   : v^(k+1) = v^(k) + P_k v^(k)_{l-2^k} on the local rows (k >= 1)
- *   casc_seq_last    : y = C v + (C P_Ne) v_{l-2^Ne} + D u  (Ne == 0: y = (C Bbar + D) u + C Abar Bbar u_{l-1})
- * All pointers DEVICE; stream-ordered; errors as casc_apply (CASC_ERR_DIM if 2^k > H).
+ * a7  Sequence-sharded apply (BASELINE configs[3] "per-stage NCCL halo exchange").
+ *     Rank r of `world` owns global time rows [r*L_loc, (r+1)*L_loc) of every sequence of ONE
+ *     system (m, p, q multiples of 64). The cascade's stage k reads
+ *     v_{l-2^k}, so before stage k each rank receives the last 2^k time rows of v^(k) from rank
+ *     r-1 (zeros on rank 0: x_{-1} = 0); the fused first step needs one row of u,
+ *     the fused last step (y = C v + C P_Ne v_{l-2^Ne} + D u, R21) 2^Ne rows of v.
+ *     Ne = min(N, floor(log2(L - 1))) for the GLOBAL length L = world * L_loc (R20).
+ *     The library does the exchange itself: grouped ncclSend(r -> r+1) / ncclRecv(r-1 -> r) on
+ *     `comm_stream`, overlapped with the interior rows of the same step on `compute_stream`
+ *     (rows whose operands are all local run first; the boundary rows after the halo landed).
+ *
+ *   casc_nccl_unique_id  writes the 128-byte NCCL unique id (call on rank 0; the caller
+ *                        broadcasts it, e.g. through its torch process group).
+ *   casc_comm_init       NCCL communicator of `world` ranks on the CURRENT device (the caller has
+ *                        done cudaSetDevice(local_rank)); blocks until every rank joined.
+ *   casc_comm_init_local `world` emulated ranks in ONE process on one device (tests: comms[r]
+ *                        is rank r; each rank's apply must run on its own host thread; halos are
+ *                        device copies ordered by events).
+ *   casc_comm_destroy    frees a communicator from either init.
+ *   casc_comm_rank       rank and world size of a communicator (either pointer may be NULL).
+ *
+ *   Layouts (time-major, so a halo of d rows is ONE contiguous block of d*batch*dim elements):
+ *     u_loc DEVICE [L_loc][batch][p], y_loc DEVICE [L_loc][batch][q] (storage dtype of mode);
+ *     pack from casc_powers(1, m, &N, N_max, ...); Bbar, C, D float64 as casc_apply (D may be NULL).
+ *     ws: DEVICE, >= casc_apply_seqsharded_workspace(m, p, q, L_loc, batch, N, world, mode) bytes
+ *     (derived weights, two state buffers of (2^Ne + L_loc) * batch * m elements with the halo
+ *     rows in front, and the u halo row).
+ *   Stream-ordered on compute_stream / comm_stream (distinct streams of the current device); no
+ *   host synchronisation except inside the local transport's rendezvous (host threads wait for
+ *   their neighbours to enqueue, never for the device).
+ * Errors: CASC_ERR_ARG, CASC_ERR_DIM, CASC_ERR_WORKSPACE, CASC_ERR_UNSUPPORTED (m, p, q not
+ *   multiples of 64, or world > 1 with 2^Ne > L_loc: a halo would span several ranks),
+ *   CASC_ERR_CUDA, CASC_ERR_NCCL (libnccl missing, or an NCCL call failed).
  * -------------------------------------------------------------------------------------- */
-size_t casc_seq_workspace_bytes(int m, int p, int q, int mode);
-int casc_seq_prepare(int m, int p, int q, int Ne, int N_max, int mode, const void* pack, const double* Bbar,
-                     const double* C, const double* D, void* ws, size_t ws_bytes, void* stream);
-int casc_seq_first(int m, int p, int q, int64_t L_loc, int batch, int mode, const void* ws, const void* u_ext,
-                   int64_t H, void* V, void* stream);
-int casc_seq_stage(int m, int64_t L_loc, int batch, int k, int N_max, int mode, const void* pack, int64_t H,
-                   const void* V_src, void* V_dst, void* stream);
-int casc_seq_last(int m, int p, int q, int64_t L_loc, int batch, int Ne, int mode, const void* ws, int64_t H,
-                  const void* V, const void* u_ext, int has_D, void* y, void* stream);
+int casc_nccl_unique_id(void* id_out);
+int casc_comm_init(void** comm, int rank, int world, const void* nccl_unique_id);
+int casc_comm_init_local(void** comms, int world);
+int casc_comm_destroy(void* comm);
+int casc_comm_rank(const void* comm, int* rank, int* world);
+size_t casc_apply_seqsharded_workspace(int m, int p, int q, int64_t L_loc, int batch, int N, int world, int mode);
+int casc_apply_seqsharded(void* comm, int m, int p, int q, int64_t L_loc, int batch, int N, int N_max, int mode,
+                          const void* pack, const double* Bbar, const double* C, const double* D,
+                          const void* u_loc, void* y_loc, void* ws, size_t ws_bytes, void* compute_stream,
+                          void* comm_stream);
 
 /* Number of kernel launches the last successful apply/powers call on this host thread
  * enqueued (bench evidence for "gpu_launches"). */

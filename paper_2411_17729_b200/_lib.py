@@ -34,15 +34,15 @@ SIGNATURES = {
                               c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                               c_void_p, c_size_t, c_void_p]),
     "casc_selftest_umma": (c_int, [c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
-    "casc_seq_workspace_bytes": (c_size_t, [c_int, c_int, c_int, c_int]),
-    "casc_seq_prepare": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
-                                 c_void_p, c_void_p, c_size_t, c_void_p]),
-    "casc_seq_first": (c_int, [c_int, c_int, c_int, c_int64, c_int, c_int, c_void_p, c_void_p, c_int64,
-                               c_void_p, c_void_p]),
-    "casc_seq_stage": (c_int, [c_int, c_int64, c_int, c_int, c_int, c_int, c_void_p, c_int64, c_void_p,
-                               c_void_p, c_void_p]),
-    "casc_seq_last": (c_int, [c_int, c_int, c_int, c_int64, c_int, c_int, c_int, c_void_p, c_int64,
-                              c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
+    "casc_nccl_unique_id": (c_int, [c_void_p]),
+    "casc_comm_init": (c_int, [ctypes.POINTER(c_void_p), c_int, c_int, c_void_p]),
+    "casc_comm_init_local": (c_int, [ctypes.POINTER(c_void_p), c_int]),
+    "casc_comm_destroy": (c_int, [c_void_p]),
+    "casc_comm_rank": (c_int, [c_void_p, P_int, P_int]),
+    "casc_apply_seqsharded_workspace": (c_size_t, [c_int, c_int, c_int, c_int64, c_int, c_int, c_int, c_int]),
+    "casc_apply_seqsharded": (c_int, [c_void_p, c_int, c_int, c_int, c_int64, c_int, c_int, c_int, c_int,
+                                      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_void_p, c_size_t, c_void_p, c_void_p]),
     "casc_profile_enable": (c_int, [c_int]),
     "casc_profile_reset": (c_int, []),
     "casc_profile_num_classes": (c_int, []),

@@ -178,3 +178,74 @@ def profile_read() -> dict:
                 "launches": n.value, "ms": ms.value, "bytes": by.value, "flops": fl.value,
                 "exec_bytes": xb.value, "exec_flops": xf.value, "pipe": PIPES.get(pipe.value, "none")}
     return out
+
+
+# ------------------------------------------------------------------ sequence sharding (a7)
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; the caller broadcasts it)."""
+    buf = ctypes.create_string_buffer(128)
+    check(lib().casc_nccl_unique_id(buf), "casc_nccl_unique_id")
+    return buf.raw
+
+
+class Comm:
+    """A library communicator (NCCL, or one rank of an in-process emulated group)."""
+
+    def __init__(self, handle: ctypes.c_void_p):
+        self.handle = handle
+        r, w = ctypes.c_int(0), ctypes.c_int(0)
+        check(lib().casc_comm_rank(handle, ctypes.byref(r), ctypes.byref(w)), "casc_comm_rank")
+        self.rank, self.world = r.value, w.value
+
+    def destroy(self) -> None:
+        if self.handle:
+            check(lib().casc_comm_destroy(self.handle), "casc_comm_destroy")
+            self.handle = None
+
+
+def comm_init(rank: int, world: int, unique_id: bytes) -> Comm:
+    """NCCL communicator on the current CUDA device (blocks until all ranks joined)."""
+    h = ctypes.c_void_p()
+    check(lib().casc_comm_init(ctypes.byref(h), rank, world, ctypes.create_string_buffer(unique_id, 128)),
+          "casc_comm_init")
+    return Comm(h)
+
+
+def comm_init_local(world: int) -> list:
+    """`world` emulated ranks in this process (one device); run each rank's apply on its own thread."""
+    hs = (ctypes.c_void_p * world)()
+    check(lib().casc_comm_init_local(hs, world), "casc_comm_init_local")
+    return [Comm(ctypes.c_void_p(h)) for h in hs]
+
+
+def seqsharded_workspace_bytes(m, p, q, L_loc, batch, N, world, mode) -> int:
+    return int(lib().casc_apply_seqsharded_workspace(m, p, q, L_loc, batch, N, world, _mode(mode)))
+
+
+def apply_seqsharded(comm: Comm, pw: Powers, Bbar, C, D, u_loc, y=None, ws=None, stream=None,
+                     comm_stream=None):
+    """This rank's shard: u_loc [L_loc][batch][p] (time-major, storage dtype) -> y [L_loc][batch][q].
+    The halo exchange with the neighbouring ranks happens inside the library (comm_stream)."""
+    if pw.n_sys != 1:
+        raise ValueError("apply_seqsharded() takes a single-system pack")
+    m, N, md = pw.m, pw.N[0], pw.mode
+    L_loc, batch, p = u_loc.shape
+    q = C.shape[0]
+    _need(u_loc, STORAGE[md], (L_loc, batch, p), "u_loc")
+    _need(Bbar, torch.float64, (m, p), "Bbar")
+    _need(C, torch.float64, (q, m), "C")
+    if D is not None:
+        _need(D, torch.float64, (q, p), "D")
+    if y is None:
+        y = torch.empty((L_loc, batch, q), dtype=STORAGE[md], device=u_loc.device)
+    _need(y, STORAGE[md], (L_loc, batch, q), "y")
+    if ws is None:
+        ws = torch.empty(seqsharded_workspace_bytes(m, p, q, L_loc, batch, N, comm.world, md), dtype=torch.uint8,
+                         device=u_loc.device)
+    if comm_stream is None:
+        raise ValueError("apply_seqsharded needs a comm stream distinct from the compute stream")
+    check(lib().casc_apply_seqsharded(comm.handle, m, p, q, L_loc, batch, N, pw.N_max, md, _p(pw.pack), _p(Bbar),
+                                      _p(C), _p(D), _p(u_loc), _p(y), _p(ws), ws.numel(), _stream(stream),
+                                      _stream(comm_stream)),
+          "casc_apply_seqsharded")
+    return y

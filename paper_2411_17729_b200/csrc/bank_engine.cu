@@ -89,13 +89,6 @@ bool bank_tc_path(int m, int p, int q, int mode) {
   return !force_simt && p == 1 && q == 1 && mode == CASC_FP32 && bank_tc_supported(m);
 }
 
-static int eff_order_b(int N, int64_t L) {
-  if (L <= 2) return 0;
-  int kstar = 0;
-  while (((int64_t)1 << (kstar + 1)) < L) ++kstar;
-  return N < kstar ? N : kstar;
-}
-
 size_t bank_ws_bytes(int n, int m, int64_t L, int batch, int n_max) {
   return carve_bank(nullptr, n, m, L, batch, stage_variant(m) == 't' ? pair_slots(n_max) : 0).bytes;
 }
@@ -138,7 +131,7 @@ int engine_bank_tc(int n, int m, int64_t L, int batch, const int* N_host, int N_
                    const double* Bbar, const double* C, const double* D, const void* u, void* y, void* ws,
                    size_t ws_bytes, cudaStream_t st) {
   int maxNe = 0;
-  for (int s = 0; s < n; ++s) maxNe = std::max(maxNe, eff_order_b(N_host[s], L));
+  for (int s = 0; s < n; ++s) maxNe = std::max(maxNe, eff_order(N_host[s], L));
   const int qslots = stage_variant(m) == 't' ? pair_slots(maxNe) : 0;
   int nw = n;
   while (nw > 0 && carve_bank(nullptr, nw, m, L, batch, qslots).bytes > ws_bytes) {
@@ -179,7 +172,7 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
                           DevCtx* ctx) {
   if (m != 64 || !bank_ab_enabled()) return CASC_ERR_UNSUPPORTED;
   int maxNe = 0;
-  for (int s = 0; s < n; ++s) maxNe = std::max(maxNe, eff_order_b(N_host[s], L));
+  for (int s = 0; s < n; ++s) maxNe = std::max(maxNe, eff_order(N_host[s], L));
   const int qslots = pair_slots(maxNe);
   // channels per wave (bounded memory, as engine_bank_tc)
   int nw = n;
@@ -268,7 +261,7 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
   int *Neff = meta, *Kc = Neff + n, *par = Neff + 2 * n, *order = Neff + 3 * n;
   int maxNe = 0;
   for (int s = 0; s < n; ++s) {
-    Neff[s] = eff_order_b(N_host[s], L);
+    Neff[s] = eff_order(N_host[s], L);
     Kc[s] = std::min(kHeadK, Neff[s]);
     const int nstream = Neff[s] - Kc[s];            // streaming stages of this channel
     par[s] = (variant == 't' ? (nstream + 1) / 2 : nstream) % 2;   // passes -> final buffer

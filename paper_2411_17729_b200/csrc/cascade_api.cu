@@ -26,13 +26,6 @@ namespace casc {
 extern cudaEvent_t g_timing_t0;   // bank_engine.cu (diagnostics)
 thread_local int g_launches = 0;
 
-static int eff_order(int N, int64_t L) {
-  if (L <= 2) return 0;
-  int kstar = 0;                                   // largest k with 2^k < L
-  while (((int64_t)1 << (kstar + 1)) < L) ++kstar;
-  return N < kstar ? N : kstar;
-}
-
 struct ApplyWs {
   int* meta;                        // Neff | order | direct | groupA | groupB   (5 n ints)
   double *AB64, *CP64, *CBD64, *CAB64;

@@ -41,6 +41,14 @@ inline void sync_check(const char* file, int line) {
   } while (0)
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+// Effective order for length L (R20): stages with 2^k >= L are identities, so
+// Ne = min(N, floor(log2(L - 1))) (0 for L <= 2) -- the last stage actually applied.
+inline int eff_order(int N, int64_t L) {
+  if (L <= 2) return 0;
+  int kstar = 0;                                   // largest k with 2^k < L
+  while (((int64_t)1 << (kstar + 1)) < L) ++kstar;
+  return N < kstar ? N : kstar;
+}
 // Fused output of a bank channel's last stages (R24-R26). y is linear in the state, so
 // the kernel producing v' = v^(Ne-d) writes the 2^(d+1) row scalars p_b = (C prod_{i in b} P_{j_i}) . v'
 // over the subsets b of the stages j_i = Ne-d+i (i = 0..d; stage Ne is the tail's, R21), and the

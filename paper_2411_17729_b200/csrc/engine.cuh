@@ -38,6 +38,19 @@ size_t mimo_ws_bytes(int m, int p, int q, int64_t L, int batch, int mode);
 int engine_mimo_tc(int m, int p, int q, int64_t L, int batch, int N, int N_max, int mode, const void* pack,
                    const double* Bbar, const double* C, const double* D, const void* u, void* y, void* ws,
                    size_t ws_bytes, cudaStream_t st);
+// MIMO workspace (mimo_engine.cu): derived float64 weights, their operand-format images, and the
+// two state buffers of batch * L rows of m (ping-pong)
+struct MimoWs {
+  double *AB64, *CP64, *CBD64, *CAB64;
+  void *Bb, *AB, *C, *CP, *D, *CBD, *CAB;   // operand-format weights (bf16, or tf32 hi/lo planes)
+  void *Va, *Vb;
+  size_t bytes;
+};
+MimoWs carve_mimo(void* ws, int m, int p, int q, int64_t L, int batch, int mode);
+// derived weights of the fused first / last steps (R21): Abar Bbar, C P_Ne, C Bbar + D,
+// C Abar Bbar, in float64 and rounded once to the GEMM operand format
+int mimo_derive(int m, int p, int q, int Ne, const PackLayout& P, const double* Bbar, const double* C,
+                const double* D, const MimoWs& w, bool tf32, cudaStream_t st);
 int engine_powers(int n, int m, const int* N_host, int N_max, const double* Abar, int mode,
                   void* pack, cudaStream_t st);
 }  // namespace casc

@@ -39,14 +39,7 @@ static int convert_weight(const double* src, void* dst, int64_t n, bool tf32, cu
   return CASC_OK;
 }
 
-struct MimoWs {
-  double *AB64, *CP64, *CBD64, *CAB64;
-  void *Bb, *AB, *C, *CP, *D, *CBD, *CAB;   // operand-format weights
-  void *Va, *Vb;
-  size_t bytes;
-};
-
-static MimoWs carve_mimo(void* ws, int m, int p, int q, int64_t L, int batch, int mode) {
+MimoWs carve_mimo(void* ws, int m, int p, int q, int64_t L, int batch, int mode) {
   Carver c(ws);
   MimoWs w{};
   const size_t wes = mode == CASC_FP32 ? 8 : 2;      // tf32 hi+lo pair, or bf16
@@ -81,15 +74,6 @@ size_t mimo_ws_bytes(int m, int p, int q, int64_t L, int batch, int mode) {
   return carve_mimo(nullptr, m, p, q, L, batch, mode).bytes;
 }
 
-static int eff_order_m(int N, int64_t L) {
-  if (L <= 2) return 0;
-  int kstar = 0;
-  while (((int64_t)1 << (kstar + 1)) < L) ++kstar;
-  return N < kstar ? N : kstar;
-}
-
-static int mimo_derive(int m, int p, int q, int Ne, const PackLayout& P, const double* Bbar, const double* C,
-                       const double* D, const MimoWs& w, bool tf32, cudaStream_t st);
 
 int engine_mimo_tc(int m, int p, int q, int64_t L, int batch, int N, int N_max, int mode, const void* pack,
                    const double* Bbar, const double* C, const double* D, const void* u, void* y, void* ws,
@@ -99,7 +83,7 @@ int engine_mimo_tc(int m, int p, int q, int64_t L, int batch, int N, int N_max, 
   const bool tf32 = mode == CASC_FP32;
   PackLayout P = pack_layout(const_cast<void*>(pack), 1, m, N_max, mode);
   const int64_t mm = (int64_t)m * m;
-  const int Ne = eff_order_m(N, L);
+  const int Ne = eff_order(N, L);
   const double es = tf32 ? 4.0 : 2.0;
   int rc;
   if ((rc = mimo_derive(m, p, q, Ne, P, Bbar, C, D, w, tf32, st))) return rc;
@@ -153,7 +137,7 @@ int engine_mimo_tc(int m, int p, int q, int64_t L, int batch, int N, int N_max, 
 
 // Derived weights of the fused first / last stages (R21), float64 then rounded to the
 // GEMM operand format: Abar Bbar, C P_Ne, C Bbar + D, C Abar Bbar.
-static int mimo_derive(int m, int p, int q, int Ne, const PackLayout& P, const double* Bbar, const double* C,
+int mimo_derive(int m, int p, int q, int Ne, const PackLayout& P, const double* Bbar, const double* C,
                        const double* D, const MimoWs& w, bool tf32, cudaStream_t st) {
   const int64_t mm = (int64_t)m * m;
   int rc;
@@ -187,99 +171,3 @@ static int mimo_derive(int m, int p, int q, int Ne, const PackLayout& P, const d
 }
 
 }  // namespace casc
-
-// =============================================================================================
-// Sequence-sharded execution: rank r owns time rows [r L_loc, (r+1) L_loc)
-// of every sequence. The caller (paper_2411_17729_b200/seqshard.py) keeps the states in
-// buffers [batch][H + L_loc][m] whose first H rows hold the halo received from rank r-1 before
-// each stage (zeros on rank 0), and u in [batch][1 + L_loc][p] (one halo row). The step functions
-// below run one step of the cascade on the local rows; shifted reads reach into the halo.
-// =============================================================================================
-using namespace casc;
-extern "C" {
-
-size_t casc_seq_workspace_bytes(int m, int p, int q, int mode) {
-  if (m < 1 || p < 1 || q < 1) return 0;
-  return carve_mimo(nullptr, m, p, q, 0, 0, mode).bytes;
-}
-
-int casc_seq_prepare(int m, int p, int q, int Ne, int N_max, int mode, const void* pack, const double* Bbar,
-                     const double* C, const double* D, void* ws, size_t ws_bytes, void* stream) {
-  g_launches = 0;
-  if (!pack || !Bbar || !C || !ws || Ne < 0 || Ne > N_max) return CASC_ERR_ARG;
-  if (mode != CASC_FP32 && mode != CASC_BF16) return CASC_ERR_ARG;
-  if (!mimo_tc_supported(m, p, q)) return CASC_ERR_UNSUPPORTED;
-  MimoWs w = carve_mimo(ws, m, p, q, 0, 0, mode);
-  if (ws_bytes < w.bytes) return CASC_ERR_WORKSPACE;
-  PackLayout P = pack_layout(const_cast<void*>(pack), 1, m, N_max, mode);
-  return mimo_derive(m, p, q, Ne, P, Bbar, C, D, w, mode == CASC_FP32, (cudaStream_t)stream);
-}
-
-int casc_seq_first(int m, int p, int q, int64_t L_loc, int batch, int mode, const void* ws, const void* u_ext,
-                   int64_t H, void* V, void* stream) {
-  g_launches = 0;
-  if (!ws || !u_ext || !V || L_loc < 1 || batch < 1 || H < 1) return CASC_ERR_ARG;
-  if (!mimo_tc_supported(m, p, q)) return CASC_ERR_UNSUPPORTED;
-  MimoWs w = carve_mimo(const_cast<void*>(ws), m, p, q, 0, 0, mode);
-  MimoGemm g{};
-  g.src[0] = {u_ext, w.Bb, p, 0};
-  g.src[1] = {u_ext, w.AB, p, 1};
-  g.src[0].row0 = g.src[1].row0 = 1;
-  g.n_src = 2; g.out = V; g.out_row0 = H; g.n_out = m; g.L = L_loc; g.batch = batch;
-  const double es = mode == CASC_FP32 ? 4.0 : 2.0, rows = (double)batch * L_loc;
-  ProfScope ps((cudaStream_t)stream, K_MIMO_FIRST, rows * (p + m) * es, rows * 4.0 * m * p);
-  return launch_mimo_gemm(g, mode == CASC_FP32, (cudaStream_t)stream);
-}
-
-int casc_seq_stage(int m, int64_t L_loc, int batch, int k, int N_max, int mode, const void* pack, int64_t H,
-                   const void* V_src, void* V_dst, void* stream) {
-  g_launches = 0;
-  if (!pack || !V_src || !V_dst || L_loc < 1 || batch < 1 || k < 0 || k > N_max) return CASC_ERR_ARG;
-  if (((int64_t)1 << k) > H) return CASC_ERR_DIM;
-  if (!mimo_tc_supported(m, 64, 64)) return CASC_ERR_UNSUPPORTED;
-  PackLayout P = pack_layout(const_cast<void*>(pack), 1, m, N_max, mode);
-  const int64_t mm = (int64_t)m * m;
-  const bool tf32 = mode == CASC_FP32;
-  const void* Wk = tf32 ? static_cast<const void*>(P.f32 + k * 2 * mm) : static_cast<const void*>(P.b16 + k * mm);
-  MimoGemm g{};
-  g.src[0] = {V_src, Wk, m, (int64_t)1 << k};
-  g.src[0].row0 = H;
-  g.n_src = 1; g.R = V_src; g.R_row0 = H; g.out = V_dst; g.out_row0 = H;
-  g.n_out = m; g.L = L_loc; g.batch = batch;
-  const double es = tf32 ? 4.0 : 2.0, rows = (double)batch * L_loc;
-  ProfScope ps((cudaStream_t)stream, K_MIMO_STAGE, rows * m * es * 2.0, rows * 2.0 * (double)mm);
-  return launch_mimo_gemm(g, tf32, (cudaStream_t)stream);
-}
-
-int casc_seq_last(int m, int p, int q, int64_t L_loc, int batch, int Ne, int mode, const void* ws, int64_t H,
-                  const void* V, const void* u_ext, int has_D, void* y, void* stream) {
-  g_launches = 0;
-  if (!ws || !u_ext || !y || L_loc < 1 || batch < 1 || Ne < 0) return CASC_ERR_ARG;
-  if (Ne > 0 && (!V || ((int64_t)1 << Ne) > H)) return CASC_ERR_DIM;
-  if (!mimo_tc_supported(m, p, q)) return CASC_ERR_UNSUPPORTED;
-  MimoWs w = carve_mimo(const_cast<void*>(ws), m, p, q, 0, 0, mode);
-  const bool tf32 = mode == CASC_FP32;
-  MimoGemm g{};
-  if (Ne == 0) {                      // y = (C Bbar + D) u_l + (C Abar Bbar) u_{l-1}
-    g.src[0] = {u_ext, w.CBD, p, 0};
-    g.src[1] = {u_ext, w.CAB, p, 1};
-    g.src[0].row0 = g.src[1].row0 = 1;
-    g.n_src = 2;
-  } else {                            // y = C v + (C P_Ne) v_{l-2^Ne} + D u
-    g.src[0] = {V, w.C, m, 0};
-    g.src[1] = {V, w.CP, m, (int64_t)1 << Ne};
-    g.src[0].row0 = g.src[1].row0 = H;
-    g.n_src = 2;
-    if (has_D) {
-      g.src[2] = {u_ext, w.D, p, 0};
-      g.src[2].row0 = 1;
-      g.n_src = 3;
-    }
-  }
-  g.out = y; g.n_out = q; g.L = L_loc; g.batch = batch;
-  const double es = tf32 ? 4.0 : 2.0, rows = (double)batch * L_loc;
-  ProfScope ps((cudaStream_t)stream, K_MIMO_LAST, rows * (m + p + q) * es, rows * (4.0 * q * m + 2.0 * q * p));
-  return launch_mimo_gemm(g, tf32, (cudaStream_t)stream);
-}
-
-}  // extern "C"

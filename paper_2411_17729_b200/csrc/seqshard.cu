@@ -1,0 +1,419 @@
+// Sequence-sharded cascade (BASELINE configs[3] "per-stage NCCL halo
+// exchange"), owned by the library: communicators, the halo exchange and its overlap with the
+// stage GEMMs.
+//
+// Rank r of R owns time rows [r L_loc, (r+1) L_loc) of every sequence of ONE system. The cascade's
+// stage k adds P_k v_{l-2^k}, so before stage k a rank needs the last 2^k time
+// rows of v^(k) held by rank r-1 (zeros on rank 0: x_{-1} = 0). The fused first step
+// v^(1) = Bbar u_l + Abar Bbar u_{l-1} needs one row of u, the fused last step
+// y = C v + (C P_Ne) v_{l-2^Ne} + D u needs 2^Ne rows of v^(Ne) (R21).
+//
+// Layout: time-major. u_loc [L_loc][batch][p], y_loc [L_loc][batch][q], and the two state buffers
+// [H + L_loc][batch][m] with H = 2^Ne halo rows in front: seen as one matrix of rows
+// (l, b) -> l * batch + b, a time shift by s is a row shift by s * batch, and a halo of d time rows
+// is ONE contiguous block of d * batch * m elements -- sent straight from the sender's state buffer
+// and received straight into the receiver's halo rows (no packing, no copies).
+//
+// Per step, the GEMM (mimo_tc*.cu) runs in two launches: interior rows (l_loc >= s: every operand
+// is local) first, then -- after the halo has landed -- the boundary rows [0, s). The exchange of
+// step k's halo runs on the comm stream while step k-1's boundary launch and step k's interior
+// launch run on the compute stream; it starts as soon as the rows it sends are written.
+//
+// Transports behind the same schedule:
+//   NCCL   one rank per process and GPU: grouped ncclSend(r -> r+1) / ncclRecv(r-1 -> r) on the
+//          comm stream (NVLink / NVSwitch on a B200 box). libnccl is resolved at run time (the copy
+//          torch already loaded, else the system one); casc_comm_init fails with CASC_ERR_NCCL
+//          when it is missing.
+//   local  R emulated ranks in one process on one device (tests): each rank's apply runs on its own
+//          host thread and streams; a halo is a device copy ordered by CUDA events, with a host
+//          rendezvous per exchange. Ranks never spin on each other inside a kernel.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <condition_variable>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "engine.cuh"
+#include "kernels.cuh"
+#include "mimo_tc.cuh"
+#include "profile.cuh"
+
+namespace casc {
+
+// ------------------------------------------------------------------------------ NCCL (run time)
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    // the copy already in the process (torch's), else whatever the loader finds
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    a.CommInitRank = (decltype(a.CommInitRank))dlsym(h, "ncclCommInitRank");
+    a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
+    a.Send = (decltype(a.Send))dlsym(h, "ncclSend");
+    a.Recv = (decltype(a.Recv))dlsym(h, "ncclRecv");
+    a.GroupStart = (decltype(a.GroupStart))dlsym(h, "ncclGroupStart");
+    a.GroupEnd = (decltype(a.GroupEnd))dlsym(h, "ncclGroupEnd");
+    a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.GroupStart && a.GroupEnd;
+    return a;
+  }();
+  return api;
+}
+
+#define CASC_NCCL(x)                                                                          \
+  do {                                                                                        \
+    ncclResult_t r_ = (x);                                                                    \
+    if (r_ != ncclSuccess) {                                                                  \
+      if (getenv("CASC_DEBUG"))                                                               \
+        fprintf(stderr, "casc: %s failed: %s\n", #x,                                          \
+                nccl().GetErrorString ? nccl().GetErrorString(r_) : "?");                     \
+      return CASC_ERR_NCCL;                                                                   \
+    }                                                                                         \
+  } while (0)
+
+// ------------------------------------------------------------------------------ local transport
+// Mailboxes of one emulated group: post(from, to, tag) -> (pointer, event) and a completion event
+// back. Keys are (receiver or sender rank, exchange tag); entries live until the group is freed.
+struct LocalGroup {
+  int world = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  struct Post { const void* src = nullptr; size_t bytes = 0; cudaEvent_t ready = nullptr; };
+  std::map<std::pair<int, long>, Post> sends;          // keyed by receiving rank
+  std::map<std::pair<int, long>, cudaEvent_t> copied;  // keyed by sending rank
+  std::vector<cudaEvent_t> owned;
+  ~LocalGroup() {
+    for (auto e : owned) cudaEventDestroy(e);
+  }
+};
+
+struct Comm {
+  int kind = 0;                 // 0 NCCL, 1 local
+  int rank = 0, world = 1;
+  ncclComm_t nc = nullptr;
+  std::shared_ptr<LocalGroup> grp;
+  long tag = 0;                 // exchanges issued by this rank (same sequence on every rank)
+};
+
+// One halo exchange on the comm stream `cs`: send `sbytes` from `sbuf` to rank+1 (if any),
+// receive `rbytes` into `rbuf` from rank-1 (if any). `after` (may be null) orders the send after
+// the producing work; returns with an event on `cs` recorded in `done` (the exchange finished).
+static int exchange(Comm* c, const void* sbuf, size_t sbytes, void* rbuf, size_t rbytes, cudaEvent_t after,
+                    cudaStream_t cs, cudaEvent_t done) {
+  if (after) CASC_TRY(cudaStreamWaitEvent(cs, after, 0));
+  const bool send = c->rank + 1 < c->world, recv = c->rank > 0;
+  const long tag = c->tag++;
+  if (c->kind == 0) {
+    if (send || recv) {
+      const NcclApi& n = nccl();
+      CASC_NCCL(n.GroupStart());
+      if (send) CASC_NCCL(n.Send(sbuf, sbytes, ncclUint8, c->rank + 1, c->nc, cs));
+      if (recv) CASC_NCCL(n.Recv(rbuf, rbytes, ncclUint8, c->rank - 1, c->nc, cs));
+      CASC_NCCL(n.GroupEnd());
+    }
+  } else {
+    LocalGroup& g = *c->grp;
+    if (send) {                                          // publish: where the rows are, and when
+      cudaEvent_t ready;
+      CASC_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+      CASC_TRY(cudaEventRecord(ready, cs));
+      std::lock_guard<std::mutex> lk(g.mu);
+      g.owned.push_back(ready);
+      g.sends[{c->rank + 1, tag}] = LocalGroup::Post{sbuf, sbytes, ready};
+      g.cv.notify_all();
+    }
+    if (recv) {                                          // wait for rank-1's post, copy, report back
+      LocalGroup::Post p;
+      {
+        std::unique_lock<std::mutex> lk(g.mu);
+        g.cv.wait(lk, [&] { return g.sends.count({c->rank, tag}) > 0; });
+        p = g.sends[{c->rank, tag}];
+      }
+      if (p.bytes != rbytes) return CASC_ERR_DIM;
+      CASC_TRY(cudaStreamWaitEvent(cs, p.ready, 0));
+      CASC_TRY(cudaMemcpyAsync(rbuf, p.src, rbytes, cudaMemcpyDeviceToDevice, cs));
+      cudaEvent_t cp;
+      CASC_TRY(cudaEventCreateWithFlags(&cp, cudaEventDisableTiming));
+      CASC_TRY(cudaEventRecord(cp, cs));
+      std::lock_guard<std::mutex> lk(g.mu);
+      g.owned.push_back(cp);
+      g.copied[{c->rank - 1, tag}] = cp;
+      g.cv.notify_all();
+    }
+    if (send) {                                          // the send completes when rank+1 has copied
+      cudaEvent_t cp;
+      {
+        std::unique_lock<std::mutex> lk(g.mu);
+        g.cv.wait(lk, [&] { return g.copied.count({c->rank, tag}) > 0; });
+        cp = g.copied[{c->rank, tag}];
+      }
+      CASC_TRY(cudaStreamWaitEvent(cs, cp, 0));
+    }
+  }
+  CASC_TRY(cudaEventRecord(done, cs));
+  return CASC_OK;
+}
+
+// ------------------------------------------------------------------------------ workspace
+struct SeqWs {
+  MimoWs mw;           // derived weights (no state buffers: L = 0)
+  void* u_edge;        // [batch + B1][p]: u halo row (batch rows) + the first B1 local rows of u
+  void *Va, *Vb;       // [(H + L_loc) * batch][m]
+  size_t bytes;
+};
+static constexpr int64_t kRowBlock = 256;            // boundary granularity: one CTA-pair tile
+
+// boundary rows of a step with time shift s: the row blocks that read rows l - s < 0
+static int64_t boundary_rows(int64_t s, int batch, int64_t rows) {
+  return std::min(rows, ceil_div(s * batch, kRowBlock) * kRowBlock);
+}
+
+static SeqWs carve_seq(void* ws, int m, int p, int q, int64_t L_loc, int batch, int Ne, int mode) {
+  SeqWs w{};
+  w.mw = carve_mimo(ws, m, p, q, 0, 0, mode);
+  Carver c(ws);
+  c.off = w.mw.bytes;
+  const size_t es = mode == CASC_FP32 ? 4 : 2;
+  const int64_t rows = L_loc * batch, H = Ne > 0 ? ((int64_t)1 << Ne) : 0;
+  const int64_t B1 = boundary_rows(1, batch, rows);
+  w.u_edge = c.take<char>((size_t)(batch + B1) * p * es);
+  w.Va = c.take<char>((size_t)(H * batch + rows) * m * es);
+  w.Vb = c.take<char>((size_t)(H * batch + rows) * m * es);
+  w.bytes = c.bytes();
+  return w;
+}
+
+// A row range [0, rows) of one step as a MIMO GEMM over the time-major matrix (batch folded into
+// the rows): sources get row shifts s * batch; t_first skips the boundary tiles.
+static int step_gemm(MimoGemm g, int64_t rows, int t_first, bool tf32, cudaStream_t st) {
+  g.L = rows;
+  g.batch = 1;
+  g.t_first = t_first;
+  return launch_mimo_gemm(g, tf32, st);
+}
+
+}  // namespace casc
+
+using namespace casc;
+extern "C" {
+
+int casc_nccl_unique_id(void* id_out) {
+  if (!id_out) return CASC_ERR_ARG;
+  if (!nccl().ok) return CASC_ERR_NCCL;
+  ncclUniqueId id;
+  CASC_NCCL(nccl().GetUniqueId(&id));
+  memcpy(id_out, &id, sizeof(id));
+  return CASC_OK;
+}
+
+int casc_comm_init(void** comm, int rank, int world, const void* nccl_unique_id) {
+  if (!comm || !nccl_unique_id || world < 1 || rank < 0 || rank >= world) return CASC_ERR_ARG;
+  *comm = nullptr;
+  if (!nccl().ok) return CASC_ERR_NCCL;
+  ncclUniqueId id;
+  memcpy(&id, nccl_unique_id, sizeof(id));
+  auto* c = new Comm();
+  c->kind = 0;
+  c->rank = rank;
+  c->world = world;
+  const ncclResult_t r = nccl().CommInitRank(&c->nc, world, id, rank);
+  if (r != ncclSuccess) {
+    if (getenv("CASC_DEBUG"))
+      fprintf(stderr, "casc: ncclCommInitRank: %s\n", nccl().GetErrorString ? nccl().GetErrorString(r) : "?");
+    delete c;
+    return CASC_ERR_NCCL;
+  }
+  *comm = c;
+  return CASC_OK;
+}
+
+int casc_comm_init_local(void** comms, int world) {
+  if (!comms || world < 1) return CASC_ERR_ARG;
+  auto grp = std::make_shared<LocalGroup>();
+  grp->world = world;
+  for (int r = 0; r < world; ++r) {
+    auto* c = new Comm();
+    c->kind = 1;
+    c->rank = r;
+    c->world = world;
+    c->grp = grp;
+    comms[r] = c;
+  }
+  return CASC_OK;
+}
+
+int casc_comm_destroy(void* comm) {
+  if (!comm) return CASC_ERR_ARG;
+  auto* c = static_cast<Comm*>(comm);
+  int rc = CASC_OK;
+  if (c->kind == 0 && c->nc && nccl().CommDestroy(c->nc) != ncclSuccess) rc = CASC_ERR_NCCL;
+  delete c;
+  return rc;
+}
+
+int casc_comm_rank(const void* comm, int* rank, int* world) {
+  if (!comm) return CASC_ERR_ARG;
+  auto* c = static_cast<const Comm*>(comm);
+  if (rank) *rank = c->rank;
+  if (world) *world = c->world;
+  return CASC_OK;
+}
+
+size_t casc_apply_seqsharded_workspace(int m, int p, int q, int64_t L_loc, int batch, int N, int world, int mode) {
+  if (m < 1 || p < 1 || q < 1 || L_loc < 1 || batch < 1 || N < 0 || world < 1) return 0;
+  return carve_seq(nullptr, m, p, q, L_loc, batch, eff_order(N, L_loc * world), mode).bytes;
+}
+
+int casc_apply_seqsharded(void* comm, int m, int p, int q, int64_t L_loc, int batch, int N, int N_max, int mode,
+                          const void* pack, const double* Bbar, const double* C, const double* D, const void* u_loc,
+                          void* y_loc, void* ws, size_t ws_bytes, void* compute_stream, void* comm_stream) {
+  g_launches = 0;
+  auto* c = static_cast<Comm*>(comm);
+  if (!c || !pack || !Bbar || !C || !u_loc || !y_loc || !ws || !comm_stream) return CASC_ERR_ARG;
+  int rc = validate_common(1, m, p, q, L_loc, batch, N_max, mode);
+  if (rc) return rc;
+  if (N < 0 || N > N_max) return CASC_ERR_DIM;
+  if (!mimo_tc_supported(m, p, q)) return CASC_ERR_UNSUPPORTED;
+  const int64_t L = L_loc * c->world;
+  const int Ne = eff_order(N, L);
+  // each halo must come from the immediate predecessor (holds for configs[3] up to 8 ranks)
+  if (c->world > 1 && Ne > 0 && ((int64_t)1 << Ne) > L_loc) return CASC_ERR_UNSUPPORTED;
+  SeqWs w = carve_seq(ws, m, p, q, L_loc, batch, Ne, mode);
+  if (ws_bytes < w.bytes) return CASC_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)compute_stream, cs = (cudaStream_t)comm_stream;
+  const bool tf32 = mode == CASC_FP32;
+  const size_t es = tf32 ? 4 : 2;
+  const int64_t rows = L_loc * batch, H = Ne > 0 ? ((int64_t)1 << Ne) : 0, Hr = H * batch;
+  PackLayout P = pack_layout(const_cast<void*>(pack), 1, m, N_max, mode);
+  const int64_t mm = (int64_t)m * m;
+  if ((rc = mimo_derive(m, p, q, Ne, P, Bbar, C, D, w.mw, tf32, st))) return rc;
+
+  std::vector<cudaEvent_t> evs;
+  struct EvFree {
+    std::vector<cudaEvent_t>& v;
+    ~EvFree() { for (auto e : v) cudaEventDestroy(e); }   // released once the device is done
+  } ev_free{evs};
+  auto new_event = [&](cudaEvent_t* e) -> int {
+    CASC_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    evs.push_back(*e);
+    return CASC_OK;
+  };
+  cudaEvent_t ev_in, ev_halo;
+  if ((rc = new_event(&ev_in)) || (rc = new_event(&ev_halo))) return rc;
+  // rank 0's halo rows stay zero (x_{-1} = 0); the others are overwritten by each exchange
+  if (Hr > 0) {
+    CASC_TRY(cudaMemsetAsync(w.Va, 0, (size_t)Hr * m * es, st));
+    CASC_TRY(cudaMemsetAsync(w.Vb, 0, (size_t)Hr * m * es, st));
+  }
+  CASC_TRY(cudaMemsetAsync(w.u_edge, 0, (size_t)batch * p * es, st));
+  const int64_t B1 = boundary_rows(1, batch, rows);
+  CASC_TRY(cudaMemcpyAsync((char*)w.u_edge + (size_t)batch * p * es, u_loc, (size_t)B1 * p * es,
+                           cudaMemcpyDeviceToDevice, st));
+  CASC_TRY(cudaEventRecord(ev_in, st));
+
+  // ---- u halo: the last time row of rank r-1's u (one row of batch * p)
+  {
+    ProfScope ps(cs, K_SEQ_HALO, 2.0 * batch * p * es, 0.0);
+    if ((rc = exchange(c, (const char*)u_loc + (size_t)(rows - batch) * p * es, (size_t)batch * p * es, w.u_edge,
+                       (size_t)batch * p * es, ev_in, cs, ev_halo)))
+      return rc;
+  }
+  const double dr = (double)rows;
+  const int pipe = tf32 ? PIPE_TF32 : PIPE_BF16;
+  const double xf = tf32 ? 3.0 : 1.0;
+  auto two_launches = [&](MimoGemm g, MimoGemm gb, int64_t s_time, int cls, double bytes, double flops) -> int {
+    // interior rows (every operand local) now; boundary rows once the halo has landed
+    const int64_t Bs = boundary_rows(s_time, batch, rows);
+    int r2;
+    {
+      ProfScope ps(st, cls, bytes * (dr - Bs) / dr, flops * (dr - Bs) / dr);
+      ps.exec(bytes * (dr - Bs) / dr, xf * flops * (dr - Bs) / dr, pipe);
+      if (Bs < rows && (r2 = step_gemm(g, rows, (int)(Bs / 128), tf32, st))) return r2;
+    }
+    CASC_TRY(cudaStreamWaitEvent(st, ev_halo, 0));
+    ProfScope ps(st, cls, bytes * Bs / dr, flops * Bs / dr);
+    ps.exec(bytes * Bs / dr, xf * flops * Bs / dr, pipe);
+    return step_gemm(gb, Bs, 0, tf32, st);
+  };
+
+  if (Ne == 0) {                       // y = (C Bbar + D) u_l + (C Abar Bbar) u_{l-1}
+    MimoGemm g{}, gb{};
+    g.src[0] = {u_loc, w.mw.CBD, p, 0};
+    g.src[1] = {u_loc, w.mw.CAB, p, batch};
+    g.n_src = 2; g.out = y_loc; g.n_out = q;
+    gb = g;
+    gb.src[0] = {w.u_edge, w.mw.CBD, p, 0};
+    gb.src[1] = {w.u_edge, w.mw.CAB, p, batch};
+    gb.src[0].row0 = gb.src[1].row0 = batch;
+    return two_launches(g, gb, 1, K_MIMO_LAST, dr * (p + q) * es, dr * 4.0 * q * p);
+  }
+  // ---- first: v^(1) = Bbar u_l + Abar Bbar u_{l-1} -> Va (local rows behind the halo)
+  {
+    MimoGemm g{};
+    g.src[0] = {u_loc, w.mw.Bb, p, 0};
+    g.src[1] = {u_loc, w.mw.AB, p, batch};
+    g.n_src = 2; g.out = w.Va; g.out_row0 = Hr; g.n_out = m;
+    MimoGemm gb = g;
+    gb.src[0] = {w.u_edge, w.mw.Bb, p, 0};
+    gb.src[1] = {w.u_edge, w.mw.AB, p, batch};
+    gb.src[0].row0 = gb.src[1].row0 = batch;
+    if ((rc = two_launches(g, gb, 1, K_MIMO_FIRST, dr * (p + m) * es, dr * 4.0 * m * p))) return rc;
+  }
+  // ---- stages k = 1 .. Ne-1 and the last step: halo of 2^k rows of v^(k) before each
+  for (int k = 1; k <= Ne; ++k) {
+    void* Vs = (k - 1) % 2 == 0 ? w.Va : w.Vb;       // holds v^(k)
+    void* Vd = (k % 2 == 0) ? w.Va : w.Vb;
+    const int64_t d = ((int64_t)1 << k) * batch;     // halo rows of this step
+    cudaEvent_t ev_tail;
+    if ((rc = new_event(&ev_tail))) return rc;
+    CASC_TRY(cudaEventRecord(ev_tail, st));          // v^(k) complete on every local row
+    {
+      ProfScope ps(cs, K_SEQ_HALO, 2.0 * d * m * es, 0.0);
+      if ((rc = exchange(c, (const char*)Vs + (size_t)(Hr + rows - d) * m * es, (size_t)d * m * es,
+                         (char*)Vs + (size_t)(Hr - d) * m * es, (size_t)d * m * es, ev_tail, cs, ev_halo)))
+        return rc;
+    }
+    MimoGemm g{};
+    if (k < Ne) {
+      const void* Wk = tf32 ? static_cast<const void*>(P.f32 + k * 2 * mm) : static_cast<const void*>(P.b16 + k * mm);
+      g.src[0] = {Vs, Wk, m, d};
+      g.src[0].row0 = Hr;
+      g.n_src = 1; g.R = Vs; g.R_row0 = Hr; g.out = Vd; g.out_row0 = Hr; g.n_out = m;
+      if ((rc = two_launches(g, g, (int64_t)1 << k, K_MIMO_STAGE, dr * m * es * 2.0, dr * 2.0 * (double)mm))) return rc;
+    } else {                           // y = C v + (C P_Ne) v_{l-2^Ne} + D u
+      g.src[0] = {Vs, w.mw.C, m, 0};
+      g.src[1] = {Vs, w.mw.CP, m, d};
+      g.src[0].row0 = g.src[1].row0 = Hr;
+      g.n_src = 2;
+      if (D) { g.src[2] = {u_loc, w.mw.D, p, 0}; g.n_src = 3; }
+      g.out = y_loc; g.n_out = q;
+      if ((rc = two_launches(g, g, (int64_t)1 << k, K_MIMO_LAST, dr * (m + p + q) * es,
+                             dr * (4.0 * q * m + (D ? 2.0 * q * p : 0.0)))))
+        return rc;
+    }
+  }
+  return CASC_OK;
+}
+
+}  // extern "C"

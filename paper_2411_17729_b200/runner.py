@@ -85,43 +85,50 @@ class DeviceWorkload:
 
 class SeqShardedWorkload:
     """This rank's time shard of a single-system workload (BASELINE configs[3] at N > 1 GPUs):
-    rows [rank L_loc, (rank+1) L_loc) of every sequence, run with seqshard.run over DistComm
-    (per-stage halo exchange with the neighbouring ranks)."""
+    rows [rank L_loc, (rank+1) L_loc) of every sequence, time-major [L_loc][batch][p], run by
+    casc_apply_seqsharded with the library's own per-stage NCCL halo exchange (comm stream)."""
 
-    def __init__(self, wl, rank: int, world: int, device="cuda", group=None):
-        from . import seqshard
+    def __init__(self, wl, rank: int, world: int, device="cuda", comm=None, group=None):
         if wl.kind != "mimo" or wl.L % world:
             raise ValueError("sequence sharding takes one system with L divisible by the rank count")
         self.wl, self.rank, self.world = wl, rank, world
         self.L_loc = wl.L // world
         self.N = int(wl.N[0])
-        self.Ne = seqshard.effective_order(self.N, wl.L)
-        self.H = seqshard.shard_H(self.N, wl.L)
+        md = api._mode(wl.mode)
         d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
         self.Abar, self.Bbar, self.C = d(wl.Abar[0]), d(wl.Bbar[0]), d(wl.C[0])
         self.D = d(wl.D[0]) if np.any(wl.D[0]) else None
         l0 = rank * self.L_loc
-        u = np.stack([wl.u_window(0, b, l0, l0 + self.L_loc) for b in range(wl.batch)])   # storage-exact f64
-        self.u = torch.from_numpy(u).to(api.STORAGE[api._mode(wl.mode)]).to(device)
-        self.steps = seqshard.CudaSteps(wl.m, wl.p, wl.q, wl.mode, device)
-        self.shard = seqshard.make_shard(self.u, wl.m, wl.q, self.H)
-        self.comm = seqshard.DistComm(group) if world > 1 else seqshard.LocalComm()
-        self._seqshard = seqshard
-
-    @property
-    def y(self):
-        return self.shard.y
+        u = np.stack([wl.u_window(0, b, l0, l0 + self.L_loc) for b in range(wl.batch)], axis=1)   # [L_loc][batch][p]
+        self.u = torch.from_numpy(u).to(api.STORAGE[md]).to(device)
+        self.y = torch.empty((self.L_loc, wl.batch, wl.q), dtype=api.STORAGE[md], device=device)
+        self.pack = torch.empty(api.pack_bytes(1, wl.m, self.N, md), dtype=torch.uint8, device=device)
+        self.ws = torch.empty(api.seqsharded_workspace_bytes(wl.m, wl.p, wl.q, self.L_loc, wl.batch, self.N, world, md),
+                              dtype=torch.uint8, device=device)
+        if comm is None:
+            if world > 1:
+                from .seqshard import comm_from_process_group
+                comm = comm_from_process_group(group, device=torch.device(device))
+            else:
+                comm = api.comm_init(0, 1, api.nccl_unique_id())
+        self.comm = comm
+        self.comm_stream = torch.cuda.Stream(device=device)
 
     def step(self, stream=None) -> int:
-        """powers + derived weights + the sharded cascade; returns the number of kernel launches."""
-        launches = self.steps.prepare(self.Abar, self.Bbar, self.C, self.D, self.N, self.Ne, stream=stream)
-        launches += self.Ne + 1 if self.Ne > 0 else 1              # first + stages + last
-        self._seqshard.run(self.steps, self.comm, [self.shard], self.N, self.wl.L)
-        return launches
+        """powers + the sharded cascade; returns the number of kernel launches."""
+        pw = api.powers(self.Abar, self.N, self.wl.mode, stream=stream, out=self.pack)
+        n = api.last_launch_count()
+        api.apply_seqsharded(self.comm, pw, self.Bbar, self.C, self.D, self.u, y=self.y, ws=self.ws, stream=stream,
+                             comm_stream=self.comm_stream)
+        return n + api.last_launch_count()
 
     def run_host(self, u_h: torch.Tensor, y_h: torch.Tensor) -> int:
         """End to end from pinned host buffers: H2D of the local u, step, D2H of the local y."""
-        self.shard.u_ext[:, 1:, :].copy_(u_h, non_blocking=True)
+        self.u.copy_(u_h, non_blocking=True)
         n = self.step()
-        y_h.copy_(self.shard.y, non_blocking=True)
+        y_h.copy_(self.y, non_blocking=True)
         return n
+
+    def y_f64(self) -> np.ndarray:
+        """This shard's y as float64 [batch][L_loc][q] (CPU)."""
+        return self.y.float().cpu().double().numpy().transpose(1, 0, 2)

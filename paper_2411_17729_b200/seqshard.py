@@ -1,171 +1,32 @@
-"""Sequence-sharded cascade (BASELINE configs[3]).
-
-Rank r of R owns time rows [r L_loc, (r+1) L_loc) of every sequence of one MIMO system. The
-cascade's stage k adds P_k v_{l-2^k}, so before stage k each rank needs the
-last 2^k rows of v^(k) held by rank r-1 (zeros for rank 0, i.e. x_{-1} = 0): one
-point-to-point halo exchange per stage, the only communication of the method. The first stage
-needs one row of u (u_{l-1}), the last stage 2^Ne rows of v^(Ne).
-
-States live in buffers [batch][H + L_loc][m] whose first H = 2^Ne rows hold the halo; the CUDA
-step functions (include/cascade.h, casc_seq_*) read shifted rows straight from the halo, so no
-packing of the local rows is needed.
-
-Communicators (the same stage loop drives both):
-  DistComm   one shard per process; the halo goes through torch.distributed batched P2P
-             (NCCL over NVLink on B200, gloo on CPU for the world_size-2 tests).
-  LocalComm  several shards in one process (emulated ranks on one GPU): the halo is a device copy.
-Restriction: 2^Ne <= L_loc (each halo comes from the immediate predecessor), which holds for
-BASELINE configs[3] at up to 8 GPUs (2^11 << 2^20 / 8).
-"""
+"""Sequence sharding plumbing: build the library's NCCL communicator from
+a torch.distributed process group. torch only carries the 128-byte NCCL unique id from rank 0 to
+the other ranks; the halo exchange itself is inside libcascade_b200 (casc_apply_seqsharded)."""
 from __future__ import annotations
-
-import ctypes
-import math
-from dataclasses import dataclass
 
 import torch
 
 from . import api
-from ._lib import check, lib
 
 
-def effective_order(N: int, L: int) -> int:
-    """Ne = min(N, floor(log2(L-1))): stages with 2^k >= L are identities (R20)."""
-    if L <= 2:
-        return 0
-    return min(N, (L - 1).bit_length() - 1)        # exact integer floor(log2(L - 1))
+def broadcast_unique_id(group=None, device=None) -> bytes:
+    """Rank 0 creates the NCCL unique id (casc_nccl_unique_id); every rank of `group` returns it.
+    The broadcast goes through the group's own backend (a CUDA tensor for nccl, CPU for gloo)."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    if rank == 0:
+        t = torch.frombuffer(bytearray(api.nccl_unique_id()), dtype=torch.uint8).clone()
+    else:
+        t = torch.zeros(128, dtype=torch.uint8)
+    if dist.get_backend(group) == "nccl":
+        t = t.to(device if device is not None else torch.device("cuda", torch.cuda.current_device()))
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    dist.broadcast(t, src=src, group=group)
+    return bytes(t.cpu().numpy().tobytes())
 
 
-@dataclass
-class Shard:
-    """One rank's share: u_ext [batch][1+L_loc][p], V [batch][H+L_loc][m] x 2, y [batch][L_loc][q]."""
-    u_ext: torch.Tensor
-    Va: torch.Tensor
-    Vb: torch.Tensor
-    y: torch.Tensor
-
-
-class DistComm:
-    """Halo exchange with the neighbouring ranks through torch.distributed point-to-point ops."""
-
-    def __init__(self, group=None):
-        import torch.distributed as dist
-        self.dist = dist
-        self.group = group
-        self.rank = dist.get_rank(group)
-        self.world = dist.get_world_size(group)
-
-    def exchange(self, tensors, H: int, rows: int) -> None:
-        """tensors: [t] (one shard). Send the last `rows` local rows to rank+1, receive rank-1's
-        into halo rows [H - rows, H)."""
-        dist = self.dist
-        (t,) = tensors
-        ops, recv = [], None
-        if self.rank + 1 < self.world:
-            send = t[:, t.shape[1] - rows:, :].contiguous()
-            ops.append(dist.P2POp(dist.isend, send, self._peer(self.rank + 1), self.group))
-        if self.rank > 0:
-            recv = torch.empty((t.shape[0], rows, t.shape[2]), dtype=t.dtype, device=t.device)
-            ops.append(dist.P2POp(dist.irecv, recv, self._peer(self.rank - 1), self.group))
-        if ops:
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
-        if recv is not None:
-            t[:, H - rows:H, :].copy_(recv)
-
-    def _peer(self, r: int) -> int:
-        return self.dist.get_global_rank(self.group, r) if self.group is not None else r
-
-
-class LocalComm:
-    """Emulated ranks in one process: shard i's halo is copied from shard i-1's tail."""
-
-    def exchange(self, tensors, H: int, rows: int) -> None:
-        for i in range(len(tensors) - 1, 0, -1):          # descending: reads precede overwrites
-            prev, cur = tensors[i - 1], tensors[i]
-            cur[:, H - rows:H, :].copy_(prev[:, prev.shape[1] - rows:, :])
-
-
-class CudaSteps:
-    """The casc_seq_* C-ABI steps for one system (marshalling only)."""
-
-    def __init__(self, m, p, q, mode, device="cuda"):
-        self.m, self.p, self.q, self.md = m, p, q, api._mode(mode)
-        self.device = device
-        self.dtype = api.STORAGE[self.md]
-        self.ws = torch.empty(int(lib().casc_seq_workspace_bytes(m, p, q, self.md)), dtype=torch.uint8,
-                              device=device)
-        self.pw = None
-        self.has_D = False
-
-    def prepare(self, Abar, Bbar, C, D, N: int, Ne: int, stream=None) -> int:
-        """Powers and the derived weights. Abar/Bbar/C/D float64 on device.
-        Returns the number of kernel launches enqueued."""
-        self.pw = api.powers(Abar, N, self.md, stream=stream)
-        n = api.last_launch_count()
-        self.has_D = D is not None
-        self.N_max = N
-        check(lib().casc_seq_prepare(self.m, self.p, self.q, Ne, N, self.md, api._p(self.pw.pack), api._p(Bbar),
-                                     api._p(C), api._p(D), api._p(self.ws), self.ws.numel(), api._stream(stream)),
-              "casc_seq_prepare")
-        return n + api.last_launch_count()
-
-    def first(self, sh: Shard, H: int, stream=None) -> None:
-        batch, L_loc = sh.y.shape[0], sh.y.shape[1]
-        check(lib().casc_seq_first(self.m, self.p, self.q, L_loc, batch, self.md, api._p(self.ws), api._p(sh.u_ext),
-                                   H, api._p(sh.Va), api._stream(stream)), "casc_seq_first")
-
-    def stage(self, k: int, sh: Shard, src, dst, H: int, stream=None) -> None:
-        batch, L_loc = sh.y.shape[0], sh.y.shape[1]
-        check(lib().casc_seq_stage(self.m, L_loc, batch, k, self.N_max, self.md, api._p(self.pw.pack), H,
-                                   api._p(src), api._p(dst), api._stream(stream)), "casc_seq_stage")
-
-    def last(self, Ne: int, sh: Shard, V, H: int, stream=None) -> None:
-        batch, L_loc = sh.y.shape[0], sh.y.shape[1]
-        check(lib().casc_seq_last(self.m, self.p, self.q, L_loc, batch, Ne, self.md, api._p(self.ws), H,
-                                  api._p(V), api._p(sh.u_ext), 1 if self.has_D else 0, api._p(sh.y),
-                                  api._stream(stream)), "casc_seq_last")
-
-
-def make_shard(u_loc: torch.Tensor, m: int, q: int, H: int) -> Shard:
-    """Allocate one shard's buffers (halo rows zero: rank 0's halo is x_{-1} = 0)."""
-    batch, L_loc, p = u_loc.shape
-    dev, dt = u_loc.device, u_loc.dtype
-    u_ext = torch.zeros((batch, 1 + L_loc, p), dtype=dt, device=dev)
-    u_ext[:, 1:, :].copy_(u_loc)
-    Va = torch.zeros((batch, H + L_loc, m), dtype=dt, device=dev)
-    Vb = torch.zeros_like(Va)
-    y = torch.empty((batch, L_loc, q), dtype=dt, device=dev)
-    return Shard(u_ext, Va, Vb, y)
-
-
-def run(steps, comm, shards, N: int, L_global: int) -> None:
-    """The sharded cascade over `shards` (this process's shards, in rank order): steps.prepare must
-    have been called with the same effective order. Results land in shard.y."""
-    Ne = effective_order(N, L_global)
-    H = max(1, 1 << Ne) if Ne > 0 else 1
-    L_loc = shards[0].y.shape[1]
-    if Ne > 0 and (1 << Ne) > L_loc:
-        raise NotImplementedError(f"halo 2^{Ne} exceeds the shard length {L_loc}")
-    comm.exchange([s.u_ext for s in shards], 1, 1)             # u_{-1} for the first stage
-    if Ne == 0:
-        for s in shards:
-            steps.last(0, s, None, H)
-        return
-    for s in shards:
-        steps.first(s, H)                                         # v^(1) into Va
-    src = [s.Va for s in shards]
-    dst = [s.Vb for s in shards]
-    for k in range(1, Ne):
-        comm.exchange(src, H, 1 << k)                             # halo: last 2^k rows of v^(k)
-        for s, a, b in zip(shards, src, dst):
-            steps.stage(k, s, a, b, H)
-        src, dst = dst, src
-    comm.exchange(src, H, 1 << Ne)
-    for s, a in zip(shards, src):
-        steps.last(Ne, s, a, H)
-
-
-def shard_H(N: int, L_global: int) -> int:
-    Ne = effective_order(N, L_global)
-    return (1 << Ne) if Ne > 0 else 1
+def comm_from_process_group(group=None, device=None) -> api.Comm:
+    """The library communicator over the ranks of `group` (one rank per process and GPU; the
+    caller has selected this rank's device)."""
+    import torch.distributed as dist
+    uid = broadcast_unique_id(group, device)
+    return api.comm_init(dist.get_rank(group), dist.get_world_size(group), uid)

@@ -1,0 +1,134 @@
+"""Test-side model of the library's sequence-sharded schedule (csrc/seqshard.cu), in float64 torch.
+
+It reproduces the schedule the CUDA path runs -- time-major buffers [H + L_loc][batch][dim] with
+the halo rows in front, the one-row u halo before the fused first step, a halo of the last 2^k
+time rows of v^(k) before stage k, 2^Ne rows before the fused last step (R21), rank 0's
+halo zero (x_{-1} = 0) -- with the per-step arithmetic written out in float64, so
+the exchange bookkeeping can be checked on the CPU against the oracle: with the real
+torch.distributed exchange (gloo, world_size 2, DistComm) and with emulated ranks (LocalComm).
+Every halo is one contiguous block of the time-major buffer, as in the library.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+
+def effective_order(N: int, L: int) -> int:
+    """Ne = min(N, floor(log2(L-1))) (R20), exact integer arithmetic."""
+    if L <= 2:
+        return 0
+    return min(N, (L - 1).bit_length() - 1)
+
+
+@dataclass
+class Shard:
+    """One rank's buffers: u_ext [1 + L_loc][batch][p] (row 0 = u_{-1} of this shard),
+    Va/Vb [H + L_loc][batch][m] (rows [H - d, H) = the halo of a step with shift d), y [L_loc][batch][q]."""
+    u_ext: torch.Tensor
+    Va: torch.Tensor
+    Vb: torch.Tensor
+    y: torch.Tensor
+
+
+def make_shard(u_loc: torch.Tensor, m: int, q: int, H: int) -> Shard:
+    """u_loc: [L_loc][batch][p]. Halo rows start at zero (rank 0 keeps them)."""
+    L_loc, batch, p = u_loc.shape
+    dt = u_loc.dtype
+    u_ext = torch.zeros((1 + L_loc, batch, p), dtype=dt)
+    u_ext[1:] = u_loc
+    Va = torch.zeros((H + L_loc, batch, m), dtype=dt)
+    return Shard(u_ext, Va, torch.zeros_like(Va), torch.empty((L_loc, batch, q), dtype=dt))
+
+
+class DistComm:
+    """Halo exchange through torch.distributed P2P: send the last `rows` local rows of `t` to
+    rank+1, receive rank-1's into rows [H - rows, H). Both are contiguous in the time-major layout."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+
+    def exchange(self, tensors, H: int, rows: int) -> None:
+        dist = self.dist
+        (t,) = tensors
+        ops = []
+        if self.rank + 1 < self.world:
+            ops.append(dist.P2POp(dist.isend, t[t.shape[0] - rows:], self.rank + 1, self.group))
+        if self.rank > 0:
+            ops.append(dist.P2POp(dist.irecv, t[H - rows:H], self.rank - 1, self.group))
+        for r in dist.batch_isend_irecv(ops) if ops else []:
+            r.wait()
+
+
+class LocalComm:
+    """Emulated ranks in one process: shard i's halo is copied from shard i-1's tail."""
+
+    def exchange(self, tensors, H: int, rows: int) -> None:
+        for i in range(len(tensors) - 1, 0, -1):
+            prev, cur = tensors[i - 1], tensors[i]
+            cur[H - rows:H] = prev[prev.shape[0] - rows:]
+
+
+class F64Steps:
+    """The per-step arithmetic of the schedule in float64 (what each GEMM launch computes)."""
+
+    def __init__(self, P, Abar, Bbar, C, D, Ne):
+        t = torch.from_numpy
+        self.P = [t(x) for x in P]
+        Ab, Bb, Cm = t(Abar), t(Bbar), t(C)
+        Dm = torch.zeros((C.shape[0], Bbar.shape[1]), dtype=torch.float64) if D is None else t(D)
+        self.Bb, self.AB = Bb, Ab @ Bb
+        self.C, self.CP, self.D = Cm, Cm @ self.P[Ne], Dm
+        self.CBD, self.CAB = Cm @ Bb + Dm, Cm @ (Ab @ Bb)
+
+    def first(self, sh, H):
+        u = sh.u_ext
+        sh.Va[H:] = u[1:] @ self.Bb.T + u[:-1] @ self.AB.T
+
+    def stage(self, k, sh, src, dst, H):
+        L = sh.y.shape[0]
+        s = 1 << k
+        dst[H:] = src[H:] + src[H - s:H - s + L] @ self.P[k].T
+
+    def last(self, Ne, sh, V, H):
+        u = sh.u_ext
+        if Ne == 0:
+            sh.y[:] = u[1:] @ self.CBD.T + u[:-1] @ self.CAB.T
+            return
+        L = sh.y.shape[0]
+        s = 1 << Ne
+        sh.y[:] = V[H:] @ self.C.T + V[H - s:H - s + L] @ self.CP.T + u[1:] @ self.D.T
+
+
+def run(steps, comm, shards, N: int, L_global: int) -> None:
+    """The sharded cascade over `shards` (this process's shards, in rank order)."""
+    Ne = effective_order(N, L_global)
+    H = (1 << Ne) if Ne > 0 else 0
+    L_loc = shards[0].y.shape[0]
+    if Ne > 0 and (1 << Ne) > L_loc:
+        raise NotImplementedError(f"halo 2^{Ne} exceeds the shard length {L_loc}")
+    comm.exchange([s.u_ext for s in shards], 1, 1)             # u_{-1} for the first step
+    if Ne == 0:
+        for s in shards:
+            steps.last(0, s, None, H)
+        return
+    for s in shards:
+        steps.first(s, H)
+    src = [s.Va for s in shards]
+    dst = [s.Vb for s in shards]
+    for k in range(1, Ne):
+        comm.exchange(src, H, 1 << k)                             # last 2^k rows of v^(k)
+        for s, a, b in zip(shards, src, dst):
+            steps.stage(k, s, a, b, H)
+        src, dst = dst, src
+    comm.exchange(src, H, 1 << Ne)
+    for s, a in zip(shards, src):
+        steps.last(Ne, s, a, H)
+
+
+def shard_H(N: int, L_global: int) -> int:
+    Ne = effective_order(N, L_global)
+    return (1 << Ne) if Ne > 0 else 0

@@ -1,7 +1,13 @@
-"""Sequence-sharded path on one GPU: R emulated ranks in one process (LocalComm) run the CUDA
-step functions casc_seq_*; the result must be bitwise the unsharded run (each output row's
-accumulation order does not depend on the shard it lives in) and within tolerance
-of the float64 oracle. (Separate processes waiting on each other on one GPU are not used.)"""
+"""Library-owned sequence sharding (casc_apply_seqsharded, csrc/seqshard.cu) on one GPU.
+
+R emulated ranks (casc_comm_init_local: one host thread and one pair of streams per rank, halos as
+device copies ordered by events -- ranks never spin on each other inside a kernel) run the same
+schedule as the NCCL transport. The result must be bitwise the 1-rank run over an NCCL
+communicator (world 1) and bitwise the unsharded casc_apply (each output row's accumulation
+order does not depend on the shard or tile it lives in; SURVEY pin T15), and within tolerance of
+the float64 oracle."""
+import threading
+
 import numpy as np
 import pytest
 import torch
@@ -13,28 +19,95 @@ pytestmark = pytest.mark.gpu
 TOL = {"fp32": 1e-5, "bf16": 2e-2}
 
 
-@pytest.mark.parametrize("mode", ["bf16", "fp32"])
-@pytest.mark.parametrize("R,m,p,q,L,N", [(2, 128, 64, 64, 4096, 8), (4, 64, 64, 64, 2048, 9), (8, 128, 64, 128, 8192, 6),
-                                         (2, 64, 64, 64, 256, 0)])
-def test_emulated_ranks_bitwise_equal_unsharded(mode, R, m, p, q, L, N):
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
     if not torch.cuda.is_available():
-        pytest.skip("no CUDA")
-    from paper_2411_17729_b200 import seqshard
+        pytest.skip("no CUDA device")
+    import paper_2411_17729_b200 as pk
+    pk.lib()
+
+
+def _sharded(wl, R, comms):
+    """Run R ranks of casc_apply_seqsharded, each on its own thread; returns y [L][batch][q]."""
+    import paper_2411_17729_b200 as pk
+    md = wl.mode
+    N = int(wl.N[0])
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    Abar, Bbar, C = d(wl.Abar[0]), d(wl.Bbar[0]), d(wl.C[0])
+    D = d(wl.D[0]) if np.any(wl.D[0]) else None
+    u = torch.from_numpy(wl.u_all()[0].transpose(1, 0, 2).copy()).to(pk.STORAGE[pk.api._mode(md)]).cuda()
+    L_loc = wl.L // R
+    pw = pk.powers(Abar, N, md)
+    torch.cuda.synchronize()
+    ys = [None] * R
+    errs = []
+
+    def rank(r):
+        try:
+            st, cs = torch.cuda.Stream(), torch.cuda.Stream()
+            u_loc = u[r * L_loc:(r + 1) * L_loc].contiguous()
+            torch.cuda.synchronize()
+            with torch.cuda.stream(st):
+                ys[r] = pk.apply_seqsharded(comms[r], pw, Bbar, C, D, u_loc, stream=st, comm_stream=cs)
+            st.synchronize()
+        except Exception as e:                    # reported by the main thread
+            errs.append(e)
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(R)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    if errs:
+        raise errs[0]
+    torch.cuda.synchronize()
+    return torch.cat(ys, dim=0)
+
+
+CASES = [  # (R, m, p, q, L, N)
+    (2, 128, 64, 64, 4096, 8),
+    (4, 64, 64, 64, 2048, 9),       # 2^Ne = 512 = L_loc: the halo is a whole shard
+    (8, 128, 64, 128, 8192, 6),
+    (2, 64, 64, 64, 256, 0),        # Ne = 0: one fused step
+    (3, 256, 64, 64, 3000, 7),      # rows not a multiple of the 256-row blocks
+]
+
+
+@pytest.mark.parametrize("mode", ["bf16", "fp32"])
+@pytest.mark.parametrize("case", CASES)
+def test_emulated_ranks_bitwise(mode, case):
+    import paper_2411_17729_b200 as pk
+    R, m, p, q, L, N = case
+    wl = S.make_random_mimo(m, p, q, L=L, batch=3, N=N, rho=0.97, mode=mode)
+    comms = pk.comm_init_local(R)
+    try:
+        y_R = _sharded(wl, R, comms)
+    finally:
+        for c in comms:
+            c.destroy()
+    one = pk.comm_init(0, 1, pk.nccl_unique_id())                   # NCCL transport, one rank
+    try:
+        y_1 = _sharded(wl, 1, [one])
+    finally:
+        one.destroy()
+    assert torch.equal(y_R, y_1), "R emulated ranks differ from one rank"
     from paper_2411_17729_b200.runner import DeviceWorkload
-    wl = S.make_random_mimo(m, p, q, L=L, batch=2, N=N, rho=0.97, mode=mode)
     dw = DeviceWorkload(wl)
     dw.step()
-    y_full = dw.y.clone()
-    Ne = seqshard.effective_order(N, L)
-    H = seqshard.shard_H(N, L)
-    steps = seqshard.CudaSteps(m, p, q, mode)
-    steps.prepare(dw.Abar[0], dw.Bbar, dw.C, dw.D, N, Ne)
-    L_loc = L // R
-    shards = [seqshard.make_shard(dw.u[:, r * L_loc:(r + 1) * L_loc, :], m, q, H) for r in range(R)]
-    seqshard.run(steps, seqshard.LocalComm(), shards, N, L)
     torch.cuda.synchronize()
-    y = torch.cat([s.y for s in shards], dim=1)
-    assert torch.equal(y, y_full)
+    assert torch.equal(y_1.permute(1, 0, 2), dw.y), "sharded (time-major) differs from unsharded casc_apply"
     ref = oracle.apply_workload(wl)[0]
-    yn = y.float().cpu().double().numpy()
+    yn = y_R.permute(1, 0, 2).float().cpu().double().numpy()
     assert np.linalg.norm(yn - ref) / np.linalg.norm(ref) <= TOL[mode]
+
+
+def test_halo_longer_than_shard_is_unsupported():
+    import paper_2411_17729_b200 as pk
+    wl = S.make_random_mimo(64, 64, 64, L=1024, batch=1, N=9, rho=0.9, mode="bf16")   # 2^9 > L/4
+    comms = pk.comm_init_local(4)
+    try:
+        with pytest.raises(pk.CascadeError, match="UNSUPPORTED"):
+            _sharded(wl, 4, comms)
+    finally:
+        for c in comms:
+            c.destroy()
