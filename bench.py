@@ -409,7 +409,8 @@ def run_ours(args, world, rank, local_rank):
                "h2d_bytes_per_step": int(u_h.numel() * u_h.element_size()),
                "d2h_bytes_per_step": int(y_h.numel() * y_h.element_size()),
                "ms_per_step": float(te.item()) / args.e2e_steps,
-               "api": "SeqShardedWorkload.run_host (pinned local u -> device, casc_seq_* steps with NCCL halos, y -> host)"}
+               "api": ("SeqShardedWorkload.run_host (pinned local u [L_loc][batch][p] -> device, powers + "
+                       "casc_apply_seqsharded with the library's NCCL halos, y -> host; copies not overlapped)")}
     elif not args.no_e2e:
         n = len(chans)
         f = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
@@ -482,6 +483,9 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    # NCCL prints its version banner on stdout at communicator creation: keep stdout to the one
+    # JSON line (warnings still go to stderr)
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     if world > 1:
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))

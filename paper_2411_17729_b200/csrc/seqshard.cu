@@ -334,9 +334,10 @@ int casc_apply_seqsharded(void* comm, int m, int p, int q, int64_t L_loc, int ba
 
   // ---- u halo: the last time row of rank r-1's u (one row of batch * p)
   {
+    CASC_TRY(cudaStreamWaitEvent(cs, ev_in, 0));      // before the scope: it times the transfer only
     ProfScope ps(cs, K_SEQ_HALO, 2.0 * batch * p * es, 0.0);
     if ((rc = exchange(c, (const char*)u_loc + (size_t)(rows - batch) * p * es, (size_t)batch * p * es, w.u_edge,
-                       (size_t)batch * p * es, ev_in, cs, ev_halo)))
+                       (size_t)batch * p * es, nullptr, cs, ev_halo)))
       return rc;
   }
   const double dr = (double)rows;
@@ -389,9 +390,10 @@ int casc_apply_seqsharded(void* comm, int m, int p, int q, int64_t L_loc, int ba
     if ((rc = new_event(&ev_tail))) return rc;
     CASC_TRY(cudaEventRecord(ev_tail, st));          // v^(k) complete on every local row
     {
+      CASC_TRY(cudaStreamWaitEvent(cs, ev_tail, 0));
       ProfScope ps(cs, K_SEQ_HALO, 2.0 * d * m * es, 0.0);
       if ((rc = exchange(c, (const char*)Vs + (size_t)(Hr + rows - d) * m * es, (size_t)d * m * es,
-                         (char*)Vs + (size_t)(Hr - d) * m * es, (size_t)d * m * es, ev_tail, cs, ev_halo)))
+                         (char*)Vs + (size_t)(Hr - d) * m * es, (size_t)d * m * es, nullptr, cs, ev_halo)))
         return rc;
     }
     MimoGemm g{};

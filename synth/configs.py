@@ -65,6 +65,43 @@ def trapezoid(A: np.ndarray, B: np.ndarray | None, delta: float):
     return Abar, Bbar
 
 
+def exponential(A: np.ndarray, B: np.ndarray | None, delta: float):
+    """Exponential (zero-order-hold) discretisation of PAPER.md:306-311 (§5):
+    Abar = exp(D A), Bbar = (D A)^-1 [exp(D A) - I] D B  (= int_0^D exp(A s) ds B).
+
+    Reading (R27): the paper prints Bbar = (DA)^-1[exp(DA) - I] DA, which is m x m and
+    has no B; the dimensionally consistent zero-order hold ends in D B.
+    Both blocks come from ONE matrix exponential of the augmented generator (Van Loan's identity):
+        exp(D [[A, B], [0, 0]]) = [[exp(D A), int_0^D exp(A s) ds B], [0, I]],
+    computed by scipy.linalg.expm (scaling and squaring with Pade; a library primitive). No
+    inverse of A is formed, so the recipe holds for singular A too."""
+    from scipy.linalg import expm
+    m = A.shape[0]
+    p = 0 if B is None else B.shape[1]
+    G = np.zeros((m + p, m + p))
+    G[:m, :m] = A
+    if p:
+        G[:m, m:] = B
+    E = expm(delta * G)
+    Abar = E[:m, :m].copy()
+    if not np.any(np.triu(A, 1)):
+        # exp of a lower-triangular matrix is lower triangular; Pade's pivoted solves can leave
+        # rounding-level entries above the diagonal, which are zero in exact arithmetic
+        Abar = np.tril(Abar)
+    Bbar = None if B is None else E[:m, m:].copy()
+    return Abar, Bbar
+
+
+def discretize(A: np.ndarray, B: np.ndarray | None, delta: float, scheme: str = "trapezoid"):
+    """Abar, Bbar by the bilinear/trapezoidal rule (Eq. 10, the paper's examples) or the
+    exponential zero-order hold."""
+    if scheme == "trapezoid":
+        return trapezoid(A, B, delta)
+    if scheme == "exponential":
+        return exponential(A, B, delta)
+    raise ValueError(scheme)
+
+
 def spectral_radius(A: np.ndarray) -> float:
     return float(np.max(np.abs(np.linalg.eigvals(A))))
 
@@ -231,9 +268,10 @@ def make_E1(L: int = 4096, batch: int = 1, N: int = 11, seed: int = 0, mode: str
 
 def make_hippo_bank(name: str, n_ch: int, L: int, batch: int, dmin: float, dmax: float,
                     tol: float, N_cap: int | None, m: int = 64, seed: int = 0,
-                    stream: int = 102, mode: str = "fp32") -> Workload:
-    """configs[1] / configs[4]: HiPPO-LegS SISO channels, Delta_c log-uniform, trapezoid Abar/Bbar,
-    B_n = sqrt(2n+1), C ~ N(0,1/m), D ~ N(0,1); N_c from ||Abar^(2^(N+1))||_2 <= tol."""
+                    stream: int = 102, mode: str = "fp32", scheme: str = "trapezoid") -> Workload:
+    """configs[1] / configs[4]: HiPPO-LegS SISO channels, Delta_c log-uniform, trapezoid Abar/Bbar
+    (scheme='exponential': the zero-order hold of PAPER.md:306-311, NEXT-4), B_n = sqrt(2n+1),
+    C ~ N(0,1/m), D ~ N(0,1); N_c from ||Abar^(2^(N+1))||_2 <= tol."""
     g = np.random.default_rng(seed)
     deltas = 10.0 ** g.uniform(math.log10(dmin), math.log10(dmax), n_ch)
     Cs = g.normal(0.0, 1.0 / math.sqrt(m), (n_ch, 1, m))
@@ -243,21 +281,27 @@ def make_hippo_bank(name: str, n_ch: int, L: int, batch: int, dmin: float, dmax:
     cap = n_cap_for_length(L) if N_cap is None else min(N_cap, n_cap_for_length(L))
     Abars, Bbars, Ns = [], [], []
     for c in range(n_ch):
-        Abar, Bbar = trapezoid(A, B, float(deltas[c]))
+        Abar, Bbar = discretize(A, B, float(deltas[c]), scheme)
         Abars.append(Abar)
         Bbars.append(Bbar)
         Ns.append(plan_N(Abar, tol, cap))
     return Workload(name, "bank", mode, m, 1, 1, L, batch, np.stack(Abars), np.stack(Bbars),
                     Cs, Ds, np.array(Ns), u_seed=seed, u_stream=stream,
-                    meta={"delta": deltas, "tol": tol, "N_cap": cap})
+                    meta={"delta": deltas, "tol": tol, "N_cap": cap, "scheme": scheme})
 
 
-def make_E2(n_ch: int = 256, L: int = 16384, batch: int = 4, seed: int = 0, mode: str = "fp32") -> Workload:
-    return make_hippo_bank("E2", n_ch, L, batch, 1e-3, 1e-1, 1e-6, None, seed=seed, stream=102, mode=mode)
+def make_E2(n_ch: int = 256, L: int = 16384, batch: int = 4, seed: int = 0, mode: str = "fp32",
+            scheme: str = "trapezoid") -> Workload:
+    name = "E2" if scheme == "trapezoid" else "E2x"
+    return make_hippo_bank(name, n_ch, L, batch, 1e-3, 1e-1, 1e-6, None, seed=seed, stream=102, mode=mode,
+                           scheme=scheme)
 
 
-def make_E5(n_ch: int = 4096, L: int = 65536, batch: int = 8, seed: int = 0, mode: str = "fp32") -> Workload:
-    return make_hippo_bank("E5", n_ch, L, batch, 1e-4, 1e-1, 1e-6, 15, seed=seed, stream=105, mode=mode)
+def make_E5(n_ch: int = 4096, L: int = 65536, batch: int = 8, seed: int = 0, mode: str = "fp32",
+            scheme: str = "trapezoid") -> Workload:
+    name = "E5" if scheme == "trapezoid" else "E5x"
+    return make_hippo_bank(name, n_ch, L, batch, 1e-4, 1e-1, 1e-6, 15, seed=seed, stream=105, mode=mode,
+                           scheme=scheme)
 
 
 def make_E3(L: int = 65536, batch: int = 16, N: int = 13, m: int = 256, p: int = 64,

@@ -74,3 +74,20 @@ def test_E4_full_size_sampled():
     L = wl.L
     windows = [(0, 0), (2, 4095), (5, L // 2 + 3), (7, L - 48)]
     sampled_windows(wl, dw, windows, 48, 2e-2)
+
+
+def test_E2_exponential_full_size_sampled_channels():
+    """E2's shape (256 channels, L = 16384, batch 4) with the exponential scheme (NEXT-4): channels
+    spanning the N_c range checked over their whole length against the float64 oracle."""
+    wl = S.make_E2(scheme="exponential")
+    dw = run_full(wl)
+    order = np.argsort(wl.N, kind="stable")
+    for c in sorted({int(order[0]), int(order[len(order) // 2]), int(order[-1])}):
+        y = dw.y[c].float().cpu().double().numpy()
+        u = np.stack([wl.u_window(c, b, 0, wl.L)[:, 0] for b in range(wl.batch)])
+        N = int(wl.N[c])
+        ref = oracle.cascade(oracle.powers(wl.Abar[c], N), wl.Bbar[c], wl.C[c], wl.D[c], u[:, :, None], N)[:, :, 0]
+        Du = u * wl.D[c, 0, 0]
+        e, es = rel(y, ref), rel(y - Du, ref - Du)
+        print(f"E2x channel {c} N={N}: rel {e:.3e} state {es:.3e}")
+        assert e <= 1e-5 and es <= 1e-5, (c, N, e, es)

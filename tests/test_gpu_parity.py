@@ -236,3 +236,12 @@ def test_run_host_mimo_single_chunk_bitwise(mode):
                      dtype=torch.uint8, device="cuda")
     pk.run_host(f(wl.Abar), f(wl.Bbar), f(wl.C), f(wl.D), u_h, y_h, list(wl.N), mode, ws)
     assert np.array_equal(y_h.float().double().numpy(), y_dev)
+
+
+# ------------------------------------------------------------------ NEXT-4: exponential discretisation
+def test_exponential_scheme_bank():
+    """HiPPO channels discretised by the exponential zero-order hold (DESIGN.md
+    R27) through the same bank path: N_c planned from the new Abar, parity at 1e-5."""
+    wl = S.make_E2(n_ch=12, L=4096, batch=2, scheme="exponential")
+    e, es = check_parity(wl)
+    print(f"E2x rel {e:.2e} state {es:.2e}")

@@ -75,3 +75,67 @@ def test_E4_recipe_small():
     u = wl.u_all()
     assert np.array_equal(S.round_to_storage(u, "bf16"), u)   # already bf16-exact
     assert math.isfinite(wl.flops_ns())
+
+
+# ------------------------------------------------------------------ exponential scheme (NEXT-4)
+def test_exponential_scalar_closed_form():
+    """PAPER.md:306-311 with the zero-order-hold reading (R27): scalar a = -2, b = 1,
+    Delta = 0.5e-3 -> Abar = e^(-0.001) = 0.99900049983... (SPEC.md:153), Bbar = (1 - e^(-0.001)) / 2."""
+    Ab, Bb = S.exponential(np.array([[-2.0]]), np.array([[1.0]]), 0.5e-3)
+    assert abs(Ab[0, 0] - math.exp(-0.001)) <= 1e-16
+    assert abs(Ab[0, 0] - 0.99900049983) < 1e-11
+    assert abs(Bb[0, 0] / ((1.0 - math.exp(-0.001)) / 2.0) - 1.0) <= 1e-13
+
+
+def test_exponential_diagonal_and_inverse_formula():
+    """Diagonal A: elementwise e^(D a_i), (e^(D a_i) - 1) b_i / a_i. General invertible A: the
+    augmented-exponential Bbar equals A^-1 (exp(DA) - I) B formed by a solve (a different route)."""
+    a = np.array([-0.5, -3.0, -10.0, -0.01])
+    b = np.array([[1.0], [2.0], [-1.0], [0.5]])
+    d = 0.3
+    Ab, Bb = S.exponential(np.diag(a), b, d)
+    assert np.allclose(Ab, np.diag(np.exp(d * a)), rtol=1e-13, atol=1e-16)
+    assert np.allclose(Bb[:, 0], (np.exp(d * a) - 1.0) * b[:, 0] / a, rtol=1e-13)
+    g = np.random.default_rng(4)
+    A = -np.eye(6) + 0.3 * g.standard_normal((6, 6))
+    B = g.standard_normal((6, 2))
+    Ab, Bb = S.exponential(A, B, 0.2)
+    Bb2 = np.linalg.solve(A, (Ab - np.eye(6)) @ B)
+    assert np.max(np.abs(Bb - Bb2)) <= 1e-13 * np.max(np.abs(Bb))
+
+
+def test_exponential_semigroup_and_zoh_additivity():
+    """exp((D1 + D2) A) = exp(D2 A) exp(D1 A); the hold composes as
+    Bbar(D1 + D2) = exp(D2 A) Bbar(D1) + Bbar(D2)."""
+    A = S.hippo(16)
+    B = S.hippo_B(16)
+    A1, B1 = S.exponential(A, B, 0.01)
+    A2, B2 = S.exponential(A, B, 0.03)
+    A3, B3 = S.exponential(A, B, 0.04)
+    assert np.max(np.abs(A3 - A2 @ A1)) <= 1e-13
+    assert np.max(np.abs(B3 - (A2 @ B1 + B2))) <= 1e-13 * np.max(np.abs(B3))
+
+
+def test_exponential_hippo_structure_and_trapezoid_agreement():
+    """HiPPO A is lower triangular, so exp(DA) is too (its strict upper part exactly zero) with
+    diagonal exp(-D(n+1)), n = 1..m; the bilinear rule (a (1,1) Pade approximant of the same
+    exponential) agrees to third order: the difference shrinks ~1000x per 10x smaller D."""
+    m = 64
+    A, B = S.hippo(m), S.hippo_B(m)
+    diffs = []
+    for d in (1e-6, 1e-5, 1e-4):
+        Ab, Bb = S.exponential(A, B, d)
+        assert np.all(np.triu(Ab, 1) == 0.0)
+        assert np.max(np.abs(np.diag(Ab) - np.exp(-d * np.arange(2, m + 2)))) <= 1e-14
+        At, Bt = S.trapezoid(A, B, d)
+        diffs.append(np.max(np.abs(Ab - At)))
+    for hi, lo in zip(diffs[1:], diffs[:-1]):
+        assert 500.0 < hi / lo < 2000.0, diffs
+
+
+def test_exponential_bank_recipe():
+    wl = S.make_E2(n_ch=6, L=4096, batch=1, scheme="exponential")
+    assert wl.name == "E2x" and wl.meta["scheme"] == "exponential"
+    for c in range(wl.n_ch):
+        assert np.all(np.triu(wl.Abar[c], 1) == 0.0)
+        assert S.spectral_radius(wl.Abar[c]) < 1.0
