@@ -31,6 +31,16 @@ static constexpr int kMetaInts = 4;   // per-channel host table: Neff | Kc | par
 
 // the fused output parts (R24-R26) for m = 64; CASC_BANK_AB=0 stores v and runs the separate tail
 // (tests compare the two)
+// NEXT-3: skip the zero upper blocks of lower-triangular stage weights (CASC_BANK_TRI=0: dense MMAs;
+// the tests compare the two bitwise)
+static bool bank_tri_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CASC_BANK_TRI");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static bool bank_ab_enabled() {
   static const bool on = [] {
     const char* e = getenv("CASC_BANK_AB");
@@ -56,6 +66,7 @@ struct BankWs {
   double* Q64;    // [n][m][m] scratch for one pair weight
   float* Q32;     // [n][qslots][2][m][m] pair weights, tf32 hi/lo planes
   float* parts;   // [kMaxParts][n * batch * L] fused output parts of the last stages (R24-R26)
+  int* tri;       // [n] Abar lower triangular (NEXT-3: the stage kernel skips the zero blocks)
   void *Va, *Vb;
   size_t bytes;
 };
@@ -74,6 +85,7 @@ static BankWs carve_bank(void* ws, int n, int m, int64_t L, int batch, int qslot
   w.Q64 = c.take<double>(qslots ? (size_t)n * m * m : 0);
   w.Q32 = c.take<float>((size_t)n * qslots * 2 * m * m);
   w.parts = c.take<float>(m == 64 ? (size_t)kMaxParts * n * batch * (size_t)L : 0);
+  w.tri = c.take<int>((size_t)n);
   const size_t vbytes = (size_t)n * batch * (size_t)L * m * sizeof(float);
   w.Va = c.take<char>(vbytes);
   w.Vb = c.take<char>(vbytes);
@@ -332,7 +344,7 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     CASC_TRY(cudaStreamWaitEvent(qs, q_start, 0));
     ProfScope ps(st, K_DERIVED, 0.0, 2.0 * n * (double)m * m * 128);
     if ((rc = launch_bank_derived(P.p64, N_max + 1, Bbar, C, D, dNeff, dKc, w.Kr64, w.krT, w.w64, w.w32, w.c32,
-                                  w.d32, use_ab ? w.pvec : nullptr, fold, n, m, st)))
+                                  w.d32, use_ab ? w.pvec : nullptr, w.tri, fold, n, m, st)))
       return rc;
     for (int j = 0; j < qslots; ++j) {          // Q_k = P_{k+1} P_k for pass j (k = 7 + 2j)
       const int k = kHeadK + 2 * j;
@@ -423,8 +435,6 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
   tmark("head done");
   if (q_done) CASC_TRY(cudaStreamWaitEvent(st, q_done, 0));   // the pair weights
   // ---- streaming stages k >= kHeadK over the channels with Neff > k (prefixes of `order`)
-  // fraction of the dense MMA work a stage pass issues (1: every K block of the weights)
-  const double tri_frac = 1.0;
   int pass = 0;
   for (int k = kHeadK; k < maxNe; k += (variant == 't' ? 2 : 1), ++pass) {
     const float* Vs = static_cast<const float*>(pass % 2 == 0 ? w.Va : w.Vb);
@@ -466,10 +476,16 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
       // bytes of the schedule run (SURVEY 8d B_fused): one read + one write of the state for the two
       // stages this pass applies; flops of both stages (bench.py derives the unfused B_ns from them)
       ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt2 * batch * L * m * 4.0, 4.0 * cnt2 * batch * L * (double)mm);
-      // executed: three sources x three tf32 products (3xTF32) per row; triangular skips below
-      ps.exec(2.0 * cnt2 * batch * L * m * 4.0, 9.0 * 2.0 * cnt2 * batch * L * (double)mm * tri_frac, PIPE_TF32);
+      // executed: three sources x three tf32 products (3xTF32) per row, dense; the history kernel
+      // counts what it actually issues (zero blocks of triangular weights skipped, NEXT-3)
+      ps.exec(2.0 * cnt2 * batch * L * m * 4.0, 9.0 * 2.0 * cnt2 * batch * L * (double)mm, PIPE_TF32);
+      g.tri = bank_tri_enabled() ? w.tri : nullptr;
+      g.flop_counter = ps.device_flops();
       rc = launch_bank_hist(g, st);
-      if (rc == CASC_ERR_UNSUPPORTED) rc = launch_mimo_gemm(g, true, st);
+      if (rc == CASC_ERR_UNSUPPORTED) {
+        ps.drop_device_flops();
+        rc = launch_mimo_gemm(g, true, st);
+      }
       if (rc) return rc;
     }
     if (cnt1 > 0) {                                // single stage k for Ne == k + 1 (none with fold)
@@ -484,9 +500,14 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
         g.t_first = 0;
       }
       ProfScope ps(st, K_BANK_STAGE, 2.0 * cnt1 * batch * L * m * 4.0, 2.0 * cnt1 * batch * L * (double)mm);
-      ps.exec(2.0 * cnt1 * batch * L * m * 4.0, 3.0 * 2.0 * cnt1 * batch * L * (double)mm * tri_frac, PIPE_TF32);
+      ps.exec(2.0 * cnt1 * batch * L * m * 4.0, 3.0 * 2.0 * cnt1 * batch * L * (double)mm, PIPE_TF32);
+      g.tri = bank_tri_enabled() ? w.tri : nullptr;
+      g.flop_counter = ps.device_flops();
       rc = launch_bank_hist(g, st);
-      if (rc == CASC_ERR_UNSUPPORTED) rc = launch_mimo_gemm(g, true, st);
+      if (rc == CASC_ERR_UNSUPPORTED) {
+        ps.drop_device_flops();
+        rc = launch_mimo_gemm(g, true, st);
+      }
       if (rc) return rc;
     }
     if ((rc = emit(count_lp_ge(k + 3), count_lp_ge(k + 1)))) return rc;   // channels with Lp in {k + 1, k + 2}

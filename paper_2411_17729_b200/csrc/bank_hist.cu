@@ -93,6 +93,8 @@ struct HistArg {
   int64_t n_pos, gt;                    // positions in all, per CTA
   OutParts op;                          // fused output parts (R24-R26); planes == null: always store v
   float* out;                           // destination state [nseq][L][64]
+  const int* tri;                       // per system: weights lower triangular (NEXT-3), or null
+  unsigned long long* flops;            // issued tensor flops counter (profiling), or null
 };
 
 // One item of the CTA's walk: a compute tile or a history-only (warm-up) tile.
@@ -220,6 +222,8 @@ __global__ void __launch_bounds__(THREADS, 1) bank_hist_kernel(const __grid_cons
     // =========================================================== MMA issuer (whole warp, elected lane)
     const uint32_t idesc = make_idesc(FMT_TF32, HBM, HM), idesc128 = make_idesc(FMT_TF32, HBM, 2 * HM);
     int cur_sys = -1;
+    bool lower = false;                              // this system's weights are lower triangular
+    unsigned long long cols = 0;                     // issued N-columns x K-steps (profiling)
     uint32_t wph = 0;
     int64_t z = 0, tl = 0;
     for (HWalk w(a); w.valid(); w.next(a), ++z) {
@@ -242,6 +246,8 @@ __global__ void __launch_bounds__(THREADS, 1) bank_hist_kernel(const __grid_cons
         mbar_wait_u(&w_full, wph);
         wph ^= 1;
         cur_sys = it.sys;
+        // warp-uniform (broadcast from lane 0): the MMA branch below must not diverge
+        lower = __shfl_sync(0xffffffffu, a.tri ? a.tri[it.sys] : 0, 0) != 0;
       }
       const int acc = (int)(tl % NACC);
       mbar_wait_u(&tempty[acc], (uint32_t)(((tl / NACC) & 1) ^ 1));
@@ -259,7 +265,14 @@ __global__ void __launch_bounds__(THREADS, 1) bank_hist_kernel(const __grid_cons
           for (int kc = 0; kc < 2; ++kc) {
             const uint32_t ah = C::HB + (uint32_t)u * 128 + kc * 64, al = ah + 32;
             const uint64_t wd = make_sdesc(smem_u32(sW + ((c - 1) * 2 + kc) * 2 * WCHUNK), 16, 1024, LAYOUT_SW128);
-            mma_3xtf32_ts_chunk8_w(d, dc, ah, al, wd, idesc128, idesc, first ? 0u : 1u);
+            if (lower) {                              // NEXT-3: skip the all-zero upper blocks
+              if (kc == 0) mma_3xtf32_ts_chunk8_tri_w<0>(d, dc, ah, al, wd, first ? 0u : 1u);
+              else mma_3xtf32_ts_chunk8_tri_w<1>(d, dc, ah, al, wd, first ? 0u : 1u);
+              cols += kc == 0 ? tri_chunk_cols<0>() : tri_chunk_cols<1>();
+            } else {
+              mma_3xtf32_ts_chunk8_w(d, dc, ah, al, wd, idesc128, idesc, first ? 0u : 1u);
+              cols += 4 * (2 * HM + HM);
+            }
             first = false;
           }
         }
@@ -269,6 +282,8 @@ __global__ void __launch_bounds__(THREADS, 1) bank_hist_kernel(const __grid_cons
       mma_commit_w(&tfull[acc]);
       ++tl;
     }
+    // issued flops: each column x K-step of an M = 128, K = 8 MMA is 2 * 128 * 8 flops
+    if (a.flops && lane == 0) atomicAdd(a.flops, cols * (unsigned long long)(2 * HBM * 8));
   } else if (warp >= 6) {
     // =========================================================== split every tile once into its TMEM unit
     const int row = (warp & 3) * 32 + lane;
@@ -427,6 +442,8 @@ int launch_bank_hist(const MimoGemm& g, cudaStream_t st) {
   a.ns = g.n_src; a.S = S; a.nt = nt; a.t_first = g.t_first; a.nt_eff = nt - g.t_first;
   a.L = g.L; a.batch = g.batch; a.sys_list = g.sys_list; a.n_list = g.sys_list ? g.n_list : 1;
   a.op = g.parts;
+  a.tri = g.tri;
+  a.flops = g.flop_counter;
   const int64_t nseq_total = (int64_t)(g.n_sys_total > 0 ? g.n_sys_total : 1) * g.batch;
   if (!map3d(&maps.V, g.R, true, HM, g.L, nseq_total, HBM)) return CASC_ERR_CUDA;
   a.out = static_cast<float*>(g.out);

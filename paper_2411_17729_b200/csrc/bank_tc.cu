@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(256) bank_derived_kernel(const double* p64, in
                                                            const double* C, const double* D, const int* Neff,
                                                            const int* Kc, double* Kr64, float* krT, double* w64,
                                                            float* w32, float* c32, float* d32, float* pvec,
-                                                           int fold, int ms) {
+                                                           int* tri, int fold, int ms) {
   extern __shared__ double dsm[];
   double* Ps = dsm;                         // [ms][ms+1]
   double* Kr = Ps + ms * (ms + 1);          // [ms][129]
@@ -227,6 +227,15 @@ __global__ void __launch_bounds__(256) bank_derived_kernel(const double* p64, in
   const int64_t mm = (int64_t)ms * ms;
   const int kc = Kc[s];
   const double* Ps0 = p64 + (int64_t)s * slots * mm;
+  // NEXT-3: is Abar (slot 0) lower triangular? Then so are all its powers and the pair weights
+  // (every upper entry of a product of lower-triangular matrices is a sum of products with a zero
+  // factor: exactly 0), and the stage kernel skips their zero upper blocks.
+  {
+    int upper = 0;
+    for (int e = tid; e < ms * ms; e += 256) upper |= (e % ms > e / ms) && Ps0[e] != 0.0;
+    upper = __syncthreads_or(upper);
+    if (tid == 0 && tri) tri[s] = upper ? 0 : 1;
+  }
   for (int e = tid; e < ms * 128; e += 256) Kr[(e / 128) * 129 + e % 128] = (e % 128 == 0) ? Bbar[(int64_t)s * ms + e / 128] : 0.0;
   for (int i = 0; i < kc; ++i) {
     __syncthreads();
@@ -319,12 +328,12 @@ __global__ void __launch_bounds__(256) bank_derived_kernel(const double* p64, in
 
 int launch_bank_derived(const double* p64, int slots, const double* Bbar, const double* C, const double* D,
                         const int* Neff, const int* Kc, double* Kr64, float* krT, double* w64, float* w32,
-                        float* c32, float* d32, float* pvec, int fold, int n, int ms, cudaStream_t st) {
+                        float* c32, float* d32, float* pvec, int* tri, int fold, int n, int ms, cudaStream_t st) {
   const size_t smem = (size_t)(ms * (ms + 1) + ms * 129) * sizeof(double);
   if (cudaFuncSetAttribute(bank_derived_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return CASC_ERR_CUDA;
   bank_derived_kernel<<<n, 256, smem, st>>>(p64, slots, Bbar, C, D, Neff, Kc, Kr64, krT, w64, w32, c32, d32, pvec,
-                                            fold, ms);
+                                            tri, fold, ms);
   CASC_LAUNCHED();
   return CASC_OK;
 }

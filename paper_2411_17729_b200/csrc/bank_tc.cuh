@@ -44,6 +44,6 @@ int launch_bank_tail(int m, const BankTailArg& a, cudaStream_t st);
 int launch_bank_ab_tail(const BankAbTailArg& a, cudaStream_t st);
 int launch_bank_derived(const double* p64, int slots, const double* Bbar, const double* C, const double* D,
                         const int* Neff, const int* Kc, double* Kr64, float* krT, double* w64, float* w32,
-                        float* c32, float* d32, float* pvec, int fold, int n, int ms, cudaStream_t st);
+                        float* c32, float* d32, float* pvec, int* tri, int fold, int n, int ms, cudaStream_t st);
 
 }  // namespace casc

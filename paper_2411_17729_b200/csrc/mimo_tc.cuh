@@ -47,6 +47,10 @@ struct MimoGemm {
   // general fused output (R24-R26, common.cuh) for the history-resident stage kernel; parts_deep:
   // some channel of this pass writes more than the two R24 parts (the multi-source GEMM cannot)
   OutParts parts; int parts_deep = 0;
+  // bank stage kernel only (bank_hist.cu): per-system lower-triangular weight flags (the zero upper
+  // blocks are skipped, NEXT-3) and the profiler's issued-flop counter
+  const int* tri = nullptr;
+  unsigned long long* flop_counter = nullptr;
 };
 
 bool mimo_tc_supported(int m, int p, int q);

@@ -14,10 +14,14 @@ struct ProfRec {
   double bytes, flops;
   double xbytes, xflops;   // executed (ProfScope::exec); default = algorithmic
   int pipe;
+  int counter;             // index of a device flop counter (device_flops), -1: none
 };
 struct ProfState {
   bool on = false;
   std::vector<ProfRec> recs;
+  unsigned long long* counters = nullptr;   // device [kCounters]
+  int n_counters = 0;
+  static constexpr int kCounters = 1 << 16;
   std::vector<cudaEvent_t> pool;
   cudaEvent_t get() {
     if (!pool.empty()) {
@@ -34,7 +38,7 @@ static thread_local ProfState g_prof;
 
 ProfScope::ProfScope(cudaStream_t st, int cls, double bytes, double flops) : st_(st), idx_(-1) {
   if (!g_prof.on) return;
-  ProfRec r{g_prof.get(), g_prof.get(), cls, bytes, flops, bytes, flops, PIPE_NONE};
+  ProfRec r{g_prof.get(), g_prof.get(), cls, bytes, flops, bytes, flops, PIPE_NONE, -1};
   cudaEventRecord(r.a, st);
   g_prof.recs.push_back(r);
   idx_ = (int)g_prof.recs.size() - 1;
@@ -45,6 +49,17 @@ void ProfScope::exec(double bytes, double flops, int pipe) {
   r.xbytes = bytes;
   r.xflops = flops;
   r.pipe = pipe;
+}
+// the counters are allocated and zeroed by casc_profile_enable / casc_profile_reset (outside any
+// timed region): a scope only takes the next slot
+unsigned long long* ProfScope::device_flops() {
+  if (idx_ < 0 || !g_prof.counters || g_prof.n_counters >= ProfState::kCounters) return nullptr;
+  const int i = g_prof.n_counters++;
+  g_prof.recs[idx_].counter = i;
+  return g_prof.counters + i;
+}
+void ProfScope::drop_device_flops() {
+  if (idx_ >= 0) g_prof.recs[idx_].counter = -1;
 }
 ProfScope::~ProfScope() {
   if (idx_ >= 0) cudaEventRecord(g_prof.recs[idx_].b, st_);
@@ -60,8 +75,23 @@ static const char* kNames[K_NCLASS] = {"powers_square", "powers_pack", "derived"
 using namespace casc;
 extern "C" {
 
+static int zero_counters() {
+  if (!g_prof.counters &&
+      cudaMalloc(&g_prof.counters, sizeof(unsigned long long) * ProfState::kCounters) != cudaSuccess) {
+    g_prof.counters = nullptr;
+    return CASC_ERR_CUDA;
+  }
+  if (cudaMemset(g_prof.counters, 0, sizeof(unsigned long long) * ProfState::kCounters) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess)
+    return CASC_ERR_CUDA;
+  g_prof.n_counters = 0;
+  return CASC_OK;
+}
+
+// Diagnostics mode (bench.py): enabling allocates and zeroes the device counters once, synchronously.
 int casc_profile_enable(int on) {
   g_prof.on = on != 0;
+  if (g_prof.on && g_prof.n_counters == 0 && !g_prof.counters) return zero_counters();
   return CASC_OK;
 }
 
@@ -71,6 +101,8 @@ int casc_profile_reset(void) {
     g_prof.pool.push_back(r.b);
   }
   g_prof.recs.clear();
+  if (g_prof.counters) return zero_counters();
+  g_prof.n_counters = 0;
   return CASC_OK;
 }
 
@@ -106,7 +138,15 @@ int casc_profile_read_exec(int cls, double* exec_bytes, double* exec_flops, int*
   for (auto& r : g_prof.recs) {
     if (r.cls != cls) continue;
     by += r.xbytes;
-    fl += r.xflops;
+    if (r.counter >= 0) {                   // counted by the kernel itself
+      unsigned long long v = 0;
+      if (cudaEventSynchronize(r.b) != cudaSuccess ||
+          cudaMemcpy(&v, g_prof.counters + r.counter, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return CASC_ERR_CUDA;
+      fl += (double)v;
+    } else {
+      fl += r.xflops;
+    }
     if (r.pipe != PIPE_NONE) pp = r.pipe;
   }
   if (exec_bytes) *exec_bytes = by;

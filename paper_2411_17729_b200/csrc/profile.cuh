@@ -19,6 +19,11 @@ class ProfScope {
   // the EXECUTED work of the schedule run: HBM bytes the kernel must move and the math-pipe flops
   // it issues (3xTF32 = three tf32 products per source; zero blocks skipped are not executed)
   void exec(double bytes, double flops, int pipe);
+  // A zeroed device counter (unsigned long long) the launch adds its ISSUED math-pipe flops to
+  // (the kernel counts the MMAs it issues), or nullptr when profiling is off. When set, it replaces
+  // the host estimate of exec() flops at read time.
+  unsigned long long* device_flops();
+  void drop_device_flops();            // the launch did not use the counter (host estimate stands)
  private:
   cudaStream_t st_;
   int idx_;

@@ -192,6 +192,47 @@ __device__ __forceinline__ void mma_3xtf32_ts_chunk8_w(uint32_t d, uint32_t dc, 
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [l3], w3, %7, 1;\n\t}"
       ::"r"(d), "r"(dc), "r"(ah), "r"(al), "l"(wd), "r"(idesc128), "r"(acc), "r"(idesc64));
 }
+// The same chunk for a LOWER-TRIANGULAR weight W (W[n][k] = 0 for k > n: powers of a lower-
+// triangular Abar, "structured representation"). K-step t of the
+// 64 x 64 product (k in [8t, 8t + 8), t = 4 KC + i) meets only rows n >= 8t of W, so each MMA starts
+// at row n0 = 16 floor(t / 2) (UMMA N granularity 16): the B descriptor moves down n0 rows (n0 * 128
+// B: whole 1024-B SW128 atoms), the accumulator columns move right by n0 and N shrinks by n0
+//   hi.[W hi | W lo]: rows n0 .. 127 of the stacked operand (N = 128 - n0) into d + n0 (the hi.lo
+//                     half keeps all 64 rows: its zero rows are computed, not skipped)
+//   lo.W hi:          rows n0 .. 63 (N = 64 - n0) into dc + n0.
+// The skipped products are exact zeros, so every accumulator column receives the same non-zero
+// terms in the same order as the dense chunk. The first MMA of a tile has t = 0 (n0 = 0) and still
+// initialises all 128 columns. Issued work per chunk: sum_i (192 - 2 n0_i) / (4 * 192) of dense.
+template <int KC>
+__device__ __forceinline__ void mma_3xtf32_ts_chunk8_tri_w(uint32_t d, uint32_t dc, uint32_t ah, uint32_t al,
+                                                           uint64_t wd, uint32_t acc) {
+  constexpr uint32_t n0a = 32 * KC, n0b = 32 * KC + 16;                   // K-steps 0-1 / 2-3
+  constexpr uint32_t i128a = make_idesc(FMT_TF32, 128, 128 - n0a), i64a = make_idesc(FMT_TF32, 128, 64 - n0a);
+  constexpr uint32_t i128b = make_idesc(FMT_TF32, 128, 128 - n0b), i64b = make_idesc(FMT_TF32, 128, 64 - n0b);
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 d0, d1, c0, c1, a1, a2, a3, l1, l2, l3;\n\t.reg .b64 w0, w1, w2, w3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\t"
+      "add.u32 d0, %0, %6;\n\tadd.u32 d1, %0, %7;\n\tadd.u32 c0, %1, %6;\n\tadd.u32 c1, %1, %7;\n\t"
+      "add.u32 a1, %2, 8;\n\tadd.u32 a2, %2, 16;\n\tadd.u32 a3, %2, 24;\n\t"
+      "add.u32 l1, %3, 8;\n\tadd.u32 l2, %3, 16;\n\tadd.u32 l3, %3, 24;\n\t"
+      "add.u64 w0, %4, %8;\n\tadd.u64 w1, %4, %9;\n\tadd.u64 w2, %4, %10;\n\tadd.u64 w3, %4, %11;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [d0], [%2], w0, %12, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [c0], [%3], w0, %13, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [d0], [a1], w1, %12, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [c0], [l1], w1, %13, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], [a2], w2, %14, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [c1], [l2], w2, %15, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [d1], [a3], w3, %14, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [c1], [l3], w3, %15, 1;\n\t}"
+      ::"r"(d), "r"(dc), "r"(ah), "r"(al), "l"(wd), "r"(acc), "n"(n0a), "n"(n0b),
+        "n"(n0a * 8 + 0), "n"(n0a * 8 + 2), "n"(n0b * 8 + 4), "n"(n0b * 8 + 6),
+        "n"(i128a), "n"(i64a), "n"(i128b), "n"(i64b));
+}
+// MMA work of one triangular chunk relative to the dense chunk8 (in units of N-columns x K-steps)
+template <int KC>
+__host__ __device__ constexpr uint32_t tri_chunk_cols() {
+  return 2 * ((128 - 32 * KC) + (64 - 32 * KC)) + 2 * ((128 - 32 * KC - 16) + (64 - 32 * KC - 16));
+}
 __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
   asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
                "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"

@@ -116,3 +116,26 @@ def test_fold_matches_single_stage_pass():
     _check(wl, y_fold)
     y_single = _gpu_y(wl, {"CASC_BANK_FOLD": "0"})
     assert rel(y_fold, y_single) < 2e-6
+
+
+# ------------------------------------------------------------------ NEXT-3: triangular skip
+def test_triangular_skip_bitwise_equal_dense():
+    """HiPPO Abar is lower triangular, so are its powers and the pair weights
+    Q_k = P_{k+1} P_k; the stage kernel skips the all-zero upper blocks of every K step
+    (SURVEY NEXT-3). The skipped products are exact zeros: y must be bitwise the
+    dense kernel's (CASC_BANK_TRI=0), for pairs, single stages (fold off) and the exponential
+    scheme's triangular Abar, and within 1e-5 of the oracle."""
+    for wl, env in ((_bank(8, 128 * 48, 2, ORDERS), {}),
+                    (_bank(6, 128 * 48 - 37, 2, [8, 9, 10, 11, 12, 13]), {"CASC_BANK_FOLD": "0"})):
+        y_tri = _gpu_y(wl, env or None)
+        y_dense = _gpu_y(wl, {**env, "CASC_BANK_TRI": "0"})
+        assert np.array_equal(y_tri, y_dense)
+        _check(wl, y_tri)
+
+
+def test_triangular_flag_off_for_dense_abar():
+    """A bank whose Abar has entries above the diagonal must run the dense MMAs: one channel with a
+    single non-zero upper entry among HiPPO channels; parity with the oracle catches a skipped block."""
+    wl = _bank(4, 128 * 32, 2, [9, 10, 11, 12])
+    wl.Abar[2][3, 40] = 1e-3                         # breaks the structure of channel 2 only
+    _check(wl, _gpu_y(wl))
