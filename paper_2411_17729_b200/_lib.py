@@ -5,7 +5,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcascade_b200.so")
+LIB_PATH = _DEFAULT = os.path.join(_HERE, "libcascade_b200.so")
 # diagnostics only: A/B two builds of the library within one process launch environment
 if os.environ.get("CASC_LIB_OVERRIDE"):
     LIB_PATH = os.path.abspath(os.environ["CASC_LIB_OVERRIDE"])
@@ -70,6 +70,8 @@ def lib() -> ctypes.CDLL:
                 "(the cascade has no CPU fallback)")
         l = ctypes.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
+            if LIB_PATH != _DEFAULT and not hasattr(l, name):
+                continue                     # A/B against an older build: only what it exports
             f = getattr(l, name)
             f.restype = res
             f.argtypes = args

@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(THREADS, 1) bank_hist_kernel(const __grid_cons
     const uint32_t idesc = make_idesc(FMT_TF32, HBM, HM), idesc128 = make_idesc(FMT_TF32, HBM, 2 * HM);
     int cur_sys = -1;
     bool lower = false;                              // this system's weights are lower triangular
-    unsigned long long cols = 0;                     // issued N-columns x K-steps (profiling)
+    unsigned n_tri = 0, n_dense = 0;                 // sources issued with / without the triangular skip
     uint32_t wph = 0;
     int64_t z = 0, tl = 0;
     for (HWalk w(a); w.valid(); w.next(a), ++z) {
@@ -253,37 +254,47 @@ __global__ void __launch_bounds__(THREADS, 1) bank_hist_kernel(const __grid_cons
       mbar_wait_u(&tempty[acc], (uint32_t)(((tl / NACC) & 1) ^ 1));
       tc_fence_after();
       const uint32_t d = acc * 128, dc = d + HM;
-      bool first = true;
+      // the tile's MMAs, instantiated once per weight structure so neither path carries the other's
+      // branches (the issuing warp's instruction stream bounds this kernel)
+      auto issue = [&](auto tri_tag) {
+        constexpr bool TRI = decltype(tri_tag)::value;
+        bool first = true;
 #pragma unroll
-      for (int c = NS; c >= 1; --c) {                 // oldest source first: its unit is freed early
-        const int64_t y = z - c;                      // the source item
-        if (it.t >= c * S) {
-          const int u = (int)(y % NH);
-          mbar_wait_u(&hist_ready[u], (uint32_t)((y / NH) & 1));
-          tc_fence_after();
+        for (int c = NS; c >= 1; --c) {               // oldest source first: its unit is freed early
+          const int64_t y = z - c;                    // the source item
+          if (it.t >= c * S) {
+            const int u = (int)(y % NH);
+            mbar_wait_u(&hist_ready[u], (uint32_t)((y / NH) & 1));
+            tc_fence_after();
 #pragma unroll
-          for (int kc = 0; kc < 2; ++kc) {
-            const uint32_t ah = C::HB + (uint32_t)u * 128 + kc * 64, al = ah + 32;
-            const uint64_t wd = make_sdesc(smem_u32(sW + ((c - 1) * 2 + kc) * 2 * WCHUNK), 16, 1024, LAYOUT_SW128);
-            if (lower) {                              // NEXT-3: skip the all-zero upper blocks
-              if (kc == 0) mma_3xtf32_ts_chunk8_tri_w<0>(d, dc, ah, al, wd, first ? 0u : 1u);
-              else mma_3xtf32_ts_chunk8_tri_w<1>(d, dc, ah, al, wd, first ? 0u : 1u);
-              cols += kc == 0 ? tri_chunk_cols<0>() : tri_chunk_cols<1>();
-            } else {
-              mma_3xtf32_ts_chunk8_w(d, dc, ah, al, wd, idesc128, idesc, first ? 0u : 1u);
-              cols += 4 * (2 * HM + HM);
+            for (int kc = 0; kc < 2; ++kc) {
+              const uint32_t ah = C::HB + (uint32_t)u * 128 + kc * 64, al = ah + 32;
+              const uint64_t wd = make_sdesc(smem_u32(sW + ((c - 1) * 2 + kc) * 2 * WCHUNK), 16, 1024, LAYOUT_SW128);
+              if constexpr (TRI) {                    // NEXT-3: skip the all-zero upper blocks
+                if (kc == 0) mma_3xtf32_ts_chunk8_tri_w<0>(d, dc, ah, al, wd, first ? 0u : 1u);
+                else mma_3xtf32_ts_chunk8_tri_w<1>(d, dc, ah, al, wd, first ? 0u : 1u);
+              } else {
+                mma_3xtf32_ts_chunk8_w(d, dc, ah, al, wd, idesc128, idesc, first ? 0u : 1u);
+              }
+              first = false;
             }
-            first = false;
+            if constexpr (TRI) ++n_tri; else ++n_dense;
           }
+          // the unit of item z - NS is read last by these (source c = NS) MMAs
+          if (c == NS) release(it.t >= NS * S);
         }
-        // the unit of item z - NS is read last by these (source c = NS) MMAs
-        if (c == NS) release(it.t >= NS * S);
-      }
+      };
+      if (lower) issue(std::true_type{});
+      else issue(std::false_type{});
       mma_commit_w(&tfull[acc]);
       ++tl;
     }
-    // issued flops: each column x K-step of an M = 128, K = 8 MMA is 2 * 128 * 8 flops
-    if (a.flops && lane == 0) atomicAdd(a.flops, cols * (unsigned long long)(2 * HBM * 8));
+    // issued flops (profiling): N-columns x K-steps per source, each worth 2 * 128 * 8 flops (M = 128, K = 8)
+    if (a.flops && lane == 0) {
+      const unsigned long long cols = (unsigned long long)n_tri * (tri_chunk_cols<0>() + tri_chunk_cols<1>()) +
+                                      (unsigned long long)n_dense * 2 * 4 * (2 * HM + HM);
+      atomicAdd(a.flops, cols * (unsigned long long)(2 * HBM * 8));
+    }
   } else if (warp >= 6) {
     // =========================================================== split every tile once into its TMEM unit
     const int row = (warp & 3) * 32 + lane;
