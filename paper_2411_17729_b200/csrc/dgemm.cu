@@ -64,10 +64,72 @@ __global__ void __launch_bounds__(256) dgemm_batched_kernel(DgemmArg a) {
   }
 }
 
+// The same batched GEMM on the fp64 tensor path (mma.sync m8n8k4 f64, DMMA): 64 x 64 output tile
+// per 256-thread CTA, warp w owns rows 8w..8w+7 (eight 8 x 8 column tiles), K in chunks of 32 staged
+// through shared memory (zero-filled past M, N, K). Per element a float64 dot product of the same
+// terms as dgemm_batched_kernel in another summation order (both are float64 FMA chains). The
+// MIMO squarings (m = 256: E3, m = 1024: E4, 11 squarings of 2 m^3 flops per step) run here.
+__global__ void __launch_bounds__(256) dgemm_mma_kernel(DgemmArg a) {
+  const int s = blockIdx.z;
+  if (a.skip_below && a.skip_below[s] < a.level) return;
+  const int64_t selA = a.selA ? a.selA[s] : 0, selB = a.selB ? a.selB[s] : 0;
+  const double* A = a.A + s * a.sA + selA * a.nA;
+  const double* B = a.B + s * a.sB + selB * a.nB;
+  double* C = a.C + s * a.sC;
+  const double* Cadd = a.Cadd ? a.Cadd + s * a.sCadd : nullptr;
+  constexpr int LA = 36, LB = 72;                        // padded strides (doubles)
+  __shared__ double As[64 * LA];                         // [row][k]
+  __shared__ double Bs[32 * LB];                         // [k][col]
+  const int tid = threadIdx.x, w = tid / 32, lane = tid % 32, g = lane >> 2, t4 = lane & 3;
+  const int row0 = blockIdx.y * 64, col0 = blockIdx.x * 64;
+  double d[8][2];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) d[n][0] = d[n][1] = 0.0;
+  for (int k0 = 0; k0 < a.K; k0 += 32) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = tid + i * 256;
+      const int r = e / 32, kk = e % 32;                 // A chunk 64 x 32 (k fastest: coalesced rows)
+      const int gr = row0 + r, gk = k0 + kk;
+      As[r * LA + kk] = (gr < a.M && gk < a.K) ? A[(int64_t)gr * a.lda + gk] : 0.0;
+      const int kb = e / 64, c = e % 64;                 // B chunk 32 x 64
+      const int gkb = k0 + kb, gc = col0 + c;
+      Bs[kb * LB + c] = (gkb < a.K && gc < a.N) ? B[(int64_t)gkb * a.ldb + gc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const double av = As[(8 * w + g) * LA + 4 * ks + t4];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        const double bv = Bs[(4 * ks + t4) * LB + 8 * n + g];
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                     : "+d"(d[n][0]), "+d"(d[n][1]) : "d"(av), "d"(bv));
+      }
+    }
+    __syncthreads();
+  }
+  const int gr = row0 + 8 * w + g;
+  if (gr >= a.M) return;
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int gc = col0 + 8 * n + 2 * t4 + h;
+      if (gc >= a.N) continue;
+      double v = d[n][h];
+      if (Cadd) v += Cadd[(int64_t)gr * a.ldc + gc];
+      C[(int64_t)gr * a.ldc + gc] = v;
+    }
+  }
+}
+
 int launch_dgemm(const DgemmArg& a, int n_sys, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0 || n_sys <= 0) return CASC_OK;
   dim3 grid((unsigned)ceil_div(a.N, 64), (unsigned)ceil_div(a.M, 64), (unsigned)n_sys);
-  dgemm_batched_kernel<<<grid, 256, 0, st>>>(a);
+  // the tensor path for full-width products; thin ones (a row vector times a matrix) on FMA
+  if (a.M >= 32 && a.N >= 32) dgemm_mma_kernel<<<grid, 256, 0, st>>>(a);
+  else dgemm_batched_kernel<<<grid, 256, 0, st>>>(a);
   CASC_LAUNCHED();
   return CASC_OK;
 }

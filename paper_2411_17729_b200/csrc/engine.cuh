@@ -41,14 +41,15 @@ int engine_mimo_tc(int m, int p, int q, int64_t L, int batch, int N, int N_max, 
 // MIMO workspace (mimo_engine.cu): derived float64 weights, their operand-format images, and the
 // two state buffers of batch * L rows of m (ping-pong)
 struct MimoWs {
-  double *AB64, *CP64, *CBD64, *CAB64;
-  void *Bb, *AB, *C, *CP, *D, *CBD, *CAB;   // operand-format weights (bf16, or tf32 hi/lo planes)
+  double *AB64, *CP64, *CBD64, *CAB64, *A2B64, *A3B64;
+  void *Bb, *AB, *C, *CP, *D, *CBD, *CAB, *A2B, *A3B;   // operand-format weights (bf16, or tf32 hi/lo planes)
   void *Va, *Vb;
   size_t bytes;
 };
 MimoWs carve_mimo(void* ws, int m, int p, int q, int64_t L, int batch, int mode);
 // derived weights of the fused first / last steps (R21): Abar Bbar, C P_Ne, C Bbar + D,
-// C Abar Bbar, in float64 and rounded once to the GEMM operand format
+// C Abar Bbar, and for Ne >= 2 the Krylov head's Abar^2 Bbar, Abar^3 Bbar (R28), in float64 and
+// rounded once to the GEMM operand format
 int mimo_derive(int m, int p, int q, int Ne, const PackLayout& P, const double* Bbar, const double* C,
                 const double* D, const MimoWs& w, bool tf32, cudaStream_t st);
 int engine_powers(int n, int m, const int* N_host, int N_max, const double* Abar, int mode,

@@ -48,6 +48,8 @@ MimoWs carve_mimo(void* ws, int m, int p, int q, int64_t L, int batch, int mode)
   w.CP64 = c.take<double>((size_t)q * m);
   w.CBD64 = c.take<double>((size_t)q * p);
   w.CAB64 = c.take<double>((size_t)q * p);
+  w.A2B64 = c.take<double>((size_t)m * p);
+  w.A3B64 = c.take<double>((size_t)m * p);
   w.Bb = c.take<char>((size_t)m * p * wes);
   w.AB = c.take<char>((size_t)m * p * wes);
   w.C = c.take<char>((size_t)q * m * wes);
@@ -55,6 +57,8 @@ MimoWs carve_mimo(void* ws, int m, int p, int q, int64_t L, int batch, int mode)
   w.D = c.take<char>((size_t)q * p * wes);
   w.CBD = c.take<char>((size_t)q * p * wes);
   w.CAB = c.take<char>((size_t)q * p * wes);
+  w.A2B = c.take<char>((size_t)m * p * wes);
+  w.A3B = c.take<char>((size_t)m * p * wes);
   const size_t vbytes = (size_t)batch * (size_t)L * m * ses;
   w.Va = c.take<char>(vbytes);
   w.Vb = c.take<char>(vbytes);
@@ -99,16 +103,26 @@ int engine_mimo_tc(int m, int p, int q, int64_t L, int batch, int N, int N_max, 
     ps.exec(rows * (p + q) * es, rows * 4.0 * q * p * xf, pipe);
     return launch_mimo_gemm(g, tf32, st);
   }
+  // a2 + a3: the Krylov head (R28) -- v^(2)_l = sum_{j<4} (Abar^j Bbar) u_{l-j}, the expanded product
+  // of Bbar u and the factors k = 0, 1 of Eq. 5, one 4-source GEMM with K = 4p instead
+  // of the first step (K = 2p) and stage 1 (K = m); with Ne = 1 the fused first step alone
+  const int k0 = Ne >= 2 ? 2 : 1;                // first streaming stage
   {
     MimoGemm g{};
     g.src[0] = {u, w.Bb, p, 0};
     g.src[1] = {u, w.AB, p, 1};
-    g.n_src = 2; g.out = w.Va; g.n_out = m; g.L = L; g.batch = batch;
-    ProfScope ps(st, K_MIMO_FIRST, rows * (p + m) * es, rows * 4.0 * m * p);
-    ps.exec(rows * (p + m) * es, rows * 4.0 * m * p * xf, pipe);
+    g.n_src = 2;
+    if (k0 == 2) {
+      g.src[2] = {u, w.A2B, p, 2};
+      g.src[3] = {u, w.A3B, p, 3};
+      g.n_src = 4;
+    }
+    g.out = k0 == 2 ? w.Vb : w.Va; g.n_out = m; g.L = L; g.batch = batch;
+    ProfScope ps(st, K_MIMO_FIRST, rows * (p + m) * es, rows * 2.0 * g.n_src * m * p);
+    ps.exec(rows * (p + m) * es, rows * 2.0 * g.n_src * m * p * xf, pipe);
     if ((rc = launch_mimo_gemm(g, tf32, st))) return rc;
   }
-  for (int k = 1; k <= Ne - 1; ++k) {
+  for (int k = k0; k <= Ne - 1; ++k) {
     void* Vs = (k - 1) % 2 == 0 ? w.Va : w.Vb;
     void* Vd = (k % 2 == 0) ? w.Va : w.Vb;
     // stage weight P_k: bf16 [m][m] or the tf32 pair [2][m][m] of the pack
@@ -166,6 +180,18 @@ int mimo_derive(int m, int p, int q, int Ne, const PackLayout& P, const double* 
     if ((rc = convert_weight(w.CBD64, w.CBD, (int64_t)q * p, tf32, st))) return rc;
     if ((rc = convert_weight(w.CAB64, w.CAB, (int64_t)q * p, tf32, st))) return rc;
     if (D && (rc = convert_weight(D, w.D, (int64_t)q * p, tf32, st))) return rc;
+    if (Ne >= 2) {                                                 // Krylov head (R28)
+      a = DgemmArg{};                                              // Abar^2 Bbar = P_1 Bbar
+      a.M = m; a.N = p; a.K = m;
+      a.A = P.p64 + mm; a.lda = m; a.B = Bbar; a.ldb = p; a.C = w.A2B64; a.ldc = p;
+      if ((rc = launch_dgemm(a, 1, st))) return rc;
+      a = DgemmArg{};                                              // Abar^3 Bbar = P_1 (Abar Bbar)
+      a.M = m; a.N = p; a.K = m;
+      a.A = P.p64 + mm; a.lda = m; a.B = w.AB64; a.ldb = p; a.C = w.A3B64; a.ldc = p;
+      if ((rc = launch_dgemm(a, 1, st))) return rc;
+      if ((rc = convert_weight(w.A2B64, w.A2B, (int64_t)m * p, tf32, st))) return rc;
+      if ((rc = convert_weight(w.A3B64, w.A3B, (int64_t)m * p, tf32, st))) return rc;
+    }
   }
   return CASC_OK;
 }

@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
       int64_t t_local = 0, j = 0;                 // tiles / chunks consumed by this CTA
       int nch_tile = 0;                           // K chunks per tile, all sources in order
 #pragma unroll
-      for (int q = 0; q < 3; ++q) if (q < a.n_src) nch_tile += a.K[q] / BK;
+      for (int q = 0; q < kMaxSrc; ++q) if (q < a.n_src) nch_tile += a.K[q] / BK;
       for (Walk w(n_tiles, a.gt); w.valid(); w.next(), ++t_local) {
         const TileCoord tc = decode(w.tile(), a, n_nblk, nt_eff);
         const int acc = (int)(t_local & 1);

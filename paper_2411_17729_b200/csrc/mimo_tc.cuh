@@ -6,18 +6,19 @@
 
 namespace casc {
 
+constexpr int kMaxSrc = 4;        // sources of one shifted GEMM (the MIMO head uses four lags)
 struct MimoMaps {                 // passed as one __grid_constant__ kernel parameter
-  CUtensorMap A[3];               // source signals [seq][L][K_src]    box {128 B, 128, 1}
-  CUtensorMap W[3];               // weight planes [plane][n_out][K]   box {128 B, BN, 1}
+  CUtensorMap A[kMaxSrc];         // source signals [seq][L][K_src]    box {128 B, 128, 1}
+  CUtensorMap W[kMaxSrc];         // weight planes [plane][n_out][K]   box {128 B, BN, 1}
   CUtensorMap R;                  // residual [seq][L][n_out]          box {128 B, 128, 1}
   CUtensorMap out;                // output   [seq][L][n_out]          box {128 B, 128, 1}
 };
 struct MimoArg {
-  int n_src; int K[3]; int64_t shift[3]; int w_plane_off[3]; int w_plane_stride[3];
+  int n_src; int K[kMaxSrc]; int64_t shift[kMaxSrc]; int w_plane_off[kMaxSrc]; int w_plane_stride[kMaxSrc];
   int64_t L; int batch; int n_out; int has_residual;
   const int* sys_list; int n_list;   // systems processed (bank channels); null: one system
   int t_first;                       // first 128-step time tile processed in each sequence
-  int a_row0[3], r_row0, out_row0;   // rows in front of local row 0 (sequence-shard halo)
+  int a_row0[kMaxSrc], r_row0, out_row0;   // rows in front of local row 0 (sequence-shard halo)
   // Bank output fusion (fp32 n_out = 64): for systems with ab_neff[sys] == ab_level this stage
   // is their last streaming stage; instead of storing v^(Ne) the epilogue writes
   // ab planes (c . v_l, w . v_l) with c = C, w = C P_Ne (R24)
@@ -34,7 +35,7 @@ struct MimoSrc {
   int64_t row0 = 0;                  // halo rows stored in front of local row 0 of A
 };
 struct MimoGemm {
-  MimoSrc src[3]; int n_src;
+  MimoSrc src[kMaxSrc]; int n_src;
   const void* R; void* out; int n_out;
   int64_t L; int batch;
   const int* sys_list = nullptr; int n_list = 1; int n_sys_total = 1;

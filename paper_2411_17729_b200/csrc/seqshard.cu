@@ -178,7 +178,7 @@ static int exchange(Comm* c, const void* sbuf, size_t sbytes, void* rbuf, size_t
 // ------------------------------------------------------------------------------ workspace
 struct SeqWs {
   MimoWs mw;           // derived weights (no state buffers: L = 0)
-  void* u_edge;        // [batch + B1][p]: u halo row (batch rows) + the first B1 local rows of u
+  void* u_edge;        // [(uh + Bu) batch][p]: the u halo (uh time rows) + the first Bu local rows of u
   void *Va, *Vb;       // [(H + L_loc) * batch][m]
   size_t bytes;
 };
@@ -189,6 +189,10 @@ static int64_t boundary_rows(int64_t s, int batch, int64_t rows) {
   return std::min(rows, ceil_div(s * batch, kRowBlock) * kRowBlock);
 }
 
+// time rows of u the first step reads before l: 3 for the Krylov head (Ne >= 2, lags 0..3, R28),
+// else 1 (the fused first step, or y directly when Ne = 0)
+static int u_halo_rows(int Ne) { return Ne >= 2 ? 3 : 1; }
+
 static SeqWs carve_seq(void* ws, int m, int p, int q, int64_t L_loc, int batch, int Ne, int mode) {
   SeqWs w{};
   w.mw = carve_mimo(ws, m, p, q, 0, 0, mode);
@@ -196,8 +200,9 @@ static SeqWs carve_seq(void* ws, int m, int p, int q, int64_t L_loc, int batch, 
   c.off = w.mw.bytes;
   const size_t es = mode == CASC_FP32 ? 4 : 2;
   const int64_t rows = L_loc * batch, H = Ne > 0 ? ((int64_t)1 << Ne) : 0;
-  const int64_t B1 = boundary_rows(1, batch, rows);
-  w.u_edge = c.take<char>((size_t)(batch + B1) * p * es);
+  const int uh = u_halo_rows(Ne);
+  const int64_t Bu = boundary_rows(uh, batch, rows);
+  w.u_edge = c.take<char>((size_t)(uh * batch + Bu) * p * es);
   w.Va = c.take<char>((size_t)(H * batch + rows) * m * es);
   w.Vb = c.take<char>((size_t)(H * batch + rows) * m * es);
   w.bytes = c.bytes();
@@ -298,7 +303,8 @@ int casc_apply_seqsharded(void* comm, int m, int p, int q, int64_t L_loc, int ba
   const int64_t L = L_loc * c->world;
   const int Ne = eff_order(N, L);
   // each halo must come from the immediate predecessor (holds for configs[3] up to 8 ranks)
-  if (c->world > 1 && Ne > 0 && ((int64_t)1 << Ne) > L_loc) return CASC_ERR_UNSUPPORTED;
+  const int uh = u_halo_rows(Ne);
+  if (c->world > 1 && ((Ne > 0 && ((int64_t)1 << Ne) > L_loc) || uh > L_loc)) return CASC_ERR_UNSUPPORTED;
   SeqWs w = carve_seq(ws, m, p, q, L_loc, batch, Ne, mode);
   if (ws_bytes < w.bytes) return CASC_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)compute_stream, cs = (cudaStream_t)comm_stream;
@@ -326,18 +332,18 @@ int casc_apply_seqsharded(void* comm, int m, int p, int q, int64_t L_loc, int ba
     CASC_TRY(cudaMemsetAsync(w.Va, 0, (size_t)Hr * m * es, st));
     CASC_TRY(cudaMemsetAsync(w.Vb, 0, (size_t)Hr * m * es, st));
   }
-  CASC_TRY(cudaMemsetAsync(w.u_edge, 0, (size_t)batch * p * es, st));
-  const int64_t B1 = boundary_rows(1, batch, rows);
-  CASC_TRY(cudaMemcpyAsync((char*)w.u_edge + (size_t)batch * p * es, u_loc, (size_t)B1 * p * es,
-                           cudaMemcpyDeviceToDevice, st));
+  const size_t uhb = (size_t)uh * batch * p * es;     // bytes of the u halo
+  CASC_TRY(cudaMemsetAsync(w.u_edge, 0, uhb, st));
+  const int64_t Bu = boundary_rows(uh, batch, rows);
+  CASC_TRY(cudaMemcpyAsync((char*)w.u_edge + uhb, u_loc, (size_t)Bu * p * es, cudaMemcpyDeviceToDevice, st));
   CASC_TRY(cudaEventRecord(ev_in, st));
 
-  // ---- u halo: the last time row of rank r-1's u (one row of batch * p)
+  // ---- u halo: the last uh time rows of rank r-1's u (one contiguous block of uh * batch * p)
   {
     CASC_TRY(cudaStreamWaitEvent(cs, ev_in, 0));      // before the scope: it times the transfer only
-    ProfScope ps(cs, K_SEQ_HALO, 2.0 * batch * p * es, 0.0);
-    if ((rc = exchange(c, (const char*)u_loc + (size_t)(rows - batch) * p * es, (size_t)batch * p * es, w.u_edge,
-                       (size_t)batch * p * es, nullptr, cs, ev_halo)))
+    ProfScope ps(cs, K_SEQ_HALO, 2.0 * uhb, 0.0);
+    if ((rc = exchange(c, (const char*)u_loc + (size_t)(rows - (int64_t)uh * batch) * p * es, uhb, w.u_edge, uhb,
+                       nullptr, cs, ev_halo)))
       return rc;
   }
   const double dr = (double)rows;
@@ -366,23 +372,27 @@ int casc_apply_seqsharded(void* comm, int m, int p, int q, int64_t L_loc, int ba
     gb = g;
     gb.src[0] = {w.u_edge, w.mw.CBD, p, 0};
     gb.src[1] = {w.u_edge, w.mw.CAB, p, batch};
-    gb.src[0].row0 = gb.src[1].row0 = batch;
+    gb.src[0].row0 = gb.src[1].row0 = uh * batch;
     return two_launches(g, gb, 1, K_MIMO_LAST, dr * (p + q) * es, dr * 4.0 * q * p);
   }
-  // ---- first: v^(1) = Bbar u_l + Abar Bbar u_{l-1} -> Va (local rows behind the halo)
+  // ---- first step: the Krylov head v^(2) = sum_{j<4} (Abar^j Bbar) u_{l-j} -> Vb for Ne >= 2 (R28),
+  // else v^(1) = Bbar u_l + Abar Bbar u_{l-1} -> Va (local rows behind the halo)
+  const int k0 = Ne >= 2 ? 2 : 1;
   {
+    const void* Wj[4] = {w.mw.Bb, w.mw.AB, w.mw.A2B, w.mw.A3B};
     MimoGemm g{};
-    g.src[0] = {u_loc, w.mw.Bb, p, 0};
-    g.src[1] = {u_loc, w.mw.AB, p, batch};
-    g.n_src = 2; g.out = w.Va; g.out_row0 = Hr; g.n_out = m;
+    g.n_src = Ne >= 2 ? 4 : 2;
+    for (int j = 0; j < g.n_src; ++j) g.src[j] = {u_loc, Wj[j], p, (int64_t)j * batch};
+    g.out = k0 == 2 ? w.Vb : w.Va; g.out_row0 = Hr; g.n_out = m;
     MimoGemm gb = g;
-    gb.src[0] = {w.u_edge, w.mw.Bb, p, 0};
-    gb.src[1] = {w.u_edge, w.mw.AB, p, batch};
-    gb.src[0].row0 = gb.src[1].row0 = batch;
-    if ((rc = two_launches(g, gb, 1, K_MIMO_FIRST, dr * (p + m) * es, dr * 4.0 * m * p))) return rc;
+    for (int j = 0; j < g.n_src; ++j) {
+      gb.src[j] = {w.u_edge, Wj[j], p, (int64_t)j * batch};
+      gb.src[j].row0 = uh * batch;
+    }
+    if ((rc = two_launches(g, gb, uh, K_MIMO_FIRST, dr * (p + m) * es, dr * 2.0 * g.n_src * m * p))) return rc;
   }
-  // ---- stages k = 1 .. Ne-1 and the last step: halo of 2^k rows of v^(k) before each
-  for (int k = 1; k <= Ne; ++k) {
+  // ---- stages k = k0 .. Ne-1 and the last step: halo of 2^k rows of v^(k) before each
+  for (int k = k0; k <= Ne; ++k) {
     void* Vs = (k - 1) % 2 == 0 ? w.Va : w.Vb;       // holds v^(k)
     void* Vd = (k % 2 == 0) ? w.Va : w.Vb;
     const int64_t d = ((int64_t)1 << k) * batch;     // halo rows of this step

@@ -1,9 +1,11 @@
 """Test-side model of the library's sequence-sharded schedule (csrc/seqshard.cu), in float64 torch.
 
 It reproduces the schedule the CUDA path runs -- time-major buffers [H + L_loc][batch][dim] with
-the halo rows in front, the one-row u halo before the fused first step, a halo of the last 2^k
-time rows of v^(k) before stage k, 2^Ne rows before the fused last step (R21), rank 0's
-halo zero (x_{-1} = 0) -- with the per-step arithmetic written out in float64, so
+the halo rows in front, a u halo of uh time rows before the first step (uh = 3 for the Krylov head
+v^(2) = sum_{j<4} Abar^j Bbar u_{l-j} when Ne >= 2, R28; uh = 1 for the fused first step),
+a halo of the last 2^k time rows of v^(k) before stage k, 2^Ne rows before the fused last step
+(R21), rank 0's halo zero (x_{-1} = 0) -- with the per-step arithmetic written out in
+float64, so
 the exchange bookkeeping can be checked on the CPU against the oracle: with the real
 torch.distributed exchange (gloo, world_size 2, DistComm) and with emulated ranks (LocalComm).
 Every halo is one contiguous block of the time-major buffer, as in the library.
@@ -24,7 +26,7 @@ def effective_order(N: int, L: int) -> int:
 
 @dataclass
 class Shard:
-    """One rank's buffers: u_ext [1 + L_loc][batch][p] (row 0 = u_{-1} of this shard),
+    """One rank's buffers: u_ext [uh + L_loc][batch][p] (rows 0..uh-1 = u_{-uh..-1} of this shard),
     Va/Vb [H + L_loc][batch][m] (rows [H - d, H) = the halo of a step with shift d), y [L_loc][batch][q]."""
     u_ext: torch.Tensor
     Va: torch.Tensor
@@ -32,12 +34,16 @@ class Shard:
     y: torch.Tensor
 
 
-def make_shard(u_loc: torch.Tensor, m: int, q: int, H: int) -> Shard:
+def u_halo_rows(Ne: int) -> int:
+    return 3 if Ne >= 2 else 1
+
+
+def make_shard(u_loc: torch.Tensor, m: int, q: int, H: int, uh: int = 1) -> Shard:
     """u_loc: [L_loc][batch][p]. Halo rows start at zero (rank 0 keeps them)."""
     L_loc, batch, p = u_loc.shape
     dt = u_loc.dtype
-    u_ext = torch.zeros((1 + L_loc, batch, p), dtype=dt)
-    u_ext[1:] = u_loc
+    u_ext = torch.zeros((uh + L_loc, batch, p), dtype=dt)
+    u_ext[uh:] = u_loc
     Va = torch.zeros((H + L_loc, batch, m), dtype=dt)
     return Shard(u_ext, Va, torch.zeros_like(Va), torch.empty((L_loc, batch, q), dtype=dt))
 
@@ -81,12 +87,18 @@ class F64Steps:
         Ab, Bb, Cm = t(Abar), t(Bbar), t(C)
         Dm = torch.zeros((C.shape[0], Bbar.shape[1]), dtype=torch.float64) if D is None else t(D)
         self.Bb, self.AB = Bb, Ab @ Bb
+        self.Kr = [Bb, self.AB, Ab @ self.AB, Ab @ (Ab @ self.AB)]     # Abar^j Bbar, j < 4 (head)
         self.C, self.CP, self.D = Cm, Cm @ self.P[Ne], Dm
         self.CBD, self.CAB = Cm @ Bb + Dm, Cm @ (Ab @ Bb)
 
     def first(self, sh, H):
-        u = sh.u_ext
+        u = sh.u_ext                                  # uh = 1
         sh.Va[H:] = u[1:] @ self.Bb.T + u[:-1] @ self.AB.T
+
+    def head(self, sh, H):
+        u = sh.u_ext                                  # uh = 3: v^(2) into Vb
+        L = sh.y.shape[0]
+        sh.Vb[H:] = sum(u[3 - j:3 - j + L] @ self.Kr[j].T for j in range(4))
 
     def stage(self, k, sh, src, dst, H):
         L = sh.y.shape[0]
@@ -95,12 +107,13 @@ class F64Steps:
 
     def last(self, Ne, sh, V, H):
         u = sh.u_ext
+        uh = u.shape[0] - sh.y.shape[0]
         if Ne == 0:
-            sh.y[:] = u[1:] @ self.CBD.T + u[:-1] @ self.CAB.T
+            sh.y[:] = u[uh:] @ self.CBD.T + u[uh - 1:-1] @ self.CAB.T
             return
         L = sh.y.shape[0]
         s = 1 << Ne
-        sh.y[:] = V[H:] @ self.C.T + V[H - s:H - s + L] @ self.CP.T + u[1:] @ self.D.T
+        sh.y[:] = V[H:] @ self.C.T + V[H - s:H - s + L] @ self.CP.T + u[uh:] @ self.D.T
 
 
 def run(steps, comm, shards, N: int, L_global: int) -> None:
@@ -110,16 +123,21 @@ def run(steps, comm, shards, N: int, L_global: int) -> None:
     L_loc = shards[0].y.shape[0]
     if Ne > 0 and (1 << Ne) > L_loc:
         raise NotImplementedError(f"halo 2^{Ne} exceeds the shard length {L_loc}")
-    comm.exchange([s.u_ext for s in shards], 1, 1)             # u_{-1} for the first step
+    uh = u_halo_rows(Ne)
+    comm.exchange([s.u_ext for s in shards], uh, uh)           # u_{-uh..-1} for the first step
     if Ne == 0:
         for s in shards:
             steps.last(0, s, None, H)
         return
-    for s in shards:
-        steps.first(s, H)
-    src = [s.Va for s in shards]
-    dst = [s.Vb for s in shards]
-    for k in range(1, Ne):
+    if Ne >= 2:                                               # Krylov head: v^(2) in Vb
+        for s in shards:
+            steps.head(s, H)
+        src, dst, k0 = [s.Vb for s in shards], [s.Va for s in shards], 2
+    else:
+        for s in shards:
+            steps.first(s, H)
+        src, dst, k0 = [s.Va for s in shards], [s.Vb for s in shards], 1
+    for k in range(k0, Ne):
         comm.exchange(src, H, 1 << k)                             # last 2^k rows of v^(k)
         for s, a, b in zip(shards, src, dst):
             steps.stage(k, s, a, b, H)

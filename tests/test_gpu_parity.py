@@ -111,11 +111,16 @@ def test_E4_reduced_bf16():
 
 @pytest.mark.parametrize("m,p,q,L,batch,N", [(128, 64, 64, 1000, 3, 6), (64, 64, 64, 300, 2, 0),
                                               (256, 128, 64, 4096, 2, 11), (192, 64, 128, 129, 1, 3),
-                                              (128, 64, 64, 2, 2, 5), (128, 64, 64, 1, 1, 2)])
+                                              (128, 64, 64, 2, 2, 5), (128, 64, 64, 1, 1, 2),
+                                              # Ne = 1 (fused first step only), Ne = 2 (Krylov head,
+                                              # no streaming stage), L = 5 (Ne capped at 2 by L)
+                                              (128, 64, 64, 500, 2, 1), (128, 64, 64, 500, 2, 2),
+                                              (64, 64, 64, 5, 3, 6)])
 @pytest.mark.parametrize("mode", ["bf16", "fp32"])
 def test_mimo_tensor_core_path(m, p, q, L, batch, N, mode):
     """MIMO systems with m, p, q multiples of 64 take the TMA + tcgen05 GEMM path
-    (kind::f16 in bf16 mode, 3xTF32 in fp32 mode)."""
+    (kind::f16 in bf16 mode, 3xTF32 in fp32 mode): the Krylov head (four lags of u) for Ne >= 2,
+    the fused first step for Ne = 1, y directly for Ne = 0."""
     wl = S.make_random_mimo(m, p, q, L=L, batch=batch, N=N, rho=0.98, mode=mode)
     check_parity(wl)
 

@@ -43,7 +43,10 @@ def test_local_emulated_ranks_match_oracle(R, L, N):
     L_loc = L // R
     if Ne > 0 and (1 << Ne) > L_loc:
         pytest.skip("halo longer than a shard")
-    shards = [model.make_shard(u[r * L_loc:(r + 1) * L_loc], wl.m, wl.q, H) for r in range(R)]
+    uh = model.u_halo_rows(Ne)
+    if uh > L_loc:
+        pytest.skip("u halo longer than a shard")
+    shards = [model.make_shard(u[r * L_loc:(r + 1) * L_loc], wl.m, wl.q, H, uh) for r in range(R)]
     model.run(_steps(wl, N, L), model.LocalComm(), shards, N, R * L_loc)
     y = torch.cat([s.y for s in shards], dim=0).numpy()
     ref = _ref(wl, u[:R * L_loc], N)
@@ -74,7 +77,8 @@ def _worker(rank, world, port, L, N, out_path):
         wl, u = _system(L, N)
         H = model.shard_H(N, L)
         L_loc = L // world
-        sh = model.make_shard(u[rank * L_loc:(rank + 1) * L_loc].contiguous(), wl.m, wl.q, H)
+        uh = model.u_halo_rows(model.effective_order(N, L))
+        sh = model.make_shard(u[rank * L_loc:(rank + 1) * L_loc].contiguous(), wl.m, wl.q, H, uh)
         model.run(_steps(wl, N, L), model.DistComm(), [sh], N, L)
         gathered = [torch.empty_like(sh.y) for _ in range(world)]
         dist.all_gather(gathered, sh.y)          # test-side collection only
