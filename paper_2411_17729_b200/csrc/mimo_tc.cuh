@@ -54,6 +54,23 @@ struct MimoGemm {
   unsigned long long* flop_counter = nullptr;
 };
 
+// Tile order of the CTA-pair GEMMs (mimo_tc2.cu, mimo_tc3.cu): pair p walks t = p, p + P, ... and
+// t maps to the physical tile T = row block * n_nblk + column block. In full groups of P * n_nblk
+// tiles, pair p takes the n_nblk column blocks of ONE row block back to back (T = g*P*n_nblk +
+// p*n_nblk + nb), so the row block's A operand is re-read by the same SM pair while it is in its
+// die's L2 instead of by n_nblk pairs spread over both dies; the last partial group keeps the
+// identity order. A bijection of [0, n_tiles) either way.
+__device__ __forceinline__ int64_t pair_tile_order(int64_t t, int64_t n_pairs, int n_nblk, int64_t n_tiles) {
+#ifdef CASC_PAIR_NATURAL_ORDER
+  return t;
+#else
+  const int64_t G = n_pairs * n_nblk, g = t / G;
+  if ((g + 1) * G > n_tiles) return t;
+  const int64_t u = t - g * G;
+  return g * G + (u % n_pairs) * n_nblk + u / n_pairs;
+#endif
+}
+
 bool mimo_tc_supported(int m, int p, int q);
 // 3-D tensor map [d2][d1][d0] (d0 contiguous), box {128 B, rows, 1}, SWIZZLE_128B (fp32 or bf16)
 bool map3d(CUtensorMap* m, const void* base, bool f32, int64_t d0, int64_t d1, int64_t d2, int rows);

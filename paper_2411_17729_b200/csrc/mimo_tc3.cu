@@ -166,7 +166,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     int s = 0;
     uint32_t ph = 0;
     for (int64_t t = pair; t < n_tiles; t += n_pairs) {
-      const PairCoord3 tc = decode3<BN>(t, a, n_nblk, nb_eff, t0_blk, rank);
+      const PairCoord3 tc = decode3<BN>(pair_tile_order(t, n_pairs, n_nblk, n_tiles), a, n_nblk, nb_eff, t0_blk, rank);
       for (int src = 0; src < a.n_src; ++src) {
         const int nk = a.K[src] / BK;
         const int plane = a.w_plane_off[src];
@@ -191,7 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     int rs = 0;
     uint32_t rph = 0;
     for (int64_t t = pair; t < n_tiles; t += n_pairs) {
-      const PairCoord3 tc = decode3<BN>(t, a, n_nblk, nb_eff, t0_blk, rank);
+      const PairCoord3 tc = decode3<BN>(pair_tile_order(t, n_pairs, n_nblk, n_tiles), a, n_nblk, nb_eff, t0_blk, rank);
       for (int j = 0; j < NCH; ++j) {
         mbar_wait(&rempty[rs], rph ^ 1);
         if (!issue) {
@@ -276,7 +276,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     int rs = 0, prev_rs = -1;
     uint32_t rph = 0;
     for (int64_t t = pair; t < n_tiles; t += n_pairs, ++t_local) {
-      const PairCoord3 tc = decode3<BN>(t, a, n_nblk, nb_eff, t0_blk, rank);
+      const PairCoord3 tc = decode3<BN>(pair_tile_order(t, n_pairs, n_nblk, n_tiles), a, n_nblk, nb_eff, t0_blk, rank);
       const int acc = (int)(t_local % NACC);
       mbar_wait_u(&tfull[acc], (uint32_t)((t_local / NACC) & 1));
       tc_fence_after();
