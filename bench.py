@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-seqshard", action="store_true",
                     help="E4: run the sequence-sharded code path even at one rank (validation)")
+    ap.add_argument("--halo", default="per_stage", choices=["per_stage", "oneshot_u"],
+                    help="E4 sequence sharding: per-stage halo (BASELINE configs[3]) or one-shot u halo (NEXT-2)")
     return ap.parse_args()
 
 
@@ -75,8 +77,8 @@ def make_workload(cfg: str, world: int, rank: int):
         wl = S.make_E4()
         return wl, [0], {"workload": "E4", "m": 1024, "p": 256, "q": 256, "L": wl.L, "batch": wl.batch,
                          "N": int(wl.N[0]),
-                         "parallelism": (f"sequence-sharded x{world}: L_loc = {wl.L // world}, per-stage halo of "
-                                         "2^k rows from rank r-1 (NCCL P2P)") if world > 1 else "single"}
+                         "parallelism": (f"sequence-sharded x{world}: L_loc = {wl.L // world}, halo from rank r-1 over "
+                                         "NCCL inside the library") if world > 1 else "single"}
     if cfg == "E5":
         wl = S.make_E5()
         chans = e5_channels(wl.N, world, rank)
@@ -338,8 +340,10 @@ def run_ours(args, world, rank, local_rank):
     wl, chans, cfgd = make_workload(args.config, world, rank)
     sharded = args.config == "E4" and (world > 1 or args.force_seqshard)
     if sharded:
+        cfgd = dict(cfgd, halo=args.halo, layout="time-major [L_loc][batch][dim] per rank")
+    if sharded:
         from paper_2411_17729_b200.runner import SeqShardedWorkload
-        dw = SeqShardedWorkload(wl, rank, world, device=f"cuda:{dev}")
+        dw = SeqShardedWorkload(wl, rank, world, device=f"cuda:{dev}", halo=args.halo)
     else:
         dw = DeviceWorkload(wl, device=f"cuda:{dev}", channels=chans)
     stream = torch.cuda.current_stream()

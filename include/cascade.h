@@ -177,7 +177,7 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
  *   Layouts (time-major, so a halo of d rows is ONE contiguous block of d*batch*dim elements):
  *     u_loc DEVICE [L_loc][batch][p], y_loc DEVICE [L_loc][batch][q] (storage dtype of mode);
  *     pack from casc_powers(1, m, &N, N_max, ...); Bbar, C, D float64 as casc_apply (D may be NULL).
- *     ws: DEVICE, >= casc_apply_seqsharded_workspace(m, p, q, L_loc, batch, N, world, mode) bytes
+ *     ws: DEVICE, >= casc_apply_seqsharded_workspace(m, p, q, L_loc, batch, N, world, mode, halo) bytes
  *     (derived weights, two state buffers of (2^Ne + L_loc) * batch * m elements with the halo
  *     rows in front, and the u halo row).
  *   Stream-ordered on compute_stream / comm_stream (distinct streams of the current device); no
@@ -192,9 +192,19 @@ int casc_comm_init(void** comm, int rank, int world, const void* nccl_unique_id)
 int casc_comm_init_local(void** comms, int world);
 int casc_comm_destroy(void* comm);
 int casc_comm_rank(const void* comm, int* rank, int* world);
-size_t casc_apply_seqsharded_workspace(int m, int p, int q, int64_t L_loc, int batch, int N, int world, int mode);
+/* halo: how the shard boundary is crossed
+ *   CASC_HALO_PER_STAGE  (BASELINE configs[3]) one exchange per step as above; compute = the shard.
+ *   CASC_HALO_ONESHOT_U one exchange of Hu = 2^(Ne+1) - 1 time rows of u from rank
+ *                        r-1 (the cascade is a polynomial of degree 2^(Ne+1) - 1 in the shift,
+ *                        PAPER.md:137-141), then the cascade runs on the window [l0 - Hu, l0 + L_loc)
+ *                        with no further communication: Hu / L_loc extra rows of work (E4 at 8 ranks:
+ *                        3.1%). Requires Hu <= L_loc when world > 1.
+ * Both give the same y bit for bit (each output row is computed by the same operations). */
+enum { CASC_HALO_PER_STAGE = 0, CASC_HALO_ONESHOT_U = 1 };
+size_t casc_apply_seqsharded_workspace(int m, int p, int q, int64_t L_loc, int batch, int N, int world, int mode,
+                                       int halo);
 int casc_apply_seqsharded(void* comm, int m, int p, int q, int64_t L_loc, int batch, int N, int N_max, int mode,
-                          const void* pack, const double* Bbar, const double* C, const double* D,
+                          int halo, const void* pack, const double* Bbar, const double* C, const double* D,
                           const void* u_loc, void* y_loc, void* ws, size_t ws_bytes, void* compute_stream,
                           void* comm_stream);
 

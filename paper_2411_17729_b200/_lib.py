@@ -39,8 +39,9 @@ SIGNATURES = {
     "casc_comm_init_local": (c_int, [ctypes.POINTER(c_void_p), c_int]),
     "casc_comm_destroy": (c_int, [c_void_p]),
     "casc_comm_rank": (c_int, [c_void_p, P_int, P_int]),
-    "casc_apply_seqsharded_workspace": (c_size_t, [c_int, c_int, c_int, c_int64, c_int, c_int, c_int, c_int]),
-    "casc_apply_seqsharded": (c_int, [c_void_p, c_int, c_int, c_int, c_int64, c_int, c_int, c_int, c_int,
+    "casc_apply_seqsharded_workspace": (c_size_t, [c_int, c_int, c_int, c_int64, c_int, c_int, c_int, c_int,
+                                                   c_int]),
+    "casc_apply_seqsharded": (c_int, [c_void_p, c_int, c_int, c_int, c_int64, c_int, c_int, c_int, c_int, c_int,
                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                       c_void_p, c_size_t, c_void_p, c_void_p]),
     "casc_profile_enable": (c_int, [c_int]),

@@ -218,14 +218,18 @@ def comm_init_local(world: int) -> list:
     return [Comm(ctypes.c_void_p(h)) for h in hs]
 
 
-def seqsharded_workspace_bytes(m, p, q, L_loc, batch, N, world, mode) -> int:
-    return int(lib().casc_apply_seqsharded_workspace(m, p, q, L_loc, batch, N, world, _mode(mode)))
+HALOS = {"per_stage": 0, "oneshot_u": 1}
+
+
+def seqsharded_workspace_bytes(m, p, q, L_loc, batch, N, world, mode, halo="per_stage") -> int:
+    return int(lib().casc_apply_seqsharded_workspace(m, p, q, L_loc, batch, N, world, _mode(mode), HALOS[halo]))
 
 
 def apply_seqsharded(comm: Comm, pw: Powers, Bbar, C, D, u_loc, y=None, ws=None, stream=None,
-                     comm_stream=None):
+                     comm_stream=None, halo="per_stage"):
     """This rank's shard: u_loc [L_loc][batch][p] (time-major, storage dtype) -> y [L_loc][batch][q].
-    The halo exchange with the neighbouring ranks happens inside the library (comm_stream)."""
+    The halo exchange with the neighbouring ranks happens inside the library (comm_stream):
+    halo='per_stage' (one exchange per step) or 'oneshot_u' (2^(Ne+1)-1 rows of u once, NEXT-2)."""
     if pw.n_sys != 1:
         raise ValueError("apply_seqsharded() takes a single-system pack")
     m, N, md = pw.m, pw.N[0], pw.mode
@@ -240,11 +244,12 @@ def apply_seqsharded(comm: Comm, pw: Powers, Bbar, C, D, u_loc, y=None, ws=None,
         y = torch.empty((L_loc, batch, q), dtype=STORAGE[md], device=u_loc.device)
     _need(y, STORAGE[md], (L_loc, batch, q), "y")
     if ws is None:
-        ws = torch.empty(seqsharded_workspace_bytes(m, p, q, L_loc, batch, N, comm.world, md), dtype=torch.uint8,
-                         device=u_loc.device)
+        ws = torch.empty(seqsharded_workspace_bytes(m, p, q, L_loc, batch, N, comm.world, md, halo),
+                         dtype=torch.uint8, device=u_loc.device)
     if comm_stream is None:
         raise ValueError("apply_seqsharded needs a comm stream distinct from the compute stream")
-    check(lib().casc_apply_seqsharded(comm.handle, m, p, q, L_loc, batch, N, pw.N_max, md, _p(pw.pack), _p(Bbar),
+    check(lib().casc_apply_seqsharded(comm.handle, m, p, q, L_loc, batch, N, pw.N_max, md, HALOS[halo],
+                                      _p(pw.pack), _p(Bbar),
                                       _p(C), _p(D), _p(u_loc), _p(y), _p(ws), ws.numel(), _stream(stream),
                                       _stream(comm_stream)),
           "casc_apply_seqsharded")

@@ -218,6 +218,110 @@ static int step_gemm(MimoGemm g, int64_t rows, int t_first, bool tf32, cudaStrea
   return launch_mimo_gemm(g, tf32, st);
 }
 
+// NEXT-2, one-shot u halo: the cascade is a polynomial of degree 2^(Ne+1) - 1 in the shift
+// (PAPER.md:137-141), so the local outputs need exactly Hu = 2^(Ne+1) - 1 time rows of u before the
+// shard (pin T14: the windowed cascade equals the global one). One exchange of those rows, then
+// the whole cascade runs on the extended window [l0 - Hu, l0 + L_loc) with no further
+// communication; y is formed on the local rows only.
+struct OneShotWs {
+  MimoWs mw;
+  void* u_ext;         // [(Hu + L_loc) batch][p]
+  void *Va, *Vb;       // [(Hu + L_loc) batch][m]
+  size_t bytes;
+};
+static int64_t oneshot_halo_rows(int Ne) { return Ne > 0 ? ((int64_t)2 << Ne) - 1 : 1; }
+static OneShotWs carve_oneshot(void* ws, int m, int p, int q, int64_t L_loc, int batch, int Ne, int mode) {
+  OneShotWs w{};
+  w.mw = carve_mimo(ws, m, p, q, 0, 0, mode);
+  Carver c(ws);
+  c.off = w.mw.bytes;
+  const size_t es = mode == CASC_FP32 ? 4 : 2;
+  const int64_t ext = (oneshot_halo_rows(Ne) + L_loc) * batch;
+  w.u_ext = c.take<char>((size_t)ext * p * es);
+  w.Va = c.take<char>((size_t)ext * m * es);
+  w.Vb = c.take<char>((size_t)ext * m * es);
+  w.bytes = c.bytes();
+  return w;
+}
+
+static int apply_oneshot(Comm* c, int m, int p, int q, int64_t L_loc, int batch, int Ne, int N_max, int mode,
+                         const PackLayout& P, const double* Bbar, const double* C, const double* D, const void* u_loc,
+                         void* y_loc, void* ws, size_t ws_bytes, cudaStream_t st, cudaStream_t cs) {
+  OneShotWs w = carve_oneshot(ws, m, p, q, L_loc, batch, Ne, mode);
+  if (ws_bytes < w.bytes) return CASC_ERR_WORKSPACE;
+  const bool tf32 = mode == CASC_FP32;
+  const size_t es = tf32 ? 4 : 2;
+  const int64_t Hu = oneshot_halo_rows(Ne), rows = L_loc * batch, hr = Hu * batch, ext = hr + rows;
+  const int64_t mm = (int64_t)m * m;
+  int rc;
+  if ((rc = mimo_derive(m, p, q, Ne, P, Bbar, C, D, w.mw, tf32, st))) return rc;
+  cudaEvent_t ev_in = nullptr, ev_halo = nullptr;
+  struct EvFree {
+    cudaEvent_t* a; cudaEvent_t* b;
+    ~EvFree() { if (*a) cudaEventDestroy(*a); if (*b) cudaEventDestroy(*b); }
+  } ev_free{&ev_in, &ev_halo};
+  CASC_TRY(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+  CASC_TRY(cudaEventCreateWithFlags(&ev_halo, cudaEventDisableTiming));
+  // the window: Hu rows of rank r-1's u (zeros on rank 0), then the local rows
+  CASC_TRY(cudaMemsetAsync(w.u_ext, 0, (size_t)hr * p * es, st));
+  CASC_TRY(cudaMemcpyAsync((char*)w.u_ext + (size_t)hr * p * es, u_loc, (size_t)rows * p * es,
+                           cudaMemcpyDeviceToDevice, st));
+  CASC_TRY(cudaEventRecord(ev_in, st));
+  {
+    CASC_TRY(cudaStreamWaitEvent(cs, ev_in, 0));
+    ProfScope ps(cs, K_SEQ_HALO, 2.0 * hr * p * es, 0.0);
+    if ((rc = exchange(c, (const char*)u_loc + (size_t)(rows - hr) * p * es, (size_t)hr * p * es, w.u_ext,
+                       (size_t)hr * p * es, nullptr, cs, ev_halo)))
+      return rc;
+  }
+  CASC_TRY(cudaStreamWaitEvent(st, ev_halo, 0));
+  const double dr = (double)ext;
+  const int pipe = tf32 ? PIPE_TF32 : PIPE_BF16;
+  const double xf = tf32 ? 3.0 : 1.0;
+  auto run = [&](MimoGemm g, int64_t n_rows, int cls, double bytes, double flops) -> int {
+    ProfScope ps(st, cls, bytes, flops);
+    ps.exec(bytes, xf * flops, pipe);
+    return step_gemm(g, n_rows, 0, tf32, st);
+  };
+  if (Ne == 0) {                       // y = (C Bbar + D) u_l + (C Abar Bbar) u_{l-1}, local rows
+    MimoGemm g{};
+    g.src[0] = {w.u_ext, w.mw.CBD, p, 0};
+    g.src[1] = {w.u_ext, w.mw.CAB, p, batch};
+    g.src[0].row0 = g.src[1].row0 = hr;
+    g.n_src = 2; g.out = y_loc; g.n_out = q;
+    return run(g, rows, K_MIMO_LAST, (double)rows * (p + q) * es, (double)rows * 4.0 * q * p);
+  }
+  const int k0 = Ne >= 2 ? 2 : 1;
+  {                                    // head (Ne >= 2, R28) or fused first step over the window
+    const void* Wj[4] = {w.mw.Bb, w.mw.AB, w.mw.A2B, w.mw.A3B};
+    MimoGemm g{};
+    g.n_src = Ne >= 2 ? 4 : 2;
+    for (int j = 0; j < g.n_src; ++j) g.src[j] = {w.u_ext, Wj[j], p, (int64_t)j * batch};
+    g.out = k0 == 2 ? w.Vb : w.Va; g.n_out = m;
+    if ((rc = run(g, ext, K_MIMO_FIRST, dr * (p + m) * es, dr * 2.0 * g.n_src * m * p))) return rc;
+  }
+  for (int k = k0; k <= Ne - 1; ++k) {  // stages over the window (rows before it read zeros)
+    void* Vs = (k - 1) % 2 == 0 ? w.Va : w.Vb;
+    void* Vd = (k % 2 == 0) ? w.Va : w.Vb;
+    const void* Wk = tf32 ? static_cast<const void*>(P.f32 + k * 2 * mm) : static_cast<const void*>(P.b16 + k * mm);
+    MimoGemm g{};
+    g.src[0] = {Vs, Wk, m, ((int64_t)1 << k) * batch};
+    g.n_src = 1; g.R = Vs; g.out = Vd; g.n_out = m;
+    if ((rc = run(g, ext, K_MIMO_STAGE, dr * m * es * 2.0, dr * 2.0 * (double)mm))) return rc;
+  }
+  void* V = (Ne - 1) % 2 == 0 ? w.Va : w.Vb;   // y on the local rows: y = C v + (C P_Ne) v_{l-2^Ne} + D u
+  MimoGemm g{};
+  g.src[0] = {V, w.mw.C, m, 0};
+  g.src[1] = {V, w.mw.CP, m, ((int64_t)1 << Ne) * batch};
+  g.src[0].row0 = g.src[1].row0 = hr;
+  g.n_src = 2;
+  if (D) { g.src[2] = {u_loc, w.mw.D, p, 0}; g.n_src = 3; }
+  g.out = y_loc; g.n_out = q;
+  return run(g, rows, K_MIMO_LAST, (double)rows * (m + p + q) * es,
+             (double)rows * (4.0 * q * m + (D ? 2.0 * q * p : 0.0)));
+}
+
+
 }  // namespace casc
 
 using namespace casc;
@@ -285,14 +389,18 @@ int casc_comm_rank(const void* comm, int* rank, int* world) {
   return CASC_OK;
 }
 
-size_t casc_apply_seqsharded_workspace(int m, int p, int q, int64_t L_loc, int batch, int N, int world, int mode) {
+size_t casc_apply_seqsharded_workspace(int m, int p, int q, int64_t L_loc, int batch, int N, int world, int mode,
+                                       int halo) {
   if (m < 1 || p < 1 || q < 1 || L_loc < 1 || batch < 1 || N < 0 || world < 1) return 0;
-  return carve_seq(nullptr, m, p, q, L_loc, batch, eff_order(N, L_loc * world), mode).bytes;
+  const int Ne = eff_order(N, L_loc * world);
+  if (halo == CASC_HALO_ONESHOT_U) return carve_oneshot(nullptr, m, p, q, L_loc, batch, Ne, mode).bytes;
+  return carve_seq(nullptr, m, p, q, L_loc, batch, Ne, mode).bytes;
 }
 
 int casc_apply_seqsharded(void* comm, int m, int p, int q, int64_t L_loc, int batch, int N, int N_max, int mode,
-                          const void* pack, const double* Bbar, const double* C, const double* D, const void* u_loc,
-                          void* y_loc, void* ws, size_t ws_bytes, void* compute_stream, void* comm_stream) {
+                          int halo, const void* pack, const double* Bbar, const double* C, const double* D,
+                          const void* u_loc, void* y_loc, void* ws, size_t ws_bytes, void* compute_stream,
+                          void* comm_stream) {
   g_launches = 0;
   auto* c = static_cast<Comm*>(comm);
   if (!c || !pack || !Bbar || !C || !u_loc || !y_loc || !ws || !comm_stream) return CASC_ERR_ARG;
@@ -300,8 +408,16 @@ int casc_apply_seqsharded(void* comm, int m, int p, int q, int64_t L_loc, int ba
   if (rc) return rc;
   if (N < 0 || N > N_max) return CASC_ERR_DIM;
   if (!mimo_tc_supported(m, p, q)) return CASC_ERR_UNSUPPORTED;
+  if (halo != CASC_HALO_PER_STAGE && halo != CASC_HALO_ONESHOT_U) return CASC_ERR_ARG;
   const int64_t L = L_loc * c->world;
   const int Ne = eff_order(N, L);
+  if (halo == CASC_HALO_ONESHOT_U) {
+    // the Hu-row window must come from the immediate predecessor
+    if (c->world > 1 && oneshot_halo_rows(Ne) > L_loc) return CASC_ERR_UNSUPPORTED;
+    return apply_oneshot(c, m, p, q, L_loc, batch, Ne, N_max, mode,
+                         pack_layout(const_cast<void*>(pack), 1, m, N_max, mode), Bbar, C, D, u_loc, y_loc, ws,
+                         ws_bytes, (cudaStream_t)compute_stream, (cudaStream_t)comm_stream);
+  }
   // each halo must come from the immediate predecessor (holds for configs[3] up to 8 ranks)
   const int uh = u_halo_rows(Ne);
   if (c->world > 1 && ((Ne > 0 && ((int64_t)1 << Ne) > L_loc) || uh > L_loc)) return CASC_ERR_UNSUPPORTED;

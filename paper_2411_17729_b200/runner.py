@@ -88,7 +88,7 @@ class SeqShardedWorkload:
     rows [rank L_loc, (rank+1) L_loc) of every sequence, time-major [L_loc][batch][p], run by
     casc_apply_seqsharded with the library's own per-stage NCCL halo exchange (comm stream)."""
 
-    def __init__(self, wl, rank: int, world: int, device="cuda", comm=None, group=None):
+    def __init__(self, wl, rank: int, world: int, device="cuda", comm=None, group=None, halo="per_stage"):
         if wl.kind != "mimo" or wl.L % world:
             raise ValueError("sequence sharding takes one system with L divisible by the rank count")
         self.wl, self.rank, self.world = wl, rank, world
@@ -103,8 +103,9 @@ class SeqShardedWorkload:
         self.u = torch.from_numpy(u).to(api.STORAGE[md]).to(device)
         self.y = torch.empty((self.L_loc, wl.batch, wl.q), dtype=api.STORAGE[md], device=device)
         self.pack = torch.empty(api.pack_bytes(1, wl.m, self.N, md), dtype=torch.uint8, device=device)
-        self.ws = torch.empty(api.seqsharded_workspace_bytes(wl.m, wl.p, wl.q, self.L_loc, wl.batch, self.N, world, md),
-                              dtype=torch.uint8, device=device)
+        self.halo = halo
+        self.ws = torch.empty(api.seqsharded_workspace_bytes(wl.m, wl.p, wl.q, self.L_loc, wl.batch, self.N, world, md,
+                                                             halo), dtype=torch.uint8, device=device)
         if comm is None:
             if world > 1:
                 from .seqshard import comm_from_process_group
@@ -119,7 +120,7 @@ class SeqShardedWorkload:
         pw = api.powers(self.Abar, self.N, self.wl.mode, stream=stream, out=self.pack)
         n = api.last_launch_count()
         api.apply_seqsharded(self.comm, pw, self.Bbar, self.C, self.D, self.u, y=self.y, ws=self.ws, stream=stream,
-                             comm_stream=self.comm_stream)
+                             comm_stream=self.comm_stream, halo=self.halo)
         return n + api.last_launch_count()
 
     def run_host(self, u_h: torch.Tensor, y_h: torch.Tensor) -> int:

@@ -150,3 +150,24 @@ def run(steps, comm, shards, N: int, L_global: int) -> None:
 def shard_H(N: int, L_global: int) -> int:
     Ne = effective_order(N, L_global)
     return (1 << Ne) if Ne > 0 else 0
+
+
+def run_oneshot(steps_factory, comm, u_locs, m: int, q: int, N: int, L_global: int):
+    """NEXT-2 schedule (casc_apply_seqsharded, CASC_HALO_ONESHOT_U): one exchange of
+    Hu = 2^(Ne+1) - 1 rows of u, then the unsharded cascade on the window [l0 - Hu, l0 + L_loc) of
+    each shard (zeros before t = 0) and y kept on the local rows. Returns the local y's."""
+    Ne = effective_order(N, L_global)
+    Hu = (2 << Ne) - 1 if Ne > 0 else 1
+    L_loc, batch, p = u_locs[0].shape
+    exts = []
+    for u in u_locs:
+        e = torch.zeros((Hu + L_loc, batch, p), dtype=u.dtype)
+        e[Hu:] = u
+        exts.append(e)
+    comm.exchange(exts, Hu, Hu)                                   # the only exchange
+    ys = []
+    for e in exts:
+        sh = make_shard(e, m, q, shard_H(N, L_global), u_halo_rows(Ne))
+        run(steps_factory(), LocalComm(), [sh], N, L_global)     # one window, no further exchange
+        ys.append(sh.y[Hu:])
+    return ys

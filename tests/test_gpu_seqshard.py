@@ -27,7 +27,7 @@ def _cuda():
     pk.lib()
 
 
-def _sharded(wl, R, comms):
+def _sharded(wl, R, comms, halo="per_stage"):
     """Run R ranks of casc_apply_seqsharded, each on its own thread; returns y [L][batch][q]."""
     import paper_2411_17729_b200 as pk
     md = wl.mode
@@ -48,7 +48,7 @@ def _sharded(wl, R, comms):
             u_loc = u[r * L_loc:(r + 1) * L_loc].contiguous()
             torch.cuda.synchronize()
             with torch.cuda.stream(st):
-                ys[r] = pk.apply_seqsharded(comms[r], pw, Bbar, C, D, u_loc, stream=st, comm_stream=cs)
+                ys[r] = pk.apply_seqsharded(comms[r], pw, Bbar, C, D, u_loc, stream=st, comm_stream=cs, halo=halo)
             st.synchronize()
         except Exception as e:                    # reported by the main thread
             errs.append(e)
@@ -111,3 +111,34 @@ def test_halo_longer_than_shard_is_unsupported():
     finally:
         for c in comms:
             c.destroy()
+
+
+@pytest.mark.parametrize("mode", ["bf16", "fp32"])
+@pytest.mark.parametrize("case", [c for c in CASES if c[0] == 1 or ((2 << min(c[5], (c[4] - 1).bit_length() - 1)) - 1)
+                                  <= c[4] // c[0]])
+def test_oneshot_u_halo_bitwise(mode, case):
+    """NEXT-2: one exchange of 2^(Ne+1) - 1 rows of u, then the whole cascade on the window
+    [l0 - Hu, l0 + L_loc) (exact by the window property, pin T14): bitwise the per-stage result and
+    the unsharded casc_apply, since every output row is computed by the same operations."""
+    import paper_2411_17729_b200 as pk
+    R, m, p, q, L, N = case
+    wl = S.make_random_mimo(m, p, q, L=L, batch=3, N=N, rho=0.97, mode=mode)
+    comms = pk.comm_init_local(R)
+    try:
+        y_one = _sharded(wl, R, comms, halo="oneshot_u")
+    finally:
+        for c in comms:
+            c.destroy()
+    comms = pk.comm_init_local(R)
+    try:
+        y_per = _sharded(wl, R, comms, halo="per_stage")
+    finally:
+        for c in comms:
+            c.destroy()
+    assert torch.equal(y_one, y_per)
+    from paper_2411_17729_b200.runner import DeviceWorkload
+    dw = DeviceWorkload(wl)
+    dw.step()
+    torch.cuda.synchronize()
+    assert torch.equal(y_one.permute(1, 0, 2), dw.y)
+

@@ -123,3 +123,19 @@ def test_gloo_world2_nccl_unique_id_broadcast(tmp_path):
     mp.spawn(_uid_worker, args=(2, _free_port(), out), nprocs=2, join=True)
     a, b = np.load(out + ".0.npy"), np.load(out + ".1.npy")
     assert a.shape == (128,) and np.array_equal(a, b) and a.any()
+
+
+@pytest.mark.parametrize("R,L,N", [(4, 1024, 5), (2, 200, 3), (8, 4096, 8), (3, 90, 0)])
+def test_oneshot_u_halo_schedule_matches_oracle(R, L, N):
+    """NEXT-2 on the CPU: one exchange of 2^(Ne+1) - 1 rows of u and a rank-local cascade on the
+    window give the global outputs (window property, pin T14)."""
+    wl, u = _system(L, N)
+    L_loc = L // R
+    Ne = model.effective_order(N, L)
+    if ((2 << Ne) - 1 if Ne else 1) > L_loc:
+        pytest.skip("window longer than a shard")
+    ys = model.run_oneshot(lambda: _steps(wl, N, L), model.LocalComm(),
+                           [u[r * L_loc:(r + 1) * L_loc] for r in range(R)], wl.m, wl.q, N, L)
+    y = torch.cat(ys, dim=0).numpy()
+    ref = _ref(wl, u[:R * L_loc], N)
+    assert np.max(np.abs(y - ref)) <= 1e-12 * np.max(np.abs(ref))
