@@ -57,8 +57,25 @@ static ApplyWs carve_apply(void* ws, int n, int m, int p, int q, int64_t L, int 
   return w;
 }
 
+// bf16 SISO banks (bf16 storage of u and y) run the fp32 tensor-core bank path on fp32 copies of
+// u and y carved in front of its workspace: the arithmetic is the fp32 path's (3xTF32, at least
+// the bf16 mode's fp32 accumulation), y is rounded once to bf16 (RN-even)
+static bool bank_bf16_path(int m, int p, int q, int mode) {
+  return mode == CASC_BF16 && bank_tc_path(m, p, q, CASC_FP32);
+}
+__global__ void bf16_to_f32_kernel(const __nv_bfloat16* src, float* dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __bfloat162float(src[i]);
+}
+__global__ void f32_to_bf16_kernel(const float* src, __nv_bfloat16* dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __float2bfloat16_rn(src[i]);
+}
+
 size_t apply_ws_bytes(int n, int m, int p, int q, int64_t L, int batch, int mode, int n_max) {
   if (bank_tc_path(m, p, q, mode)) return bank_ws_bytes(n, m, L, batch, n_max);
+  if (bank_bf16_path(m, p, q, mode))
+    return align_up((size_t)2 * n * batch * L * sizeof(float), 256) + bank_ws_bytes(n, m, L, batch, n_max);
   if (mimo_tc_path(n, m, p, q, mode)) return mimo_ws_bytes(m, p, q, L, batch, mode);
   return carve_apply(nullptr, n, m, p, q, L, batch, mode).bytes;
 }
@@ -83,6 +100,23 @@ int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_
     if (N_host[s] < 0 || N_host[s] > N_max) return CASC_ERR_DIM;
   if (bank_tc_path(m, p, q, mode))
     return engine_bank_tc(n, m, L, batch, N_host, N_max, pack, Bbar, C, D, u, y, ws, ws_bytes, st);
+  if (bank_bf16_path(m, p, q, mode)) {
+    const int64_t cnt = (int64_t)n * batch * L;
+    const size_t front = align_up((size_t)2 * cnt * sizeof(float), 256);
+    if (ws_bytes <= front) return CASC_ERR_WORKSPACE;
+    float* u32 = static_cast<float*>(ws);
+    float* y32 = u32 + cnt;
+    const int blocks = (int)std::min<int64_t>(ceil_div(cnt, 256), 148 * 8);
+    bf16_to_f32_kernel<<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(u), u32, cnt);
+    CASC_LAUNCHED();
+    // the bf16 pack of a bank-sized system also holds the tf32 planes (common.cuh pack_layout)
+    int rc2 = engine_bank_tc(n, m, L, batch, N_host, N_max, pack, Bbar, C, D, u32, y32, (char*)ws + front,
+                             ws_bytes - front, st);
+    if (rc2) return rc2;
+    f32_to_bf16_kernel<<<blocks, 256, 0, st>>>(y32, static_cast<__nv_bfloat16*>(y), cnt);
+    CASC_LAUNCHED();
+    return CASC_OK;
+  }
   if (mimo_tc_path(n, m, p, q, mode))
     return engine_mimo_tc(m, p, q, L, batch, N_host[0], N_max, mode, pack, Bbar, C, D, u, y, ws, ws_bytes, st);
   ApplyWs w = carve_apply(ws, n, m, p, q, L, batch, mode);

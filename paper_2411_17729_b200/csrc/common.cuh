@@ -107,8 +107,10 @@ inline PackLayout pack_layout(void* pack, int n_sys, int m, int N_max, int mode)
   L.p64 = c.take<double>(slots * mm);
   L.f32 = nullptr;
   L.b16 = nullptr;
-  if (mode == CASC_FP32) L.f32 = c.take<float>(slots * 2 * mm);
-  else L.b16 = c.take<__nv_bfloat16>(slots * mm);
+  // tf32 hi/lo planes in fp32 mode, and also in bf16 mode for m <= 64 (bank sizes: the bf16 SISO
+  // bank runs the fp32 tensor-core bank path, cascade_api.cu); the fp32-mode layout is a prefix
+  if (mode == CASC_FP32 || m <= 64) L.f32 = c.take<float>(slots * 2 * mm);
+  if (mode != CASC_FP32) L.b16 = c.take<__nv_bfloat16>(slots * mm);
   L.bytes = c.bytes();
   return L;
 }

@@ -152,9 +152,8 @@ __global__ void pack_powers_kernel(const int* hdr, const double* p64, float* f32
       float lo = tf32_rna((float)(p - (double)hi));
       f32[slot * 2 * mm + ij] = hi;
       f32[slot * 2 * mm + mm + ij] = lo;
-    } else {
-      b16[e] = __float2bfloat16_rn((float)p);
     }
+    if (b16) b16[e] = __float2bfloat16_rn((float)p);
   }
 }
 
@@ -192,9 +191,8 @@ __global__ void __launch_bounds__(256) powers_small_kernel(const double* Abar, c
         const float hi = tf32_rna((float)p);
         f32[slot * 2 * mm + e] = hi;
         f32[slot * 2 * mm + mm + e] = tf32_rna((float)(p - (double)hi));
-      } else {
-        b16[slot * mm + e] = __float2bfloat16_rn((float)p);
       }
+      if (b16) b16[slot * mm + e] = __float2bfloat16_rn((float)p);
     }
     if (k == Ns) break;
     if (m == 64) {

@@ -43,7 +43,9 @@ def test_version_and_status_strings(lib):
 def test_size_queries(lib):
     a = lib.casc_pack_bytes(1, 64, 13, 0)
     b = lib.casc_pack_bytes(1, 64, 13, 1)
-    assert a > b > 14 * 64 * 64 * 8           # fp64 powers + storage copy
+    assert b > a > 14 * 64 * 64 * 8           # fp64 powers + tf32 hi/lo (bf16, m <= 64: + bf16 copy)
+    a2, b2 = lib.casc_pack_bytes(1, 256, 13, 0), lib.casc_pack_bytes(1, 256, 13, 1)
+    assert a2 > b2 > 14 * 256 * 256 * 8       # m > 64: bf16 mode keeps only the bf16 image
     assert lib.casc_pack_bytes(0, 64, 13, 0) == 0
     ws = lib.casc_apply_workspace_bytes(256, 64, 64, 65536, 16, 13, 0)
     assert ws >= 2 * 65536 * 16 * 256 * 4      # two fp32 state buffers

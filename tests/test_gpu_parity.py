@@ -250,3 +250,25 @@ def test_exponential_scheme_bank():
     wl = S.make_E2(n_ch=12, L=4096, batch=2, scheme="exponential")
     e, es = check_parity(wl)
     print(f"E2x rel {e:.2e} state {es:.2e}")
+
+
+@pytest.mark.parametrize("m", [16, 32, 64])
+def test_bf16_siso_bank_on_tensor_cores(m):
+    """bf16 storage of a SISO bank: the library converts u to fp32, runs the tensor-core bank path
+    (Krylov head, stage passes, fused output) and rounds y once to bf16; parity at the bf16 bound,
+    and the y is the fp32 path's y rounded to bf16 (RN-even), bit for bit."""
+    import paper_2411_17729_b200 as pk
+    wl = S.make_E2(n_ch=6, L=2048, batch=2, mode="bf16") if m == 64 else \
+        S.make_random_mimo(m, 1, 1, L=1500, batch=2, N=9, rho=0.97, mode="bf16")
+    check_parity(wl)
+    pk.profile_reset()
+    pk.profile_enable(True)
+    y_bf, _ = run_gpu(wl)
+    torch.cuda.synchronize()
+    prof = pk.profile_read()
+    pk.profile_enable(False)
+    assert "direct" not in prof and "stage" not in prof, prof        # no CUDA-core GEMM classes
+    wl32 = S.Workload(**{**wl.__dict__, "mode": "fp32"})             # same values (bf16-exact u)
+    y32, _ = run_gpu(wl32)
+    y32_bf = torch.from_numpy(y32).float().to(torch.bfloat16).double().numpy()
+    assert np.array_equal(y_bf, y32_bf)
