@@ -512,31 +512,87 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
     const int64_t in_bytes = (int64_t)es * batch * L * p;
     const int chunks = chunks_env ? chunks_env : (int)std::min<int64_t>(8, std::max<int64_t>(1, ceil_div(in_bytes, (int64_t)64 << 20)));
     const int nc = std::min(batch, chunks);
-    std::vector<cudaEvent_t> ev((size_t)2 * nc, nullptr);
-    for (auto& e : ev)
-      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) { rc = CASC_ERR_CUDA; break; }
-    const size_t in_row = es * (size_t)L * p, out_row = es * (size_t)L * q;
+    // derived weights once for all chunks (Ne is that of the full length L)
+    const int Ne = eff_order(N_host[0], L);
+    {
+      MimoWs w = carve_mimo(h.apply_ws, m, p, q, L, batch, mode);
+      if (h.apply_bytes < w.bytes) return CASC_ERR_WORKSPACE;
+      PackLayout P = pack_layout(h.pack, 1, m, N_max, mode);
+      if ((rc = mimo_derive(m, p, q, Ne, P, h.Bbar, h.C, D_h ? h.D : nullptr, w, mode == CASC_FP32, st))) return rc;
+    }
+    // The first and the last chunk are exposed (nothing to overlap their input / output copy with).
+    // When such a chunk is a single sequence and the impulse response is short against L, it runs
+    // as kW time windows (rows [r0, r1) computed from inputs [r0 - Hu, r1), Hu = 2^(Ne+1) - 1, exact:
+    // PAPER.md:137-141, pin T14): the first chunk's compute starts after its first window's input
+    // landed, the last chunk's output leaves window by window.
+    constexpr int kW = 4;
+    const int64_t Hu = Ne > 0 ? ((int64_t)2 << Ne) - 1 : 0;
+    const int64_t Lw = ceil_div(L, kW);
     std::vector<int> b0(nc + 1);
     for (int i = 0; i <= nc; ++i) b0[i] = (int)((int64_t)batch * i / nc);
+    auto windowed = [&](int i) { return nc > 1 && (i == 0 || i == nc - 1) && b0[i + 1] - b0[i] == 1 && Ne > 0 && Lw >= 8 * Hu; };
+    std::vector<cudaEvent_t> ev((size_t)2 * nc + 2 * kW, nullptr);
+    for (auto& e : ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) { rc = CASC_ERR_CUDA; break; }
+    cudaEvent_t* wev = ev.data() + 2 * nc;            // window events: inputs (first chunk), outputs (last)
+    const size_t in_row = es * (size_t)L * p, out_row = es * (size_t)L * q;
     auto ok = [&](cudaError_t e) { if (e != cudaSuccess && rc == CASC_OK) rc = CASC_ERR_CUDA; return rc == CASC_OK; };
+    auto win = [&](int j, int64_t* r0, int64_t* r1) { *r0 = std::min<int64_t>(L, j * Lw); *r1 = std::min<int64_t>(L, (j + 1) * Lw); };
     // chunk i+1's input is submitted after chunk i's work is queued: the small table upload inside
     // each chunk's apply queues behind every copy submitted before it on the copy engine
     auto submit = [&](int i) {
+      if (i == 0 && windowed(0)) {                    // window by window
+        for (int j = 0; j < kW; ++j) {
+          int64_t r0, r1;
+          win(j, &r0, &r1);
+          if (!ok(cudaMemcpyAsync((char*)h.u + r0 * es * p, (const char*)u_h + r0 * es * p, (size_t)(r1 - r0) * es * p,
+                                  cudaMemcpyHostToDevice, ctx->in)) || !ok(cudaEventRecord(wev[j], ctx->in)))
+            return false;
+        }
+        return ok(cudaEventRecord(ev[0], ctx->in));
+      }
       return ok(cudaMemcpyAsync((char*)h.u + b0[i] * in_row, (const char*)u_h + b0[i] * in_row,
                                 (size_t)(b0[i + 1] - b0[i]) * in_row, cudaMemcpyHostToDevice, ctx->in)) &&
              ok(cudaEventRecord(ev[2 * i], ctx->in));
     };
+    auto run_windows = [&](int i) {                   // one sequence: b0[i]
+      const char* us = (const char*)h.u + b0[i] * in_row;
+      char* ys = (char*)h.y + b0[i] * out_row;
+      for (int j = 0; j < kW && rc == CASC_OK; ++j) {
+        int64_t r0, r1;
+        win(j, &r0, &r1);
+        if (r1 <= r0) break;
+        if (i == 0 && !ok(cudaStreamWaitEvent(st, wev[j], 0))) break;
+        const int64_t a = std::max<int64_t>(0, r0 - Hu);
+        rc = mimo_run(m, p, q, r1 - a, 1, Ne, N_max, mode, h.pack, D_h != nullptr, us + a * es * p, ys + r0 * es * q,
+                      r0 - a, h.apply_ws, h.apply_bytes, st);
+        if (rc) break;
+        if (i == nc - 1) {                            // this window's output leaves now
+          if (!ok(cudaEventRecord(wev[kW + j], st)) || !ok(cudaStreamWaitEvent(ctx->out, wev[kW + j], 0)) ||
+              !ok(cudaMemcpyAsync((char*)y_h + b0[i] * out_row + r0 * es * q, ys + r0 * es * q,
+                                  (size_t)(r1 - r0) * es * q, cudaMemcpyDeviceToHost, ctx->out)))
+            break;
+        }
+      }
+    };
     if (rc == CASC_OK && ok(cudaStreamWaitEvent(ctx->in, ctx->inputs_free, 0)) && submit(0)) {
       for (int i = 0; i < nc; ++i) {
-        if (!ok(cudaStreamWaitEvent(st, ev[2 * i], 0))) break;
-        rc = engine_apply(1, m, p, q, L, b0[i + 1] - b0[i], N_host, N_max, mode, h.pack, h.Bbar, h.C,
-                          D_h ? h.D : nullptr, (const char*)h.u + b0[i] * in_row, (char*)h.y + b0[i] * out_row,
-                          h.apply_ws, h.apply_bytes, st);
+        const bool wi = windowed(i);
+        if (!(wi && i == 0) && !ok(cudaStreamWaitEvent(st, ev[2 * i], 0))) break;
+        if (wi) {
+          run_windows(i);
+        } else {
+          rc = mimo_run(m, p, q, L, b0[i + 1] - b0[i], Ne, N_max, mode, h.pack, D_h != nullptr,
+                        (const char*)h.u + b0[i] * in_row, (char*)h.y + b0[i] * out_row, 0, h.apply_ws,
+                        h.apply_bytes, st);
+        }
         if (rc) break;
-        if (!ok(cudaEventRecord(ev[2 * i + 1], st)) || !ok(cudaStreamWaitEvent(ctx->out, ev[2 * i + 1], 0)) ||
-            !ok(cudaMemcpyAsync((char*)y_h + b0[i] * out_row, (const char*)h.y + b0[i] * out_row,
-                                (size_t)(b0[i + 1] - b0[i]) * out_row, cudaMemcpyDeviceToHost, ctx->out)))
-          break;
+        if (!(wi && i == nc - 1)) {                   // the whole chunk's output
+          if (!ok(cudaEventRecord(ev[2 * i + 1], st)) || !ok(cudaStreamWaitEvent(ctx->out, ev[2 * i + 1], 0)) ||
+              !ok(cudaMemcpyAsync((char*)y_h + b0[i] * out_row, (const char*)h.y + b0[i] * out_row,
+                                  (size_t)(b0[i + 1] - b0[i]) * out_row, cudaMemcpyDeviceToHost, ctx->out)))
+            break;
+        }
         if (i + 1 < nc && !submit(i + 1)) break;
       }
     }

@@ -52,6 +52,10 @@ MimoWs carve_mimo(void* ws, int m, int p, int q, int64_t L, int batch, int mode)
 // rounded once to the GEMM operand format
 int mimo_derive(int m, int p, int q, int Ne, const PackLayout& P, const double* Bbar, const double* C,
                 const double* D, const MimoWs& w, bool tf32, cudaStream_t st);
+// the MIMO cascade steps with the derived weights already in ws (engine_mimo_tc = derive + run);
+// out_skip: leading window rows of history that are not written to y (batch == 1)
+int mimo_run(int m, int p, int q, int64_t L, int batch, int Ne, int N_max, int mode, const void* pack, bool has_D,
+             const void* u, void* y, int64_t out_skip, void* ws, size_t ws_bytes, cudaStream_t st);
 int engine_powers(int n, int m, const int* N_host, int N_max, const double* Abar, int mode,
                   void* pack, cudaStream_t st);
 }  // namespace casc

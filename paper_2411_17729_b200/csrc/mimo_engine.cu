@@ -84,14 +84,29 @@ int engine_mimo_tc(int m, int p, int q, int64_t L, int batch, int N, int N_max, 
                    size_t ws_bytes, cudaStream_t st) {
   MimoWs w = carve_mimo(ws, m, p, q, L, batch, mode);
   if (ws_bytes < w.bytes) return CASC_ERR_WORKSPACE;
+  PackLayout P = pack_layout(const_cast<void*>(pack), 1, m, N_max, mode);
+  const int Ne = eff_order(N, L);
+  int rc;
+  if ((rc = mimo_derive(m, p, q, Ne, P, Bbar, C, D, w, mode == CASC_FP32, st))) return rc;
+  return mimo_run(m, p, q, L, batch, Ne, N_max, mode, pack, D != nullptr, u, y, 0, ws, ws_bytes, st);
+}
+
+// The cascade steps of one MIMO system on `batch` sequences of L rows, derived weights already in
+// ws (mimo_derive). out_skip > 0 (one sequence only): a window whose first out_skip rows are input
+// history -- y is written for rows [out_skip, L) only, to y (which points at the first kept row);
+// exact when out_skip >= 2^(Ne+1) - 1 or the window starts at the sequence start (PAPER.md:137-141,
+// pin T14).
+int mimo_run(int m, int p, int q, int64_t L, int batch, int Ne, int N_max, int mode, const void* pack, bool has_D,
+             const void* u, void* y, int64_t out_skip, void* ws, size_t ws_bytes, cudaStream_t st) {
+  MimoWs w = carve_mimo(ws, m, p, q, L, batch, mode);
+  if (ws_bytes < w.bytes) return CASC_ERR_WORKSPACE;
+  if (out_skip < 0 || out_skip >= L || (out_skip > 0 && (batch != 1 || Ne == 0))) return CASC_ERR_ARG;
   const bool tf32 = mode == CASC_FP32;
   PackLayout P = pack_layout(const_cast<void*>(pack), 1, m, N_max, mode);
   const int64_t mm = (int64_t)m * m;
-  const int Ne = eff_order(N, L);
   const double es = tf32 ? 4.0 : 2.0;
   int rc;
-  if ((rc = mimo_derive(m, p, q, Ne, P, Bbar, C, D, w, tf32, st))) return rc;
-  const double rows = (double)batch * L;
+  const double rows = (double)batch * L, yrows = (double)batch * (L - out_skip);
   const double xf = tf32 ? 3.0 : 1.0;            // executed products per source: 3xTF32 or one bf16
   const int pipe = tf32 ? PIPE_TF32 : PIPE_BF16;
   if (Ne == 0) {
@@ -139,11 +154,16 @@ int engine_mimo_tc(int m, int p, int q, int64_t L, int batch, int N, int N_max, 
     MimoGemm g{};
     g.src[0] = {V, w.C, m, 0};
     g.src[1] = {V, w.CP, m, (int64_t)1 << Ne};
+    g.src[0].row0 = g.src[1].row0 = out_skip;       // window history rows in front (out_skip > 0)
     g.n_src = 2;
-    if (D) { g.src[2] = {u, w.D, p, 0}; g.n_src = 3; }
-    g.out = y; g.n_out = q; g.L = L; g.batch = batch;
-    ProfScope ps(st, K_MIMO_LAST, rows * (m + p + q) * es, rows * (4.0 * q * m + 2.0 * q * p));
-    ps.exec(rows * (m + p + q) * es, rows * (4.0 * q * m + (D ? 2.0 * q * p : 0.0)) * xf, pipe);
+    if (has_D) {
+      g.src[2] = {u, w.D, p, 0};
+      g.src[2].row0 = out_skip;
+      g.n_src = 3;
+    }
+    g.out = y; g.n_out = q; g.L = L - out_skip; g.batch = batch;
+    ProfScope ps(st, K_MIMO_LAST, yrows * (m + p + q) * es, yrows * (4.0 * q * m + 2.0 * q * p));
+    ps.exec(yrows * (m + p + q) * es, yrows * (4.0 * q * m + (has_D ? 2.0 * q * p : 0.0)) * xf, pipe);
     if ((rc = launch_mimo_gemm(g, tf32, st))) return rc;
   }
   return CASC_OK;

@@ -272,3 +272,13 @@ def test_bf16_siso_bank_on_tensor_cores(m):
     y32, _ = run_gpu(wl32)
     y32_bf = torch.from_numpy(y32).float().to(torch.bfloat16).double().numpy()
     assert np.array_equal(y_bf, y32_bf)
+
+
+@pytest.mark.parametrize("m,p", [(256, 64), (512, 128), (1024, 256)])
+def test_fp32_headroom_grows_with_K(m, p):
+    """3xTF32 accuracy vs the contraction length: the fp32 tensor-core accumulator truncates at
+    every MMA, so the error grows with K = m. E3 uses m = 256; m = 512 and 1024
+    (E4's state size in fp32 mode) must stay within the 1e-5 bound too. Prints the margin."""
+    wl = S.make_random_mimo(m, p, p, L=1024, batch=2, N=9, rho=0.98, mode="fp32", seed=m)
+    e, es = check_parity(wl)
+    print(f"fp32 m={m}: rel {e:.2e} state {es:.2e} (bound 1e-5)")
