@@ -268,8 +268,13 @@ def test_bf16_siso_bank_on_tensor_cores(m):
     prof = pk.profile_read()
     pk.profile_enable(False)
     assert "direct" not in prof and "stage" not in prof, prof        # no CUDA-core GEMM classes
-    wl32 = S.Workload(**{**wl.__dict__, "mode": "fp32"})             # same values (bf16-exact u)
-    y32, _ = run_gpu(wl32)
+    from paper_2411_17729_b200.runner import DeviceWorkload
+    wl32 = S.Workload(**{**wl.__dict__, "mode": "fp32"})
+    u32 = S.bf16_bits_to_f64(wl.u_storage()).astype(np.float32)       # the same (bf16-exact) input values
+    dw32 = DeviceWorkload(wl32, u_host=u32)
+    dw32.step()
+    torch.cuda.synchronize()
+    y32 = dw32.y_f64()
     y32_bf = torch.from_numpy(y32).float().to(torch.bfloat16).double().numpy()
     assert np.array_equal(y_bf, y32_bf)
 
