@@ -39,12 +39,19 @@ constexpr int CW = 32;                    // epilogue chunk width (fp32 columns 
 constexpr int THREADS = 11 * 32;          // 0 TMA, 1 MMA, 2-5 epilogue, 6-9 transform, 10 residual
 // BN output columns per pair tile: 64 or 128 (two TMEM accumulators, 4 ring slots) or 256 (the
 // state chunk is staged and split once for all 256 columns; one accumulator, 3 ring slots)
-template <int BN>
+// SPLIT: main (hi.hi) accumulators per tile. The tensor core truncates its fp32 accumulator at every
+// MMA, so the main chain's error grows with K / 8; long contractions (K > 512) spread
+// the main chain over SPLIT = 3 accumulators (one third of the K chunks each, summed with
+// round-to-nearest in the epilogue), at the price of a single accumulator set (SPLIT mains + corr =
+// 4 x 128 = 512 TMEM columns, no double buffering).
+template <int BN, int SPLIT = 1>
 struct PCfg {
   static constexpr uint32_t W_BYTES = (BN / 2) * 128;             // this CTA's BN/2 weight rows, hi or lo
   static constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * W_BYTES;   // A hi | A lo | W hi | W lo
   static constexpr int STAGES = BN == 256 ? 3 : 4;
-  static constexpr int NACC = BN == 256 ? 1 : 2;
+  static constexpr int NACC = (BN == 256 || SPLIT > 1) ? 1 : 2;
+  static constexpr uint32_t ACC_COLS = (SPLIT + 1) * BN;           // SPLIT mains | corr
+  static_assert(NACC * ACC_COLS <= 512, "TMEM");
   static constexpr int NCH = BN / CW;
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE_BYTES + RS * R_BYTES;
 };
@@ -115,10 +122,10 @@ __device__ __forceinline__ PairCoord3 decode3(int64_t tile, const MimoArg& a, in
 }
 }  // namespace
 
-template <int BN>
+template <int BN, int SPLIT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     mimo_gemm_pair_tf32_kernel(const __grid_constant__ MimoMaps maps, MimoArg a) {
-  using C = PCfg<BN>;
+  using C = PCfg<BN, SPLIT>;
   constexpr int STAGES = C::STAGES, NACC = C::NACC, NCH = C::NCH;
   constexpr uint32_t STAGE_BYTES = C::STAGE_BYTES, W_BYTES = C::W_BYTES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -215,11 +222,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const int acc = (int)(t_local % NACC);
         mbar_wait_u(&tempty[acc], (uint32_t)((t_local / NACC) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tbase + acc * 2 * BN, dc = d + BN;
-        bool first = true;
+        const uint32_t d0 = tbase + acc * C::ACC_COLS, dc = d0 + SPLIT * BN;
+        int nk_all = 0;
+        for (int src = 0; src < a.n_src; ++src) nk_all += a.K[src] / BK;
+        bool fm[SPLIT], fc = true;                    // first write of each main / of the correction
+#pragma unroll
+        for (int i = 0; i < SPLIT; ++i) fm[i] = true;
+        int j = 0;                                    // K chunk of the tile, all sources in order
         for (int src = 0; src < a.n_src; ++src) {
           const int nk = a.K[src] / BK;
-          for (int kc = 0; kc < nk; ++kc) {
+          for (int kc = 0; kc < nk; ++kc, ++j) {
+            const int mi = SPLIT > 1 ? j * SPLIT / nk_all : 0;   // this chunk's main accumulator
+            const uint32_t d = d0 + mi * BN;
             mbar_wait_u(&full_w[s], ph);
             mbar_wait_u(&lo_ready[s], ph);
             tc_fence_after();
@@ -227,14 +241,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             const uint64_t al0 = make_sdesc(smem_u32(stAlo(s)), 16, 1024, LAYOUT_SW128);
             const uint64_t wd0 = make_sdesc(smem_u32(stW(s)), 16, 1024, LAYOUT_SW128);
             const uint64_t wl0 = make_sdesc(smem_u32(stW(s) + W_BYTES), 16, 1024, LAYOUT_SW128);
+            bool first_m = false;
+#pragma unroll
+            for (int i = 0; i < SPLIT; ++i)
+              if (i == mi) { first_m = fm[i]; fm[i] = false; }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint64_t ad = sdesc_add(ad0, k * 32), wd = sdesc_add(wd0, k * 32);
-              mma_tf32_pair_w(d, ad, wd, idesc, first ? 0u : 1u);                        // main: hi.hi
-              mma_tf32_pair_w(dc, sdesc_add(al0, k * 32), wd, idesc, first ? 0u : 1u);   // corr: lo.hi
+              mma_tf32_pair_w(d, ad, wd, idesc, (first_m && k == 0) ? 0u : 1u);           // main: hi.hi
+              mma_tf32_pair_w(dc, sdesc_add(al0, k * 32), wd, idesc, (fc && k == 0) ? 0u : 1u);   // corr: lo.hi
               mma_tf32_pair_w(dc, ad, sdesc_add(wl0, k * 32), idesc, 1u);                //     + hi.lo
-              first = false;
             }
+            fc = false;
             mma_commit_pair3(&empty[s]);
             if (++s == STAGES) { s = 0; ph ^= 1; }
           }
@@ -283,13 +301,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       for (int j = 0; j < NCH; ++j) {
         uint8_t* rbuf = sR + rs * R_BYTES;
         uint32_t vm[32], vc[32];
-        const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + acc * 2 * BN + j * CW;
-        tmem_ld32_3(taddr, vm);
-        tmem_ld32_3(taddr + BN, vc);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + acc * C::ACC_COLS + j * CW;
         float f[32];
+        if constexpr (SPLIT == 1) {
+          tmem_ld32_3(taddr, vm);
+          tmem_ld32_3(taddr + BN, vc);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int e = 0; e < 32; ++e) f[e] = __uint_as_float(vm[e]) + __uint_as_float(vc[e]);   // main + corr
+          for (int e = 0; e < 32; ++e) f[e] = __uint_as_float(vm[e]) + __uint_as_float(vc[e]);   // main + corr
+        } else {                                      // ((main_0 + main_1) + ...) + corr, round-to-nearest
+          tmem_ld32_3(taddr, vm);
+          tmem_ld32_3(taddr + SPLIT * BN, vc);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int e = 0; e < 32; ++e) f[e] = __uint_as_float(vm[e]);
+#pragma unroll
+          for (int i = 1; i < SPLIT; ++i) {
+            tmem_ld32_3(taddr + i * BN, vm);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int e = 0; e < 32; ++e) f[e] += __uint_as_float(vm[e]);
+          }
+#pragma unroll
+          for (int e = 0; e < 32; ++e) f[e] += __uint_as_float(vc[e]);
+        }
         if (j == NCH - 1) {                       // accumulator drained (values consumed): release it
           tc_fence_before();
           if (is_leader) mbar_arrive(&tempty[acc]);
@@ -341,9 +376,9 @@ bool mimo_pair_tf32_ok(const MimoGemm& g) {
   return true;
 }
 
-template <int BN>
+template <int BN, int SPLIT>
 static int launch_pt(const MimoGemm& g, cudaStream_t st) {
-  using C = PCfg<BN>;
+  using C = PCfg<BN, SPLIT>;
   MimoMaps maps;
   memset(&maps, 0, sizeof(maps));
   MimoArg a{};
@@ -370,18 +405,23 @@ static int launch_pt(const MimoGemm& g, cudaStream_t st) {
   a.out_row0 = (int)g.out_row0;
   if (g.R && !map3d(&maps.R, g.R, true, g.n_out, g.R_row0 + g.L, nseq_total, HM)) return CASC_ERR_CUDA;
   if (!map3d(&maps.out, g.out, true, g.n_out, g.out_row0 + g.L, nseq_total, HM)) return CASC_ERR_CUDA;
-  if (cudaFuncSetAttribute(mimo_gemm_pair_tf32_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(mimo_gemm_pair_tf32_kernel<BN, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)C::SMEM) != cudaSuccess)
     return CASC_ERR_CUDA;
   const int64_t blocks = (g.L + 2 * HM - 1) / (2 * HM) - g.t_first / 2;
   const int64_t tiles = (int64_t)g.batch * blocks * (g.n_out / BN);
   if (tiles <= 0) return CASC_OK;
   const int pairs = (int)std::min<int64_t>(tiles, 74);
-  mimo_gemm_pair_tf32_kernel<BN><<<2 * pairs, THREADS, C::SMEM, st>>>(maps, a);
+  mimo_gemm_pair_tf32_kernel<BN, SPLIT><<<2 * pairs, THREADS, C::SMEM, st>>>(maps, a);
   CASC_LAUNCHED();
   return CASC_OK;
 }
 
-int launch_mimo_gemm_pair_tf32(const MimoGemm& g, cudaStream_t st) { return launch_pt<128>(g, st); }
+int launch_mimo_gemm_pair_tf32(const MimoGemm& g, cudaStream_t st) {
+  int K = 0;
+  for (int s = 0; s < g.n_src; ++s) K += g.src[s].K;
+  // contractions longer than 512 (E3: 256) split the main chain (PCfg) to keep fp32 accuracy
+  return K > 512 ? launch_pt<128, 3>(g, st) : launch_pt<128, 1>(g, st);
+}
 
 }  // namespace casc

@@ -168,12 +168,12 @@ def test_bf16_every_row_E4_shape():
 
 @pytest.mark.parametrize("mode", ["fp32", "bf16"])
 def test_run_host_mimo_time_windows_bitwise(mode):
-    """Single-sequence first and last chunks run as 4 time windows (inputs [r0 - Hu, r1) for outputs
+    """Single-sequence first and last chunks run as 8 time windows (inputs [r0 - Hu, r1) for outputs
     [r0, r1), Hu = 2^(Ne+1) - 1: exact by the window property, pin T14), so the
     first window's compute starts before the chunk's whole input landed and the last chunk's output
     leaves window by window. Every kept row is computed by the same operations: bitwise the
     device-resident path, and within tolerance of the oracle."""
-    case = (128, 64, 64, 4096, 3, 5, mode)             # Ne = 5: Hu = 63, windows of 1024 rows
+    case = (128, 64, 64, 8192, 3, 5, mode)             # Ne = 5: Hu = 63, windows of 1024 rows
     y_win = _chunked_y(case, 3)                        # 3 chunks of one sequence each
     wl, u = _inputs(_mimo(*case), 1)
     y_dev = _device_y(wl, u)
