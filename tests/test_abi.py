@@ -72,3 +72,30 @@ def test_argument_validation_without_gpu(lib):
     assert lib.casc_apply_bank(2, 8, 10, 1, Nb, 3, 0, v, v, v, None, v, v, v, 1 << 30, None) == 2
     # run_host: bank requires SISO
     assert lib.casc_run_host(2, 8, 2, 1, 10, 1, Nb, 9, 0, v, v, v, None, v, v, v, 1 << 40, None) == 4
+
+
+def test_sharded_api_validation_without_gpu(lib):
+    """The sequence-sharded entry points validate before any CUDA call: an in-process group's
+    communicators carry rank / world; bad arguments return CASC_ERR_ARG / _DIM / _UNSUPPORTED."""
+    comms = (ctypes.c_void_p * 3)()
+    assert lib.casc_comm_init_local(comms, 3) == 0
+    r, w = ctypes.c_int(-1), ctypes.c_int(-1)
+    for i in range(3):
+        assert lib.casc_comm_rank(comms[i], ctypes.byref(r), ctypes.byref(w)) == 0
+        assert (r.value, w.value) == (i, 3)
+    v = ctypes.c_void_p(8)
+    args = lambda comm, m, p, q, L, N, Nmax, halo: (comm, m, p, q, L, 2, N, Nmax, 1, halo,  # noqa: E731
+                                                    v, v, v, None, v, v, v, 1 << 40, v, v)
+    assert lib.casc_apply_seqsharded(*args(None, 128, 64, 64, 1024, 5, 5, 0)) == 1          # no comm
+    assert lib.casc_apply_seqsharded(*args(comms[1], 128, 64, 64, 1024, 5, 5, 7)) == 1      # bad halo mode
+    assert lib.casc_apply_seqsharded(*args(comms[1], 128, 64, 64, 1024, 6, 5, 0)) == 2      # N > N_max
+    assert lib.casc_apply_seqsharded(*args(comms[1], 96, 64, 64, 1024, 5, 5, 0)) == 4       # m % 64 != 0
+    # world 3, L_loc = 100: 2^Ne = 64 fits, the one-shot window 2^(Ne+1) - 1 = 127 does not
+    assert lib.casc_apply_seqsharded(*args(comms[1], 128, 64, 64, 100, 6, 6, 1)) == 4
+    # workspaces: per-stage halo (2^Ne rows per state buffer) vs one-shot (2^(Ne+1)-1 rows of u and v)
+    per = lib.casc_apply_seqsharded_workspace(128, 64, 64, 100, 2, 6, 3, 1, 0)
+    one = lib.casc_apply_seqsharded_workspace(128, 64, 64, 100, 2, 6, 3, 1, 1)
+    assert per >= 2 * (64 + 100) * 2 * 128 * 2 and one >= 2 * (127 + 100) * 2 * 128 * 2
+    for i in range(3):
+        assert lib.casc_comm_destroy(comms[i]) == 0
+    assert lib.casc_comm_destroy(None) == 1
