@@ -157,8 +157,10 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
  *     Rank r of `world` owns global time rows [r*L_loc, (r+1)*L_loc) of every sequence of ONE
  *     system (m, p, q multiples of 64). The cascade's stage k reads
  *     v_{l-2^k}, so before stage k each rank receives the last 2^k time rows of v^(k) from rank
- *     r-1 (zeros on rank 0: x_{-1} = 0); the fused first step needs one row of u,
- *     the fused last step (y = C v + C P_Ne v_{l-2^Ne} + D u, R21) 2^Ne rows of v.
+ *     r-1 (zeros on rank 0: x_{-1} = 0); the first step needs 3 rows of u (the
+ *     Krylov head over four lags, R28; 1 row when Ne = 1), the output step the rows of v
+ *     it reads before l: 2^Ne of v^(Ne) (y = C v + C P_Ne v_{l-2^Ne} + D u, R21) or, for Ne >= 3,
+ *     3 * 2^(Ne-1) of v^(Ne-1) (the last stage folded into y, R31).
  *     Ne = min(N, floor(log2(L - 1))) for the GLOBAL length L = world * L_loc (R20).
  *     The library does the exchange itself: grouped ncclSend(r -> r+1) / ncclRecv(r-1 -> r) on
  *     `comm_stream`, overlapped with the interior rows of the same step on `compute_stream`
@@ -184,7 +186,7 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
  *   host synchronisation except inside the local transport's rendezvous (host threads wait for
  *   their neighbours to enqueue, never for the device).
  * Errors: CASC_ERR_ARG, CASC_ERR_DIM, CASC_ERR_WORKSPACE, CASC_ERR_UNSUPPORTED (m, p, q not
- *   multiples of 64, or world > 1 with 2^Ne > L_loc: a halo would span several ranks),
+ *   multiples of 64, or world > 1 with a halo longer than L_loc: it would span several ranks),
  *   CASC_ERR_CUDA, CASC_ERR_NCCL (libnccl missing, or an NCCL call failed).
  * -------------------------------------------------------------------------------------- */
 int casc_nccl_unique_id(void* id_out);

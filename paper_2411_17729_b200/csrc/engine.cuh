@@ -41,8 +41,8 @@ int engine_mimo_tc(int m, int p, int q, int64_t L, int batch, int N, int N_max, 
 // MIMO workspace (mimo_engine.cu): derived float64 weights, their operand-format images, and the
 // two state buffers of batch * L rows of m (ping-pong)
 struct MimoWs {
-  double *AB64, *CP64, *CBD64, *CAB64, *A2B64, *A3B64;
-  void *Bb, *AB, *C, *CP, *D, *CBD, *CAB, *A2B, *A3B;   // operand-format weights (bf16, or tf32 hi/lo planes)
+  double *AB64, *CP64, *CBD64, *CAB64, *A2B64, *A3B64, *CP1_64, *CP3_64;
+  void *Bb, *AB, *C, *CP, *D, *CBD, *CAB, *A2B, *A3B, *CP1, *CP3;   // operand-format weights (bf16, or tf32 hi/lo)
   void *Va, *Vb;
   size_t bytes;
 };
@@ -52,6 +52,18 @@ MimoWs carve_mimo(void* ws, int m, int p, int q, int64_t L, int batch, int mode)
 // rounded once to the GEMM operand format
 int mimo_derive(int m, int p, int q, int Ne, const PackLayout& P, const double* Bbar, const double* C,
                 const double* D, const MimoWs& w, bool tf32, cudaStream_t st);
+// R31 (the MIMO output fold): with Ne >= 3 the last stage Ne-1 is folded into the output step,
+// y = C v' + (C P_{Ne-1}) v'_{l-h} + (C P_Ne) v'_{l-2h} + (C P_Ne P_{Ne-1}) v'_{l-3h} + D u_l,
+// v' = v^(Ne-1), h = 2^(Ne-1); the streaming stages run k0 .. Ne-2
+inline bool mimo_fold(int Ne) { return Ne >= 3; }
+// time rows of v the output step reads before l: 3 h (fold) or 2^Ne
+inline int64_t mimo_out_halo(int Ne) { return Ne <= 0 ? 0 : (mimo_fold(Ne) ? 3 * ((int64_t)1 << (Ne - 1)) : (int64_t)1 << Ne); }
+// the output step as a shifted GEMM over the buffer V holding v^(Ne) (or v^(Ne-1) with the fold):
+// sources at row shifts (0, h, 2h, 3h) x unit (unit = batch for time-major shards, 1 otherwise),
+// reading V and u with row0 halo rows in front; D (q x p) as the last source when present
+struct MimoGemm;
+void mimo_output_gemm(MimoGemm& g, const MimoWs& w, int Ne, int m, int p, int q, const void* V, int64_t v_row0,
+                      const void* u, int64_t u_row0, bool has_D, int64_t unit);
 // the MIMO cascade steps with the derived weights already in ws (engine_mimo_tc = derive + run);
 // out_skip: leading window rows of history that are not written to y (batch == 1)
 int mimo_run(int m, int p, int q, int64_t L, int batch, int Ne, int N_max, int mode, const void* pack, bool has_D,

@@ -50,6 +50,8 @@ MimoWs carve_mimo(void* ws, int m, int p, int q, int64_t L, int batch, int mode)
   w.CAB64 = c.take<double>((size_t)q * p);
   w.A2B64 = c.take<double>((size_t)m * p);
   w.A3B64 = c.take<double>((size_t)m * p);
+  w.CP1_64 = c.take<double>((size_t)q * m);
+  w.CP3_64 = c.take<double>((size_t)q * m);
   w.Bb = c.take<char>((size_t)m * p * wes);
   w.AB = c.take<char>((size_t)m * p * wes);
   w.C = c.take<char>((size_t)q * m * wes);
@@ -59,6 +61,8 @@ MimoWs carve_mimo(void* ws, int m, int p, int q, int64_t L, int batch, int mode)
   w.CAB = c.take<char>((size_t)q * p * wes);
   w.A2B = c.take<char>((size_t)m * p * wes);
   w.A3B = c.take<char>((size_t)m * p * wes);
+  w.CP1 = c.take<char>((size_t)q * m * wes);
+  w.CP3 = c.take<char>((size_t)q * m * wes);
   const size_t vbytes = (size_t)batch * (size_t)L * m * ses;
   w.Va = c.take<char>(vbytes);
   w.Vb = c.take<char>(vbytes);
@@ -137,7 +141,8 @@ int mimo_run(int m, int p, int q, int64_t L, int batch, int Ne, int N_max, int m
     ps.exec(rows * (p + m) * es, rows * 2.0 * g.n_src * m * p * xf, pipe);
     if ((rc = launch_mimo_gemm(g, tf32, st))) return rc;
   }
-  for (int k = k0; k <= Ne - 1; ++k) {
+  const int kl = mimo_fold(Ne) ? Ne - 1 : Ne;     // the state level the output step reads (R31)
+  for (int k = k0; k <= kl - 1; ++k) {
     void* Vs = (k - 1) % 2 == 0 ? w.Va : w.Vb;
     void* Vd = (k % 2 == 0) ? w.Va : w.Vb;
     // stage weight P_k: bf16 [m][m] or the tf32 pair [2][m][m] of the pack
@@ -150,23 +155,39 @@ int mimo_run(int m, int p, int q, int64_t L, int batch, int Ne, int N_max, int m
     if ((rc = launch_mimo_gemm(g, tf32, st))) return rc;
   }
   {
-    void* V = (Ne - 1) % 2 == 0 ? w.Va : w.Vb;
+    void* V = (kl - 1) % 2 == 0 ? w.Va : w.Vb;     // holds v^(kl)
     MimoGemm g{};
-    g.src[0] = {V, w.C, m, 0};
-    g.src[1] = {V, w.CP, m, (int64_t)1 << Ne};
-    g.src[0].row0 = g.src[1].row0 = out_skip;       // window history rows in front (out_skip > 0)
-    g.n_src = 2;
-    if (has_D) {
-      g.src[2] = {u, w.D, p, 0};
-      g.src[2].row0 = out_skip;
-      g.n_src = 3;
-    }
+    mimo_output_gemm(g, w, Ne, m, p, q, V, out_skip, u, out_skip, has_D, 1);
     g.out = y; g.n_out = q; g.L = L - out_skip; g.batch = batch;
-    ProfScope ps(st, K_MIMO_LAST, yrows * (m + p + q) * es, yrows * (4.0 * q * m + 2.0 * q * p));
-    ps.exec(yrows * (m + p + q) * es, yrows * (4.0 * q * m + (has_D ? 2.0 * q * p : 0.0)) * xf, pipe);
+    const double k_in = (double)(g.n_src - (has_D ? 1 : 0)) * m + (has_D ? p : 0);
+    ProfScope ps(st, K_MIMO_LAST, yrows * (m + p + q) * es, yrows * 2.0 * q * k_in);
+    ps.exec(yrows * (m + p + q) * es, yrows * 2.0 * q * k_in * xf, pipe);
     if ((rc = launch_mimo_gemm(g, tf32, st))) return rc;
   }
   return CASC_OK;
+}
+
+void mimo_output_gemm(MimoGemm& g, const MimoWs& w, int Ne, int m, int p, int q, const void* V, int64_t v_row0,
+                      const void* u, int64_t u_row0, bool has_D, int64_t unit) {
+  (void)q;
+  if (mimo_fold(Ne)) {
+    const int64_t h = ((int64_t)1 << (Ne - 1)) * unit;
+    g.src[0] = {V, w.C, m, 0};
+    g.src[1] = {V, w.CP1, m, h};
+    g.src[2] = {V, w.CP, m, 2 * h};
+    g.src[3] = {V, w.CP3, m, 3 * h};
+    g.n_src = 4;
+  } else {
+    g.src[0] = {V, w.C, m, 0};
+    g.src[1] = {V, w.CP, m, ((int64_t)1 << Ne) * unit};
+    g.n_src = 2;
+  }
+  for (int i = 0; i < g.n_src; ++i) g.src[i].row0 = v_row0;
+  if (has_D) {
+    g.src[g.n_src] = {u, w.D, p, 0};
+    g.src[g.n_src].row0 = u_row0;
+    ++g.n_src;
+  }
 }
 
 // Derived weights of the fused first / last stages (R21), float64 then rounded to the
@@ -211,6 +232,18 @@ int mimo_derive(int m, int p, int q, int Ne, const PackLayout& P, const double* 
       if ((rc = launch_dgemm(a, 1, st))) return rc;
       if ((rc = convert_weight(w.A2B64, w.A2B, (int64_t)m * p, tf32, st))) return rc;
       if ((rc = convert_weight(w.A3B64, w.A3B, (int64_t)m * p, tf32, st))) return rc;
+    }
+    if (mimo_fold(Ne)) {                                           // output fold (R31)
+      a = DgemmArg{};                                              // C P_{Ne-1}
+      a.M = q; a.N = m; a.K = m;
+      a.A = C; a.lda = m; a.B = P.p64 + (Ne - 1) * mm; a.ldb = m; a.C = w.CP1_64; a.ldc = m;
+      if ((rc = launch_dgemm(a, 1, st))) return rc;
+      a = DgemmArg{};                                              // (C P_Ne) P_{Ne-1}
+      a.M = q; a.N = m; a.K = m;
+      a.A = w.CP64; a.lda = m; a.B = P.p64 + (Ne - 1) * mm; a.ldb = m; a.C = w.CP3_64; a.ldc = m;
+      if ((rc = launch_dgemm(a, 1, st))) return rc;
+      if ((rc = convert_weight(w.CP1_64, w.CP1, (int64_t)q * m, tf32, st))) return rc;
+      if ((rc = convert_weight(w.CP3_64, w.CP3, (int64_t)q * m, tf32, st))) return rc;
     }
   }
   return CASC_OK;

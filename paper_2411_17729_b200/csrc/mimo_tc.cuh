@@ -6,7 +6,7 @@
 
 namespace casc {
 
-constexpr int kMaxSrc = 4;        // sources of one shifted GEMM (the MIMO head uses four lags)
+constexpr int kMaxSrc = 5;        // sources of one shifted GEMM (MIMO head: four lags; folded output: 4 + D)
 struct MimoMaps {                 // passed as one __grid_constant__ kernel parameter
   CUtensorMap A[kMaxSrc];         // source signals [seq][L][K_src]    box {128 B, 128, 1}
   CUtensorMap W[kMaxSrc];         // weight planes [plane][n_out][K]   box {128 B, BN, 1}

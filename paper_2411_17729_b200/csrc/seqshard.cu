@@ -199,7 +199,7 @@ static SeqWs carve_seq(void* ws, int m, int p, int q, int64_t L_loc, int batch, 
   Carver c(ws);
   c.off = w.mw.bytes;
   const size_t es = mode == CASC_FP32 ? 4 : 2;
-  const int64_t rows = L_loc * batch, H = Ne > 0 ? ((int64_t)1 << Ne) : 0;
+  const int64_t rows = L_loc * batch, H = mimo_out_halo(Ne);
   const int uh = u_halo_rows(Ne);
   const int64_t Bu = boundary_rows(uh, batch, rows);
   w.u_edge = c.take<char>((size_t)(uh * batch + Bu) * p * es);
@@ -300,7 +300,8 @@ static int apply_oneshot(Comm* c, int m, int p, int q, int64_t L_loc, int batch,
     g.out = k0 == 2 ? w.Vb : w.Va; g.n_out = m;
     if ((rc = run(g, ext, K_MIMO_FIRST, dr * (p + m) * es, dr * 2.0 * g.n_src * m * p))) return rc;
   }
-  for (int k = k0; k <= Ne - 1; ++k) {  // stages over the window (rows before it read zeros)
+  const int kl = mimo_fold(Ne) ? Ne - 1 : Ne;   // the level the output step reads (R31)
+  for (int k = k0; k <= kl - 1; ++k) {  // stages over the window (rows before it read zeros)
     void* Vs = (k - 1) % 2 == 0 ? w.Va : w.Vb;
     void* Vd = (k % 2 == 0) ? w.Va : w.Vb;
     const void* Wk = tf32 ? static_cast<const void*>(P.f32 + k * 2 * mm) : static_cast<const void*>(P.b16 + k * mm);
@@ -309,16 +310,12 @@ static int apply_oneshot(Comm* c, int m, int p, int q, int64_t L_loc, int batch,
     g.n_src = 1; g.R = Vs; g.out = Vd; g.n_out = m;
     if ((rc = run(g, ext, K_MIMO_STAGE, dr * m * es * 2.0, dr * 2.0 * (double)mm))) return rc;
   }
-  void* V = (Ne - 1) % 2 == 0 ? w.Va : w.Vb;   // y on the local rows: y = C v + (C P_Ne) v_{l-2^Ne} + D u
+  void* V = (kl - 1) % 2 == 0 ? w.Va : w.Vb;   // y on the local rows from v^(kl) (R21 / R31) + D u
   MimoGemm g{};
-  g.src[0] = {V, w.mw.C, m, 0};
-  g.src[1] = {V, w.mw.CP, m, ((int64_t)1 << Ne) * batch};
-  g.src[0].row0 = g.src[1].row0 = hr;
-  g.n_src = 2;
-  if (D) { g.src[2] = {u_loc, w.mw.D, p, 0}; g.n_src = 3; }
+  mimo_output_gemm(g, w.mw, Ne, m, p, q, V, hr, u_loc, 0, D != nullptr, batch);
   g.out = y_loc; g.n_out = q;
-  return run(g, rows, K_MIMO_LAST, (double)rows * (m + p + q) * es,
-             (double)rows * (4.0 * q * m + (D ? 2.0 * q * p : 0.0)));
+  const double k_in = (double)(g.n_src - (D ? 1 : 0)) * m + (D ? p : 0);
+  return run(g, rows, K_MIMO_LAST, (double)rows * (m + p + q) * es, (double)rows * 2.0 * q * k_in);
 }
 
 
@@ -420,13 +417,13 @@ int casc_apply_seqsharded(void* comm, int m, int p, int q, int64_t L_loc, int ba
   }
   // each halo must come from the immediate predecessor (holds for configs[3] up to 8 ranks)
   const int uh = u_halo_rows(Ne);
-  if (c->world > 1 && ((Ne > 0 && ((int64_t)1 << Ne) > L_loc) || uh > L_loc)) return CASC_ERR_UNSUPPORTED;
+  if (c->world > 1 && (mimo_out_halo(Ne) > L_loc || uh > L_loc)) return CASC_ERR_UNSUPPORTED;
   SeqWs w = carve_seq(ws, m, p, q, L_loc, batch, Ne, mode);
   if (ws_bytes < w.bytes) return CASC_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)compute_stream, cs = (cudaStream_t)comm_stream;
   const bool tf32 = mode == CASC_FP32;
   const size_t es = tf32 ? 4 : 2;
-  const int64_t rows = L_loc * batch, H = Ne > 0 ? ((int64_t)1 << Ne) : 0, Hr = H * batch;
+  const int64_t rows = L_loc * batch, H = mimo_out_halo(Ne), Hr = H * batch;
   PackLayout P = pack_layout(const_cast<void*>(pack), 1, m, N_max, mode);
   const int64_t mm = (int64_t)m * m;
   if ((rc = mimo_derive(m, p, q, Ne, P, Bbar, C, D, w.mw, tf32, st))) return rc;
@@ -507,11 +504,14 @@ int casc_apply_seqsharded(void* comm, int m, int p, int q, int64_t L_loc, int ba
     }
     if ((rc = two_launches(g, gb, uh, K_MIMO_FIRST, dr * (p + m) * es, dr * 2.0 * g.n_src * m * p))) return rc;
   }
-  // ---- stages k = k0 .. Ne-1 and the last step: halo of 2^k rows of v^(k) before each
-  for (int k = k0; k <= Ne; ++k) {
+  // ---- stages k = k0 .. kl-1 and the output step (from v^(kl), kl = Ne or Ne - 1 with the fold,
+  // R31): before each, the halo of the rows of v^(k) it reads before l (2^k, or mimo_out_halo)
+  const int kl = mimo_fold(Ne) ? Ne - 1 : Ne;
+  for (int k = k0; k <= kl; ++k) {
     void* Vs = (k - 1) % 2 == 0 ? w.Va : w.Vb;       // holds v^(k)
     void* Vd = (k % 2 == 0) ? w.Va : w.Vb;
-    const int64_t d = ((int64_t)1 << k) * batch;     // halo rows of this step
+    const int64_t d_time = k < kl ? ((int64_t)1 << k) : mimo_out_halo(Ne);
+    const int64_t d = d_time * batch;                // halo rows of this step
     cudaEvent_t ev_tail;
     if ((rc = new_event(&ev_tail))) return rc;
     CASC_TRY(cudaEventRecord(ev_tail, st));          // v^(k) complete on every local row
@@ -523,21 +523,17 @@ int casc_apply_seqsharded(void* comm, int m, int p, int q, int64_t L_loc, int ba
         return rc;
     }
     MimoGemm g{};
-    if (k < Ne) {
+    if (k < kl) {
       const void* Wk = tf32 ? static_cast<const void*>(P.f32 + k * 2 * mm) : static_cast<const void*>(P.b16 + k * mm);
       g.src[0] = {Vs, Wk, m, d};
       g.src[0].row0 = Hr;
       g.n_src = 1; g.R = Vs; g.R_row0 = Hr; g.out = Vd; g.out_row0 = Hr; g.n_out = m;
       if ((rc = two_launches(g, g, (int64_t)1 << k, K_MIMO_STAGE, dr * m * es * 2.0, dr * 2.0 * (double)mm))) return rc;
-    } else {                           // y = C v + (C P_Ne) v_{l-2^Ne} + D u
-      g.src[0] = {Vs, w.mw.C, m, 0};
-      g.src[1] = {Vs, w.mw.CP, m, d};
-      g.src[0].row0 = g.src[1].row0 = Hr;
-      g.n_src = 2;
-      if (D) { g.src[2] = {u_loc, w.mw.D, p, 0}; g.n_src = 3; }
+    } else {                           // y = C v + (C P_Ne) v_{l-2^Ne} + D u, or the folded form (R31)
+      mimo_output_gemm(g, w.mw, Ne, m, p, q, Vs, Hr, u_loc, 0, D != nullptr, batch);
       g.out = y_loc; g.n_out = q;
-      if ((rc = two_launches(g, g, (int64_t)1 << k, K_MIMO_LAST, dr * (m + p + q) * es,
-                             dr * (4.0 * q * m + (D ? 2.0 * q * p : 0.0)))))
+      const double k_in = (double)(g.n_src - (D ? 1 : 0)) * m + (D ? p : 0);
+      if ((rc = two_launches(g, g, d_time, K_MIMO_LAST, dr * (m + p + q) * es, dr * 2.0 * q * k_in)))
         return rc;
     }
   }

@@ -3,8 +3,9 @@
 It reproduces the schedule the CUDA path runs -- time-major buffers [H + L_loc][batch][dim] with
 the halo rows in front, a u halo of uh time rows before the first step (uh = 3 for the Krylov head
 v^(2) = sum_{j<4} Abar^j Bbar u_{l-j} when Ne >= 2, R28; uh = 1 for the fused first step),
-a halo of the last 2^k time rows of v^(k) before stage k, 2^Ne rows before the fused last step
-(R21), rank 0's halo zero (x_{-1} = 0) -- with the per-step arithmetic written out in
+a halo of the last 2^k time rows of v^(k) before stage k, and before the output step the rows it
+reads: 2^Ne of v^(Ne) (R21), or with the output fold for Ne >= 3 (R31) 3*2^(Ne-1) rows of
+v^(Ne-1) (stage Ne-1 folded into y); rank 0's halo zero (x_{-1} = 0) -- with the per-step arithmetic written out in
 float64, so
 the exchange bookkeeping can be checked on the CPU against the oracle: with the real
 torch.distributed exchange (gloo, world_size 2, DistComm) and with emulated ranks (LocalComm).
@@ -89,6 +90,8 @@ class F64Steps:
         self.Bb, self.AB = Bb, Ab @ Bb
         self.Kr = [Bb, self.AB, Ab @ self.AB, Ab @ (Ab @ self.AB)]     # Abar^j Bbar, j < 4 (head)
         self.C, self.CP, self.D = Cm, Cm @ self.P[Ne], Dm
+        if Ne >= 3:                                                    # output fold (R31)
+            self.CP1, self.CP3 = Cm @ self.P[Ne - 1], (Cm @ self.P[Ne]) @ self.P[Ne - 1]
         self.CBD, self.CAB = Cm @ Bb + Dm, Cm @ (Ab @ Bb)
 
     def first(self, sh, H):
@@ -112,6 +115,11 @@ class F64Steps:
             sh.y[:] = u[uh:] @ self.CBD.T + u[uh - 1:-1] @ self.CAB.T
             return
         L = sh.y.shape[0]
+        if Ne >= 3:                                   # V holds v^(Ne-1): y from four shifts (R31)
+            h = 1 << (Ne - 1)
+            sh.y[:] = (V[H:] @ self.C.T + V[H - h:H - h + L] @ self.CP1.T + V[H - 2 * h:H - 2 * h + L] @ self.CP.T
+                       + V[H - 3 * h:H - 3 * h + L] @ self.CP3.T + u[uh:] @ self.D.T)
+            return
         s = 1 << Ne
         sh.y[:] = V[H:] @ self.C.T + V[H - s:H - s + L] @ self.CP.T + u[uh:] @ self.D.T
 
@@ -119,10 +127,10 @@ class F64Steps:
 def run(steps, comm, shards, N: int, L_global: int) -> None:
     """The sharded cascade over `shards` (this process's shards, in rank order)."""
     Ne = effective_order(N, L_global)
-    H = (1 << Ne) if Ne > 0 else 0
+    H = out_halo(Ne)
     L_loc = shards[0].y.shape[0]
-    if Ne > 0 and (1 << Ne) > L_loc:
-        raise NotImplementedError(f"halo 2^{Ne} exceeds the shard length {L_loc}")
+    if H > L_loc:
+        raise NotImplementedError(f"halo {H} exceeds the shard length {L_loc}")
     uh = u_halo_rows(Ne)
     comm.exchange([s.u_ext for s in shards], uh, uh)           # u_{-uh..-1} for the first step
     if Ne == 0:
@@ -137,19 +145,26 @@ def run(steps, comm, shards, N: int, L_global: int) -> None:
         for s in shards:
             steps.first(s, H)
         src, dst, k0 = [s.Va for s in shards], [s.Vb for s in shards], 1
-    for k in range(k0, Ne):
+    kl = Ne - 1 if Ne >= 3 else Ne                            # the level the output step reads
+    for k in range(k0, kl):
         comm.exchange(src, H, 1 << k)                             # last 2^k rows of v^(k)
         for s, a, b in zip(shards, src, dst):
             steps.stage(k, s, a, b, H)
         src, dst = dst, src
-    comm.exchange(src, H, 1 << Ne)
+    comm.exchange(src, H, H)
     for s, a in zip(shards, src):
         steps.last(Ne, s, a, H)
 
 
+def out_halo(Ne: int) -> int:
+    """Rows of v the output step reads before l: 3*2^(Ne-1) with the fold (Ne >= 3), else 2^Ne."""
+    if Ne <= 0:
+        return 0
+    return 3 * (1 << (Ne - 1)) if Ne >= 3 else 1 << Ne
+
+
 def shard_H(N: int, L_global: int) -> int:
-    Ne = effective_order(N, L_global)
-    return (1 << Ne) if Ne > 0 else 0
+    return out_halo(effective_order(N, L_global))
 
 
 def run_oneshot(steps_factory, comm, u_locs, m: int, q: int, N: int, L_global: int):

@@ -66,7 +66,8 @@ def _sharded(wl, R, comms, halo="per_stage"):
 
 CASES = [  # (R, m, p, q, L, N)
     (2, 128, 64, 64, 4096, 8),
-    (4, 64, 64, 64, 2048, 9),       # 2^Ne = 512 = L_loc: the halo is a whole shard
+    (2, 64, 64, 64, 2048, 9),       # output halo 3 * 2^8 = 768 of L_loc = 1024 rows (R31)
+    (4, 64, 64, 64, 1024, 2),       # Ne = 2: no fold, head only
     (8, 128, 64, 128, 8192, 6),
     (2, 64, 64, 64, 256, 0),        # Ne = 0: one fused step
     (3, 256, 64, 64, 3000, 7),      # rows not a multiple of the 256-row blocks
