@@ -222,7 +222,7 @@ def roofline(prof: dict, mode: str, cfg: str):
     out.update({
         "traffic": ncu_traffic(cls, cfg), "kernel": cls, "launches_timed": r["launches"],
         "avg_launch_ms": t * 1e3, "peak_note": note,
-        "executed": {"bytes_per_launch": xby, "flops_per_launch": xfl, "pipe": pipe,
+        "executed": {"bytes_per_launch": xby, "flops_per_launch": xfl, "pipe": pipe, "tensor_peak": which,
                      "t_roof_hbm_ms": t_hbm * 1e3, "t_roof_tensor_ms": t_ten * 1e3,
                      "frac_of_binding_roof": max(t_hbm, t_ten) / t},
         "algorithmic": {"bytes_per_launch": by, "flops_per_launch": fl,
