@@ -30,6 +30,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <condition_variable>
 #include <cstdio>
 #include <cstring>
@@ -108,6 +109,10 @@ struct LocalGroup {
   }
 };
 
+// how long an emulated rank waits for its neighbour to enqueue an exchange before reporting the
+// group broken (CASC_ERR_NCCL): only host enqueue progress is awaited, never device work
+static constexpr std::chrono::seconds kRendezvous{300};
+
 struct Comm {
   int kind = 0;                 // 0 NCCL, 1 local
   int rank = 0, world = 1;
@@ -147,7 +152,8 @@ static int exchange(Comm* c, const void* sbuf, size_t sbytes, void* rbuf, size_t
       LocalGroup::Post p;
       {
         std::unique_lock<std::mutex> lk(g.mu);
-        g.cv.wait(lk, [&] { return g.sends.count({c->rank, tag}) > 0; });
+        // a neighbour that failed before posting would leave this rank waiting: bounded wait
+        if (!g.cv.wait_for(lk, kRendezvous, [&] { return g.sends.count({c->rank, tag}) > 0; })) return CASC_ERR_NCCL;
         p = g.sends[{c->rank, tag}];
       }
       if (p.bytes != rbytes) return CASC_ERR_DIM;
@@ -165,7 +171,7 @@ static int exchange(Comm* c, const void* sbuf, size_t sbytes, void* rbuf, size_t
       cudaEvent_t cp;
       {
         std::unique_lock<std::mutex> lk(g.mu);
-        g.cv.wait(lk, [&] { return g.copied.count({c->rank, tag}) > 0; });
+        if (!g.cv.wait_for(lk, kRendezvous, [&] { return g.copied.count({c->rank, tag}) > 0; })) return CASC_ERR_NCCL;
         cp = g.copied[{c->rank, tag}];
       }
       CASC_TRY(cudaStreamWaitEvent(cs, cp, 0));
