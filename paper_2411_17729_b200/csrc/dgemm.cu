@@ -265,18 +265,4 @@ int launch_f64_to_f32(const double* src, float* dst, int64_t n, cudaStream_t st)
   return CASC_OK;
 }
 
-__global__ void fill_f64_kernel(double* dst, int64_t n, double v) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = v;
-}
-
-int launch_fill_f64(double* dst, int64_t n, double v, cudaStream_t st) {
-  if (n <= 0) return CASC_OK;
-  int blocks = (int)std::min<int64_t>(ceil_div(n, 256), 148 * 8);
-  fill_f64_kernel<<<blocks, 256, 0, st>>>(dst, n, v);
-  CASC_LAUNCHED();
-  return CASC_OK;
-}
-
 }  // namespace casc

@@ -18,7 +18,6 @@ int launch_dgemm(const DgemmArg& a, int n_sys, cudaStream_t st);
 int launch_pack(const PackLayout& P, int n_sys, int N_max, int m, cudaStream_t st);
 int launch_powers_small(const PackLayout& P, const double* Abar, int n_sys, int N_max, int m, cudaStream_t st);
 int launch_f64_to_f32(const double* src, float* dst, int64_t n, cudaStream_t st);
-int launch_fill_f64(double* dst, int64_t n, double v, cudaStream_t st);
 
 // ---------------------------------------------------------------- shifted multi-source GEMM
 // out[s][b][l][n] = sum_src sum_j A_src[s][b][l - shift_src(s)][j] * W_src[s][n][j]

@@ -112,13 +112,6 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
       ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
-__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                        uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-      ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
 // Warp-collective issue: the whole converged warp executes these and one lane (elect.sync)
 // issues. The operands stay warp-uniform, so ptxas keeps them in uniform registers; issuing from
 // a single divergent lane instead wraps every MMA in a per-lane waterfall loop with R2UR
@@ -133,43 +126,10 @@ __device__ __forceinline__ void mma_f16_w(uint32_t d, uint64_t adesc, uint64_t b
                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
                ::"r"(d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
-// A operand in TMEM (lane = row, one 32-bit element per column)
-__device__ __forceinline__ void mma_tf32_ts_w(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-  asm volatile("{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-               "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
-               ::"r"(d), "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc));
-}
-// One K chunk (32 tf32 = 4 K-steps) of the 3xTF32 product with A in TMEM, in ONE asm block:
-//   d  (+)= A_hi W_hi        dc (+)= A_lo W_hi + A_hi W_lo
-// ah/al: TMEM column addresses of the chunk's hi / lo parts (8 columns per K-step); wd/wl: SW128
-// K-major descriptors of W hi / lo (32 B per K-step = +2 in the start field). `acc` = 0 starts both
-// accumulators. Passing the base operands once lets ptxas form the twelve MMAs' operands with
-// uniform-register adds instead of converting every operand per MMA (R2UR), which dominated the
-// issue time of the per-MMA helpers.
-__device__ __forceinline__ void mma_3xtf32_ts_chunk_w(uint32_t d, uint32_t dc, uint32_t ah, uint32_t al, uint64_t wd,
-                                                      uint64_t wl, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t.reg .b32 a1, a2, a3, l1, l2, l3;\n\t.reg .b64 w1, w2, w3, v1, v2, v3;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %7, 0;\n\t"
-      "add.u32 a1, %2, 8;\n\tadd.u32 a2, %2, 16;\n\tadd.u32 a3, %2, 24;\n\t"
-      "add.u32 l1, %3, 8;\n\tadd.u32 l2, %3, 16;\n\tadd.u32 l3, %3, 24;\n\t"
-      "add.u64 w1, %4, 2;\n\tadd.u64 w2, %4, 4;\n\tadd.u64 w3, %4, 6;\n\t"
-      "add.u64 v1, %5, 2;\n\tadd.u64 v2, %5, 4;\n\tadd.u64 v3, %5, 6;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %4, %6, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%3], %4, %6, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%2], %5, %6, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a1], w1, %6, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [l1], w1, %6, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [a1], v1, %6, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a2], w2, %6, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [l2], w2, %6, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [a2], v2, %6, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a3], w3, %6, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [l3], w3, %6, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [a3], v3, %6, 1;\n\t}"
-      ::"r"(d), "r"(dc), "r"(ah), "r"(al), "l"(wd), "l"(wl), "r"(idesc), "r"(acc));
-}
-// The same chunk with 8 MMAs: the hi.hi and hi.lo products share A = a_hi, so one N = 2*64 MMA
+// One K chunk (32 tf32 = 4 K-steps) of the 3xTF32 product with A in TMEM (ah / al: TMEM columns of
+// the chunk's hi / lo parts, 8 columns per K-step; wd: SW128 K-major descriptor of [W hi | W lo],
+// 32 B per K-step = +2 in the start field), in ONE asm block so ptxas forms the operands with
+// uniform-register adds. The hi.hi and hi.lo products share A = a_hi, so one N = 2*64 MMA
 // against [W hi | W lo] (lo stored right after hi: one K-major SW128 operand of 128 rows) writes
 // hi.hi to d and hi.lo to d + 64 = dc; lo.hi then accumulates into dc. Fewer MMA instructions and
 // operands per chunk (the issuing warp's instruction stream bounds the N = 64 bank stage).
@@ -247,18 +207,6 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                ::"r"(smem_u32(bar)) : "memory");
 }
-
-// ------------------------------------------------------------------ cp.async (16 B, L2 only)
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem),
-               "r"(valid ? 16 : 0) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 }  // namespace sm100
 }  // namespace casc
