@@ -180,3 +180,14 @@ def test_run_host_mimo_time_windows_bitwise(mode):
     assert np.array_equal(y_win, y_dev)
     assert rel(y_win, _oracle(wl)) <= TOL[mode]
 
+
+
+def test_bank_run_host_bf16_bitwise():
+    """casc_run_host for a bf16 SISO bank (fp32 tensor-core bank path on converted copies, serial
+    host path): bitwise the device-resident path, within the bf16 bound of the oracle."""
+    wl = S.make_E2(n_ch=5, L=2048, batch=2, seed=9, mode="bf16")
+    for k in range(2):
+        wlk, u = _inputs(wl, k)
+        y_host = _run_host(wlk, u)
+        assert np.array_equal(y_host, _device_y(wlk, u))
+        assert rel(y_host, _oracle(wlk)) <= TOL["bf16"]
