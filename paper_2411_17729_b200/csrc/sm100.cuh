@@ -126,6 +126,36 @@ __device__ __forceinline__ void mma_f16_w(uint32_t d, uint64_t adesc, uint64_t b
                "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
                ::"r"(d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
+// The 12-MMA form of the chunk below (tools/ubench/ubench_tc.cu measures both): in ONE asm block:
+//   d  (+)= A_hi W_hi        dc (+)= A_lo W_hi + A_hi W_lo
+// ah/al: TMEM column addresses of the chunk's hi / lo parts (8 columns per K-step); wd/wl: SW128
+// K-major descriptors of W hi / lo (32 B per K-step = +2 in the start field). `acc` = 0 starts both
+// accumulators. Passing the base operands once lets ptxas form the twelve MMAs' operands with
+// uniform-register adds instead of converting every operand per MMA (R2UR), which dominated the
+// issue time of the per-MMA helpers.
+__device__ __forceinline__ void mma_3xtf32_ts_chunk_w(uint32_t d, uint32_t dc, uint32_t ah, uint32_t al, uint64_t wd,
+                                                      uint64_t wl, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 a1, a2, a3, l1, l2, l3;\n\t.reg .b64 w1, w2, w3, v1, v2, v3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %7, 0;\n\t"
+      "add.u32 a1, %2, 8;\n\tadd.u32 a2, %2, 16;\n\tadd.u32 a3, %2, 24;\n\t"
+      "add.u32 l1, %3, 8;\n\tadd.u32 l2, %3, 16;\n\tadd.u32 l3, %3, 24;\n\t"
+      "add.u64 w1, %4, 2;\n\tadd.u64 w2, %4, 4;\n\tadd.u64 w3, %4, 6;\n\t"
+      "add.u64 v1, %5, 2;\n\tadd.u64 v2, %5, 4;\n\tadd.u64 v3, %5, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %4, %6, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%3], %4, %6, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [%2], %5, %6, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a1], w1, %6, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [l1], w1, %6, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [a1], v1, %6, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a2], w2, %6, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [l2], w2, %6, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [a2], v2, %6, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [a3], w3, %6, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [l3], w3, %6, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%1], [a3], v3, %6, 1;\n\t}"
+      ::"r"(d), "r"(dc), "r"(ah), "r"(al), "l"(wd), "l"(wl), "r"(idesc), "r"(acc));
+}
 // One K chunk (32 tf32 = 4 K-steps) of the 3xTF32 product with A in TMEM (ah / al: TMEM columns of
 // the chunk's hi / lo parts, 8 columns per K-step; wd: SW128 K-major descriptor of [W hi | W lo],
 // 32 B per K-step = +2 in the start field), in ONE asm block so ptxas forms the operands with
