@@ -511,7 +511,23 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
     }();
     const int64_t in_bytes = (int64_t)es * batch * L * p;
     const int chunks = chunks_env ? chunks_env : (int)std::min<int64_t>(8, std::max<int64_t>(1, ceil_div(in_bytes, (int64_t)64 << 20)));
-    const int nc = std::min(batch, chunks);
+    // chunk boundaries: when chunks would hold several sequences, ramp up from and down to one
+    // sequence (1, 2, 4, ..., 4, 2, 1): the exposed first input / last output copy is one sequence,
+    // and each chunk's input (the copy is ~2x faster than the compute per sequence on E3) lands
+    // while the previous chunk computes
+    std::vector<int> sizes;
+    if (chunks < batch && batch >= 4) {
+      std::vector<int> up;
+      int total = 0;
+      for (int M = 1; 2 * (total + M) <= batch; M *= 2) { up.push_back(M); total += M; }
+      sizes = up;
+      for (int rest = batch - 2 * total; rest > 0;) { const int t = std::min(up.back(), rest); sizes.push_back(t); rest -= t; }
+      sizes.insert(sizes.end(), up.rbegin(), up.rend());
+    } else {
+      const int n0 = std::min(batch, chunks);
+      for (int i = 0; i < n0; ++i) sizes.push_back((int)((int64_t)batch * (i + 1) / n0 - (int64_t)batch * i / n0));
+    }
+    const int nc = (int)sizes.size();
     // derived weights once for all chunks (Ne is that of the full length L)
     const int Ne = eff_order(N_host[0], L);
     {
@@ -528,8 +544,8 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
     constexpr int kW = 8;
     const int64_t Hu = Ne > 0 ? ((int64_t)2 << Ne) - 1 : 0;
     const int64_t Lw = ceil_div(L, kW);
-    std::vector<int> b0(nc + 1);
-    for (int i = 0; i <= nc; ++i) b0[i] = (int)((int64_t)batch * i / nc);
+    std::vector<int> b0(nc + 1, 0);
+    for (int i = 0; i < nc; ++i) b0[i + 1] = b0[i] + sizes[i];
     auto windowed = [&](int i) { return nc > 1 && (i == 0 || i == nc - 1) && b0[i + 1] - b0[i] == 1 && Ne > 0 && Lw >= 8 * Hu; };
     std::vector<cudaEvent_t> ev((size_t)2 * nc + 2 * kW, nullptr);
     for (auto& e : ev)
