@@ -321,6 +321,11 @@ int engine_powers(int n, int m, const int* N_host, int N_max, const double* Abar
     ps.exec(16.0 * n * mm * (maxN + 1), 2.0 * n * (double)mm * m * maxN, PIPE_FP64);
     return launch_powers_small(P, Abar, n, N_max, m, st);
   }
+  if (n == 1) {                                   // MIMO: one cooperative launch (squarings + pack)
+    ProfScope ps(st, K_POWERS, 16.0 * mm * (N_host[0] + 1), 2.0 * (double)mm * m * N_host[0]);
+    ps.exec(24.0 * mm * N_host[0] + 16.0 * mm * (N_host[0] + 1), 2.0 * (double)mm * m * N_host[0], PIPE_FP64);
+    return launch_powers_coop(P, Abar, N_host[0], m, st);
+  }
   // P_0 = Abar (strided copy into slot 0 of every system)
   CASC_TRY(cudaMemcpy2DAsync(P.p64, sys * sizeof(double), Abar, mm * sizeof(double),
                              mm * sizeof(double), n, cudaMemcpyDeviceToDevice, st));

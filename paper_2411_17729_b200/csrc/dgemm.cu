@@ -3,8 +3,12 @@
 // (Abar Bbar, C P_N, C Bbar + D, C Abar Bbar). Powers are formed in float64 and rounded
 // once afterwards, as PAPER.md:275-277 suggests ("powers ... can always be computed with a
 // large number of accurate digits and used with as many digits as the application requires").
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace casc {
 
@@ -69,32 +73,27 @@ __global__ void __launch_bounds__(256) dgemm_batched_kernel(DgemmArg a) {
 // through shared memory (zero-filled past M, N, K). Per element a float64 dot product of the same
 // terms as dgemm_batched_kernel in another summation order (both are float64 FMA chains). The
 // MIMO squarings (m = 256: E3, m = 1024: E4, 11 squarings of 2 m^3 flops per step) run here.
-__global__ void __launch_bounds__(256) dgemm_mma_kernel(DgemmArg a) {
-  const int s = blockIdx.z;
-  if (a.skip_below && a.skip_below[s] < a.level) return;
-  const int64_t selA = a.selA ? a.selA[s] : 0, selB = a.selB ? a.selB[s] : 0;
-  const double* A = a.A + s * a.sA + selA * a.nA;
-  const double* B = a.B + s * a.sB + selB * a.nB;
-  double* C = a.C + s * a.sC;
-  const double* Cadd = a.Cadd ? a.Cadd + s * a.sCadd : nullptr;
+// One 64 x 64 output tile C[row0:, col0:] (+ Cadd) of C = A B on the fp64 tensor path (mma.sync
+// m8n8k4 f64, DMMA) by a 256-thread CTA: warp w owns rows 8w..8w+7 (eight 8 x 8 column tiles), K in
+// chunks of 32 staged through shared memory (zero-filled past M, N, K).
+__device__ __forceinline__ void dmma_tile(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                                          int64_t ldc, const double* Cadd, int M, int N, int K, int row0, int col0,
+                                          double* As, double* Bs) {
   constexpr int LA = 36, LB = 72;                        // padded strides (doubles)
-  __shared__ double As[64 * LA];                         // [row][k]
-  __shared__ double Bs[32 * LB];                         // [k][col]
   const int tid = threadIdx.x, w = tid / 32, lane = tid % 32, g = lane >> 2, t4 = lane & 3;
-  const int row0 = blockIdx.y * 64, col0 = blockIdx.x * 64;
   double d[8][2];
 #pragma unroll
   for (int n = 0; n < 8; ++n) d[n][0] = d[n][1] = 0.0;
-  for (int k0 = 0; k0 < a.K; k0 += 32) {
+  for (int k0 = 0; k0 < K; k0 += 32) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int e = tid + i * 256;
       const int r = e / 32, kk = e % 32;                 // A chunk 64 x 32 (k fastest: coalesced rows)
       const int gr = row0 + r, gk = k0 + kk;
-      As[r * LA + kk] = (gr < a.M && gk < a.K) ? A[(int64_t)gr * a.lda + gk] : 0.0;
+      As[r * LA + kk] = (gr < M && gk < K) ? A[(int64_t)gr * lda + gk] : 0.0;
       const int kb = e / 64, c = e % 64;                 // B chunk 32 x 64
       const int gkb = k0 + kb, gc = col0 + c;
-      Bs[kb * LB + c] = (gkb < a.K && gc < a.N) ? B[(int64_t)gkb * a.ldb + gc] : 0.0;
+      Bs[kb * LB + c] = (gkb < K && gc < N) ? B[(int64_t)gkb * ldb + gc] : 0.0;
     }
     __syncthreads();
 #pragma unroll
@@ -110,18 +109,125 @@ __global__ void __launch_bounds__(256) dgemm_mma_kernel(DgemmArg a) {
     __syncthreads();
   }
   const int gr = row0 + 8 * w + g;
-  if (gr >= a.M) return;
+  if (gr >= M) return;
 #pragma unroll
   for (int n = 0; n < 8; ++n) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int gc = col0 + 8 * n + 2 * t4 + h;
-      if (gc >= a.N) continue;
+      if (gc >= N) continue;
       double v = d[n][h];
-      if (Cadd) v += Cadd[(int64_t)gr * a.ldc + gc];
-      C[(int64_t)gr * a.ldc + gc] = v;
+      if (Cadd) v += Cadd[(int64_t)gr * ldc + gc];
+      C[(int64_t)gr * ldc + gc] = v;
     }
   }
+}
+
+// The same batched GEMM on the fp64 tensor path: one 64 x 64 tile per CTA. Per element a float64
+// dot product of the same terms as dgemm_batched_kernel in another summation order (both are
+// float64 FMA chains).
+__global__ void __launch_bounds__(256) dgemm_mma_kernel(DgemmArg a) {
+  const int s = blockIdx.z;
+  if (a.skip_below && a.skip_below[s] < a.level) return;
+  const int64_t selA = a.selA ? a.selA[s] : 0, selB = a.selB ? a.selB[s] : 0;
+  __shared__ double As[64 * 36];
+  __shared__ double Bs[32 * 72];
+  dmma_tile(a.A + s * a.sA + selA * a.nA, a.lda, a.B + s * a.sB + selB * a.nB, a.ldb, a.C + s * a.sC, a.ldc,
+            a.Cadd ? a.Cadd + s * a.sCadd : nullptr, a.M, a.N, a.K, blockIdx.y * 64, blockIdx.x * 64, As, Bs);
+}
+
+// a1 for one system with m > 64 (MIMO: E3 m = 256, E4 m = 1024) in ONE cooperative launch: P_0 =
+// Abar, then N squarings P_k = P_{k-1} P_{k-1} (each level's 64 x 64 tiles spread over the resident
+// CTAs, a grid-wide barrier between levels), then every P_k rounded once to its storage image (tf32
+// hi/lo or bf16). Replaces N + 2 launches whose fixed latency dominated at m = 256 (16 tiles per
+// level: 13 launches of ~29 us for 33 MFLOP each).
+__global__ void __launch_bounds__(256) powers_coop_kernel(const double* Abar, double* p64, float* f32,
+                                                          __nv_bfloat16* b16, int N, int m) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double As[64 * 36];
+  __shared__ double Bs[32 * 72];
+  const int64_t mm = (int64_t)m * m;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gsz = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = gtid; e < mm; e += gsz) p64[e] = Abar[e];
+  grid.sync();
+  const int tn = (m + 63) / 64, tiles = tn * tn;
+  for (int k = 1; k <= N; ++k) {
+    const double* Pk = p64 + (k - 1) * mm;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x)
+      dmma_tile(Pk, m, Pk, m, p64 + k * mm, m, nullptr, m, m, m, (t / tn) * 64, (t % tn) * 64, As, Bs);
+    grid.sync();
+  }
+  for (int64_t e = gtid; e < (int64_t)(N + 1) * mm; e += gsz) {
+    const int64_t slot = e / mm, ij = e % mm;
+    const double p = p64[e];
+    if (f32) {
+      const float hi = tf32_rna((float)p);
+      f32[slot * 2 * mm + ij] = hi;
+      f32[slot * 2 * mm + mm + ij] = tf32_rna((float)(p - (double)hi));
+    }
+    if (b16) b16[e] = __float2bfloat16_rn((float)p);
+  }
+}
+
+__global__ void __launch_bounds__(256) derived_coop_kernel(const __grid_constant__ DerivedPlan pl) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double As[64 * 36];
+  __shared__ double Bs[32 * 72];
+  for (int ph = 0; ph < 2; ++ph) {
+    int base = 0;                                          // tiles of this phase's jobs, concatenated
+    for (int j = 0; j < pl.n_jobs; ++j) {
+      const DJob& J = pl.jobs[j];
+      if (J.phase != ph) continue;
+      const int tm = (J.M + 63) / 64, tn = (J.N + 63) / 64;
+      for (int t = (int)blockIdx.x - base; t < tm * tn; t += gridDim.x)
+        if (t >= 0) dmma_tile(J.A, J.lda, J.B, J.ldb, J.C, J.ldc, J.Cadd, J.M, J.N, J.K, (t / tn) * 64, (t % tn) * 64, As, Bs);
+      base = (base + tm * tn) % gridDim.x;                 // spread the next job's tiles onto other CTAs
+    }
+    grid.sync();
+  }
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gsz = (int64_t)gridDim.x * blockDim.x;
+  for (int c = 0; c < pl.n_convs; ++c) {
+    const DConv& C = pl.convs[c];
+    for (int64_t e = gtid; e < C.n; e += gsz) {
+      const double x = C.src[e];
+      if (pl.tf32) {
+        float* d = static_cast<float*>(C.dst);
+        const float hi = tf32_rna((float)x);
+        d[e] = hi;
+        d[C.n + e] = tf32_rna((float)(x - (double)hi));
+      } else {
+        static_cast<__nv_bfloat16*>(C.dst)[e] = __float2bfloat16_rn((float)x);
+      }
+    }
+  }
+}
+
+int launch_derived_coop(const DerivedPlan& plan, cudaStream_t st) {
+  int dev = 0, sms = 148, per_sm = 0;
+  CASC_TRY(cudaGetDevice(&dev));
+  CASC_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CASC_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, derived_coop_kernel, 256, 0));
+  const int grid = sms * std::max(1, std::min(per_sm, 2));
+  void* args[] = {(void*)&plan};
+  CASC_TRY(cudaLaunchCooperativeKernel((const void*)derived_coop_kernel, dim3(grid), dim3(256), args, 0, st));
+  CASC_LAUNCHED();
+  return CASC_OK;
+}
+
+int launch_powers_coop(const PackLayout& P, const double* Abar, int N, int m, cudaStream_t st) {
+  int dev = 0, sms = 148, per_sm = 0;
+  CASC_TRY(cudaGetDevice(&dev));
+  CASC_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CASC_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, powers_coop_kernel, 256, 0));
+  const int tn = (m + 63) / 64;
+  int grid = std::min(sms * std::max(per_sm, 1), std::max(tn * tn, sms));
+  double* p64 = P.p64;
+  float* f32 = P.f32;
+  __nv_bfloat16* b16 = P.b16;
+  void* args[] = {(void*)&Abar, (void*)&p64, (void*)&f32, (void*)&b16, (void*)&N, (void*)&m};
+  CASC_TRY(cudaLaunchCooperativeKernel((const void*)powers_coop_kernel, dim3(grid), dim3(256), args, 0, st));
+  CASC_LAUNCHED();
+  return CASC_OK;
 }
 
 int launch_dgemm(const DgemmArg& a, int n_sys, cudaStream_t st) {

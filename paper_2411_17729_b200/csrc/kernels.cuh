@@ -15,7 +15,23 @@ struct DgemmArg {
   const int* skip_below; int level;                         // skip s if skip_below[s] < level
 };
 int launch_dgemm(const DgemmArg& a, int n_sys, cudaStream_t st);
+// Small dependent fp64 products and their operand-format images in ONE cooperative launch
+// (the MIMO derived weights, mimo_engine.cu): jobs of phase 0, grid barrier, phase 1, grid
+// barrier, conversions (tf32 hi/lo planes [2][n] or bf16 [n]).
+struct DJob {
+  const double* A; const double* B; double* C; const double* Cadd;
+  int lda, ldb, ldc, M, N, K, phase;
+};
+struct DConv { const double* src; void* dst; int64_t n; };
+struct DerivedPlan {
+  DJob jobs[8]; int n_jobs;
+  DConv convs[12]; int n_convs;
+  int tf32;
+};
+int launch_derived_coop(const DerivedPlan& plan, cudaStream_t st);
 int launch_pack(const PackLayout& P, int n_sys, int N_max, int m, cudaStream_t st);
+// a1 for ONE system with m > 64: all squarings and the packing in one cooperative launch
+int launch_powers_coop(const PackLayout& P, const double* Abar, int N, int m, cudaStream_t st);
 int launch_powers_small(const PackLayout& P, const double* Abar, int n_sys, int N_max, int m, cudaStream_t st);
 int launch_f64_to_f32(const double* src, float* dst, int64_t n, cudaStream_t st);
 

@@ -15,30 +15,6 @@
 
 namespace casc {
 
-__global__ void f64_to_bf16_kernel(const double* src, __nv_bfloat16* dst, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    dst[i] = __float2bfloat16_rn((float)src[i]);
-}
-// dst[0][i] = tf32 hi, dst[1][i] = tf32 lo of the float64 src[i] (R17)
-__global__ void f64_to_tf32pair_kernel(const double* src, float* dst, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double x = src[i];
-    const float hi = tf32_rna((float)x);
-    dst[i] = hi;
-    dst[n + i] = tf32_rna((float)(x - (double)hi));
-  }
-}
-
-// Convert a float64 weight to the GEMM's operand format: bf16 [n] or tf32 pair [2][n].
-static int convert_weight(const double* src, void* dst, int64_t n, bool tf32, cudaStream_t st) {
-  if (n <= 0) return CASC_OK;
-  const int blocks = (int)std::min<int64_t>(ceil_div(n, 256), 148 * 8);
-  if (tf32) f64_to_tf32pair_kernel<<<blocks, 256, 0, st>>>(src, static_cast<float*>(dst), n);
-  else f64_to_bf16_kernel<<<blocks, 256, 0, st>>>(src, static_cast<__nv_bfloat16*>(dst), n);
-  CASC_LAUNCHED();
-  return CASC_OK;
-}
-
 MimoWs carve_mimo(void* ws, int m, int p, int q, int64_t L, int batch, int mode) {
   Carver c(ws);
   MimoWs w{};
@@ -190,63 +166,53 @@ void mimo_output_gemm(MimoGemm& g, const MimoWs& w, int Ne, int m, int p, int q,
   }
 }
 
-// Derived weights of the fused first / last stages (R21), float64 then rounded to the
-// GEMM operand format: Abar Bbar, C P_Ne, C Bbar + D, C Abar Bbar.
+// Derived weights of the fused first / last steps (R21, R28, R31), in float64, then rounded
+// once to the GEMM operand format -- all in ONE cooperative launch (launch_derived_coop, dgemm.cu):
+//   phase 1: Abar Bbar, Abar^2 Bbar = P_1 Bbar, C P_Ne, C P_{Ne-1}, C Bbar + D
+//   phase 2: Abar^3 Bbar = P_1 (Abar Bbar), (C P_Ne) P_{Ne-1}, C (Abar Bbar)
+//   phase 3: every weight to tf32 hi/lo planes (fp32 mode) or bf16
 int mimo_derive(int m, int p, int q, int Ne, const PackLayout& P, const double* Bbar, const double* C,
-                       const double* D, const MimoWs& w, bool tf32, cudaStream_t st) {
+                const double* D, const MimoWs& w, bool tf32, cudaStream_t st) {
   const int64_t mm = (int64_t)m * m;
-  int rc;
-  {
-    ProfScope ps(st, K_DERIVED, 0.0, 2.0 * ((double)m * m * p + (double)q * m * m + 2.0 * q * m * p));
-    DgemmArg a{};
-    a.M = m; a.N = p; a.K = m;                                     // Abar Bbar
-    a.A = P.p64; a.lda = m; a.B = Bbar; a.ldb = p; a.C = w.AB64; a.ldc = p;
-    if ((rc = launch_dgemm(a, 1, st))) return rc;
-    a = DgemmArg{};                                                // C P_Ne
-    a.M = q; a.N = m; a.K = m;
-    a.A = C; a.lda = m; a.B = P.p64 + Ne * mm; a.ldb = m; a.C = w.CP64; a.ldc = m;
-    if ((rc = launch_dgemm(a, 1, st))) return rc;
-    a = DgemmArg{};                                                // C Bbar + D
-    a.M = q; a.N = p; a.K = m;
-    a.A = C; a.lda = m; a.B = Bbar; a.ldb = p; a.C = w.CBD64; a.ldc = p; a.Cadd = D;
-    if ((rc = launch_dgemm(a, 1, st))) return rc;
-    a = DgemmArg{};                                                // C Abar Bbar
-    a.M = q; a.N = p; a.K = m;
-    a.A = C; a.lda = m; a.B = w.AB64; a.ldb = p; a.C = w.CAB64; a.ldc = p;
-    if ((rc = launch_dgemm(a, 1, st))) return rc;
-    if ((rc = convert_weight(Bbar, w.Bb, (int64_t)m * p, tf32, st))) return rc;
-    if ((rc = convert_weight(w.AB64, w.AB, (int64_t)m * p, tf32, st))) return rc;
-    if ((rc = convert_weight(C, w.C, (int64_t)q * m, tf32, st))) return rc;
-    if ((rc = convert_weight(w.CP64, w.CP, (int64_t)q * m, tf32, st))) return rc;
-    if ((rc = convert_weight(w.CBD64, w.CBD, (int64_t)q * p, tf32, st))) return rc;
-    if ((rc = convert_weight(w.CAB64, w.CAB, (int64_t)q * p, tf32, st))) return rc;
-    if (D && (rc = convert_weight(D, w.D, (int64_t)q * p, tf32, st))) return rc;
-    if (Ne >= 2) {                                                 // Krylov head (R28)
-      a = DgemmArg{};                                              // Abar^2 Bbar = P_1 Bbar
-      a.M = m; a.N = p; a.K = m;
-      a.A = P.p64 + mm; a.lda = m; a.B = Bbar; a.ldb = p; a.C = w.A2B64; a.ldc = p;
-      if ((rc = launch_dgemm(a, 1, st))) return rc;
-      a = DgemmArg{};                                              // Abar^3 Bbar = P_1 (Abar Bbar)
-      a.M = m; a.N = p; a.K = m;
-      a.A = P.p64 + mm; a.lda = m; a.B = w.AB64; a.ldb = p; a.C = w.A3B64; a.ldc = p;
-      if ((rc = launch_dgemm(a, 1, st))) return rc;
-      if ((rc = convert_weight(w.A2B64, w.A2B, (int64_t)m * p, tf32, st))) return rc;
-      if ((rc = convert_weight(w.A3B64, w.A3B, (int64_t)m * p, tf32, st))) return rc;
-    }
-    if (mimo_fold(Ne)) {                                           // output fold (R31)
-      a = DgemmArg{};                                              // C P_{Ne-1}
-      a.M = q; a.N = m; a.K = m;
-      a.A = C; a.lda = m; a.B = P.p64 + (Ne - 1) * mm; a.ldb = m; a.C = w.CP1_64; a.ldc = m;
-      if ((rc = launch_dgemm(a, 1, st))) return rc;
-      a = DgemmArg{};                                              // (C P_Ne) P_{Ne-1}
-      a.M = q; a.N = m; a.K = m;
-      a.A = w.CP64; a.lda = m; a.B = P.p64 + (Ne - 1) * mm; a.ldb = m; a.C = w.CP3_64; a.ldc = m;
-      if ((rc = launch_dgemm(a, 1, st))) return rc;
-      if ((rc = convert_weight(w.CP1_64, w.CP1, (int64_t)q * m, tf32, st))) return rc;
-      if ((rc = convert_weight(w.CP3_64, w.CP3, (int64_t)q * m, tf32, st))) return rc;
-    }
+  DerivedPlan pl{};
+  auto job = [&](int ph, const double* A, int lda, const double* B, int ldb, double* Cm, int ldc, int M, int N,
+                 const double* Cadd) {
+    DJob& j = pl.jobs[pl.n_jobs++];
+    j = DJob{A, B, Cm, Cadd, lda, ldb, ldc, M, N, m, ph};
+  };
+  auto cvt = [&](const double* src, void* dst, int64_t n) {
+    DConv& c = pl.convs[pl.n_convs++];
+    c = DConv{src, dst, n};
+  };
+  job(0, P.p64, m, Bbar, p, w.AB64, p, m, p, nullptr);                          // Abar Bbar
+  job(0, C, m, P.p64 + Ne * mm, m, w.CP64, m, q, m, nullptr);                  // C P_Ne
+  job(0, C, m, Bbar, p, w.CBD64, p, q, p, D);                                   // C Bbar + D
+  job(1, C, m, w.AB64, p, w.CAB64, p, q, p, nullptr);                           // C Abar Bbar
+  cvt(Bbar, w.Bb, (int64_t)m * p);
+  cvt(w.AB64, w.AB, (int64_t)m * p);
+  cvt(C, w.C, (int64_t)q * m);
+  cvt(w.CP64, w.CP, (int64_t)q * m);
+  cvt(w.CBD64, w.CBD, (int64_t)q * p);
+  cvt(w.CAB64, w.CAB, (int64_t)q * p);
+  if (D) cvt(D, w.D, (int64_t)q * p);
+  if (Ne >= 2) {                                                                // Krylov head (R28)
+    job(0, P.p64 + mm, m, Bbar, p, w.A2B64, p, m, p, nullptr);                 // P_1 Bbar
+    job(1, P.p64 + mm, m, w.AB64, p, w.A3B64, p, m, p, nullptr);               // P_1 (Abar Bbar)
+    cvt(w.A2B64, w.A2B, (int64_t)m * p);
+    cvt(w.A3B64, w.A3B, (int64_t)m * p);
   }
-  return CASC_OK;
+  if (mimo_fold(Ne)) {                                                          // output fold (R31)
+    job(0, C, m, P.p64 + (Ne - 1) * mm, m, w.CP1_64, m, q, m, nullptr);        // C P_{Ne-1}
+    job(1, w.CP64, m, P.p64 + (Ne - 1) * mm, m, w.CP3_64, m, q, m, nullptr);   // (C P_Ne) P_{Ne-1}
+    cvt(w.CP1_64, w.CP1, (int64_t)q * m);
+    cvt(w.CP3_64, w.CP3, (int64_t)q * m);
+  }
+  pl.tf32 = tf32 ? 1 : 0;
+  double fl = 0.0;
+  for (int i = 0; i < pl.n_jobs; ++i) fl += 2.0 * pl.jobs[i].M * pl.jobs[i].N * pl.jobs[i].K;
+  ProfScope ps(st, K_DERIVED, 0.0, fl);
+  ps.exec(0.0, fl, PIPE_FP64);
+  return launch_derived_coop(pl, st);
 }
 
 }  // namespace casc
