@@ -321,7 +321,9 @@ int engine_powers(int n, int m, const int* N_host, int N_max, const double* Abar
     ps.exec(16.0 * n * mm * (maxN + 1), 2.0 * n * (double)mm * m * maxN, PIPE_FP64);
     return launch_powers_small(P, Abar, n, N_max, m, st);
   }
-  if (n == 1) {                                   // MIMO: one cooperative launch (squarings + pack)
+  // MIMO with m <= 512: one cooperative launch (squarings + pack); E3 powers 0.38 -> 0.28 ms. At
+  // m = 1024 (256 tiles per level) the per-level launches measured faster (E4: 2.08 vs 2.39 ms, A/B)
+  if (n == 1 && m <= 512) {
     ProfScope ps(st, K_POWERS, 16.0 * mm * (N_host[0] + 1), 2.0 * (double)mm * m * N_host[0]);
     ps.exec(24.0 * mm * N_host[0] + 16.0 * mm * (N_host[0] + 1), 2.0 * (double)mm * m * N_host[0], PIPE_FP64);
     return launch_powers_coop(P, Abar, N_host[0], m, st);

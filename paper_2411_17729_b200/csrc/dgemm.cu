@@ -74,39 +74,62 @@ __global__ void __launch_bounds__(256) dgemm_batched_kernel(DgemmArg a) {
 // terms as dgemm_batched_kernel in another summation order (both are float64 FMA chains). The
 // MIMO squarings (m = 256: E3, m = 1024: E4, 11 squarings of 2 m^3 flops per step) run here.
 // One 64 x 64 output tile C[row0:, col0:] (+ Cadd) of C = A B on the fp64 tensor path (mma.sync
-// m8n8k4 f64, DMMA) by a 256-thread CTA: warp w owns rows 8w..8w+7 (eight 8 x 8 column tiles), K in
-// chunks of 32 staged through shared memory (zero-filled past M, N, K).
+// m8n8k4 f64, DMMA) by a 256-thread CTA: warp w owns rows 8w..8w+7 (eight 8 x 8 column tiles); K in
+// chunks of 16 staged through shared memory with cp.async double buffering (the next chunk's loads
+// overlap this chunk's DMMAs; zero-filled past M, N, K).
+constexpr int kDKC = 16, kDLA = 20, kDLB = 72;           // K chunk, padded strides (doubles)
+struct DmmaSmem {
+  double A[2][64 * kDLA];
+  double B[2][kDKC * kDLB];
+};
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(valid ? src : nullptr), "r"(valid ? 8 : 0) : "memory");
+}
 __device__ __forceinline__ void dmma_tile(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                                           int64_t ldc, const double* Cadd, int M, int N, int K, int row0, int col0,
-                                          double* As, double* Bs) {
-  constexpr int LA = 36, LB = 72;                        // padded strides (doubles)
+                                          DmmaSmem& sm) {
   const int tid = threadIdx.x, w = tid / 32, lane = tid % 32, g = lane >> 2, t4 = lane & 3;
+  auto load = [&](int buf, int k0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = tid + i * 256;
+      const int r = e / kDKC, kk = e % kDKC;               // A chunk 64 x 16
+      const int gr = row0 + r, gk = k0 + kk;
+      const bool va = gr < M && gk < K;
+      cp_async8(&sm.A[buf][r * kDLA + kk], A + (va ? (int64_t)gr * lda + gk : 0), va);
+      const int kb = e / 64, c = e % 64;                 // B chunk 16 x 64
+      const int gkb = k0 + kb, gc = col0 + c;
+      const bool vb = gkb < K && gc < N;
+      cp_async8(&sm.B[buf][kb * kDLB + c], B + (vb ? (int64_t)gkb * ldb + gc : 0), vb);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
   double d[8][2];
 #pragma unroll
   for (int n = 0; n < 8; ++n) d[n][0] = d[n][1] = 0.0;
-  for (int k0 = 0; k0 < K; k0 += 32) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int e = tid + i * 256;
-      const int r = e / 32, kk = e % 32;                 // A chunk 64 x 32 (k fastest: coalesced rows)
-      const int gr = row0 + r, gk = k0 + kk;
-      As[r * LA + kk] = (gr < M && gk < K) ? A[(int64_t)gr * lda + gk] : 0.0;
-      const int kb = e / 64, c = e % 64;                 // B chunk 32 x 64
-      const int gkb = k0 + kb, gc = col0 + c;
-      Bs[kb * LB + c] = (gkb < K && gc < N) ? B[(int64_t)gkb * ldb + gc] : 0.0;
+  const int nch = (K + kDKC - 1) / kDKC;
+  load(0, 0);
+  for (int c = 0; c < nch; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nch) {
+      load(buf ^ 1, (c + 1) * kDKC);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
 #pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      const double av = As[(8 * w + g) * LA + 4 * ks + t4];
+    for (int ks = 0; ks < kDKC / 4; ++ks) {
+      const double av = sm.A[buf][(8 * w + g) * kDLA + 4 * ks + t4];
 #pragma unroll
       for (int n = 0; n < 8; ++n) {
-        const double bv = Bs[(4 * ks + t4) * LB + 8 * n + g];
+        const double bv = sm.B[buf][(4 * ks + t4) * kDLB + 8 * n + g];
         asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                      : "+d"(d[n][0]), "+d"(d[n][1]) : "d"(av), "d"(bv));
       }
     }
-    __syncthreads();
+    __syncthreads();                                     // buf is refilled by the next iteration's prefetch
   }
   const int gr = row0 + 8 * w + g;
   if (gr >= M) return;
@@ -130,10 +153,9 @@ __global__ void __launch_bounds__(256) dgemm_mma_kernel(DgemmArg a) {
   const int s = blockIdx.z;
   if (a.skip_below && a.skip_below[s] < a.level) return;
   const int64_t selA = a.selA ? a.selA[s] : 0, selB = a.selB ? a.selB[s] : 0;
-  __shared__ double As[64 * 36];
-  __shared__ double Bs[32 * 72];
+  __shared__ DmmaSmem sm;
   dmma_tile(a.A + s * a.sA + selA * a.nA, a.lda, a.B + s * a.sB + selB * a.nB, a.ldb, a.C + s * a.sC, a.ldc,
-            a.Cadd ? a.Cadd + s * a.sCadd : nullptr, a.M, a.N, a.K, blockIdx.y * 64, blockIdx.x * 64, As, Bs);
+            a.Cadd ? a.Cadd + s * a.sCadd : nullptr, a.M, a.N, a.K, blockIdx.y * 64, blockIdx.x * 64, sm);
 }
 
 // a1 for one system with m > 64 (MIMO: E3 m = 256, E4 m = 1024) in ONE cooperative launch: P_0 =
@@ -141,11 +163,10 @@ __global__ void __launch_bounds__(256) dgemm_mma_kernel(DgemmArg a) {
 // CTAs, a grid-wide barrier between levels), then every P_k rounded once to its storage image (tf32
 // hi/lo or bf16). Replaces N + 2 launches whose fixed latency dominated at m = 256 (16 tiles per
 // level: 13 launches of ~29 us for 33 MFLOP each).
-__global__ void __launch_bounds__(256) powers_coop_kernel(const double* Abar, double* p64, float* f32,
+__global__ void __launch_bounds__(256, 2) powers_coop_kernel(const double* Abar, double* p64, float* f32,
                                                           __nv_bfloat16* b16, int N, int m) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double As[64 * 36];
-  __shared__ double Bs[32 * 72];
+  __shared__ DmmaSmem sm;
   const int64_t mm = (int64_t)m * m;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gsz = (int64_t)gridDim.x * blockDim.x;
   for (int64_t e = gtid; e < mm; e += gsz) p64[e] = Abar[e];
@@ -154,7 +175,7 @@ __global__ void __launch_bounds__(256) powers_coop_kernel(const double* Abar, do
   for (int k = 1; k <= N; ++k) {
     const double* Pk = p64 + (k - 1) * mm;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x)
-      dmma_tile(Pk, m, Pk, m, p64 + k * mm, m, nullptr, m, m, m, (t / tn) * 64, (t % tn) * 64, As, Bs);
+      dmma_tile(Pk, m, Pk, m, p64 + k * mm, m, nullptr, m, m, m, (t / tn) * 64, (t % tn) * 64, sm);
     grid.sync();
   }
   for (int64_t e = gtid; e < (int64_t)(N + 1) * mm; e += gsz) {
@@ -169,10 +190,9 @@ __global__ void __launch_bounds__(256) powers_coop_kernel(const double* Abar, do
   }
 }
 
-__global__ void __launch_bounds__(256) derived_coop_kernel(const __grid_constant__ DerivedPlan pl) {
+__global__ void __launch_bounds__(256, 2) derived_coop_kernel(const __grid_constant__ DerivedPlan pl) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double As[64 * 36];
-  __shared__ double Bs[32 * 72];
+  __shared__ DmmaSmem sm;
   for (int ph = 0; ph < 2; ++ph) {
     int base = 0;                                          // tiles of this phase's jobs, concatenated
     for (int j = 0; j < pl.n_jobs; ++j) {
@@ -180,7 +200,7 @@ __global__ void __launch_bounds__(256) derived_coop_kernel(const __grid_constant
       if (J.phase != ph) continue;
       const int tm = (J.M + 63) / 64, tn = (J.N + 63) / 64;
       for (int t = (int)blockIdx.x - base; t < tm * tn; t += gridDim.x)
-        if (t >= 0) dmma_tile(J.A, J.lda, J.B, J.ldb, J.C, J.ldc, J.Cadd, J.M, J.N, J.K, (t / tn) * 64, (t % tn) * 64, As, Bs);
+        if (t >= 0) dmma_tile(J.A, J.lda, J.B, J.ldb, J.C, J.ldc, J.Cadd, J.M, J.N, J.K, (t / tn) * 64, (t % tn) * 64, sm);
       base = (base + tm * tn) % gridDim.x;                 // spread the next job's tiles onto other CTAs
     }
     grid.sync();
