@@ -208,7 +208,24 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
   CASC_TRY(cudaEventRecord(ev_start, st));
   CASC_TRY(cudaStreamWaitEvent(ctx->in, ev_start, 0));
   const size_t row = (size_t)batch * L * sizeof(float);
-  const int waves = (n + nw - 1) / nw;
+  // wave sizes: ramp up from nw/16 channels and back down (s, 2s, 4s, ..., nw, ..., 4s, 2s, s) so the
+  // first wave's compute starts after a sixteenth of the input and the last wave's output tail is
+  // short; each wave's input copy overlaps the previous wave's compute
+  std::vector<int> wsz;
+  const int s0 = std::max(1, nw / 16);
+  if (n >= 4 * s0 && nw >= 4) {
+    std::vector<int> up;
+    int total = 0;
+    for (int M = s0; M < nw && 2 * (total + M) <= n; M *= 2) { up.push_back(M); total += M; }
+    wsz = up;
+    for (int rest = n - 2 * total; rest > 0;) { const int t = std::min(nw, rest); wsz.push_back(t); rest -= t; }
+    wsz.insert(wsz.end(), up.rbegin(), up.rend());
+  } else {
+    for (int c0 = 0; c0 < n; c0 += nw) wsz.push_back(std::min(nw, n - c0));
+  }
+  const int waves = (int)wsz.size();
+  std::vector<int> wc0(waves + 1, 0);
+  for (int w = 0; w < waves; ++w) wc0[w + 1] = wc0[w] + wsz[w];
   std::vector<cudaEvent_t> u_ev(waves);
   for (int w = 0; w < waves; ++w)
     if ((rc = new_event(&u_ev[w]))) return rc;
@@ -219,7 +236,7 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
   PackLayout P = pack_layout(const_cast<void*>(pack), n, m, N_max, CASC_FP32);
   const int64_t slot_mm = (int64_t)(N_max + 1) * m * m;
   for (int w = 0; w < waves && rc == CASC_OK; ++w) {
-    const int c0 = w * nw, cn = std::min(nw, n - c0);
+    const int c0 = wc0[w], cn = wsz[w];
     const size_t off = (size_t)c0 * row;
     if (cudaMemcpyAsync((char*)u_dev + off, (const char*)u_h + off, (size_t)cn * row, cudaMemcpyHostToDevice,
                         ctx->in) != cudaSuccess ||
