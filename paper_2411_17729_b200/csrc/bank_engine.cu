@@ -13,7 +13,9 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
 #include <numeric>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -25,9 +27,19 @@
 
 namespace casc {
 cudaEvent_t g_timing_t0 = nullptr;   // CASC_TIMING diagnostics: origin recorded by casc_run_host
+// CASC_TIMING diagnostics: labelled events recorded without synchronising, printed by
+// engine_bank_pipelined after its final synchronisation
+static std::vector<std::pair<std::string, cudaEvent_t>> g_marks;
+static void timing_mark(const std::string& what, cudaStream_t s) {
+  if (!getenv("CASC_TIMING") || !g_timing_t0) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, s);
+  g_marks.emplace_back(what, e);
+}
 
 static constexpr int kHeadK = 7;      // Krylov head covers stages 0..6 (128 lags)
-static constexpr int kMetaInts = 4;   // per-channel host table: Neff | Kc | parity | order
+static constexpr int kMetaInts = 5;   // per-channel host table: Neff | Kc | parity | order | iota
 
 // the fused output parts (R24-R26) for m = 64; CASC_BANK_AB=0 stores v and runs the separate tail
 // (tests compare the two)
@@ -57,7 +69,7 @@ static char stage_variant(int m) { return m % 64 == 0 ? 't' : 'r'; }
 static int pair_slots(int n_max) { return n_max > kHeadK ? (n_max - kHeadK + 1) / 2 : 0; }
 
 struct BankWs {
-  int* meta;      // Neff | Kc | parity | order   (kMetaInts n ints)
+  int* meta;      // Neff | Kc | parity | order | iota   (kMetaInts n ints)
   double* Kr64;   // [n][m][128]
   float* krT;     // [n][2][m][128]
   double* w64;    // [n][m]
@@ -129,10 +141,53 @@ __global__ void pair_split_kernel(const double* Q64, float* Q32, const int* Neff
 // One wave of n channels; Pw points at the wave's first channel inside the full pack.
 struct BankStream {        // host-buffer run: output channels copied out as soon as they are final
   void* y_host = nullptr;           // pinned [n][batch][L] (null: no streaming)
+  // y_host is device-mapped pinned memory: the wave's last emission (its deepest channels, nothing
+  // left to overlap with on the last wave) is stored into it by one copy kernel (a scattered channel
+  // list in one launch; one copy per channel run costs ~4 us of copy-engine overhead each: 86
+  // scattered channels 0.72 vs 0.44 ms, tools/ubench/zc_d2h.cu). Earlier emissions stay on the copy
+  // engine: the copy kernel running beside the stage passes slowed them (E2: 2.94 vs 2.23 ms)
+  bool zero_copy = false;
   cudaStream_t cout = nullptr;      // copy-out stream
   std::vector<cudaEvent_t>* events = nullptr;   // created here, destroyed by the caller
-  cudaEvent_t u_event = nullptr;     // the wave's input copy has landed (the head waits for it)
+  // the wave's input arrives in n_chunks chunks of channels [bounds[i], bounds[i+1]) (memory order),
+  // submitted by submit_inputs() after the wave's channel table upload (a host->device copy queues
+  // behind every copy submitted before it on the copy engine); the head runs per chunk after
+  // u_events[i]
+  int n_chunks = 0;
+  const int* bounds = nullptr;
+  const cudaEvent_t* u_events = nullptr;
+  std::function<int()> submit_inputs;
+  const int* dmeta = nullptr;        // the wave's channel table, already on the device (no upload)
 };
+// copies the listed channels' rows (row4 float4 each) from device y to the device-mapped pinned
+// host buffer: a handful of CTAs saturate PCIe (tools/ubench/zc_d2h.cu: 8 CTAs 52 GB/s)
+constexpr int kEmitCtas = 16;
+__global__ void emit_rows_kernel(const float4* __restrict__ src, float4* dst, const int* __restrict__ list,
+                                 int n_list, int64_t row4) {
+  const int64_t total = (int64_t)n_list * row4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = (int64_t)list[i / row4] * row4 + i % row4;
+    dst[o] = src[o];
+  }
+}
+// the per-channel table of a wave (kMetaInts n ints): Neff | Kc | parity of the pass count (which
+// buffer holds the final state) | channels by decreasing Neff | identity. Returns max Neff.
+static int fill_meta(int n, int m, int64_t L, const int* N_host, int* meta) {
+  const char variant = stage_variant(m);
+  int *Neff = meta, *Kc = Neff + n, *par = Neff + 2 * n, *order = Neff + 3 * n, *iota = Neff + 4 * n;
+  int maxNe = 0;
+  for (int s = 0; s < n; ++s) {
+    Neff[s] = eff_order(N_host[s], L);
+    Kc[s] = std::min(kHeadK, Neff[s]);
+    const int nstream = Neff[s] - Kc[s];            // streaming stages of this channel
+    par[s] = (variant == 't' ? (nstream + 1) / 2 : nstream) % 2;   // passes -> final buffer
+    maxNe = std::max(maxNe, Neff[s]);
+  }
+  std::iota(order, order + n, 0);
+  std::iota(iota, iota + n, 0);
+  std::stable_sort(order, order + n, [&](int a, int b) { return Neff[a] > Neff[b]; });
+  return maxNe;
+}
 static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int N_max, const PackLayout& Pw,
                      const double* Bbar, const double* C, const double* D, const float* u, float* y, void* ws,
                      size_t ws_bytes, cudaStream_t st, int* pinned_meta = nullptr, const BankStream* bs = nullptr);
@@ -201,19 +256,22 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
     events.push_back(*e);
     return CASC_OK;
   };
-  cudaEvent_t ev_start;
-  if ((rc = new_event(&ev_start))) return rc;
-  // u may be overwritten only after earlier work on st (starting the copy before the parameter
-  // copies and powers measured slower on E2: 5.48 vs 4.26 ms e2e)
-  CASC_TRY(cudaEventRecord(ev_start, st));
-  CASC_TRY(cudaStreamWaitEvent(ctx->in, ev_start, 0));
+  // u may be overwritten only after earlier work on st: ctx->inputs_free, recorded by the caller
+  // after its parameter copies and before the powers (an input copy submitted ahead of the
+  // parameter copies delays them on the copy engine: E2 5.48 vs 4.26 ms e2e)
+  CASC_TRY(cudaStreamWaitEvent(ctx->in, ctx->inputs_free, 0));
   const size_t row = (size_t)batch * L * sizeof(float);
-  // wave sizes: ramp up from nw/16 channels and back down (s, 2s, 4s, ..., nw, ..., 4s, 2s, s) so the
-  // first wave's compute starts after a sixteenth of the input and the last wave's output tail is
-  // short; each wave's input copy overlaps the previous wave's compute
+  // wave sizes (CASC_WAVE_RAMP = r, 0: uniform): ramp up from nw/r channels and back down (s, 2s,
+  // ..., nw, ..., 2s, s) so the first wave's compute starts early and the last wave's output tail is
+  // short; each wave's input copy overlaps the previous wave's compute. Measured (E2 e2e, one box,
+  // with 4 input chunks): r = 0 4.58, 4 4.49, 16 5.21 ms; E5 760 ms for all (A/B, tools/ab)
   std::vector<int> wsz;
-  const int s0 = std::max(1, nw / 16);
-  if (n >= 4 * s0 && nw >= 4) {
+  static const int ramp_div = [] {
+    const char* e = getenv("CASC_WAVE_RAMP");
+    return e ? std::max(0, atoi(e)) : 4;
+  }();
+  const int s0 = ramp_div ? std::max(1, nw / ramp_div) : nw;
+  if (ramp_div && n >= 4 * s0 && nw >= 4) {
     std::vector<int> up;
     int total = 0;
     for (int M = s0; M < nw && 2 * (total + M) <= n; M *= 2) { up.push_back(M); total += M; }
@@ -226,29 +284,74 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
   const int waves = (int)wsz.size();
   std::vector<int> wc0(waves + 1, 0);
   for (int w = 0; w < waves; ++w) wc0[w + 1] = wc0[w] + wsz[w];
-  std::vector<cudaEvent_t> u_ev(waves);
-  for (int w = 0; w < waves; ++w)
-    if ((rc = new_event(&u_ev[w]))) return rc;
-  // the input copy of wave w is submitted just before the wave's own work: a small host->device copy
-  // the wave enqueues (its channel table) queues behind every copy submitted before it on the copy
-  // engine, so submitting all waves' inputs up front delayed wave 0 by the whole input (E5: 140 ms);
-  // wave w+1's copy still runs during wave w's compute
+  // input chunks per wave (CASC_E2E_CHUNKS): the head runs per chunk as it lands (E2 e2e with the
+  // ramp: 1 chunk 4.45, 4 4.49, 8 4.77 ms -- smaller head launches fill the GPU less)
+  static const int chunks = [] {
+    const char* e = getenv("CASC_E2E_CHUNKS");
+    return e ? std::max(1, atoi(e)) : 4;
+  }();
+  std::vector<std::vector<int>> bounds(waves);
+  std::vector<std::vector<cudaEvent_t>> u_ev(waves);
+  for (int w = 0; w < waves; ++w) {
+    const int nc = std::min(wsz[w], chunks);
+    bounds[w].resize(nc + 1);
+    u_ev[w].resize(nc);
+    for (int i = 0; i <= nc; ++i) bounds[w][i] = (int)((int64_t)wsz[w] * i / nc);
+    for (int i = 0; i < nc; ++i)
+      if ((rc = new_event(&u_ev[w][i]))) return rc;
+  }
+  // the input copies of wave w are submitted by the wave itself, after its channel table upload: a
+  // small host->device copy queues behind every copy submitted before it on the copy engine, so
+  // submitting all waves' inputs up front delayed wave 0 by the whole input (E5: 140 ms); wave
+  // w+1's copies still run during wave w's compute
+  // every wave's channel table in one upload ahead of the inputs (a table copy on st would queue
+  // behind the input copies on the copy engine and hold the head back until the whole input landed)
+  if ((rc = ctx->ensure_dmeta((size_t)kMetaInts * n))) return rc;
+  // outputs: stored straight into y_h when it is device-mapped pinned memory (else copied out)
+  void* y_map = const_cast<void*>(y_h);
+  bool zero_copy = false;
+  {
+    cudaPointerAttributes pa{};
+    static const bool zc_off = getenv("CASC_NO_ZERO_COPY") != nullptr;
+    if (!zc_off && cudaPointerGetAttributes(&pa, y_h) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer) {
+      y_map = pa.devicePointer;
+      zero_copy = (batch * L) % 4 == 0 && ((uintptr_t)y_map & 15) == 0;
+      if (!zero_copy) y_map = const_cast<void*>(y_h);
+    }
+    cudaGetLastError();                              // a pageable pointer may leave an error behind
+  }
+  for (int w = 0; w < waves; ++w) fill_meta(wsz[w], m, L, N_host + wc0[w], ctx->pinned + (size_t)kMetaInts * wc0[w]);
+  cudaEvent_t meta_ev;
+  if ((rc = new_event(&meta_ev))) return rc;
+  CASC_TRY(cudaMemcpyAsync(ctx->dmeta, ctx->pinned, sizeof(int) * kMetaInts * (size_t)n, cudaMemcpyHostToDevice, ctx->in));
+  CASC_TRY(cudaEventRecord(meta_ev, ctx->in));
+  CASC_TRY(cudaStreamWaitEvent(st, meta_ev, 0));
   PackLayout P = pack_layout(const_cast<void*>(pack), n, m, N_max, CASC_FP32);
   const int64_t slot_mm = (int64_t)(N_max + 1) * m * m;
   for (int w = 0; w < waves && rc == CASC_OK; ++w) {
     const int c0 = wc0[w], cn = wsz[w];
     const size_t off = (size_t)c0 * row;
-    if (cudaMemcpyAsync((char*)u_dev + off, (const char*)u_h + off, (size_t)cn * row, cudaMemcpyHostToDevice,
-                        ctx->in) != cudaSuccess ||
-        cudaEventRecord(u_ev[w], ctx->in) != cudaSuccess) {
-      rc = CASC_ERR_CUDA;
-      break;
-    }
     BankStream bs;
-    bs.y_host = (char*)const_cast<void*>(y_h) + off;
+    bs.y_host = (char*)y_map + off;
+    bs.zero_copy = zero_copy && w == waves - 1;
     bs.cout = ctx->out;
     bs.events = &events;
-    bs.u_event = u_ev[w];
+    bs.n_chunks = (int)u_ev[w].size();
+    bs.bounds = bounds[w].data();
+    bs.u_events = u_ev[w].data();
+    bs.dmeta = ctx->dmeta + (size_t)kMetaInts * c0;
+    bs.submit_inputs = [&, w, off]() -> int {
+      const std::vector<int>& b = bounds[w];
+      for (int i = 0; i + 1 < (int)b.size(); ++i) {
+        CASC_TRY(cudaMemcpyAsync((char*)u_dev + off + (size_t)b[i] * row, (const char*)u_h + off + (size_t)b[i] * row,
+                                 (size_t)(b[i + 1] - b[i]) * row, cudaMemcpyHostToDevice, ctx->in));
+        CASC_TRY(cudaEventRecord(u_ev[w][i], ctx->in));
+        timing_mark("input chunk " + std::to_string(i), ctx->in);
+      }
+      timing_mark("input copied, wave " + std::to_string(w), ctx->in);
+      return CASC_OK;
+    };
     PackLayout Pw = P;
     Pw.p64 += c0 * slot_mm;
     Pw.f32 += c0 * slot_mm * 2;
@@ -264,6 +367,13 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
     cudaDeviceSynchronize();
     float ta, tb, tc;
     cudaEventElapsedTime(&ta, g_timing_t0, a); cudaEventElapsedTime(&tb, g_timing_t0, b); cudaEventElapsedTime(&tc, g_timing_t0, c);
+    for (auto& mk : g_marks) {
+      float t;
+      cudaEventElapsedTime(&t, g_timing_t0, mk.second);
+      fprintf(stderr, "casc timing: %8.3f ms  %s\n", t, mk.first.c_str());
+      cudaEventDestroy(mk.second);
+    }
+    g_marks.clear();
     fprintf(stderr, "casc timing: input copies done %.3f, compute done %.3f, output copies done %.3f ms\n", ta, tb, tc);
     cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c);
   }
@@ -285,17 +395,13 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
   // output fusion: the producer of each channel's last state writes (C v, C P_Ne v) instead of
   // v (R24); taken with the m = 64 tensor-core stage kernels and head
   const bool use_ab = m == 64 && bank_ab_enabled();
-  std::vector<int> meta_v(pinned_meta ? 0 : (size_t)kMetaInts * n);
-  int* meta = pinned_meta ? pinned_meta : meta_v.data();
-  int *Neff = meta, *Kc = Neff + n, *par = Neff + 2 * n, *order = Neff + 3 * n;
-  int maxNe = 0;
-  for (int s = 0; s < n; ++s) {
-    Neff[s] = eff_order(N_host[s], L);
-    Kc[s] = std::min(kHeadK, Neff[s]);
-    const int nstream = Neff[s] - Kc[s];            // streaming stages of this channel
-    par[s] = (variant == 't' ? (nstream + 1) / 2 : nstream) % 2;   // passes -> final buffer
-    maxNe = std::max(maxNe, Neff[s]);
-  }
+  // with a pre-uploaded table (bs->dmeta) the host copy is rebuilt locally (the pinned staging may
+  // still be in flight)
+  const bool pre = bs && bs->dmeta;
+  std::vector<int> meta_v((pinned_meta && !pre) ? 0 : (size_t)kMetaInts * n);
+  int* meta = (pinned_meta && !pre) ? pinned_meta : meta_v.data();
+  int *Neff = meta, *Kc = Neff + n, *order = Neff + 3 * n;
+  const int maxNe = fill_meta(n, m, L, N_host, meta);
   const int qslots = variant == 't' ? pair_slots(maxNe) : 0;
   BankWs w = carve_bank(ws, n, m, L, batch, qslots);
   if (ws_bytes < w.bytes) {
@@ -305,8 +411,6 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
   const PackLayout& P = Pw;
   const int64_t mm = (int64_t)m * m;
   int rc;
-  std::iota(order, order + n, 0);
-  std::stable_sort(order, order + n, [&](int a, int b) { return Neff[a] > Neff[b]; });
   // R24-R26 (common.cuh OutParts): y is formed from parts written by the kernel producing
   // v^(Ne-d); with fold, d = 1 for an odd number of streaming stages (no single-stage pass) and
   // d = 2 for an even number >= 2 (the last stage-pair pass is skipped). Planned only where every
@@ -325,8 +429,10 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
   }
   std::vector<int> Lp(n);                          // the state level each channel's parts come from
   for (int c = 0; c < n; ++c) Lp[c] = Neff[c] - fold_depth(Neff[c], Kc[c], fold);
-  CASC_TRY(cudaMemcpyAsync(w.meta, meta, (size_t)kMetaInts * n * sizeof(int), cudaMemcpyHostToDevice, st));
-  const int *dNeff = w.meta, *dKc = w.meta + n, *dpar = w.meta + 2 * n, *dorder = w.meta + 3 * n;
+  if (!pre) CASC_TRY(cudaMemcpyAsync(w.meta, meta, (size_t)kMetaInts * n * sizeof(int), cudaMemcpyHostToDevice, st));
+  const int* dm = pre ? bs->dmeta : w.meta;
+  const int *dNeff = dm, *dKc = dm + n, *dpar = dm + 2 * n, *dorder = dm + 3 * n, *diota = dm + 4 * n;
+  if (bs && bs->submit_inputs && (rc = bs->submit_inputs())) return rc;
   auto count_ge = [&](int need) {                    // channels with Neff >= need: a prefix of order
     int c = 0;
     while (c < n && Neff[order[c]] >= need) ++c;
@@ -402,6 +508,14 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     CASC_TRY(cudaEventRecord(ev, st));
     CASC_TRY(cudaStreamWaitEvent(bs->cout, ev, 0));
     const size_t row = (size_t)batch * L * sizeof(float);
+    timing_mark("tail launched for " + std::to_string(cnt) + " channels", st);
+    if (bs->zero_copy && a0 == 0) {
+      const int64_t row4 = (int64_t)batch * L / 4;
+      emit_rows_kernel<<<kEmitCtas, 512, 0, bs->cout>>>(reinterpret_cast<const float4*>(y),
+                                                        reinterpret_cast<float4*>(bs->y_host), dlist, cnt, row4);
+      CASC_LAUNCHED();
+      return CASC_OK;
+    }
     for (int i = 0; i < cnt;) {                   // merge runs of consecutive channel ids
       int j = i + 1;
       while (j < cnt && hlist[j] == hlist[j - 1] + 1) ++j;
@@ -412,43 +526,37 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     return CASC_OK;
   };
   // ---- head: stages 0..Kc-1 (+ Bbar u), all channels
-  // the input copy of a host-buffer run is on a copy stream: the head (and the D u tail) may read u
-  // only after it landed
-  if (bs && bs->u_event) CASC_TRY(cudaStreamWaitEvent(st, bs->u_event, 0));
-  {
+  // the input of a host-buffer run arrives in chunks on a copy stream: the head runs per chunk after
+  // it landed (and the D u tails, later on st, after all of them)
+  const bool chunked = bs && bs->n_chunks > 0;
+  for (int ci = 0; ci < (chunked ? bs->n_chunks : 1); ++ci) {
+    if (ci == 0) timing_mark("before head", st);
+    if (chunked) CASC_TRY(cudaStreamWaitEvent(st, bs->u_events[ci], 0));
+    const int hc0 = chunked ? bs->bounds[ci] : 0, hcn = chunked ? bs->bounds[ci + 1] - hc0 : n;
     BankHeadArg a{};
     a.u = static_cast<const float*>(u); a.krT = w.krT; a.V = static_cast<float*>(w.Va);
-    a.sys_list = dorder; a.n_list = n; a.L = L; a.batch = batch;
+    a.sys_list = chunked ? diota + hc0 : dorder; a.n_list = hcn; a.L = L; a.batch = batch;
     if (use_ab) a.op = op;
-    ProfScope ps(st, K_BANK_HEAD, (double)n * batch * L * (1 + m) * 4.0,
-                 (double)n * batch * L * 2.0 * m * 128);
+    ProfScope ps(st, K_BANK_HEAD, (double)hcn * batch * L * (1 + m) * 4.0,
+                 (double)hcn * batch * L * 2.0 * m * 128);
     // executed: m = 64 issues three tf32 products per K step (hi.[hi|lo] at N = 128, lo.hi)
-    if (m == 64) ps.exec((double)n * batch * L * (1 + m) * 4.0, 3.0 * n * batch * L * 2.0 * m * 128, PIPE_TF32);
+    if (m == 64) ps.exec((double)hcn * batch * L * (1 + m) * 4.0, 3.0 * hcn * batch * L * 2.0 * m * 128, PIPE_TF32);
     // m = 64: warp-specialized TMA-store head (bank_head_ws.cu); m = 16, 32: CUDA-core head.
     // Measured alternatives not kept: a TMEM-operand variant (1.67 vs 1.30 ms on E2),
     // the head on CTA pairs (same 1.16 ms: the head is bound by the tensor pipe, 69% active)
     if (m == 64) {
-      a.tiles_per_cta = pick_group(ntiles, (int64_t)n * batch, 64);
-      rc = launch_bank_head_ws(m, a, (int64_t)n * batch, st);
+      a.tiles_per_cta = pick_group(ntiles, (int64_t)hcn * batch, 64);
+      rc = launch_bank_head_ws(m, a, (int64_t)n * batch, st);   // V map: every sequence of the wave
     } else {
-      a.tiles_per_cta = pick_group(ntiles, (int64_t)n * batch, 16);
+      a.tiles_per_cta = pick_group(ntiles, (int64_t)hcn * batch, 16);
       rc = launch_bank_head(m, a, st);
     }
     if (rc) return rc;
+    timing_mark("head chunk " + std::to_string(ci), st);
   }
   // cascades whose output parts come from the head (Ne <= 7; with fold also Ne = 8)
   if ((rc = emit(count_lp_ge(kHeadK + 1), n))) return rc;
-  auto tmark = [&](const char* what) {              // CASC_TIMING diagnostics
-    if (!getenv("CASC_TIMING") || !g_timing_t0) return;
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    cudaEventRecord(e, st);
-    cudaEventSynchronize(e);
-    float t;
-    cudaEventElapsedTime(&t, g_timing_t0, e);
-    fprintf(stderr, "casc timing: %s %.3f ms\n", what, t);
-    cudaEventDestroy(e);
-  };
+  auto tmark = [&](const char* what) { timing_mark(std::string(what) + " n=" + std::to_string(n), st); };
   tmark("head done");
   if (q_done) CASC_TRY(cudaStreamWaitEvent(st, q_done, 0));   // the pair weights
   // ---- streaming stages k >= kHeadK over the channels with Neff > k (prefixes of `order`)

@@ -286,6 +286,16 @@ int DevCtx::ensure_pinned(size_t n_ints) {
   return CASC_OK;
 }
 
+int DevCtx::ensure_dmeta(size_t n_ints) {
+  if (dmeta_n >= n_ints) return CASC_OK;
+  if (dmeta) cudaFree(dmeta);
+  dmeta = nullptr;
+  dmeta_n = 0;
+  CASC_TRY(cudaMalloc(&dmeta, sizeof(int) * n_ints));
+  dmeta_n = n_ints;
+  return CASC_OK;
+}
+
 DevCtx* dev_ctx() {
   static std::mutex create_mu;
   static DevCtx* ctx[64] = {};
@@ -489,6 +499,7 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
     CASC_TRY(cudaMemcpyAsync(h.Bbar, Bbar_h, sizeof(double) * n_sys * m, cudaMemcpyHostToDevice, st));
     CASC_TRY(cudaMemcpyAsync(h.C, C_h, sizeof(double) * n_sys * m, cudaMemcpyHostToDevice, st));
     if (D_h) CASC_TRY(cudaMemcpyAsync(h.D, D_h, sizeof(double) * n_sys, cudaMemcpyHostToDevice, st));
+    CASC_TRY(cudaEventRecord(ctx->inputs_free, st));   // the first wave's input copy overlaps the powers
     rc = engine_powers(n_sys, m, N_host, N_max, h.Abar, mode, h.pack, st);
     if (rc) return rc;
     rc = engine_bank_pipelined(n_sys, m, L, batch, N_host, N_max, h.pack, h.Bbar, h.C, D_h ? h.D : nullptr,

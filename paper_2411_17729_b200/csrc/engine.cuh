@@ -16,6 +16,9 @@ struct DevCtx {
   int* pinned = nullptr;
   size_t pinned_n = 0;
   int ensure_pinned(size_t n_ints);   // grow the pinned staging (caller holds mu)
+  int* dmeta = nullptr;               // device copy of the bank channel tables (all waves)
+  size_t dmeta_n = 0;
+  int ensure_dmeta(size_t n_ints);    // grow it (caller holds mu)
 };
 DevCtx* dev_ctx();                    // the current device's context; nullptr on a CUDA error
 
