@@ -50,13 +50,15 @@ def _device_y(wl, u_store):
     return dw.y_f64()
 
 
-def _run_host(wl, u_store, ws_bytes=None):
-    """casc_run_host on pinned host buffers with a NaN-filled device workspace."""
+def _run_host(wl, u_store, ws_bytes=None, pinned=True):
+    """casc_run_host on pinned (or pageable) host buffers with a NaN-filled device workspace."""
     import paper_2411_17729_b200 as pk
     from paper_2411_17729_b200.runner import storage_to_torch
     n = wl.n_ch
-    u_h = storage_to_torch(u_store, wl.mode).reshape(n, wl.batch, wl.L, wl.p).pin_memory()
-    y_h = torch.full((n, wl.batch, wl.L, wl.q), float("nan"), dtype=u_h.dtype).pin_memory()
+    u_h = storage_to_torch(u_store, wl.mode).reshape(n, wl.batch, wl.L, wl.p).clone()
+    y_h = torch.full((n, wl.batch, wl.L, wl.q), float("nan"), dtype=u_h.dtype)
+    if pinned:
+        u_h, y_h = u_h.pin_memory(), y_h.pin_memory()
     need = pk.run_host_bytes(n, wl.m, wl.p, wl.q, wl.L, wl.batch, int(wl.N.max()), wl.mode)
     ws = torch.empty(need if ws_bytes is None else ws_bytes, dtype=torch.uint8, device="cuda")
     ws.fill_(0xFF)                                   # NaN in every float lane
@@ -108,6 +110,24 @@ def test_bank_run_host_full_size_input_lands_before_use():
         assert np.all(np.isfinite(y_host))
         y_dev = _device_y(wlk, u)
         assert np.array_equal(y_host, y_dev), f"call {k}"
+
+
+def test_bank_run_host_pageable_buffers_bitwise():
+    """Pageable host buffers: the bank path cannot store the last emission straight into y_h (it is
+    not device-mapped) and copies it out instead; both runs, over >= 3 ramped waves, are bitwise
+    equal to the device-resident path."""
+    import paper_2411_17729_b200 as pk
+    wl = S.make_E2(n_ch=24, L=4096, batch=2, seed=7)
+    n = wl.n_ch
+    full = pk.run_host_bytes(n, wl.m, 1, 1, wl.L, wl.batch, int(wl.N.max()), "fp32")
+    per_ch = pk.bank_workspace_bytes(1, wl.m, wl.L, wl.batch, int(wl.N.max()), "fp32")
+    apply_full = pk.bank_workspace_bytes(n, wl.m, wl.L, wl.batch, int(wl.N.max()), "fp32")
+    ws_bytes = full - apply_full + 8 * per_ch + (per_ch // 2)     # eight channels per wave
+    wlk, u = _inputs(wl, 3)
+    y_dev = _device_y(wlk, u)
+    for pinned in (False, True):
+        y_host = _run_host(wlk, u, ws_bytes, pinned=pinned)
+        assert np.array_equal(y_host, y_dev), f"pinned={pinned}"
 
 
 # ------------------------------------------------------------------ MIMO: batch chunks
