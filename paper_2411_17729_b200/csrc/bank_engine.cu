@@ -30,12 +30,21 @@ cudaEvent_t g_timing_t0 = nullptr;   // CASC_TIMING diagnostics: origin recorded
 // CASC_TIMING diagnostics: labelled events recorded without synchronising, printed by
 // engine_bank_pipelined after its final synchronisation
 static std::vector<std::pair<std::string, cudaEvent_t>> g_marks;
-static void timing_mark(const std::string& what, cudaStream_t s) {
+void timing_mark(const std::string& what, cudaStream_t s) {
   if (!getenv("CASC_TIMING") || !g_timing_t0) return;
   cudaEvent_t e;
   cudaEventCreate(&e);
   cudaEventRecord(e, s);
   g_marks.emplace_back(what, e);
+}
+void timing_print() {                              // after a device synchronisation
+  for (auto& mk : g_marks) {
+    float t;
+    cudaEventElapsedTime(&t, g_timing_t0, mk.second);
+    fprintf(stderr, "casc timing: %8.3f ms  %s\n", t, mk.first.c_str());
+    cudaEventDestroy(mk.second);
+  }
+  g_marks.clear();
 }
 
 static constexpr int kHeadK = 7;      // Krylov head covers stages 0..6 (128 lags)
@@ -367,13 +376,7 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
     cudaDeviceSynchronize();
     float ta, tb, tc;
     cudaEventElapsedTime(&ta, g_timing_t0, a); cudaEventElapsedTime(&tb, g_timing_t0, b); cudaEventElapsedTime(&tc, g_timing_t0, c);
-    for (auto& mk : g_marks) {
-      float t;
-      cudaEventElapsedTime(&t, g_timing_t0, mk.second);
-      fprintf(stderr, "casc timing: %8.3f ms  %s\n", t, mk.first.c_str());
-      cudaEventDestroy(mk.second);
-    }
-    g_marks.clear();
+    timing_print();
     fprintf(stderr, "casc timing: input copies done %.3f, compute done %.3f, output copies done %.3f ms\n", ta, tb, tc);
     cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c);
   }

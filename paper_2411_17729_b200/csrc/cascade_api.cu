@@ -23,7 +23,7 @@
 #include "profile.cuh"
 
 namespace casc {
-extern cudaEvent_t g_timing_t0;   // bank_engine.cu (diagnostics)
+
 thread_local int g_launches = 0;
 
 struct ApplyWs {
@@ -517,6 +517,10 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
     // copy (copy-in stream) overlaps the previous chunk's compute and whose output copy (copy-out
     // stream) overlaps the next chunk's; the input copy may start before the powers (they do not
     // touch u; E3: 0.67 ms of squarings)
+    if (getenv("CASC_TIMING")) {                        // diagnostics: timeline origin
+      if (!casc::g_timing_t0) cudaEventCreate(&casc::g_timing_t0);
+      cudaEventRecord(casc::g_timing_t0, st);
+    }
     CASC_TRY(cudaEventRecord(ctx->inputs_free, st));
     rc = engine_powers(1, m, N_host, N_max, h.Abar, mode, h.pack, st);
     if (rc) return rc;
@@ -554,6 +558,7 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
       PackLayout P = pack_layout(h.pack, 1, m, N_max, mode);
       if ((rc = mimo_derive(m, p, q, Ne, P, h.Bbar, h.C, D_h ? h.D : nullptr, w, mode == CASC_FP32, st))) return rc;
     }
+    timing_mark("powers + derived", st);
     // The first and the last chunk are exposed (nothing to overlap their input / output copy with).
     // When such a chunk is a single sequence and the impulse response is short against L, it runs
     // as kW time windows (rows [r0, r1) computed from inputs [r0 - Hu, r1), Hu = 2^(Ne+1) - 1, exact:
@@ -583,11 +588,14 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
                                   cudaMemcpyHostToDevice, ctx->in)) || !ok(cudaEventRecord(wev[j], ctx->in)))
             return false;
         }
+        timing_mark("chunk 0 input landed", ctx->in);
         return ok(cudaEventRecord(ev[0], ctx->in));
       }
-      return ok(cudaMemcpyAsync((char*)h.u + b0[i] * in_row, (const char*)u_h + b0[i] * in_row,
-                                (size_t)(b0[i + 1] - b0[i]) * in_row, cudaMemcpyHostToDevice, ctx->in)) &&
-             ok(cudaEventRecord(ev[2 * i], ctx->in));
+      const bool r = ok(cudaMemcpyAsync((char*)h.u + b0[i] * in_row, (const char*)u_h + b0[i] * in_row,
+                                        (size_t)(b0[i + 1] - b0[i]) * in_row, cudaMemcpyHostToDevice, ctx->in)) &&
+                     ok(cudaEventRecord(ev[2 * i], ctx->in));
+      timing_mark("chunk " + std::to_string(i) + " input landed", ctx->in);
+      return r;
     };
     auto run_windows = [&](int i) {                   // one sequence: b0[i]
       const char* us = (const char*)h.u + b0[i] * in_row;
@@ -621,6 +629,7 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
                         h.apply_bytes, st);
         }
         if (rc) break;
+        timing_mark("chunk " + std::to_string(i) + " computed", st);
         if (!(wi && i == nc - 1)) {                   // the whole chunk's output
           if (!ok(cudaEventRecord(ev[2 * i + 1], st)) || !ok(cudaStreamWaitEvent(ctx->out, ev[2 * i + 1], 0)) ||
               !ok(cudaMemcpyAsync((char*)y_h + b0[i] * out_row, (const char*)h.y + b0[i] * out_row,
@@ -632,8 +641,10 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
     }
     // drain all three streams before returning, also on error: no copy into or out of the caller's
     // host buffers may still be in flight, and the events are destroyed only once unused
+    timing_mark("outputs copied", ctx->out);
     const cudaError_t e1 = cudaStreamSynchronize(ctx->out), e2 = cudaStreamSynchronize(st);
     const cudaError_t e3 = cudaStreamSynchronize(ctx->in);
+    if (getenv("CASC_TIMING") && g_timing_t0) timing_print();
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (rc) return rc;

@@ -1,6 +1,7 @@
 // Host engine entry points (internal).
 #pragma once
 #include <mutex>
+#include <string>
 #include "common.cuh"
 
 namespace casc {
@@ -21,6 +22,10 @@ struct DevCtx {
   int ensure_dmeta(size_t n_ints);    // grow it (caller holds mu)
 };
 DevCtx* dev_ctx();                    // the current device's context; nullptr on a CUDA error
+// CASC_TIMING diagnostics (bank_engine.cu): labelled events against the origin casc_run_host records
+void timing_mark(const std::string& what, cudaStream_t s);
+void timing_print();
+extern cudaEvent_t g_timing_t0;
 
 size_t apply_ws_bytes(int n, int m, int p, int q, int64_t L, int batch, int mode, int n_max);
 int validate_common(int n, int m, int p, int q, int64_t L, int batch, int N_max, int mode);
