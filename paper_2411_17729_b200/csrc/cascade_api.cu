@@ -314,6 +314,13 @@ DevCtx* dev_ctx() {
   return ctx[dev];
 }
 
+static int coop_max_m() {                          // diagnostics A/B: CASC_POWERS_COOP_MAX
+  static const int v = [] {
+    const char* e = getenv("CASC_POWERS_COOP_MAX");
+    return e ? atoi(e) : 512;
+  }();
+  return v;
+}
 int engine_powers(int n, int m, const int* N_host, int N_max, const double* Abar, int mode,
                   void* pack, cudaStream_t st) {
   if (n < 1 || m < 1 || N_max < 0 || !N_host || !Abar || !pack) return CASC_ERR_ARG;
@@ -333,7 +340,7 @@ int engine_powers(int n, int m, const int* N_host, int N_max, const double* Abar
   }
   // MIMO with m <= 512: one cooperative launch (squarings + pack); E3 powers 0.38 -> 0.28 ms. At
   // m = 1024 (256 tiles per level) the per-level launches measured faster (E4: 2.08 vs 2.39 ms, A/B)
-  if (n == 1 && m <= 512) {
+  if (n == 1 && m <= coop_max_m()) {
     ProfScope ps(st, K_POWERS, 16.0 * mm * (N_host[0] + 1), 2.0 * (double)mm * m * N_host[0]);
     ps.exec(24.0 * mm * N_host[0] + 16.0 * mm * (N_host[0] + 1), 2.0 * (double)mm * m * N_host[0], PIPE_FP64);
     return launch_powers_coop(P, Abar, N_host[0], m, st);
