@@ -228,19 +228,20 @@ constexpr int kPowKC = 64;
 // fragment loads per 16 DMMAs instead of 9 per 8), K chunks of 16 double-buffered. Same per-element
 // DMMA chain over K as dmma_tile: bitwise equal.
 template <int WR, int WC>
-__global__ void __launch_bounds__(32 * WR * WC) dgemm_mma_w32_kernel(DgemmArg a) {
-  constexpr int KC = 16, TR = 32 * WR, TC = 32 * WC, NT = 32 * WR * WC;
-  constexpr int LA = KC + 4, LB = TC == 32 ? 36 : 72;
-  __shared__ __align__(16) double sA[2][TR * LA];
-  __shared__ __align__(16) double sB[2][KC * LB];
-  const int s = blockIdx.z;
-  if (a.skip_below && a.skip_below[s] < a.level) return;
-  const int64_t selA = a.selA ? a.selA[s] : 0, selB = a.selB ? a.selB[s] : 0;
-  const double* A = a.A + s * a.sA + selA * a.nA;
-  const double* B = a.B + s * a.sB + selB * a.nB;
-  double* C = a.C + s * a.sC;
-  const double* Cadd = a.Cadd ? a.Cadd + s * a.sCadd : nullptr;
-  const int M = a.M, N = a.N, K = a.K, row0 = blockIdx.y * TR, col0 = blockIdx.x * TC;
+struct DmmaW32 {
+  static constexpr int KC = 16, TR = 32 * WR, TC = 32 * WC, NT = 32 * WR * WC;
+  static constexpr int LA = KC + 4, LB = TC == 32 ? 36 : 72;
+  double A[2][TR * LA];
+  double B[2][KC * LB];
+};
+template <int WR, int WC>
+__device__ __forceinline__ void dmma_tile_w32(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                                              int64_t ldc, const double* Cadd, int M, int N, int K, int row0,
+                                              int col0, DmmaW32<WR, WC>& sm) {
+  using D = DmmaW32<WR, WC>;
+  constexpr int KC = D::KC, TR = D::TR, TC = D::TC, NT = D::NT, LA = D::LA, LB = D::LB;
+  auto& sA = sm.A;
+  auto& sB = sm.B;
   const int tid = threadIdx.x, w = tid / 32, lane = tid % 32, g = lane >> 2, t4 = lane & 3;
   const int r0 = 32 * (w % WR), c0 = 32 * (w / WR);
   auto load = [&](int buf, int k0) {
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(32 * WR * WC) dgemm_mma_w32_kernel(DgemmArg a)
       const int r = e / KC, kk = e % KC;
       const int gr = row0 + r, gk = k0 + kk;
       const bool va = gr < M && gk < K;
-      cp_async8(&sA[buf][r * LA + kk], A + (va ? (int64_t)gr * a.lda + gk : 0), va);
+      cp_async8(&sA[buf][r * LA + kk], A + (va ? (int64_t)gr * lda + gk : 0), va);
     }
 #pragma unroll
     for (int i = 0; i < TC * KC / NT; ++i) {
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(32 * WR * WC) dgemm_mma_w32_kernel(DgemmArg a)
       const int kb = e / TC, c = e % TC;
       const int gkb = k0 + kb, gc = col0 + c;
       const bool vb = gkb < K && gc < N;
-      cp_async8(&sB[buf][kb * LB + c], B + (vb ? (int64_t)gkb * a.ldb + gc : 0), vb);
+      cp_async8(&sB[buf][kb * LB + c], B + (vb ? (int64_t)gkb * ldb + gc : 0), vb);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -305,10 +306,20 @@ __global__ void __launch_bounds__(32 * WR * WC) dgemm_mma_w32_kernel(DgemmArg a)
         const int gc = col0 + c0 + 8 * j + 2 * t4 + h;
         if (gc >= N) continue;
         double v = d[i][j][h];
-        if (Cadd) v += Cadd[(int64_t)gr * a.ldc + gc];
-        C[(int64_t)gr * a.ldc + gc] = v;
+        if (Cadd) v += Cadd[(int64_t)gr * ldc + gc];
+        C[(int64_t)gr * ldc + gc] = v;
       }
   }
+}
+template <int WR, int WC>
+__global__ void __launch_bounds__(32 * WR * WC) dgemm_mma_w32_kernel(DgemmArg a) {
+  __shared__ __align__(16) DmmaW32<WR, WC> sm;
+  const int s = blockIdx.z;
+  if (a.skip_below && a.skip_below[s] < a.level) return;
+  const int64_t selA = a.selA ? a.selA[s] : 0, selB = a.selB ? a.selB[s] : 0;
+  dmma_tile_w32<WR, WC>(a.A + s * a.sA + selA * a.nA, a.lda, a.B + s * a.sB + selB * a.nB, a.ldb, a.C + s * a.sC, a.ldc,
+                        a.Cadd ? a.Cadd + s * a.sCadd : nullptr, a.M, a.N, a.K, blockIdx.y * DmmaW32<WR, WC>::TR,
+                        blockIdx.x * DmmaW32<WR, WC>::TC, sm);
 }
 
 template <int KC>
