@@ -108,7 +108,7 @@ def spectral_radius(A: np.ndarray) -> float:
 
 def n_cap_for_length(L: int) -> int:
     """Largest useful N: 2^(N+1) >= L makes the cascade exact (stages with 2^k >= L are identities)."""
-    return max(0, math.ceil(math.log2(max(L, 2))) - 1)
+    return max(0, (max(L, 2) - 1).bit_length() - 1)      # ceil(log2 L) - 1 in exact integer arithmetic
 
 
 def plan_N(Abar: np.ndarray, tol: float, N_cap: int) -> int:
