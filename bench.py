@@ -49,8 +49,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-seqshard", action="store_true",
                     help="E4: run the sequence-sharded code path even at one rank (validation)")
-    ap.add_argument("--halo", default="per_stage", choices=["per_stage", "oneshot_u"],
-                    help="E4 sequence sharding: per-stage halo (BASELINE configs[3]) or one-shot u halo (NEXT-2)")
+    ap.add_argument("--halo", default="per_stage", choices=["per_stage", "oneshot_u", "peer"],
+                    help="E4 sequence sharding: per-stage halo over NCCL (BASELINE configs[3]), one-shot u halo "
+                         "(NEXT-2), or peer: halo rows stored by the producing GEMM into rank r+1 (NEXT-2 fused)")
     return ap.parse_args()
 
 

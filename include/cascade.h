@@ -194,15 +194,26 @@ int casc_comm_init(void** comm, int rank, int world, const void* nccl_unique_id)
 int casc_comm_init_local(void** comms, int world);
 int casc_comm_destroy(void* comm);
 int casc_comm_rank(const void* comm, int* rank, int* world);
-/* halo: how the shard boundary is crossed
+/* halo: how the shard boundary is crossed (all three give the same y bit for bit)
  *   CASC_HALO_PER_STAGE  (BASELINE configs[3]) one exchange per step as above; compute = the shard.
+ *   CASC_HALO_PEER       (fused) the step producing v^(k) stores the last 2^k rows
+ *                        of its output ALSO into rank r+1's halo rows, from the GEMM epilogue over a
+ *                        peer mapping (NVLink), tile by tile as they are produced; the transport
+ *                        only orders the ranks with 1-byte tokens (ready: rank r-1's producing step
+ *                        finished; consumed: rank r+1 has read the halo rows about to be
+ *                        overwritten). NCCL ranks map rank r+1's ws through CUDA IPC once per call
+ *                        (ws must be cudaMalloc memory; else every rank returns
+ *                        CASC_ERR_UNSUPPORTED); emulated ranks store into each other's ws directly.
+ *                        Needs the CTA-pair GEMMs (m a multiple of 256 in bf16, of 128 in fp32) and
+ *                        halo rows produced by the interior launch (2^k * batch <= L_loc * batch -
+ *                        boundary rows), else CASC_ERR_UNSUPPORTED.
  *   CASC_HALO_ONESHOT_U one exchange of Hu = 2^(Ne+1) - 1 time rows of u from rank
  *                        r-1 (the cascade is a polynomial of degree 2^(Ne+1) - 1 in the shift,
  *                        PAPER.md:137-141), then the cascade runs on the window [l0 - Hu, l0 + L_loc)
  *                        with no further communication: Hu / L_loc extra rows of work (E4 at 8 ranks:
  *                        3.1%). Requires Hu <= L_loc when world > 1.
- * Both give the same y bit for bit (each output row is computed by the same operations). */
-enum { CASC_HALO_PER_STAGE = 0, CASC_HALO_ONESHOT_U = 1 };
+ * (each output row is computed by the same operations in every mode). */
+enum { CASC_HALO_PER_STAGE = 0, CASC_HALO_ONESHOT_U = 1, CASC_HALO_PEER = 2 };
 size_t casc_apply_seqsharded_workspace(int m, int p, int q, int64_t L_loc, int batch, int N, int world, int mode,
                                        int halo);
 int casc_apply_seqsharded(void* comm, int m, int p, int q, int64_t L_loc, int batch, int N, int N_max, int mode,

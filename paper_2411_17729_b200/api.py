@@ -218,7 +218,7 @@ def comm_init_local(world: int) -> list:
     return [Comm(ctypes.c_void_p(h)) for h in hs]
 
 
-HALOS = {"per_stage": 0, "oneshot_u": 1}
+HALOS = {"per_stage": 0, "oneshot_u": 1, "peer": 2}
 
 
 def seqsharded_workspace_bytes(m, p, q, L_loc, batch, N, world, mode, halo="per_stage") -> int:
@@ -229,7 +229,8 @@ def apply_seqsharded(comm: Comm, pw: Powers, Bbar, C, D, u_loc, y=None, ws=None,
                      comm_stream=None, halo="per_stage"):
     """This rank's shard: u_loc [L_loc][batch][p] (time-major, storage dtype) -> y [L_loc][batch][q].
     The halo exchange with the neighbouring ranks happens inside the library (comm_stream):
-    halo='per_stage' (one exchange per step) or 'oneshot_u' (2^(Ne+1)-1 rows of u once, NEXT-2)."""
+    halo='per_stage' (one exchange per step), 'oneshot_u' (2^(Ne+1)-1 rows of u once, NEXT-2) or
+    'peer' (the producing GEMM stores the halo rows into rank r+1's buffer; tokens order the ranks)."""
     if pw.n_sys != 1:
         raise ValueError("apply_seqsharded() takes a single-system pack")
     m, N, md = pw.m, pw.N[0], pw.mode

@@ -663,6 +663,7 @@ static int launch_cfg(const MimoGemm& g, cudaStream_t st) {
 int launch_mimo_gemm(const MimoGemm& g, bool tf32, cudaStream_t st) {
   if (mimo_pair_ok(g, tf32)) return launch_mimo_gemm_pair(g, st);
   if (tf32 && mimo_pair_tf32_ok(g)) return launch_mimo_gemm_pair_tf32(g, st);
+  if (g.peer_out) return CASC_ERR_UNSUPPORTED;      // peer-halo stores: CTA-pair kernels only
   // one-CTA kernel; template arguments <BN, TF32, residual/staging chunks, resident weight chunks>
   // are the measured-best splits of shared memory: 3xTF32 N = 64 keeps 4 residual
   // chunks (3 with the resident weights of a stage pair), bf16 N = 256 four (11% faster on E4 than 2)

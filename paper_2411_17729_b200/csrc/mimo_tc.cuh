@@ -26,6 +26,10 @@ struct MimoArg {
   int64_t gt;                        // tiles per block of the CTA tile walk
   unsigned long long* dbg;           // optional wait-cycle counters (CASC_GEMM_DBG=1)
   int64_t perm_j;                    // time-tile order within a sequence (0: natural), see decode()
+  // sequence-sharded peer halo (CASC_HALO_PEER, seqshard.cu): output rows l >= peer_l_begin are also
+  // stored into the successor rank's buffer of the same layout, at storage row out_row0 + l -
+  // peer_shift (its halo rows), through a peer-mapped pointer (CTA-pair kernels only)
+  void* peer_out; int64_t peer_l_begin, peer_shift;
 };
 struct MimoSrc {
   const void* A; const void* W; int K; int64_t shift;
@@ -52,6 +56,8 @@ struct MimoGemm {
   // blocks are skipped, NEXT-3) and the profiler's issued-flop counter
   const int* tri = nullptr;
   unsigned long long* flop_counter = nullptr;
+  // see MimoArg::peer_out (the CTA-pair kernels; other kernels report CASC_ERR_UNSUPPORTED)
+  void* peer_out = nullptr; int64_t peer_l_begin = 0, peer_shift = 0;
 };
 
 // Tile order of the CTA-pair GEMMs (mimo_tc2.cu, mimo_tc3.cu): pair p walks t = p, p + P, ... and

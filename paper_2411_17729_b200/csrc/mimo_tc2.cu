@@ -268,6 +268,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         mbar_wait(&rfull[rs], rph);
         uint8_t* rrow = rbuf + row * 128;
+        // this row also goes to the successor rank's halo rows (peer halo, seqshard.cu): straight
+        // from registers over the peer mapping (NVLink), as the tile is produced
+        const int64_t lrow = (int64_t)tc.l0 + row;
+        __nv_bfloat16* prow = (a.peer_out && lrow >= a.peer_l_begin && lrow < a.L)
+            ? static_cast<__nv_bfloat16*>(a.peer_out) + ((int64_t)tc.seq * (a.out_row0 + a.L) + a.out_row0 + lrow - a.peer_shift) * a.n_out + tc.nb * BN + j * CW
+            : nullptr;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           uint4* p = reinterpret_cast<uint4*>(rrow + ((c ^ (row & 7)) * 16));
@@ -281,6 +287,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             f[4] += r2.x; f[5] += r2.y; f[6] += r3.x; f[7] += r3.y;
           }
           *p = make_uint4(pack_bf16_2(f[0], f[1]), pack_bf16_2(f[2], f[3]), pack_bf16_2(f[4], f[5]), pack_bf16_2(f[6], f[7]));
+          if (prow) *reinterpret_cast<uint4*>(prow + 8 * c) = *p;
         }
         fence_async_smem();
         named_sync2(1, 128);
@@ -297,6 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
     }
     if (leader_t) bulk_wait2<0>();
+    if (a.peer_out) __threadfence_system();       // peer stores visible before the kernel completes
   }
   tc_fence_before();
   cluster_sync();                                          // no CTA of the pair still uses TMEM
@@ -335,6 +343,7 @@ int launch_mimo_gemm_pair(const MimoGemm& g, cudaStream_t st) {
   a.has_residual = g.R != nullptr;
   a.r_row0 = (int)g.R_row0;
   a.out_row0 = (int)g.out_row0;
+  a.peer_out = g.peer_out; a.peer_l_begin = g.peer_l_begin; a.peer_shift = g.peer_shift;
   if (g.R && !map3d(&maps.R, g.R, false, g.n_out, g.R_row0 + g.L, nseq_total, HM)) return CASC_ERR_CUDA;
   if (!map3d(&maps.out, g.out, false, g.n_out, g.out_row0 + g.L, nseq_total, HM)) return CASC_ERR_CUDA;
   if (cudaFuncSetAttribute(mimo_gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess)

@@ -332,6 +332,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         mbar_wait(&rfull[rs], rph);
         uint8_t* rrow = rbuf + row * 128;         // SW128: 16-B chunk c at ((c ^ (row % 8)) * 16)
+        // the successor rank's halo rows (peer halo, seqshard.cu), from registers over the peer mapping
+        const int64_t lrow = (int64_t)tc.l0 + row;
+        float* prow = (a.peer_out && lrow >= a.peer_l_begin && lrow < a.L)
+            ? static_cast<float*>(a.peer_out) + ((int64_t)tc.seq * (a.out_row0 + a.L) + a.out_row0 + lrow - a.peer_shift) * a.n_out + tc.nb * BN + j * CW
+            : nullptr;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           float4* p = reinterpret_cast<float4*>(rrow + ((c ^ (row & 7)) * 16));
@@ -341,6 +346,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
           }
           *p = o;
+          if (prow) *reinterpret_cast<float4*>(prow + 4 * c) = o;
         }
         fence_async_smem();
         named_sync3(1, 128);
@@ -357,6 +363,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
     }
     if (leader_t) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (a.peer_out) __threadfence_system();       // peer stores visible before the kernel completes
   }
   tc_fence_before();
   cluster_sync3();                                         // no CTA of the pair still uses TMEM
@@ -401,6 +408,7 @@ static int launch_pt(const MimoGemm& g, cudaStream_t st) {
     if (!map3d(&maps.W[s], g.src[s].W, true, g.src[s].K, g.n_out, planes, BN / 2)) return CASC_ERR_CUDA;
   }
   a.has_residual = g.R != nullptr;
+  a.peer_out = g.peer_out; a.peer_l_begin = g.peer_l_begin; a.peer_shift = g.peer_shift;
   a.r_row0 = (int)g.R_row0;
   a.out_row0 = (int)g.out_row0;
   if (g.R && !map3d(&maps.R, g.R, true, g.n_out, g.R_row0 + g.L, nseq_total, HM)) return CASC_ERR_CUDA;

@@ -27,6 +27,12 @@
 //   local  R emulated ranks in one process on one device (tests): each rank's apply runs on its own
 //          host thread and streams; a halo is a device copy ordered by CUDA events, with a host
 //          rendezvous per exchange. Ranks never spin on each other inside a kernel.
+//
+// CASC_HALO_PEER (apply_peer below): no halo copies at all -- the GEMM producing v^(k) stores its
+// last 2^k rows ALSO into rank r+1's halo rows (epilogue of the CTA-pair kernels, over a peer
+// mapping of rank r+1's workspace: CUDA IPC between NCCL ranks, the plain pointer between emulated
+// ranks), and the transport carries only 1-byte ordering tokens.
+#include <cuda.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -57,6 +63,7 @@ struct NcclApi {
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -76,6 +83,7 @@ static const NcclApi& nccl() {
     a.GroupStart = (decltype(a.GroupStart))dlsym(h, "ncclGroupStart");
     a.GroupEnd = (decltype(a.GroupEnd))dlsym(h, "ncclGroupEnd");
     a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+    a.AllReduce = (decltype(a.AllReduce))dlsym(h, "ncclAllReduce");
     a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.Send && a.Recv && a.GroupStart && a.GroupEnd;
     return a;
   }();
@@ -103,6 +111,7 @@ struct LocalGroup {
   struct Post { const void* src = nullptr; size_t bytes = 0; cudaEvent_t ready = nullptr; };
   std::map<std::pair<int, long>, Post> sends;          // keyed by receiving rank
   std::map<std::pair<int, long>, cudaEvent_t> copied;  // keyed by sending rank
+  std::map<std::pair<int, long>, void*> ws_posts;      // CASC_HALO_PEER: each rank's workspace
   std::vector<cudaEvent_t> owned;
   ~LocalGroup() {
     for (auto e : owned) cudaEventDestroy(e);
@@ -119,22 +128,28 @@ struct Comm {
   ncclComm_t nc = nullptr;
   std::shared_ptr<LocalGroup> grp;
   long tag = 0;                 // exchanges issued by this rank (same sequence on every rank)
+  // CASC_HALO_PEER between NCCL ranks: IPC mappings of the successor's workspaces (opened once per
+  // allocation, closed by casc_comm_destroy) and a small device scratch for the handle exchange
+  std::vector<std::pair<cudaIpcMemHandle_t, void*>> ipc;
+  void* scratch = nullptr;
 };
 
-// One halo exchange on the comm stream `cs`: send `sbytes` from `sbuf` to rank+1 (if any),
-// receive `rbytes` into `rbuf` from rank-1 (if any). `after` (may be null) orders the send after
-// the producing work; returns with an event on `cs` recorded in `done` (the exchange finished).
+// One halo exchange on the comm stream `cs`: send `sbytes` from `sbuf` to rank+dir (if any),
+// receive `rbytes` into `rbuf` from rank-dir (if any); dir = +1 (the halo direction) or -1.
+// `after` (may be null) orders the send after the producing work; returns with an event on `cs`
+// recorded in `done` (the exchange finished).
 static int exchange(Comm* c, const void* sbuf, size_t sbytes, void* rbuf, size_t rbytes, cudaEvent_t after,
-                    cudaStream_t cs, cudaEvent_t done) {
+                    cudaStream_t cs, cudaEvent_t done, int dir = 1) {
   if (after) CASC_TRY(cudaStreamWaitEvent(cs, after, 0));
-  const bool send = c->rank + 1 < c->world, recv = c->rank > 0;
+  const int to = c->rank + dir, from = c->rank - dir;
+  const bool send = to >= 0 && to < c->world, recv = from >= 0 && from < c->world;
   const long tag = c->tag++;
   if (c->kind == 0) {
     if (send || recv) {
       const NcclApi& n = nccl();
       CASC_NCCL(n.GroupStart());
-      if (send) CASC_NCCL(n.Send(sbuf, sbytes, ncclUint8, c->rank + 1, c->nc, cs));
-      if (recv) CASC_NCCL(n.Recv(rbuf, rbytes, ncclUint8, c->rank - 1, c->nc, cs));
+      if (send) CASC_NCCL(n.Send(sbuf, sbytes, ncclUint8, to, c->nc, cs));
+      if (recv) CASC_NCCL(n.Recv(rbuf, rbytes, ncclUint8, from, c->nc, cs));
       CASC_NCCL(n.GroupEnd());
     }
   } else {
@@ -145,10 +160,10 @@ static int exchange(Comm* c, const void* sbuf, size_t sbytes, void* rbuf, size_t
       CASC_TRY(cudaEventRecord(ready, cs));
       std::lock_guard<std::mutex> lk(g.mu);
       g.owned.push_back(ready);
-      g.sends[{c->rank + 1, tag}] = LocalGroup::Post{sbuf, sbytes, ready};
+      g.sends[{to, tag}] = LocalGroup::Post{sbuf, sbytes, ready};
       g.cv.notify_all();
     }
-    if (recv) {                                          // wait for rank-1's post, copy, report back
+    if (recv) {                                          // wait for rank-dir's post, copy, report back
       LocalGroup::Post p;
       {
         std::unique_lock<std::mutex> lk(g.mu);
@@ -164,10 +179,10 @@ static int exchange(Comm* c, const void* sbuf, size_t sbytes, void* rbuf, size_t
       CASC_TRY(cudaEventRecord(cp, cs));
       std::lock_guard<std::mutex> lk(g.mu);
       g.owned.push_back(cp);
-      g.copied[{c->rank - 1, tag}] = cp;
+      g.copied[{from, tag}] = cp;
       g.cv.notify_all();
     }
-    if (send) {                                          // the send completes when rank+1 has copied
+    if (send) {                                          // the send completes when rank+dir has copied
       cudaEvent_t cp;
       {
         std::unique_lock<std::mutex> lk(g.mu);
@@ -186,6 +201,7 @@ struct SeqWs {
   MimoWs mw;           // derived weights (no state buffers: L = 0)
   void* u_edge;        // [(uh + Bu) batch][p]: the u halo (uh time rows) + the first Bu local rows of u
   void *Va, *Vb;       // [(H + L_loc) * batch][m]
+  char* tok;           // CASC_HALO_PEER ordering tokens: [0] sent, [128] received
   size_t bytes;
 };
 static constexpr int64_t kRowBlock = 256;            // boundary granularity: one CTA-pair tile
@@ -211,6 +227,7 @@ static SeqWs carve_seq(void* ws, int m, int p, int q, int64_t L_loc, int batch, 
   w.u_edge = c.take<char>((size_t)(uh * batch + Bu) * p * es);
   w.Va = c.take<char>((size_t)(H * batch + rows) * m * es);
   w.Vb = c.take<char>((size_t)(H * batch + rows) * m * es);
+  w.tok = c.take<char>(256);
   w.bytes = c.bytes();
   return w;
 }
@@ -325,6 +342,248 @@ static int apply_oneshot(Comm* c, int m, int p, int q, int64_t L_loc, int batch,
 }
 
 
+// ------------------------------------------------------------------------------ CASC_HALO_PEER
+// The successor's (rank + 1) workspace as a pointer this device can store into; null on the last
+// rank. Emulated ranks post their ws pointers through the group. NCCL ranks send a CUDA IPC handle
+// of their ws allocation (+ the offset of ws in it) to rank - 1 and map the one they receive (once
+// per allocation, cached in the comm); an allreduce makes every rank agree that the mapping worked.
+static int peer_ws(Comm* c, void* ws, cudaStream_t cs, void** succ) {
+  *succ = nullptr;
+  const long tag = c->tag++;
+  if (c->kind == 1) {
+    LocalGroup& g = *c->grp;
+    std::unique_lock<std::mutex> lk(g.mu);
+    g.ws_posts[{c->rank, tag}] = ws;
+    g.cv.notify_all();
+    if (c->rank + 1 < c->world) {
+      if (!g.cv.wait_for(lk, kRendezvous, [&] { return g.ws_posts.count({c->rank + 1, tag}) > 0; })) return CASC_ERR_NCCL;
+      *succ = g.ws_posts[{c->rank + 1, tag}];
+    }
+    return CASC_OK;
+  }
+  if (c->world == 1) return CASC_OK;
+  const NcclApi& n = nccl();
+  if (!n.AllReduce) return CASC_ERR_UNSUPPORTED;
+  struct Msg { cudaIpcMemHandle_t h; uint64_t off; int32_t ok; int32_t pad; };
+  static_assert(sizeof(Msg) <= 128, "scratch layout");
+  if (!c->scratch) CASC_TRY(cudaMalloc(&c->scratch, 512));
+  char* sc = static_cast<char*>(c->scratch);                 // [0] my msg, [128] successor's, [256] flag
+  Msg mine{};
+  {
+    using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static GetRange get_range = [] {
+      void* f = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      return (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) == cudaSuccess &&
+              q == cudaDriverEntryPointSuccess) ? reinterpret_cast<GetRange>(f) : nullptr;
+    }();
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (get_range && get_range(&base, &size, (CUdeviceptr)ws) == CUDA_SUCCESS &&
+        cudaIpcGetMemHandle(&mine.h, (void*)base) == cudaSuccess) {
+      mine.off = (uint64_t)((CUdeviceptr)ws - base);
+      mine.ok = 1;
+    }
+    cudaGetLastError();                                       // a VMM allocation has no IPC handle
+  }
+  CASC_TRY(cudaMemcpyAsync(sc, &mine, sizeof(mine), cudaMemcpyHostToDevice, cs));
+  cudaEvent_t done;
+  CASC_TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  int rc = exchange(c, sc, 128, sc + 128, 128, nullptr, cs, done, -1);   // to rank - 1, from rank + 1
+  cudaEventDestroy(done);
+  if (rc) return rc;
+  Msg theirs{};
+  if (c->rank + 1 < c->world) CASC_TRY(cudaMemcpyAsync(&theirs, sc + 128, sizeof(theirs), cudaMemcpyDeviceToHost, cs));
+  CASC_TRY(cudaStreamSynchronize(cs));
+  int ok = 1;
+  if (c->rank + 1 < c->world) {
+    ok = theirs.ok;
+    if (ok) {
+      void* mapped = nullptr;
+      for (auto& e : c->ipc)
+        if (!memcmp(&e.first, &theirs.h, sizeof(theirs.h))) mapped = e.second;
+      if (!mapped) {
+        if (cudaIpcOpenMemHandle(&mapped, theirs.h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
+          c->ipc.emplace_back(theirs.h, mapped);
+        } else {
+          cudaGetLastError();
+          mapped = nullptr;
+          ok = 0;
+        }
+      }
+      if (mapped) *succ = static_cast<char*>(mapped) + theirs.off;
+    }
+  }
+  // every rank must take the same path: agree on the minimum
+  int* flag = reinterpret_cast<int*>(sc + 256);
+  CASC_TRY(cudaMemcpyAsync(flag, &ok, sizeof(int), cudaMemcpyHostToDevice, cs));
+  CASC_NCCL(n.AllReduce(flag, flag, 1, ncclInt32, ncclMin, c->nc, cs));
+  CASC_TRY(cudaMemcpyAsync(&ok, flag, sizeof(int), cudaMemcpyDeviceToHost, cs));
+  CASC_TRY(cudaStreamSynchronize(cs));
+  if (!ok) {
+    *succ = nullptr;
+    return CASC_ERR_UNSUPPORTED;
+  }
+  return CASC_OK;
+}
+
+// The per-stage schedule of casc_apply_seqsharded with the halo rows delivered by the producing
+// GEMM itself (see the file header). Per step k, on rank r (stream order on st / cs):
+//   interior launch of step k-1 (its epilogue stores v^(k)'s last 2^k rows into rank r+1's halo
+//   rows) -> token "ready" to r+1 ... boundary launch of step k after "ready" from r-1 -> token
+//   "consumed" to r-1; the next interior launch (which overwrites rank r+1's halo rows of the other
+//   buffer) waits for "consumed" from r+1. One token exchange at the start ("my buffers are free")
+//   covers the previous call. Every rank issues the same sequence of exchanges.
+static int apply_peer(Comm* c, int m, int p, int q, int64_t L_loc, int batch, int Ne, int N_max, int mode,
+                      const PackLayout& P, const double* Bbar, const double* C, const double* D, const void* u_loc,
+                      void* y_loc, void* ws, size_t ws_bytes, cudaStream_t st, cudaStream_t cs) {
+  SeqWs w = carve_seq(ws, m, p, q, L_loc, batch, Ne, mode);
+  if (ws_bytes < w.bytes) return CASC_ERR_WORKSPACE;
+  const bool tf32 = mode == CASC_FP32;
+  const size_t es = tf32 ? 4 : 2;
+  const int64_t rows = L_loc * batch, Hr = mimo_out_halo(Ne) * batch, mm = (int64_t)m * m;
+  const int uh = u_halo_rows(Ne);
+  const int k0 = Ne >= 2 ? 2 : 1, kl = mimo_fold(Ne) ? Ne - 1 : Ne;
+  auto halo_time = [&](int k) -> int64_t { return k < kl ? ((int64_t)1 << k) : mimo_out_halo(Ne); };
+  // every pushed row must come from an interior launch
+  for (int k = k0; k <= kl; ++k) {
+    const int64_t s_prev = k == k0 ? uh : ((int64_t)1 << (k - 1));
+    if (rows - halo_time(k) * batch < boundary_rows(s_prev, batch, rows)) return CASC_ERR_UNSUPPORTED;
+  }
+  {                                                  // the state-producing GEMMs must be CTA-pair
+    MimoGemm head{}, stage{};                        // kernels (decided alike on every rank)
+    head.n_src = Ne >= 2 ? 4 : 2;
+    for (int j = 0; j < head.n_src; ++j) head.src[j].K = p;
+    head.n_out = m;
+    stage.n_src = 1; stage.src[0].K = m; stage.n_out = m;
+    auto pair = [&](const MimoGemm& g) { return mimo_pair_ok(g, tf32) || (tf32 && mimo_pair_tf32_ok(g)); };
+    if (!pair(head) || (k0 < kl && !pair(stage))) return CASC_ERR_UNSUPPORTED;
+  }
+  int rc;
+  void* succ = nullptr;
+  if ((rc = peer_ws(c, ws, cs, &succ))) return rc;
+  auto peer_of = [&](void* local) -> void* { return succ ? static_cast<char*>(succ) + (static_cast<char*>(local) - static_cast<char*>(ws)) : nullptr; };
+  if ((rc = mimo_derive(m, p, q, Ne, P, Bbar, C, D, w.mw, tf32, st))) return rc;
+
+  std::vector<cudaEvent_t> evs;
+  struct EvFree {
+    std::vector<cudaEvent_t>& v;
+    ~EvFree() { for (auto e : v) cudaEventDestroy(e); }
+  } ev_free{evs};
+  auto new_event = [&](cudaEvent_t* e) -> int {
+    CASC_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    evs.push_back(*e);
+    return CASC_OK;
+  };
+  cudaEvent_t ev_in, ev_uhalo, ev_ack;
+  if ((rc = new_event(&ev_in)) || (rc = new_event(&ev_uhalo)) || (rc = new_event(&ev_ack))) return rc;
+  // rank 0's halo rows stay zero; the others are overwritten by rank r-1's pushes
+  CASC_TRY(cudaMemsetAsync(w.Va, 0, (size_t)Hr * m * es, st));
+  CASC_TRY(cudaMemsetAsync(w.Vb, 0, (size_t)Hr * m * es, st));
+  const size_t uhb = (size_t)uh * batch * p * es;
+  CASC_TRY(cudaMemsetAsync(w.u_edge, 0, uhb, st));
+  const int64_t Bu = boundary_rows(uh, batch, rows);
+  CASC_TRY(cudaMemcpyAsync((char*)w.u_edge + uhb, u_loc, (size_t)Bu * p * es, cudaMemcpyDeviceToDevice, st));
+  CASC_TRY(cudaEventRecord(ev_in, st));
+  {                                                  // the u halo (an input: exchanged as it is)
+    CASC_TRY(cudaStreamWaitEvent(cs, ev_in, 0));
+    ProfScope ps(cs, K_SEQ_HALO, 2.0 * uhb, 0.0);
+    if ((rc = exchange(c, (const char*)u_loc + (size_t)(rows - (int64_t)uh * batch) * p * es, uhb, w.u_edge, uhb,
+                       nullptr, cs, ev_uhalo)))
+      return rc;
+  }
+  // "my halo rows are free": after the memsets (and everything before this call on st)
+  if ((rc = exchange(c, w.tok, 1, w.tok + 128, 1, ev_in, cs, ev_ack, -1))) return rc;
+
+  const double dr = (double)rows;
+  const int pipe = tf32 ? PIPE_TF32 : PIPE_BF16;
+  const double xf = tf32 ? 3.0 : 1.0;
+  // interior rows of a step; with `push`, its output rows l >= rows - d also land in rank r+1's halo
+  auto interior = [&](MimoGemm g, int64_t s_time, void* out_local, int64_t d_push, int cls, double bytes,
+                      double flops) -> int {
+    const int64_t Bs = boundary_rows(s_time, batch, rows);
+    if (d_push > 0 && succ) {
+      g.peer_out = peer_of(out_local);
+      g.peer_l_begin = rows - d_push;
+      g.peer_shift = rows;
+    }
+    CASC_TRY(cudaStreamWaitEvent(st, ev_ack, 0));    // rank r+1 has read what we overwrite
+    ProfScope ps(st, cls, bytes * (dr - Bs) / dr, flops * (dr - Bs) / dr);
+    ps.exec(bytes * (dr - Bs) / dr, xf * flops * (dr - Bs) / dr, pipe);
+    return Bs < rows ? step_gemm(g, rows, (int)(Bs / 128), tf32, st) : CASC_OK;
+  };
+  auto boundary = [&](MimoGemm g, int64_t s_time, cudaEvent_t ready, int cls, double bytes, double flops) -> int {
+    const int64_t Bs = boundary_rows(s_time, batch, rows);
+    CASC_TRY(cudaStreamWaitEvent(st, ready, 0));
+    ProfScope ps(st, cls, bytes * Bs / dr, flops * Bs / dr);
+    ps.exec(bytes * Bs / dr, xf * flops * Bs / dr, pipe);
+    return step_gemm(g, Bs, 0, tf32, st);
+  };
+  auto ready_token = [&](cudaEvent_t* ready) -> int {        // after the interior launch just queued
+    cudaEvent_t after;
+    int r2;
+    if ((r2 = new_event(&after)) || (r2 = new_event(ready))) return r2;
+    CASC_TRY(cudaEventRecord(after, st));
+    return exchange(c, w.tok, 1, w.tok + 128, 1, after, cs, *ready, 1);
+  };
+  auto consumed_token = [&]() -> int {                        // after the boundary launch just queued
+    cudaEvent_t after;
+    int r2;
+    if ((r2 = new_event(&after)) || (r2 = new_event(&ev_ack))) return r2;
+    CASC_TRY(cudaEventRecord(after, st));
+    return exchange(c, w.tok, 1, w.tok + 128, 1, after, cs, ev_ack, -1);
+  };
+
+  // ---- first step (Krylov head or fused first step): v^(k0), its last rows pushed to rank r+1
+  void* Vhead = k0 == 2 ? w.Vb : w.Va;
+  cudaEvent_t ready;
+  {
+    const void* Wj[4] = {w.mw.Bb, w.mw.AB, w.mw.A2B, w.mw.A3B};
+    MimoGemm g{};
+    g.n_src = Ne >= 2 ? 4 : 2;
+    for (int j = 0; j < g.n_src; ++j) g.src[j] = {u_loc, Wj[j], p, (int64_t)j * batch};
+    g.out = Vhead; g.out_row0 = Hr; g.n_out = m;
+    MimoGemm gb = g;
+    for (int j = 0; j < g.n_src; ++j) {
+      gb.src[j] = {w.u_edge, Wj[j], p, (int64_t)j * batch};
+      gb.src[j].row0 = uh * batch;
+    }
+    const double by = dr * (p + m) * es, fl = dr * 2.0 * g.n_src * m * p;
+    if ((rc = interior(g, uh, Vhead, halo_time(k0) * batch, K_MIMO_FIRST, by, fl))) return rc;
+    if ((rc = ready_token(&ready))) return rc;
+    if ((rc = boundary(gb, uh, ev_uhalo, K_MIMO_FIRST, by, fl))) return rc;
+  }
+  // ---- steps k = k0 .. kl (the last one is the output step)
+  for (int k = k0; k <= kl; ++k) {
+    void* Vs = (k - 1) % 2 == 0 ? w.Va : w.Vb;       // holds v^(k), halo rows pushed by rank r-1
+    void* Vd = (k % 2 == 0) ? w.Va : w.Vb;
+    const int64_t d = halo_time(k) * batch;
+    MimoGemm g{};
+    cudaEvent_t next_ready = nullptr;
+    double by, fl;
+    int cls;
+    if (k < kl) {
+      const void* Wk = tf32 ? static_cast<const void*>(P.f32 + k * 2 * mm) : static_cast<const void*>(P.b16 + k * mm);
+      g.src[0] = {Vs, Wk, m, d};
+      g.src[0].row0 = Hr;
+      g.n_src = 1; g.R = Vs; g.R_row0 = Hr; g.out = Vd; g.out_row0 = Hr; g.n_out = m;
+      by = dr * m * es * 2.0; fl = dr * 2.0 * (double)mm; cls = K_MIMO_STAGE;
+      if ((rc = interior(g, (int64_t)1 << k, Vd, halo_time(k + 1) * batch, cls, by, fl))) return rc;
+      if ((rc = ready_token(&next_ready))) return rc;
+    } else {
+      mimo_output_gemm(g, w.mw, Ne, m, p, q, Vs, Hr, u_loc, 0, D != nullptr, batch);
+      g.out = y_loc; g.n_out = q;
+      const double k_in = (double)(g.n_src - (D ? 1 : 0)) * m + (D ? p : 0);
+      by = dr * (m + p + q) * es; fl = dr * 2.0 * q * k_in; cls = K_MIMO_LAST;
+      if ((rc = interior(g, halo_time(k), nullptr, 0, cls, by, fl))) return rc;
+    }
+    if ((rc = boundary(g, k < kl ? ((int64_t)1 << k) : halo_time(k), ready, cls, by, fl))) return rc;
+    if ((rc = consumed_token())) return rc;
+    ready = next_ready;
+  }
+  return CASC_OK;
+}
+
 }  // namespace casc
 
 using namespace casc;
@@ -379,6 +638,8 @@ int casc_comm_destroy(void* comm) {
   if (!comm) return CASC_ERR_ARG;
   auto* c = static_cast<Comm*>(comm);
   int rc = CASC_OK;
+  for (auto& e : c->ipc) cudaIpcCloseMemHandle(e.second);
+  if (c->scratch) cudaFree(c->scratch);
   if (c->kind == 0 && c->nc && nccl().CommDestroy(c->nc) != ncclSuccess) rc = CASC_ERR_NCCL;
   delete c;
   return rc;
@@ -411,9 +672,14 @@ int casc_apply_seqsharded(void* comm, int m, int p, int q, int64_t L_loc, int ba
   if (rc) return rc;
   if (N < 0 || N > N_max) return CASC_ERR_DIM;
   if (!mimo_tc_supported(m, p, q)) return CASC_ERR_UNSUPPORTED;
-  if (halo != CASC_HALO_PER_STAGE && halo != CASC_HALO_ONESHOT_U) return CASC_ERR_ARG;
+  if (halo != CASC_HALO_PER_STAGE && halo != CASC_HALO_ONESHOT_U && halo != CASC_HALO_PEER) return CASC_ERR_ARG;
   const int64_t L = L_loc * c->world;
   const int Ne = eff_order(N, L);
+  if (halo == CASC_HALO_PEER && Ne > 0) {
+    if (c->world > 1 && (mimo_out_halo(Ne) > L_loc || u_halo_rows(Ne) > L_loc)) return CASC_ERR_UNSUPPORTED;
+    return apply_peer(c, m, p, q, L_loc, batch, Ne, N_max, mode, pack_layout(const_cast<void*>(pack), 1, m, N_max, mode),
+                      Bbar, C, D, u_loc, y_loc, ws, ws_bytes, (cudaStream_t)compute_stream, (cudaStream_t)comm_stream);
+  }
   if (halo == CASC_HALO_ONESHOT_U) {
     // the Hu-row window must come from the immediate predecessor
     if (c->world > 1 && oneshot_halo_rows(Ne) > L_loc) return CASC_ERR_UNSUPPORTED;

@@ -143,3 +143,72 @@ def test_oneshot_u_halo_bitwise(mode, case):
     torch.cuda.synchronize()
     assert torch.equal(y_one.permute(1, 0, 2), dw.y)
 
+
+
+PEER_CASES = [  # (R, m, p, q, L, N): the CTA-pair GEMMs (bf16: m % 256 == 0; fp32: m % 128 == 0)
+    (2, 256, 64, 64, 4096, 8),
+    (4, 256, 64, 128, 8192, 6),
+    (3, 256, 64, 64, 3000, 7),      # rows not a multiple of the 256-row blocks
+    (2, 256, 64, 64, 2048, 2),      # Ne = 2: the head's rows go straight to the output step
+    (2, 256, 64, 64, 256, 0),       # Ne = 0: no state halo (the per-stage schedule)
+]
+
+
+@pytest.mark.parametrize("mode", ["bf16", "fp32"])
+@pytest.mark.parametrize("case", PEER_CASES)
+def test_peer_halo_bitwise(mode, case):
+    """NEXT-2 fused: the GEMM producing v^(k) stores its last 2^k rows into rank r+1's halo rows
+    from its epilogue (emulated ranks: into the other rank's workspace on this device), the
+    transport only orders the ranks with tokens. Bitwise the per-stage halo and the unsharded
+    casc_apply: the halo rows are the same values, read by the same operations."""
+    import paper_2411_17729_b200 as pk
+    R, m, p, q, L, N = case
+    if mode == "fp32" and m % 128:
+        pytest.skip("fp32 peer halo needs m % 128 == 0")
+    wl = S.make_random_mimo(m, p, q, L=L, batch=3, N=N, rho=0.97, mode=mode)
+    comms = pk.comm_init_local(R)
+    try:
+        y_peer = _sharded(wl, R, comms, halo="peer")
+        y_peer2 = _sharded(wl, R, comms, halo="peer")              # a second call on the same comms
+    finally:
+        for c in comms:
+            c.destroy()
+    comms = pk.comm_init_local(R)
+    try:
+        y_per = _sharded(wl, R, comms, halo="per_stage")
+    finally:
+        for c in comms:
+            c.destroy()
+    assert torch.equal(y_peer, y_per)
+    assert torch.equal(y_peer2, y_per)
+    from paper_2411_17729_b200.runner import DeviceWorkload
+    dw = DeviceWorkload(wl)
+    dw.step()
+    torch.cuda.synchronize()
+    assert torch.equal(y_peer.permute(1, 0, 2), dw.y)
+
+
+def test_peer_halo_one_nccl_rank():
+    """One NCCL rank: no successor, no IPC mapping; the peer schedule equals the per-stage one."""
+    import paper_2411_17729_b200 as pk
+    wl = S.make_random_mimo(256, 64, 64, L=2048, batch=2, N=7, rho=0.97, mode="bf16")
+    one = pk.comm_init(0, 1, pk.nccl_unique_id())
+    try:
+        y_peer = _sharded(wl, 1, [one], halo="peer")
+        y_per = _sharded(wl, 1, [one], halo="per_stage")
+    finally:
+        one.destroy()
+    assert torch.equal(y_peer, y_per)
+
+
+def test_peer_halo_needs_pair_gemm():
+    """m = 128 in bf16 runs on the one-CTA GEMM, which cannot store into a peer: UNSUPPORTED."""
+    import paper_2411_17729_b200 as pk
+    wl = S.make_random_mimo(128, 64, 64, L=2048, batch=2, N=6, rho=0.97, mode="bf16")
+    comms = pk.comm_init_local(2)
+    try:
+        with pytest.raises(pk.CascadeError, match="UNSUPPORTED"):
+            _sharded(wl, 2, comms, halo="peer")
+    finally:
+        for c in comms:
+            c.destroy()
