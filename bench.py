@@ -312,7 +312,8 @@ def run_reference(args, world, rank):
     """--impl reference: the float64 oracle on the host cores, rank 0 only."""
     if rank != 0:
         return
-    wl, chans, cfgd = make_workload(args.config, 1, 0)
+    # the workload and config our arm reports at this world size (its rank-0 part: channels of rank 0)
+    wl, chans, cfgd = make_workload(args.config, world, 0)
     per_step = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
         oracle_sample(wl, chans, per_step / 4, max_units=1)
