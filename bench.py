@@ -328,7 +328,8 @@ def run_reference(args, world, rank):
     cores = ci["blas_threads"]
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
             "samples_per_s": tot_s / tot_t, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong" if args.config == "E5" or (args.config == "E4" and world > 1) else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE recipe)", "config": cfgd,
             "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
                              "sample": desc + f"; each step a bounded sample (~{per_step:.0f}s)", **ci},
