@@ -84,25 +84,33 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
 
   if (warp == 0) {
     // ---------------------------------------------------------------- Z producer
-    float ur[9];
-    auto load_u = [&](int i) {                    // u[t0-127 .. t0+160] (259 used)
-      const int64_t base = (tile_begin + i) * TM - (KL - 1);
+    // Window of tile i: W_i[w] = u[t0_i - 127 + w], w < 259 (Z-row w reads W_i[w .. w + 3]). The next
+    // window is this one shifted by 128: W_{i+1}[w] = W_i[w + 128] for w < 131, and 128 new values
+    // W_{i+1}[131 .. 259) = u[t0_i + 132 ..) -- so after the CTA's first tile each tile reads 128
+    // values of u, not 259.
+    float nr[4];
+    auto load_new = [&](int i) {                  // W_i[131 .. 259)
+      const int64_t base = (tile_begin + i) * TM - (KL - 1) + 131;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t t = base + lane + 32 * q;
+        nr[q] = (i < nt && t >= 0 && t < a.L) ? __ldg(u + t) : 0.f;
+      }
+    };
+    {                                             // the first window in full
+      const int64_t base = tile_begin * TM - (KL - 1);
 #pragma unroll
       for (int q = 0; q < 9; ++q) {
         const int64_t t = base + lane + 32 * q;
-        ur[q] = (i < nt && t >= 0 && t < a.L) ? __ldg(u + t) : 0.f;
+        if (lane + 32 * q < 264) Us[lane + 32 * q] = (nt > 0 && t >= 0 && t < a.L) ? __ldg(u + t) : 0.f;
       }
-    };
-    load_u(0);
+      load_new(1);
+      __syncwarp();
+    }
     for (int i = 0; i < nt; ++i) {
       const int slot = i & 1;
       if (i >= 2) mbar_wait(&z_empty[slot], (uint32_t)(((i - 2) >> 1) & 1));
       float* us = Us + slot * 264;
-#pragma unroll
-      for (int q = 0; q < 9; ++q)
-        if (lane + 32 * q < 264) us[lane + 32 * q] = ur[q];
-      __syncwarp();
-      load_u(i + 1);                              // prefetch the next window
       float* zh = Zb + slot * 2 * ZR * 4;
       float* zl = zh + ZR * 4;
 #pragma unroll
@@ -115,6 +123,15 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
       }
       fence_async_smem();
       mbar_arrive(&z_full[slot]);
+      if (i + 1 < nt) {                           // W_{i+1} into the other slot
+        float* un = Us + (slot ^ 1) * 264;
+#pragma unroll
+        for (int q = 0; q < 5; ++q)
+          if (lane + 32 * q < 131) un[lane + 32 * q] = us[lane + 32 * q + 128];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) un[131 + lane + 32 * q] = nr[q];
+        load_new(i + 2);                          // prefetch the next new values
+      }
       __syncwarp();
     }
   } else if (warp == 1) {
