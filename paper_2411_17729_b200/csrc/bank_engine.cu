@@ -267,7 +267,7 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
   };
   // u may be overwritten only after earlier work on st: ctx->inputs_free, recorded by the caller
   // after its parameter copies and before the powers (an input copy submitted ahead of the
-  // parameter copies delays them on the copy engine: E2 5.48 vs 4.26 ms e2e)
+  // parameter copies would delay them on the copy engine; round 1 measured that order slower)
   CASC_TRY(cudaStreamWaitEvent(ctx->in, ctx->inputs_free, 0));
   const size_t row = (size_t)batch * L * sizeof(float);
   // wave sizes (CASC_WAVE_RAMP = r, 0: uniform): ramp up from nw/r channels and back down (s, 2s,
