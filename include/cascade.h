@@ -91,6 +91,15 @@ int casc_target_sm(void);
 size_t casc_pack_bytes(int n_sys, int m, int N_max, int mode);
 int casc_powers(int n_sys, int m, const int* N_host, int N_max, const double* Abar, int mode,
                 void* pack, void* stream);
+/* a0 / a1 diagnostics for the planner (SURVEY §8(b) tail_norm_fro): the Frobenius norms of the
+ * float64 powers in `pack`, ||P_k||_F for k = 0..N_s, and of the first neglected power
+ * ||P_{N_s+1}||_F = ||P_{N_s} P_{N_s}||_F, whose size sets the truncation error of H_N
+ * (the error term is (z^-1 Abar)^(2^(N+1)) times a bounded factor). P_{N_s+1}
+ * is formed block by block in float64 and reduced, never stored.
+ *   pack        DEVICE, from casc_powers(n_sys, m, N_host, N_max, mode, ...).
+ *   norms_host  HOST double [n_sys][N_max + 2] (written): entry k of system s; NaN for k > N_s + 1.
+ * Synchronises `stream` (host output). Errors: CASC_ERR_ARG, CASC_ERR_DIM, CASC_ERR_CUDA. */
+int casc_powers_norms(int n_sys, int m, int N_max, int mode, const void* pack, double* norms_host, void* stream);
 
 /* ----------------------------------------------------------------------------------------
  * a2-a5  Apply one LTI system (MIMO or SISO) to `batch` sequences of length L --

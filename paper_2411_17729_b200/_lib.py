@@ -21,6 +21,7 @@ SIGNATURES = {
     "casc_last_launch_count": (c_int, []),
     "casc_pack_bytes": (c_size_t, [c_int, c_int, c_int, c_int]),
     "casc_powers": (c_int, [c_int, c_int, P_int, c_int, c_void_p, c_int, c_void_p, c_void_p]),
+    "casc_powers_norms": (c_int, [c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "casc_apply_workspace_bytes": (c_size_t, [c_int, c_int, c_int, c_int64, c_int, c_int, c_int]),
     "casc_apply": (c_int, [c_int, c_int, c_int, c_int64, c_int, c_int, c_int, c_int,
                            c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

@@ -72,6 +72,16 @@ def powers(Abar: torch.Tensor, N, mode="fp32", N_max: int | None = None, stream=
     return Powers(pack, n_sys, m, Ns, N_max, md)
 
 
+def powers_norms(pw: Powers, stream=None):
+    """||P_k||_F for k = 0..N_s + 1 of each system (the last one the first neglected power, the
+    planner's truncation indicator); numpy float64 [n_sys][N_max + 2], NaN past N_s + 1."""
+    import numpy as np
+    out = np.empty((pw.n_sys, pw.N_max + 2), dtype=np.float64)
+    check(lib().casc_powers_norms(pw.n_sys, pw.m, pw.N_max, pw.mode, _p(pw.pack),
+                                  out.ctypes.data_as(ctypes.c_void_p), _stream(stream)), "casc_powers_norms")
+    return out
+
+
 def apply_workspace_bytes(m, p, q, L, batch, N, mode) -> int:
     return int(lib().casc_apply_workspace_bytes(m, p, q, L, batch, N, _mode(mode)))
 

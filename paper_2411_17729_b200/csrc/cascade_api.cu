@@ -402,6 +402,39 @@ int casc_powers(int n_sys, int m, const int* N_host, int N_max, const double* Ab
   return engine_powers(n_sys, m, N_host, N_max, Abar, mode, pack, (cudaStream_t)stream);
 }
 
+int casc_powers_norms(int n_sys, int m, int N_max, int mode, const void* pack, double* norms_host, void* stream) {
+  g_launches = 0;
+  if (n_sys < 1 || m < 1 || N_max < 0 || !pack || !norms_host) return CASC_ERR_ARG;
+  if (mode != CASC_FP32 && mode != CASC_BF16) return CASC_ERR_ARG;
+  if (N_max > 62) return CASC_ERR_DIM;
+  cudaStream_t st = (cudaStream_t)stream;
+  DevCtx* ctx = dev_ctx();
+  if (!ctx) return CASC_ERR_CUDA;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  const size_t n = (size_t)n_sys * (N_max + 2);
+  if (ctx->dnorm_n < n) {
+    if (ctx->dnorm) cudaFree(ctx->dnorm);
+    ctx->dnorm = nullptr;
+    ctx->dnorm_n = 0;
+    CASC_TRY(cudaMalloc(&ctx->dnorm, n * sizeof(double)));
+    ctx->dnorm_n = n;
+  }
+  PackLayout P = pack_layout(const_cast<void*>(pack), n_sys, m, N_max, mode);
+  std::vector<int> Ns(n_sys);
+  CASC_TRY(cudaMemsetAsync(ctx->dnorm, 0, n * sizeof(double), st));
+  CASC_TRY(cudaMemcpyAsync(Ns.data(), P.hdr, sizeof(int) * n_sys, cudaMemcpyDeviceToHost, st));
+  int rc = launch_powers_sumsq(P, n_sys, N_max, m, ctx->dnorm, st);
+  if (rc) return rc;
+  CASC_TRY(cudaMemcpyAsync(norms_host, ctx->dnorm, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CASC_TRY(cudaStreamSynchronize(st));
+  for (int s = 0; s < n_sys; ++s)
+    for (int k = 0; k < N_max + 2; ++k) {
+      double& v = norms_host[(size_t)s * (N_max + 2) + k];
+      v = k <= Ns[s] + 1 ? sqrt(v) : NAN;
+    }
+  return CASC_OK;
+}
+
 size_t casc_apply_workspace_bytes(int m, int p, int q, int64_t L, int batch, int N, int mode) {
 
   if (m < 1 || p < 1 || q < 1 || L < 1 || batch < 1) return 0;

@@ -556,6 +556,52 @@ int launch_powers_small(const PackLayout& P, const double* Abar, int n_sys, int 
   return CASC_OK;
 }
 
+// Diagnostics for the planner (casc_powers_norms): sums of squares of the stored float64 powers
+// P_k (k <= N_s) of every system, and of the first neglected power P_{N_s+1} = P_{N_s} P_{N_s},
+// formed 16 x 16 entries per block in registers (float64 FMA) and reduced, never stored.
+// acc [n_sys][N_max + 2] (zeroed by the caller).
+__global__ void powers_sumsq_kernel(const double* p64, const int* hdr, int N_max, int m, double* acc) {
+  const int s = blockIdx.y, k = blockIdx.z;               // system, power index 0..N_max
+  if (k > hdr[s]) return;
+  const int64_t mm = (int64_t)m * m;
+  const double* P = p64 + ((int64_t)s * (N_max + 1) + k) * mm;
+  double t = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < mm; e += (int64_t)gridDim.x * blockDim.x)
+    t = fma(P[e], P[e], t);
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(acc + (int64_t)s * (N_max + 2) + k, t);
+}
+__global__ void next_power_sumsq_kernel(const double* p64, const int* hdr, int N_max, int m, double* acc) {
+  const int s = blockIdx.z, Ns = hdr[s];
+  const int64_t mm = (int64_t)m * m;
+  const double* P = p64 + ((int64_t)s * (N_max + 1) + Ns) * mm;
+  __shared__ double As[16][17], Bs[16][17];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int row = blockIdx.y * 16 + ty, col = blockIdx.x * 16 + tx;
+  double c = 0.0;
+  for (int k0 = 0; k0 < m; k0 += 16) {
+    As[ty][tx] = (row < m && k0 + tx < m) ? P[(int64_t)row * m + k0 + tx] : 0.0;
+    Bs[ty][tx] = (k0 + ty < m && col < m) ? P[(int64_t)(k0 + ty) * m + col] : 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) c = fma(As[ty][kk], Bs[kk][tx], c);
+    __syncthreads();
+  }
+  double t = c * c;
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(acc + (int64_t)s * (N_max + 2) + Ns + 1, t);
+}
+int launch_powers_sumsq(const PackLayout& P, int n_sys, int N_max, int m, double* acc, cudaStream_t st) {
+  const int64_t mm = (int64_t)m * m;
+  dim3 g1((unsigned)std::min<int64_t>(ceil_div(mm, 256), 64), (unsigned)n_sys, (unsigned)(N_max + 1));
+  powers_sumsq_kernel<<<g1, 256, 0, st>>>(P.p64, P.hdr, N_max, m, acc);
+  CASC_LAUNCHED();
+  dim3 g2((unsigned)ceil_div(m, 16), (unsigned)ceil_div(m, 16), (unsigned)n_sys);
+  next_power_sumsq_kernel<<<g2, 256, 0, st>>>(P.p64, P.hdr, N_max, m, acc);
+  CASC_LAUNCHED();
+  return CASC_OK;
+}
+
 __global__ void f64_to_f32_kernel(const double* src, float* dst, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)

@@ -17,6 +17,8 @@ struct DevCtx {
   int* pinned = nullptr;
   size_t pinned_n = 0;
   int ensure_pinned(size_t n_ints);   // grow the pinned staging (caller holds mu)
+  double* dnorm = nullptr;            // casc_powers_norms accumulators
+  size_t dnorm_n = 0;
   int* dmeta = nullptr;               // device copy of the bank channel tables (all waves)
   size_t dmeta_n = 0;
   int ensure_dmeta(size_t n_ints);    // grow it (caller holds mu)

@@ -30,6 +30,7 @@ struct DerivedPlan {
 };
 int launch_derived_coop(const DerivedPlan& plan, cudaStream_t st);
 int launch_pack(const PackLayout& P, int n_sys, int N_max, int m, cudaStream_t st);
+int launch_powers_sumsq(const PackLayout& P, int n_sys, int N_max, int m, double* acc, cudaStream_t st);
 // a1 for ONE system with m > 64: all squarings and the packing in one cooperative launch
 int launch_powers_coop(const PackLayout& P, const double* Abar, int N, int m, cudaStream_t st);
 int launch_powers_small(const PackLayout& P, const double* Abar, int n_sys, int N_max, int m, cudaStream_t st);

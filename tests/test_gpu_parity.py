@@ -74,6 +74,27 @@ def test_powers_fp64_match_oracle(m, N):
         assert abs(p64[15][0, 0] / 5.87548e-15 - 1) < 2e-5
 
 
+@pytest.mark.parametrize("m,N,mode", [(64, 13, "fp32"), (256, 9, "bf16"), (100, 15, "fp32")])
+def test_powers_norms_match_oracle(m, N, mode):
+    """casc_powers_norms: ||P_k||_F for k <= N and the first neglected power P_{N+1} = P_N P_N
+    (the planner's truncation indicator) against the oracle's float64 powers."""
+    import paper_2411_17729_b200 as pk
+    if m == 100:
+        Abar, _ = S.trapezoid(S.hippo(100), None, 5e-4)
+        Ns = [N]
+    else:
+        Abar = np.stack([S.make_random_mimo(m, 1, 1, 8, 1, 0, rho=0.99, seed=s).Abar[0] for s in range(3)])
+        Ns = [N, N - 2, 0]
+    A = torch.from_numpy(np.ascontiguousarray(Abar)).cuda()
+    pw = pk.powers(A, Ns, mode)
+    got = pk.powers_norms(pw)
+    for s, Ns_ in enumerate(Ns):
+        ref = oracle.powers(Abar if Abar.ndim == 2 else Abar[s], Ns_)
+        want = [np.linalg.norm(P) for P in ref] + [np.linalg.norm(ref[-1] @ ref[-1])]
+        assert np.allclose(got[s, :Ns_ + 2], want, rtol=1e-12, atol=1e-300), (s, got[s], want)
+        assert np.all(np.isnan(got[s, Ns_ + 2:]))
+
+
 # ------------------------------------------------------------------ configs (scaled to oracle-sized runs)
 def test_E1_full_size():
     e, es = check_parity(S.make_E1())
