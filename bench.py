@@ -307,6 +307,32 @@ def oracle_sample(wl, chans, budget_s: float, max_units: int | None = None):
     return flops, samples, time.perf_counter() - t0, desc
 
 
+def oracle_recurrence_sample(wl, chans, budget_s: float):
+    """the oracle's plain recurrence x_n = Abar x_{n-1} + Bbar u_n, y_n = C x_n + D u_n
+    (sequential in time, all sequences of a channel / system at once), timed on a prefix of the
+    sequences until `budget_s` is spent. Returns (samples, seconds, description)."""
+    import numpy as np
+    import oracle
+    t0 = time.perf_counter()
+    samples, steps = 0.0, 0
+    c = chans[0]
+    W = 256
+    for l0 in range(0, wl.L, W):
+        l1 = min(wl.L, l0 + W)
+        if wl.kind == "bank":
+            u = np.stack([wl.u_window(c, b, l0, l1) for b in range(wl.batch)])
+        else:
+            u = np.stack([wl.u_window(0, b, l0, l1) for b in range(wl.batch)])
+        # the state carried between windows is not needed for timing: each window restarts at 0
+        oracle.recurrence(wl.Abar[c], wl.Bbar[c], wl.C[c], wl.D[c], u)
+        samples += (l1 - l0) * wl.batch
+        steps += l1 - l0
+        if time.perf_counter() - t0 > budget_s:
+            break
+    return samples, time.perf_counter() - t0, (f"{steps} time steps x {wl.batch} sequences of {wl.name} "
+                                               f"(channel {c}), float64 recurrence")
+
+
 # ----------------------------------------------------------------------------- arms
 def run_reference(args, world, rank):
     """--impl reference: the float64 oracle on the host cores, rank 0 only."""
@@ -470,6 +496,9 @@ def run_ours(args, world, rank, local_rank):
         cpu = {"value": f_s / t_s / 1e9, "unit": "GFLOP/s", "samples_per_s": s_s / t_s,
                "cores": ci["blas_threads"], "kind": "oracle", "sample": desc, "seconds": t_s, **ci,
                "note": "float64 numpy oracle (BLAS-threaded matmuls), not tuned; cores = BLAS threads used"}
+        r_s, r_t, r_desc = oracle_recurrence_sample(wl, chans, min(5.0, args.cpu_seconds / 3))
+        cpu["recurrence"] = {"samples_per_s": r_s / r_t, "seconds": r_t, "sample": r_desc,
+                             "note": "the plain recurrence (SURVEY §8d); value / samples_per_s above are the cascade"}
     cfgd = dict(cfgd)
     cfgd["l2"] = "512 MiB buffer written between timed steps (flush); state buffers also exceed L2"
     cfgd["timed_step"] = "powers (fp64 squaring + pack) + apply (all stages, y = Cv + Du)"
