@@ -30,10 +30,16 @@ __device__ __forceinline__ void st8(float* p, const uint32_t* v) {
                "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]) : "memory");
 }
 
+// position -> tile in the bank pass's residue-class order: sequences of 128 tiles, within one the
+// chains r, r + S, r + 2S, ... (S = 1: the natural order)
+__device__ __forceinline__ int chain_tile(int p, int S) {
+  const int seq = p / 128, q = p % 128, J = 128 / S;
+  return seq * 128 + (q / J) + (q % J) * S;
+}
 template <int NS, bool TMA_STORE>
 __global__ void __launch_bounds__(160, 1) stream_kernel(const __grid_constant__ CUtensorMap src,
                                                         const __grid_constant__ CUtensorMap dstm, float* dst,
-                                                        int ntiles) {
+                                                        int ntiles, int S) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   __shared__ uint64_t full[NS], slot_free[NS];
@@ -51,8 +57,8 @@ __global__ void __launch_bounds__(160, 1) stream_kernel(const __grid_constant__ 
       if (x >= NS) mbar_wait(&slot_free[s], (uint32_t)((x / NS - 1) & 1));
       if (lane == 0) {
         mbar_arrive_expect_tx(&full[s], SLOT);
-        tma_load2(smem + s * SLOT, &src, &full[s], 0, t * ROWS);
-        tma_load2(smem + s * SLOT + CHUNK, &src, &full[s], 32, t * ROWS);
+        tma_load2(smem + s * SLOT, &src, &full[s], 0, chain_tile(t, S) * ROWS);
+        tma_load2(smem + s * SLOT + CHUNK, &src, &full[s], 32, chain_tile(t, S) * ROWS);
       }
       __syncwarp();
     }
@@ -75,7 +81,7 @@ __global__ void __launch_bounds__(160, 1) stream_kernel(const __grid_constant__ 
       }
       if constexpr (!TMA_STORE) {
         mbar_arrive(&slot_free[s]);
-        float* orow = dst + ((int64_t)t * ROWS + row) * COLS;
+        float* orow = dst + ((int64_t)chain_tile(t, S) * ROWS + row) * COLS;
 #pragma unroll
         for (int e = 0; e < 8; ++e) st8(orow + 8 * e, v + 8 * e);
       } else {
@@ -92,8 +98,8 @@ __global__ void __launch_bounds__(160, 1) stream_kernel(const __grid_constant__ 
         fence_async_smem();
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (row == 0) {
-          tma_store2(&dstm, smem + s * SLOT, 0, t * ROWS);
-          tma_store2(&dstm, smem + s * SLOT + CHUNK, 32, t * ROWS);
+          tma_store2(&dstm, smem + s * SLOT, 0, chain_tile(t, S) * ROWS);
+          tma_store2(&dstm, smem + s * SLOT + CHUNK, 32, chain_tile(t, S) * ROWS);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
@@ -151,16 +157,16 @@ int main() {
   map2d(&ms, src, (int64_t)ntiles * ROWS);
   map2d(&md, dst, (int64_t)ntiles * ROWS);
   const double gb = 2.0 * n * 4 / 1e9;
-  auto run = [&](auto kern, int ns, const char* name) {
+  auto run = [&](auto kern, int ns, const char* name, int S) {
     const size_t smem = 1024 + (size_t)ns * SLOT;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const double ms_ = time_ms([&] { kern<<<148, 160, smem>>>(ms, md, dst, ntiles); });
-    printf("%-28s slots %d: %.3f ms  %.0f GB/s  (%s)\n", name, ns, ms_, gb / ms_ * 1e3, cudaGetErrorString(cudaGetLastError()));
+    const double ms_ = time_ms([&] { kern<<<148, 160, smem>>>(ms, md, dst, ntiles, S); });
+    printf("%-28s slots %d S %3d: %.3f ms  %.0f GB/s  (%s)\n", name, ns, S, ms_, gb / ms_ * 1e3, cudaGetErrorString(cudaGetLastError()));
   };
-  run(stream_kernel<4, false>, 4, "tma load + st.global.v8");
-  run(stream_kernel<6, false>, 6, "tma load + st.global.v8");
-  run(stream_kernel<4, true>, 4, "tma load + tma store");
-  run(stream_kernel<6, true>, 6, "tma load + tma store");
+  for (int S : {1, 4, 16, 64}) {      // residue-class chain order of the bank pass (S = shift in tiles)
+    run(stream_kernel<4, false>, 4, "tma load + st.global.v8", S);
+    run(stream_kernel<4, true>, 4, "tma load + tma store", S);
+  }
   const double mc = time_ms([&] { copy_kernel<<<148 * 8, 256>>>((const float4*)src, (float4*)dst, n / 4); });
   printf("%-28s        : %.3f ms  %.0f GB/s\n", "float4 copy", mc, gb / mc * 1e3);
   return 0;
