@@ -333,14 +333,16 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
 #pragma unroll
       for (int q = 0; q < kMaxSrc; ++q) if (q < a.n_src) nch_tile += a.K[q] / BK;
       for (Walk w(n_tiles, a.gt); w.valid(); w.next(), ++t_local) {
-        const TileCoord tc = decode(w.tile(), a, n_nblk, nt_eff);
+        // the issuing warp needs the tile's system only for resident weights (the decode costs
+        // integer divisions and a list load per tile on the MMA warp's critical loop)
+        const int tsys = WRES ? decode(w.tile(), a, n_nblk, nt_eff).sys : 0;
         const int acc = (int)(t_local & 1);
         TWM(4, mbar_wait_u(&tempty[acc], (uint32_t)((t_local >> 1) & 1) ^ 1));
-        if (WRES && tc.sys != cur_sys) {
+        if (WRES && tsys != cur_sys) {
           if (cur_sys >= 0) mma_commit_w(&wfree);   // all MMAs issued so far used the old weights
           TWM(5, mbar_wait(&w_full, wph));
           wph ^= 1;
-          cur_sys = tc.sys;
+          cur_sys = tsys;
         }
         tc_fence_after();
         const uint32_t d = tbase + acc * ACOLS, dc = d + BN;
