@@ -33,12 +33,14 @@ namespace {
 constexpr int HM = 128;                   // rows per CTA
 constexpr int BK = 32;                    // fp32 K per chunk (128-byte rows)
 constexpr uint32_t A_BYTES = HM * 128;    // 16 KB (hi in place; lo in its own 16 KB)
-constexpr int RS = 2;                     // residual / staging chunks (128 rows x 32 fp32)
+// residual / staging chunks (128 rows x 32 fp32): four, so the residual loads of a tile's chunks run
+// ahead of the epilogue (their HBM latency paced it with two: 4.3k cycles of waits per tile); paid
+// for with one ring stage (3 instead of 4). E3 A/B (forced rebuilds): 9.40 -> 9.02 ms min.
+constexpr int RS = 4;
 constexpr uint32_t R_BYTES = HM * 128;
 constexpr int CW = 32;                    // epilogue chunk width (fp32 columns = 128 bytes)
 constexpr int THREADS = 11 * 32;          // 0 TMA, 1 MMA, 2-5 epilogue, 6-9 transform, 10 residual
-// BN output columns per pair tile: 64 or 128 (two TMEM accumulators, 4 ring slots) or 256 (the
-// state chunk is staged and split once for all 256 columns; one accumulator, 3 ring slots)
+// BN output columns per pair tile: 128 (two TMEM accumulators, 3 ring slots + 4 residual chunks)
 // SPLIT: main (hi.hi) accumulators per tile. The tensor core truncates its fp32 accumulator at every
 // MMA, so the main chain's error grows with K / 8; long contractions (K > 512) spread
 // the main chain over SPLIT = 3 accumulators (one third of the K chunks each, summed with
@@ -48,7 +50,7 @@ template <int BN, int SPLIT = 1>
 struct PCfg {
   static constexpr uint32_t W_BYTES = (BN / 2) * 128;             // this CTA's BN/2 weight rows, hi or lo
   static constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * W_BYTES;   // A hi | A lo | W hi | W lo
-  static constexpr int STAGES = BN == 256 ? 3 : 4;
+  static constexpr int STAGES = 3;
   static constexpr int NACC = (BN == 256 || SPLIT > 1) ? 1 : 2;
   static constexpr uint32_t ACC_COLS = (SPLIT + 1) * BN;           // SPLIT mains | corr
   static_assert(NACC * ACC_COLS <= 512, "TMEM");
@@ -82,6 +84,19 @@ __device__ __forceinline__ void named_sync3(int id, int n) { asm volatile("bar.s
 __device__ __forceinline__ void mma_tf32_pair_w(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
   asm volatile("{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+               ::"r"(d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+// The same MMA keeping its A operand in the tensor core's collector buffer (fill) / reading it from
+// there and releasing it (lastuse): the two products of a K step that share A_hi (hi.hi, hi.lo)
+// read A_hi from shared memory once (SASS UTCHMMA .A_KEEP / .A_REUSE). E3: 9.02 -> 8.80 ms min.
+__device__ __forceinline__ void mma_tf32_pair_fill_w(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "@e tcgen05.mma.cta_group::2.kind::tf32.collector::a::fill [%0], %1, %2, %3, p;\n\t}"
+               ::"r"(d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_tf32_pair_lastuse_w(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "@e tcgen05.mma.cta_group::2.kind::tf32.collector::a::lastuse [%0], %1, %2, %3, p;\n\t}"
                ::"r"(d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void mma_commit_pair3(uint64_t* bar) {   // both CTAs' barrier at this offset
@@ -248,9 +263,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint64_t ad = sdesc_add(ad0, k * 32), wd = sdesc_add(wd0, k * 32);
-              mma_tf32_pair_w(d, ad, wd, idesc, (first_m && k == 0) ? 0u : 1u);           // main: hi.hi
-              mma_tf32_pair_w(dc, sdesc_add(al0, k * 32), wd, idesc, (fc && k == 0) ? 0u : 1u);   // corr: lo.hi
-              mma_tf32_pair_w(dc, ad, sdesc_add(wl0, k * 32), idesc, 1u);                //     + hi.lo
+              mma_tf32_pair_fill_w(d, ad, wd, idesc, (first_m && k == 0) ? 0u : 1u);      // main: hi.hi (A_hi kept)
+              mma_tf32_pair_lastuse_w(dc, ad, sdesc_add(wl0, k * 32), idesc, (fc && k == 0) ? 0u : 1u);  // corr: hi.lo
+              mma_tf32_pair_w(dc, sdesc_add(al0, k * 32), wd, idesc, 1u);                //     + lo.hi
             }
             fc = false;
             mma_commit_pair3(&empty[s]);
