@@ -37,8 +37,21 @@ def sources():
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
 
 
+FLAGS_STAMP = os.path.join(HERE, "build", "flags.txt")
+
+
+def extra_flags() -> str:
+    return os.environ.get("CASC_NVCC_FLAGS", "").strip()
+
+
 def needs_rebuild() -> bool:
     if not os.path.exists(LIB):
+        return True
+    # a build with other diagnostics flags (CASC_NVCC_FLAGS) is a different library
+    try:
+        if open(FLAGS_STAMP).read() != extra_flags():
+            return True
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
     deps = sources() + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "cascade.h")]
@@ -78,6 +91,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
     os.replace(tmp, LIB)
+    with open(FLAGS_STAMP, "w") as f:
+        f.write(extra_flags())
     return LIB
 
 
