@@ -130,6 +130,13 @@ __device__ __forceinline__ float tf32_rna(float x) {
 __device__ __forceinline__ float4 tf32_hi4(float4 v) {
   return make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
 }
+// The tf32 part the tensor core reads from an fp32 operand in shared memory: the top 19 bits
+// (truncation; checked on B200: a remainder computed against round-to-nearest would be off by an
+// ulp and fails the 1e-5 parity). With A_hi left as the raw fp32 chunk, lo = rna(v - trunc(v)).
+__device__ __forceinline__ float4 tf32_trunc4(float4 v) {
+  return make_float4(__uint_as_float(__float_as_uint(v.x) & 0xffffe000u), __uint_as_float(__float_as_uint(v.y) & 0xffffe000u),
+                     __uint_as_float(__float_as_uint(v.z) & 0xffffe000u), __uint_as_float(__float_as_uint(v.w) & 0xffffe000u));
+}
 __device__ __forceinline__ float4 tf32_lo4(float4 v, float4 h) {
   return make_float4(tf32_rna(v.x - h.x), tf32_rna(v.y - h.y), tf32_rna(v.z - h.z), tf32_rna(v.w - h.w));
 }

@@ -435,9 +435,8 @@ __global__ void __launch_bounds__(Cfg<BN, TF32, RSO, WCH>::THREADS, 1)
             float4* out = reinterpret_cast<float4*>(WRES ? sAlo + (j & (NAU - 1)) * C::A_BYTES : stAlo(s));
 #pragma unroll
             for (int e = t; e < (int)(C::A_BYTES / 16); e += 128) {
-              const float4 v = hi[e], h = tf32_hi4(v);
-              hi[e] = h;                                // hi in place (the MMA waits for lo_ready)
-              out[e] = tf32_lo4(v, h);
+              const float4 v = hi[e];                   // hi: the raw chunk (the MMA truncates it)
+              out[e] = tf32_lo4(v, tf32_trunc4(v));
             }
             fence_async_smem();
             mbar_arrive(&lo_ready[WRES ? (int)(j & (NAU - 1)) : s]);

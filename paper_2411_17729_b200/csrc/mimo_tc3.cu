@@ -9,7 +9,8 @@
 //
 // 3xTF32 as in mimo_tc.cu: hi.hi into the main accumulator, lo.hi + hi.lo into the correction
 // accumulator (separate truncation chains), summed with round-to-nearest in the epilogue. Four
-// transform warps per CTA split the landed A chunk into hi (in place) and lo.
+// transform warps per CTA write the lo part of the landed A chunk (lo = rna(v - trunc_tf32(v)); the
+// MMA reads the raw chunk as hi, truncated by the tensor core).
 //
 // Protocol: A lands on a CTA-local barrier (its transform waits for it); both CTAs' weight loads
 // and both CTAs' transforms signal barriers in the LEADER (the weight loads through the 2-SM TMA
@@ -289,9 +290,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           float4* lo = reinterpret_cast<float4*>(stAlo(s));
 #pragma unroll
           for (int e = t; e < (int)(A_BYTES / 16); e += 128) {   // the swizzle is the same for hi and lo
-            const float4 v = hi[e], h = tf32_hi4(v);
-            hi[e] = h;
-            lo[e] = tf32_lo4(v, h);
+            // hi stays the raw chunk (the MMA reads its tf32 truncation); only lo is written: one
+            // shared-memory store stream less per chunk (E3 8.80 -> 8.36 ms min, same accuracy)
+            const float4 v = hi[e];
+            lo[e] = tf32_lo4(v, tf32_trunc4(v));
           }
           fence_async_smem();                    // generic writes -> the MMA's async proxy
           if (is_leader) mbar_arrive(&lo_ready[s]);
