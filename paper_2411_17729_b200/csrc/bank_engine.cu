@@ -294,10 +294,11 @@ int engine_bank_pipelined(int n, int m, int64_t L, int batch, const int* N_host,
   std::vector<int> wc0(waves + 1, 0);
   for (int w = 0; w < waves; ++w) wc0[w + 1] = wc0[w] + wsz[w];
   // input chunks per wave (CASC_E2E_CHUNKS): the head runs per chunk as it lands (E2 e2e with the
-  // ramp: 1 chunk 4.45, 4 4.49, 8 4.77 ms -- smaller head launches fill the GPU less)
+  // ramp, after the bank pass's walk fix: 1 chunk 4.18, 2 4.09, 4 4.23 ms -- smaller head launches
+  // fill the GPU less)
   static const int chunks = [] {
     const char* e = getenv("CASC_E2E_CHUNKS");
-    return e ? std::max(1, atoi(e)) : 4;
+    return e ? std::max(1, atoi(e)) : 2;
   }();
   std::vector<std::vector<int>> bounds(waves);
   std::vector<std::vector<cudaEvent_t>> u_ev(waves);
