@@ -26,6 +26,9 @@ def test_roofline_binding_roof_and_peak_choice():
     r = bench.roofline(prof, "bf16", "E4", {"sm_mhz": 1000.0, "sm_max_mhz": 1965.0})
     assert r["bound"] == "tensor" and abs(r["frac"] - 1.0) < 1e-9 and r["executed"]["tensor_peak"] == "sustained"
     assert r["avg_launch_ms"] == 1.0
+    # the same rate against the burst / sustained / datasheet peaks
+    fo = r["frac_other_peaks"]
+    assert abs(fo["sustained"] - 1.0) < 1e-9 and fo["burst"] < 1.0 and abs(fo["datasheet"] - fl * 2 / 2e-3 / 1e12 / 2250.0) < 1e-9
 
 
 def test_e5_round_robin_by_order_balances_stages():
