@@ -574,20 +574,32 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
     const int64_t in_bytes = (int64_t)es * batch * L * p;
     const int chunks = chunks_env ? chunks_env : (int)std::min<int64_t>(8, std::max<int64_t>(1, ceil_div(in_bytes, (int64_t)64 << 20)));
     // chunk boundaries: when chunks would hold several sequences, ramp up from and down to one
-    // sequence (1, 2, 4, ..., 4, 2, 1): the exposed first input / last output copy is one sequence,
+    // sequence (1, 2, 3, ..., 3, 2, 1): the exposed first input / last output copy is one sequence,
     // and each chunk's input (the copy is ~2x faster than the compute per sequence on E3) lands
     // while the previous chunk computes
     std::vector<int> sizes;
     if (chunks < batch && batch >= 4) {
+      // arithmetic ramp 1, 2, 3, ... (E3 e2e: 1,2,3,4,3,2,1 9.72 ms vs the doubling 1,2,4,2,4,2,1 9.93)
       std::vector<int> up;
       int total = 0;
-      for (int M = 1; 2 * (total + M) <= batch; M *= 2) { up.push_back(M); total += M; }
+      for (int M = 1; 2 * (total + M) <= batch; ++M) { up.push_back(M); total += M; }
       sizes = up;
-      for (int rest = batch - 2 * total; rest > 0;) { const int t = std::min(up.back(), rest); sizes.push_back(t); rest -= t; }
+      for (int rest = batch - 2 * total; rest > 0;) { const int t = std::min(up.back() + 1, rest); sizes.push_back(t); rest -= t; }
       sizes.insert(sizes.end(), up.rbegin(), up.rend());
     } else {
       const int n0 = std::min(batch, chunks);
       for (int i = 0; i < n0; ++i) sizes.push_back((int)((int64_t)batch * (i + 1) / n0 - (int64_t)batch * i / n0));
+    }
+    if (const char* e = getenv("CASC_MIMO_SIZES")) {   // diagnostics A/B: explicit chunk sizes "1,3,4,..."
+      std::vector<int> v;
+      int tot = 0;
+      for (const char* q = e; *q;) {
+        const int x = atoi(q);
+        if (x > 0) { v.push_back(x); tot += x; }
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
+      }
+      if (tot == batch) sizes = v;
     }
     const int nc = (int)sizes.size();
     // derived weights once for all chunks (Ne is that of the full length L)
