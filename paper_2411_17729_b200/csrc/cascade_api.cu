@@ -616,7 +616,10 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
     // as kW time windows (rows [r0, r1) computed from inputs [r0 - Hu, r1), Hu = 2^(Ne+1) - 1, exact:
     // PAPER.md:137-141, pin T14): the first chunk's compute starts after its first window's input
     // landed, the last chunk's output leaves window by window.
-    constexpr int kW = 8;
+    static const int kW = [] {                        // windows per exposed chunk (CASC_MIMO_WINDOWS: diagnostics)
+      const char* e = getenv("CASC_MIMO_WINDOWS");
+      return e ? std::min(64, std::max(2, atoi(e))) : 8;
+    }();
     const int64_t Hu = Ne > 0 ? ((int64_t)2 << Ne) - 1 : 0;
     const int64_t Lw = ceil_div(L, kW);
     std::vector<int> b0(nc + 1, 0);
