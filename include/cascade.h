@@ -27,6 +27,10 @@
  *   - Errors: returned as casc_status; nothing is thrown across the ABI. Arguments are
  *     validated before any work is enqueued. There is NO CPU fallback: a shape or mode the
  *     GPU kernels do not cover returns CASC_ERR_UNSUPPORTED.
+ *   - Empty calls: casc_powers with n_sys = 0, and casc_apply / casc_apply_bank /
+ *     casc_run_host with n = 0, L = 0 or batch = 0 (the other sizes and the mode still
+ *     valid) return CASC_OK without touching any buffer (pointers may be NULL; the *_bytes
+ *     queries return 0). casc_apply_seqsharded requires L_loc >= 1 and batch >= 1.
  *   - Precision modes: CASC_FP32 stores signals and states in fp32 and computes with fp32
  *     accuracy (3xTF32 tensor-core products, fp32 accumulation; tolerance 1e-5 relative L2,
  *     BASELINE north_star); CASC_BF16 stores signals/states in bf16 and accumulates in fp32
@@ -49,7 +53,7 @@ extern "C" {
 
 typedef enum casc_status {
   CASC_OK = 0,
-  CASC_ERR_ARG = 1,          /* null pointer, m/p/q/L/batch < 1, N < 0, bad mode            */
+  CASC_ERR_ARG = 1,          /* null pointer, m/p/q < 1, L/batch < 0, N < 0, bad mode       */
   CASC_ERR_DIM = 2,          /* inconsistent dimensions (e.g. p > m, N > N_max)               */
   CASC_ERR_NONSQUARE = 3,    /* reserved: Abar is square by construction of the ABI          */
   CASC_ERR_UNSUPPORTED = 4,  /* valid request the sm_100a kernels do not cover                */

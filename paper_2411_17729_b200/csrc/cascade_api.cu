@@ -81,11 +81,12 @@ size_t apply_ws_bytes(int n, int m, int p, int q, int64_t L, int batch, int mode
 }
 
 int validate_common(int n, int m, int p, int q, int64_t L, int batch, int N_max, int mode) {
-  if (n < 1 || m < 1 || p < 1 || q < 1 || L < 1 || batch < 1 || N_max < 0) return CASC_ERR_ARG;
+  if (n < 0 || m < 1 || p < 1 || q < 1 || L < 0 || batch < 0 || N_max < 0) return CASC_ERR_ARG;
   if (mode != CASC_FP32 && mode != CASC_BF16) return CASC_ERR_ARG;
   if (p > m || q > m) return CASC_ERR_DIM;
   if (N_max > 62) return CASC_ERR_DIM;
   if (m > 4096) return CASC_ERR_UNSUPPORTED;
+  if (n == 0 || L == 0 || batch == 0) return kEmptyCall;   // nothing to compute, no buffer touched
   return CASC_OK;
 }
 
@@ -94,6 +95,7 @@ int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_
                  int mode, const void* pack, const double* Bbar, const double* C, const double* D,
                  const void* u, void* y, void* ws, size_t ws_bytes, cudaStream_t st) {
   int rc = validate_common(n, m, p, q, L, batch, N_max, mode);
+  if (rc == kEmptyCall) return CASC_OK;
   if (rc) return rc;
   if (!N_host || !pack || !Bbar || !C || !u || !y || !ws) return CASC_ERR_ARG;
   for (int s = 0; s < n; ++s)
@@ -323,10 +325,12 @@ static int coop_max_m() {                          // diagnostics A/B: CASC_POWE
 }
 int engine_powers(int n, int m, const int* N_host, int N_max, const double* Abar, int mode,
                   void* pack, cudaStream_t st) {
-  if (n < 1 || m < 1 || N_max < 0 || !N_host || !Abar || !pack) return CASC_ERR_ARG;
+  if (n < 0 || m < 1 || N_max < 0) return CASC_ERR_ARG;
   if (mode != CASC_FP32 && mode != CASC_BF16) return CASC_ERR_ARG;
   if (N_max > 62) return CASC_ERR_DIM;
   if (m > 4096) return CASC_ERR_UNSUPPORTED;
+  if (n == 0) return CASC_OK;                       // no systems: nothing to compute
+  if (!N_host || !Abar || !pack) return CASC_ERR_ARG;
   for (int s = 0; s < n; ++s)
     if (N_host[s] < 0 || N_host[s] > N_max) return CASC_ERR_DIM;
   PackLayout P = pack_layout(pack, n, m, N_max, mode);
@@ -508,6 +512,7 @@ int casc_run_host(int n_sys, int m, int p, int q, int64_t L, int batch, const in
                   const double* C_h, const double* D_h, const void* u_h, void* y_h,
                   void* dev_ws, size_t dev_ws_bytes, void* stream) {
   int rc = validate_common(n_sys, m, p, q, L, batch, N_max, mode);
+  if (rc == kEmptyCall) return CASC_OK;
   if (rc) return rc;
   if (!N_host || !Abar_h || !Bbar_h || !C_h || !u_h || !y_h || !dev_ws) return CASC_ERR_ARG;
   if (n_sys > 1 && (p != 1 || q != 1)) return CASC_ERR_UNSUPPORTED;

@@ -30,6 +30,9 @@ void timing_print();
 extern cudaEvent_t g_timing_t0;
 
 size_t apply_ws_bytes(int n, int m, int p, int q, int64_t L, int batch, int mode, int n_max);
+// validate_common's result for a valid call with n, L or batch = 0 (the entry points return CASC_OK
+// without touching any buffer)
+constexpr int kEmptyCall = -1;
 int validate_common(int n, int m, int p, int q, int64_t L, int batch, int N_max, int mode);
 int engine_apply(int n, int m, int p, int q, int64_t L, int batch, const int* N_host, int N_max,
                  int mode, const void* pack, const double* Bbar, const double* C, const double* D,

@@ -669,6 +669,7 @@ int casc_apply_seqsharded(void* comm, int m, int p, int q, int64_t L_loc, int ba
   auto* c = static_cast<Comm*>(comm);
   if (!c || !pack || !Bbar || !C || !u_loc || !y_loc || !ws || !comm_stream) return CASC_ERR_ARG;
   int rc = validate_common(1, m, p, q, L_loc, batch, N_max, mode);
+  if (rc == kEmptyCall) return CASC_ERR_ARG;        // every rank owns at least one row and sequence
   if (rc) return rc;
   if (N < 0 || N > N_max) return CASC_ERR_DIM;
   if (!mimo_tc_supported(m, p, q)) return CASC_ERR_UNSUPPORTED;

@@ -63,8 +63,8 @@ def test_argument_validation_without_gpu(lib):
     v = ctypes.c_void_p(8)
     # p > m
     assert lib.casc_apply(4, 5, 1, 10, 1, 3, 3, 0, v, v, v, None, v, v, v, 1 << 30, None, None) == 2
-    # L < 1
-    assert lib.casc_apply(4, 1, 1, 0, 1, 3, 3, 0, v, v, v, None, v, v, v, 1 << 30, None, None) == 1
+    # L < 0
+    assert lib.casc_apply(4, 1, 1, -1, 1, 3, 3, 0, v, v, v, None, v, v, v, 1 << 30, None, None) == 1
     # workspace too small
     assert lib.casc_apply(4, 1, 1, 10, 1, 3, 3, 0, v, v, v, None, v, v, v, 16, None, None) == 5
     # bank with N_c > N_max
@@ -72,6 +72,29 @@ def test_argument_validation_without_gpu(lib):
     assert lib.casc_apply_bank(2, 8, 10, 1, Nb, 3, 0, v, v, v, None, v, v, v, 1 << 30, None) == 2
     # run_host: bank requires SISO
     assert lib.casc_run_host(2, 8, 2, 1, 10, 1, Nb, 9, 0, v, v, v, None, v, v, v, 1 << 40, None) == 4
+
+
+def test_empty_calls_return_ok_without_touching_buffers(lib):
+    """include/cascade.h 'Empty calls': n, L or batch = 0 is a valid call with nothing to compute --
+    CASC_OK with every pointer NULL (no device work, so this runs on a CPU-only host), the size
+    queries answer 0, and a bad size or mode beside the empty one is still an error."""
+    N = _lib.int_array([3])
+    e = ctypes.c_int(-1)
+    for L, batch in ((0, 4), (100, 0), (0, 0)):
+        assert lib.casc_apply(64, 64, 64, L, batch, 3, 3, 0, None, None, None, None, None, None, None, 0,
+                              ctypes.byref(e), None) == 0
+        assert e.value == 0 or (L > 0 and e.value == 4)      # #{k <= 3 : 2^k < L}
+        assert lib.casc_apply_bank(2, 64, L, batch, _lib.int_array([3, 5]), 5, 0, None, None, None, None, None,
+                                   None, None, 0, None) == 0
+        assert lib.casc_run_host(1, 64, 4, 4, L, batch, N, 3, 1, None, None, None, None, None, None, None, 0,
+                                 None) == 0
+        assert lib.casc_apply_workspace_bytes(64, 64, 64, L, batch, 3, 0) == 0
+        assert lib.casc_run_host_bytes(1, 64, 4, 4, L, batch, 3, 0) == 0
+    assert lib.casc_apply_bank(0, 64, 100, 4, None, 5, 0, None, None, None, None, None, None, None, 0, None) == 0
+    assert lib.casc_powers(0, 64, None, 5, None, 0, None, None) == 0
+    assert lib.casc_apply(64, 64, 64, 0, 4, 3, 3, 9, None, None, None, None, None, None, None, 0, None, None) == 1
+    assert lib.casc_apply(64, 65, 64, 0, 4, 3, 3, 0, None, None, None, None, None, None, None, 0, None, None) == 2
+    assert lib.casc_apply(64, 64, 64, 0, -1, 3, 3, 0, None, None, None, None, None, None, None, 0, None, None) == 1
 
 
 def test_sharded_api_validation_without_gpu(lib):

@@ -310,3 +310,42 @@ def test_fp32_headroom_grows_with_K(m, p):
     wl = S.make_random_mimo(m, p, p, L=1024, batch=2, N=9, rho=0.98, mode="fp32", seed=m)
     e, es = check_parity(wl)
     print(f"fp32 m={m}: rel {e:.2e} state {es:.2e} (bound 1e-5)")
+
+
+# ------------------------------------------------------------------ empty inputs (include/cascade.h)
+@pytest.mark.parametrize("L,batch", [(0, 3), (200, 0)])
+def test_empty_signals_through_the_python_api(L, batch):
+    """An empty signal (L = 0 or batch = 0) is a valid call: y comes back empty, nothing launches,
+    and a non-empty call on the same pack afterwards is unaffected."""
+    import paper_2411_17729_b200 as pk
+    rng = np.random.default_rng(11)
+    m, p, q, N = 64, 64, 64, 5
+    Ab = torch.from_numpy(0.5 * rng.standard_normal((m, m)) / np.sqrt(m)).cuda()
+    Bb = torch.from_numpy(rng.standard_normal((m, p))).cuda()
+    C = torch.from_numpy(rng.standard_normal((q, m))).cuda()
+    pw = pk.powers(Ab, N, "fp32")
+    u = torch.empty((batch, L, p), dtype=torch.float32, device="cuda")
+    y, eff = pk.apply(pw, Bb, C, None, u, return_stages=True)
+    torch.cuda.synchronize()
+    assert tuple(y.shape) == (batch, L, q) and pk.last_launch_count() == 0
+    assert eff == sum(1 for k in range(N + 1) if (1 << k) < L)
+    # bank: 3 channels, empty signals
+    Abk = torch.from_numpy(np.stack([0.3 * np.eye(m)] * 3)).cuda()
+    pwb = pk.powers(Abk, [2, 3, 4], "fp32")
+    ub = torch.empty((3, batch, L), dtype=torch.float32, device="cuda")
+    yb = pk.apply_bank(pwb, torch.ones((3, m), dtype=torch.float64, device="cuda"),
+                       torch.ones((3, m), dtype=torch.float64, device="cuda"), None, ub)
+    torch.cuda.synchronize()
+    assert tuple(yb.shape) == (3, batch, L)
+    # host entry point
+    uh = torch.empty((1, batch, L, p), dtype=torch.float32)
+    yh = torch.empty((1, batch, L, q), dtype=torch.float32)
+    pk.run_host(Ab.cpu()[None], Bb.cpu()[None], C.cpu()[None], None, uh, yh, N, "fp32",
+                torch.empty(0, dtype=torch.uint8, device="cuda"))
+    # the same pack on a real signal still matches the oracle
+    u2 = torch.from_numpy(rng.standard_normal((2, 300, p)).astype(np.float32)).cuda()
+    y2 = pk.apply(pw, Bb, C, None, u2)
+    torch.cuda.synchronize()
+    P = oracle.powers(Ab.cpu().numpy(), N)
+    yref = oracle.cascade(P, Bb.cpu().numpy(), C.cpu().numpy(), np.zeros((q, p)), u2.cpu().numpy().astype(np.float64), N)
+    assert rel(y2.cpu().numpy().astype(np.float64), yref) <= TOL["fp32"]
