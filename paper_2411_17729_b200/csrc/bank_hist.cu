@@ -43,13 +43,6 @@ constexpr uint32_t CHUNK = HBM * 128;        // one 32-column chunk of a tile: 1
 constexpr uint32_t SLOT = 2 * CHUNK;         // one tile (64 fp32 columns): 32 KB
 constexpr uint32_t WCHUNK = HM * 128;        // one 32-column chunk of a weight (hi or lo): 8 KB
 constexpr int THREADS = 10 * 32;
-// The epilogue releases the accumulator once main + correction are summed (every loaded register
-// consumed -- in-order issue puts the arrive after those adds, checked in the SASS), before it waits
-// for and reads the residual: E2 3.267 -> 3.249 ms, E5 711 -> 708 ms (A/B on one box; 0 = release
-// after the residual add)
-#ifndef HIST_EARLY_RELEASE
-#define HIST_EARLY_RELEASE 1
-#endif
 #ifndef HIST_SWAP
 constexpr int PRODUCER_WARP = 0, MMA_WARP = 1;
 #else
@@ -390,14 +383,6 @@ __global__ void __launch_bounds__(THREADS, 1) bank_hist_kernel(const __grid_cons
 #pragma unroll
         for (int e = 0; e < 64; ++e) vm[e] = vc[e] = 0u;
       }
-#if HIST_EARLY_RELEASE
-      // main + correction first: these adds consume every loaded register, so the accumulator can
-      // be released before the residual is waited for and read (the same sums, in the same order)
-#pragma unroll
-      for (int e = 0; e < 64; ++e) vm[e] = __float_as_uint(__uint_as_float(vm[e]) + __uint_as_float(vc[e]));
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);                      // accumulator drained (every loaded value used)
-#endif
       mbar_wait(&full[sr], (uint32_t)((x / NSLOT) & 1));   // this tile (the residual) has landed
 #pragma unroll
       for (int kc = 0; kc < 2; ++kc) {
@@ -406,26 +391,17 @@ __global__ void __launch_bounds__(THREADS, 1) bank_hist_kernel(const __grid_cons
         for (int cc = 0; cc < 8; ++cc) {
           const float4 r = *reinterpret_cast<const float4*>(rrow + (cc ^ (row & 7)) * 16);
           const int col = kc * 32 + cc * 4;
-#if HIST_EARLY_RELEASE
-          vm[col] = __float_as_uint(r.x + __uint_as_float(vm[col]));
-          vm[col + 1] = __float_as_uint(r.y + __uint_as_float(vm[col + 1]));
-          vm[col + 2] = __float_as_uint(r.z + __uint_as_float(vm[col + 2]));
-          vm[col + 3] = __float_as_uint(r.w + __uint_as_float(vm[col + 3]));
-#else
           vm[col] = __float_as_uint(r.x + (__uint_as_float(vm[col]) + __uint_as_float(vc[col])));
           vm[col + 1] = __float_as_uint(r.y + (__uint_as_float(vm[col + 1]) + __uint_as_float(vc[col + 1])));
           vm[col + 2] = __float_as_uint(r.z + (__uint_as_float(vm[col + 2]) + __uint_as_float(vc[col + 2])));
           vm[col + 3] = __float_as_uint(r.w + (__uint_as_float(vm[col + 3]) + __uint_as_float(vc[col + 3])));
-#endif
         }
       }
-#if !HIST_EARLY_RELEASE
       // Release the accumulator only now: tcgen05.wait::ld orders nothing but later uses of the
       // loaded registers (SASS has no wait instruction; the register scoreboard does it), so an
       // arrive placed before the first use let the next tile's MMA overwrite TMEM under a lagging warp.
       tc_fence_before();
       mbar_arrive(&tempty[acc]);                      // accumulator drained (every loaded value used)
-#endif
       mbar_arrive(&slot_free[sr]);                    // residual rows read
       const int64_t l = (int64_t)it.t * HBM + row;
       if (to_parts) {                                 // the 2^(depth+1) output parts of this row

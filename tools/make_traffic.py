@@ -4,7 +4,8 @@ dram__bytes_read.sum + dram__bytes_write.sum per launch of each config's dominan
   E3: the captured stage launch of mimo_gemm_pair_tf32_kernel (<tag>_e3_pair_tf32_raw.csv)
   E4: mean over the stage launches of mimo_gemm_pair_kernel in the launch list (per step the
       first pair launch is the Krylov head and the last the folded output step: excluded)
-usage: python tools/make_traffic.py <tag>   (files under profiles/)"""
+usage: python tools/make_traffic.py <tag> [E2=<tag2>]   (files under profiles/; E2=<tag2> takes the
+  E2 launch list from another capture of the same round)"""
 import collections
 import csv
 import json
@@ -36,9 +37,11 @@ def dram(d):
 
 def main():
     tag = sys.argv[1]
+    over = dict(a.split("=", 1) for a in sys.argv[2:])
+    t2 = over.get("E2", tag)
     P = os.path.join(ROOT, "profiles")
     res = {}
-    e2 = [dram(d) for k, d in launches(os.path.join(P, f"{tag}_e2_launches.csv")) if "bank_hist_kernel" in k]
+    e2 = [dram(d) for k, d in launches(os.path.join(P, f"{t2}_e2_launches.csv")) if "bank_hist_kernel" in k]
     res["E2"] = {"bank_stage": sum(e2) / len(e2)}
     raw = list(csv.reader(open(os.path.join(P, f"{tag}_e3_pair_tf32_raw.csv"))))
     h, u, v = raw[0], raw[1], raw[2]
@@ -54,8 +57,8 @@ def main():
             group = []
     res["E4"] = {"mimo_tc_stage": sum(stage) / len(stage)}
     res["_note"] = (f"dram__bytes_read.sum + dram__bytes_write.sum per launch of the class's dominant kernel "
-                    f"({tag}; tools/make_traffic.py): E2 = mean over {len(e2)} bank_hist_kernel launches "
-                    f"({tag}_e2_launches.csv); E3 = the captured mimo_gemm_pair_tf32_kernel stage launch "
+                    f"({tag}{'' if t2 == tag else ', E2 ' + t2}; tools/make_traffic.py): E2 = mean over {len(e2)} bank_hist_kernel launches "
+                    f"({t2}_e2_launches.csv); E3 = the captured mimo_gemm_pair_tf32_kernel stage launch "
                     f"({tag}_e3_pair_tf32_raw.csv); E4 = mean over {len(stage)} stage launches of "
                     f"mimo_gemm_pair_kernel ({tag}_e4_launches.csv; Krylov head and folded output step "
                     "excluded). ncu launches are cold-cache and serialised. Used as roofline.traffic by bench.py.")
