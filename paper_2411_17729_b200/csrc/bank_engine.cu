@@ -538,13 +538,14 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     if (chunked) CASC_TRY(cudaStreamWaitEvent(st, bs->u_events[ci], 0));
     const int hc0 = chunked ? bs->bounds[ci] : 0, hcn = chunked ? bs->bounds[ci + 1] - hc0 : n;
     BankHeadArg a{};
-    a.u = static_cast<const float*>(u); a.krT = w.krT; a.V = static_cast<float*>(w.Va);
+    a.u = static_cast<const float*>(u); a.krT = w.krT; a.kr64 = w.Kr64; a.V = static_cast<float*>(w.Va);
     a.sys_list = chunked ? diota + hc0 : dorder; a.n_list = hcn; a.L = L; a.batch = batch;
     if (use_ab) a.op = op;
     ProfScope ps(st, K_BANK_HEAD, (double)hcn * batch * L * (1 + m) * 4.0,
                  (double)hcn * batch * L * 2.0 * m * 128);
-    // executed: m = 64 issues three tf32 products per K step (hi.[hi|lo] at N = 128, lo.hi)
-    if (m == 64) ps.exec((double)hcn * batch * L * (1 + m) * 4.0, 3.0 * hcn * batch * L * 2.0 * m * 128, PIPE_TF32);
+    // executed: m = 64 issues three fp16 products per K step (hi.[hi|lo] at N = 128, lo.hi) on the
+    // kind::f16 pipe (the bf16 rate)
+    if (m == 64) ps.exec((double)hcn * batch * L * (1 + m) * 4.0, 3.0 * hcn * batch * L * 2.0 * m * 128, PIPE_BF16);
     // m = 64: warp-specialized TMA-store head (bank_head_ws.cu); m = 16, 32: CUDA-core head.
     // Measured alternatives not kept: a TMEM-operand variant (1.67 vs 1.30 ms on E2),
     // the head on CTA pairs (same 1.16 ms: the head is bound by the tensor pipe, 69% active)

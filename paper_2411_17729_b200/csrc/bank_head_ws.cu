@@ -2,19 +2,25 @@
 //
 //   v^(Kc)_l = sum_{j < 128} (Abar^j Bbar) u_{l-j}     (the expanded product of PAPER.md:126)
 //
-// per 128-step tile one K = 128 GEMM (3xTF32: hi.hi + lo.hi + hi.lo) whose A operand, the
-// Toeplitz matrix u_{l-j}, is a 4 KB shared-memory buffer Z read with LBO = 64 B (row r, K chunk
-// c' = Z-row r + 4c'). The Krylov weights are stored hi and lo stacked along N ([K chunk][hi 64 |
-// lo 64 rows]), so Z_hi x [B_hi | B_lo] is one N = 128 MMA writing hi.hi to the main and hi.lo to
-// the correction accumulator, and Z_lo x B_hi (N = 64) adds to the correction: the MMAs read 14 KB
-// of shared memory per K step instead of 18 KB (shared-memory bandwidth bounds this kernel).
+// per 128-step tile one K = 128 GEMM on the fp16 tensor path (kind::f16, fp32 accumulate) with the
+// operands split in two fp16 parts, x = hi + lo (hi = rn(x), lo = rn(x - hi): 22 significant bits,
+// as the 3xTF32 split; R33): hi.hi + lo.hi + hi.lo at twice the tf32 MMA rate. fp16's
+// range is handled by exact power-of-two scales: the Krylov weights per state column n
+// (max_j |W_jn| scaled into [2^14, 2^15)), the Toeplitz tile per tile (its u window likewise); the
+// epilogue multiplies the fp32 accumulators back by the inverse powers of two. The A operand, the
+// Toeplitz matrix u_{l-j}, is a 4 KB shared-memory buffer Z (16-B rows of 8 fp16) read with
+// LBO = 128 B (row r, K chunk c' = Z-row r + 8c'). The weights are stored hi and lo stacked along
+// N ([K chunk][hi 64 | lo 64 rows]), so Z_hi x [B_hi | B_lo] is one N = 128 MMA writing hi.hi to the
+// main and hi.lo to the correction accumulator, and Z_lo x B_hi (N = 64) adds to the correction.
 // Roles (192 threads, two CTAs per SM):
-//   warp 0     builds Z for the next tiles into a 2-slot ring (u staged through shared memory)
-//   warp 1     issues the 32 MMAs of a tile into one of two TMEM accumulators (main | corr)
+//   warp 0     builds Z (and the tile's scale) for the next tiles into a 2-slot ring (u staged
+//              through shared memory)
+//   warp 1     issues the 16 MMAs of a tile into one of two TMEM accumulators (main | corr)
 //   warps 2-5  drain TMEM (lane = time row) into a SWIZZLE_128B staging tile and TMA-store it
 // Each CTA walks `tiles_per_cta` consecutive tiles of one sequence, so the Krylov weights
-// (64 KB of hi/lo) are loaded once per CTA.
+// (32 KB of fp16 hi/lo, split from the float64 weights in the prologue) are built once per CTA.
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -39,15 +45,17 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 template <int MS>
 __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_constant__ CUtensorMap vmap, BankHeadArg a) {
   static_assert(MS == 64, "TMA-store epilogue written for m = 64");
-  constexpr int BCH = KL / 4;
+  constexpr int BCH = KL / 8;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // keeps the shared state space (STS/LDS, not generic ST/LD)
   float* Stg = reinterpret_cast<float*>(smem);                 // [128 rows][32] SW128 half tile, 16 KB
-  float* Bc = Stg + TM * 32;                                   // [BCH][hi MS | lo MS][4]
-  float* Zb = Bc + 2 * KL * MS;                                // [2 slots][hi|lo][ZR][4]
-  float* Us = Zb + 2 * 2 * ZR * 4;                             // [2 slots][264] u window
-  __shared__ uint64_t z_full[2], z_empty[2], tfull[2], tempty[2];
+  __half* Bc = reinterpret_cast<__half*>(Stg + TM * 32);       // [BCH][hi MS | lo MS][8] fp16, 32 KB
+  __half* Zb = Bc + 2 * KL * MS;                               // [2 slots][hi|lo][ZR][8] fp16
+  float* Us = reinterpret_cast<float*>(Zb + 2 * 2 * ZR * 8);   // [2 slots][264] u window
+  __shared__ uint64_t z_full[2], z_empty[2], tfull[2], tempty[2], sc_full[4];
   __shared__ uint32_t tmem_base;
+  __shared__ float col_inv[MS], tile_inv[4];                   // inverse scales (powers of two)
+  __shared__ int col_e[MS];
 
   const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid / 32, 0), lane = tid % 32;
   const int li = blockIdx.y / a.batch, b = blockIdx.y % a.batch;
@@ -55,12 +63,34 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
   const int seq = c * a.batch + b;
   const float* u = a.u + (int64_t)seq * a.L;
 
-  const float* kh = a.krT + (int64_t)c * 2 * MS * KL;
-  const float* kl = kh + MS * KL;
-  for (int e = tid; e < MS * BCH; e += 192) {
-    const int ch = e / MS, n = e % MS;
-    *reinterpret_cast<float4*>(Bc + (ch * 2 * MS + n) * 4) = __ldg(reinterpret_cast<const float4*>(kh + n * KL + ch * 4));
-    *reinterpret_cast<float4*>(Bc + (ch * 2 * MS + MS + n) * 4) = __ldg(reinterpret_cast<const float4*>(kl + n * KL + ch * 4));
+  // Krylov weights W[n][j] (float64, lag j) -> per-column exponent e_n (max_j |W_nj| in
+  // [2^e_n, 2^(e_n + 1))), then fp16 hi / lo of W * 2^(14 - e_n) at k' = 127 - j
+  const double* kr = a.kr64 + (int64_t)c * MS * KL;
+  for (int n = warp; n < MS; n += 6) {
+    double mx = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) mx = fmax(mx, fabs(__ldg(kr + n * KL + lane + 32 * q)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) {
+      const int e = mx > 0.0 ? max(-110, min(110, ilogb(mx))) : 0;
+      col_e[n] = e;
+      col_inv[n] = ldexpf(1.f, e - 14);
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < MS * BCH; e += 192) {                 // (column n, K chunk ch of 8)
+    const int n = e % MS, ch = e / MS;
+    const int sh = 14 - col_e[n];
+    __align__(16) __half h[8], l[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double x = ldexp(__ldg(kr + n * KL + (KL - 1 - (8 * ch + q))), sh);
+      h[q] = __double2half(x);
+      l[q] = __double2half(x - (double)__half2float(h[q]));
+    }
+    *reinterpret_cast<uint4*>(Bc + (ch * 2 * MS + n) * 8) = *reinterpret_cast<const uint4*>(h);
+    *reinterpret_cast<uint4*>(Bc + (ch * 2 * MS + MS + n) * 8) = *reinterpret_cast<const uint4*>(l);
   }
   fence_async_smem();
   if (tid == 0) {
@@ -70,6 +100,7 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 128);
     }
+    for (int s = 0; s < 4; ++s) mbar_init(&sc_full[s], 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<4 * MS>(&tmem_base);         // 2 slots x (main | corr)
@@ -111,18 +142,35 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
       const int slot = i & 1;
       if (i >= 2) mbar_wait(&z_empty[slot], (uint32_t)(((i - 2) >> 1) & 1));
       float* us = Us + slot * 264;
-      float* zh = Zb + slot * 2 * ZR * 4;
-      float* zl = zh + ZR * 4;
+      __half* zh = Zb + slot * 2 * ZR * 8;
+      __half* zl = zh + ZR * 8;
+      // the tile's scale: max |u| over the window the MMAs read (Z-rows 0..247 -> W_i[0 .. 255))
+      uint32_t mb = 0;
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {               // Z-row w = (u[t0-127+w+q], q = 0..3)
+      for (int r = 0; r < 8; ++r)
+        if (lane + 32 * r < 255) mb = max(mb, __float_as_uint(fabsf(us[lane + 32 * r])));
+      mb = __reduce_max_sync(0xffffffffu, mb);
+      const float mx = __uint_as_float(mb);
+      const int et = mx > 0.f ? max(-110, min(110, ilogbf(mx))) : 0;
+      const float sc = ldexpf(1.f, 14 - et);
+      if (lane == 0) tile_inv[i & 3] = ldexpf(1.f, et - 14);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {               // Z-row w = (u[t0-127+w+q] * 2^(14 - et), q = 0..7)
         const int w = lane + 32 * r;
-        const float4 z = make_float4(us[w], us[w + 1], us[w + 2], us[w + 3]);
-        const float4 h = tf32_hi4(z);
-        *reinterpret_cast<float4*>(zh + w * 4) = h;
-        *reinterpret_cast<float4*>(zl + w * 4) = tf32_lo4(z, h);
+        __align__(16) __half2 h[4], l[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float x0 = us[w + 2 * q] * sc, x1 = us[w + 2 * q + 1] * sc;
+          h[q] = __floats2half2_rn(x0, x1);
+          const float2 hf = __half22float2(h[q]);
+          l[q] = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+        }
+        *reinterpret_cast<uint4*>(zh + w * 8) = *reinterpret_cast<const uint4*>(h);
+        *reinterpret_cast<uint4*>(zl + w * 8) = *reinterpret_cast<const uint4*>(l);
       }
       fence_async_smem();
       mbar_arrive(&z_full[slot]);
+      if (lane == 0) mbar_arrive(&sc_full[i & 3]);   // the epilogue's inverse scale of tile i
       if (i + 1 < nt) {                           // W_{i+1} into the other slot
         float* un = Us + (slot ^ 1) * 264;
 #pragma unroll
@@ -137,22 +185,22 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
     {                                             // whole warp: operands stay in uniform registers
-      const uint32_t idesc = make_idesc(FMT_TF32, TM, MS), idesc2 = make_idesc(FMT_TF32, TM, 2 * MS);
+      const uint32_t idesc = make_idesc(FMT_F16, TM, MS), idesc2 = make_idesc(FMT_F16, TM, 2 * MS);
       const uint32_t bc = smem_u32(Bc);
       for (int i = 0; i < nt; ++i) {
         const int slot = i & 1;
         mbar_wait_u(&z_full[slot], (uint32_t)((i >> 1) & 1));
         mbar_wait_u(&tempty[slot], (uint32_t)(((i >> 1) & 1) ^ 1));
         tc_fence_after();
-        const uint32_t zh = smem_u32(Zb + slot * 2 * ZR * 4), zl = zh + ZR * 16;
+        const uint32_t zh = smem_u32(Zb + slot * 2 * ZR * 8), zl = zh + ZR * 16;
         const uint32_t acc = tbase + slot * 2 * MS;
 #pragma unroll 4
-        for (int ks = 0; ks < KL / 8; ++ks) {
-          const uint64_t azh = make_sdesc(zh + ks * 128, 64, 128, LAYOUT_NONE);
-          const uint64_t azl = make_sdesc(zl + ks * 128, 64, 128, LAYOUT_NONE);
+        for (int ks = 0; ks < KL / 16; ++ks) {     // K = 16 per MMA: two 8-element chunks
+          const uint64_t azh = make_sdesc(zh + ks * 256, 128, 128, LAYOUT_NONE);
+          const uint64_t azl = make_sdesc(zl + ks * 256, 128, 128, LAYOUT_NONE);
           const uint64_t bd = make_sdesc(bc + ks * 2 * 2 * MS * 16, 2 * MS * 16, 128, LAYOUT_NONE);
-          mma_tf32_w(acc, azh, bd, idesc2, ks > 0);          // [hi.hi | hi.lo]
-          mma_tf32_w(acc + MS, azl, bd, idesc, 1);          // corr += lo.hi
+          mma_f16_w(acc, azh, bd, idesc2, ks > 0);           // [hi.hi | hi.lo]
+          mma_f16_w(acc + MS, azl, bd, idesc, 1);           // corr += lo.hi
         }
         mma_commit_w(&z_empty[slot]);
         mma_commit_w(&tfull[slot]);
@@ -173,7 +221,9 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
     for (int i = 0; i < nt; ++i) {
       const int slot = i & 1;
       mbar_wait_u(&tfull[slot], (uint32_t)((i >> 1) & 1));
+      mbar_wait_u(&sc_full[i & 3], (uint32_t)((i >> 2) & 1));
       tc_fence_after();
+      const float ti = tile_inv[i & 3];
       float v[MS], vc[MS];
       const uint32_t tacc = tbase + ((uint32_t)(q * 32) << 16) + slot * 2 * MS;
 #pragma unroll
@@ -181,7 +231,7 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
 #pragma unroll
       for (int c0 = 0; c0 < MS; c0 += 16) tmem_ld16(tacc + MS + c0, vc + c0);
 #pragma unroll
-      for (int n = 0; n < MS; ++n) v[n] += vc[n];             // main + corr (round to nearest)
+      for (int n = 0; n < MS; ++n) v[n] = (v[n] + vc[n]) * col_inv[n] * ti;   // main + corr, unscaled (exact)
       tc_fence_before();
       mbar_arrive(&tempty[slot]);
       if (to_parts) {                             // the 2^(depth+1) output parts instead of v
@@ -228,7 +278,7 @@ int launch_bank_head_ws(int m, const BankHeadArg& a, int64_t n_seq_total, cudaSt
   if (a.n_list * (int64_t)a.batch > 65535) return CASC_ERR_UNSUPPORTED;
   CUtensorMap vmap;
   if (!map3d(&vmap, a.V, true, 64, a.L, n_seq_total, TM)) return CASC_ERR_CUDA;
-  const size_t smem = 1024 + (size_t)(TM * 32 + 2 * KL * 64 + 2 * 2 * ZR * 4 + 2 * 264) * sizeof(float);
+  const size_t smem = 1024 + (size_t)(TM * 32 + 2 * 264) * sizeof(float) + (size_t)(2 * KL * 64 + 2 * 2 * ZR * 8) * 2;
   if (cudaFuncSetAttribute(bank_head_ws_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return CASC_ERR_CUDA;

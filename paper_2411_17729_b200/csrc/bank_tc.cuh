@@ -6,7 +6,8 @@ namespace casc {
 
 struct BankHeadArg {
   const float* u;          // [n_ch][batch][L]
-  const float* krT;        // [n_ch][2][MS][128]  hi | lo of Kr^T (k' = 127 - lag)
+  const float* krT;        // [n_ch][2][MS][128]  hi | lo of Kr^T (k' = 127 - lag; CUDA-core head)
+  const double* kr64;      // [n_ch][MS][128]     Kr in float64 (lag j; the m = 64 fp16 head splits it)
   float* V;                // [n_ch][batch][L][MS]
   const int* sys_list; int n_list;
   int64_t L; int batch; int tiles_per_cta;
