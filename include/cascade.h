@@ -32,7 +32,9 @@
  *     valid) return CASC_OK without touching any buffer (pointers may be NULL; the *_bytes
  *     queries return 0). casc_apply_seqsharded requires L_loc >= 1 and batch >= 1.
  *   - Precision modes: CASC_FP32 stores signals and states in fp32 and computes with fp32
- *     accuracy (3xTF32 tensor-core products, fp32 accumulation; tolerance 1e-5 relative L2,
+ *     accuracy (two-part operand splits with 22 significant bits: 3xTF32 tensor-core products,
+ *     or, in the m = 64 bank head, the same three products of fp16 parts under exact
+ *     power-of-two scales (R33); fp32 accumulation; tolerance 1e-5 relative L2,
  *     BASELINE north_star); CASC_BF16 stores signals/states in bf16 and accumulates in fp32
  *     (tolerance 2e-2). Model parameters (Abar, Bbar, C, D) are always passed in float64 and
  *     rounded once, inside the library, to the format the kernels consume.
@@ -63,7 +65,7 @@ typedef enum casc_status {
 } casc_status;
 
 typedef enum casc_mode {
-  CASC_FP32 = 0,             /* fp32 storage, fp32-accurate math (3xTF32 tensor cores)        */
+  CASC_FP32 = 0,             /* fp32 storage, fp32-accurate math (split-operand tensor cores) */
   CASC_BF16 = 1              /* bf16 storage, fp32 accumulation                               */
 } casc_mode;
 
@@ -254,7 +256,8 @@ const char* casc_profile_class_name(int cls);
 int casc_profile_read(int cls, int* launches, double* ms, double* bytes, double* flops);
 /* The EXECUTED work of the same records (summed): the HBM bytes the schedule run moves and the
  * math-pipe flops it issues (3xTF32 counts three tf32 products; skipped zero blocks are not
- * counted); pipe: 0 none, 1 tf32, 2 bf16, 3 fp64, 4 fp32 (CUDA cores) -- the peak to judge them by. */
+ * counted); pipe: 0 none, 1 tf32, 2 bf16 (kind::f16: bf16 or fp16 operands, the same rate),
+ * 3 fp64, 4 fp32 (CUDA cores) -- the peak to judge them by. */
 int casc_profile_read_exec(int cls, double* exec_bytes, double* exec_flops, int* pipe);
 
 /* ----------------------------------------------------------------------------------------
