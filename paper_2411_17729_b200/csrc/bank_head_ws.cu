@@ -55,7 +55,6 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
   __shared__ uint64_t z_full[2], z_empty[2], tfull[2], tempty[2], sc_full[4];
   __shared__ uint32_t tmem_base;
   __shared__ float col_inv[MS], tile_inv[4];                   // inverse scales (powers of two)
-  __shared__ int col_e[MS];
 
   const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid / 32, 0), lane = tid % 32;
   const int li = blockIdx.y / a.batch, b = blockIdx.y % a.batch;
@@ -63,34 +62,28 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
   const int seq = c * a.batch + b;
   const float* u = a.u + (int64_t)seq * a.L;
 
-  // Krylov weights W[n][j] (float64, lag j) -> per-column exponent e_n (max_j |W_nj| in
-  // [2^e_n, 2^(e_n + 1))), then fp16 hi / lo of W * 2^(14 - e_n) at k' = 127 - j
+  // Krylov weights W[n][j] (float64, lag j; one warp per column n, coalesced) -> exponent e_n with
+  // max_j |W_nj| in [2^e_n, 2^(e_n + 1)), then fp16 hi / lo of W * 2^(14 - e_n) at k' = 127 - j
   const double* kr = a.kr64 + (int64_t)c * MS * KL;
   for (int n = warp; n < MS; n += 6) {
-    double mx = 0.0;
+    double x[4], mx = 0.0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) mx = fmax(mx, fabs(__ldg(kr + n * KL + lane + 32 * q)));
+    for (int q = 0; q < 4; ++q) {
+      x[q] = __ldg(kr + n * KL + lane + 32 * q);
+      mx = fmax(mx, fabs(x[q]));
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) {
-      const int e = mx > 0.0 ? max(-110, min(110, ilogb(mx))) : 0;
-      col_e[n] = e;
-      col_inv[n] = ldexpf(1.f, e - 14);
-    }
-  }
-  __syncthreads();
-  for (int e = tid; e < MS * BCH; e += 192) {                 // (column n, K chunk ch of 8)
-    const int n = e % MS, ch = e / MS;
-    const int sh = 14 - col_e[n];
-    __align__(16) __half h[8], l[8];
+    const int e = mx > 0.0 ? max(-110, min(110, ilogb(mx))) : 0;
+    if (lane == 0) col_inv[n] = ldexpf(1.f, e - 14);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const double x = ldexp(__ldg(kr + n * KL + (KL - 1 - (8 * ch + q))), sh);
-      h[q] = __double2half(x);
-      l[q] = __double2half(x - (double)__half2float(h[q]));
+    for (int q = 0; q < 4; ++q) {
+      const int kp = KL - 1 - (lane + 32 * q), ch = kp / 8, o = kp % 8;
+      const double xs = ldexp(x[q], 14 - e);
+      const __half h = __double2half(xs);
+      Bc[(ch * 2 * MS + n) * 8 + o] = h;
+      Bc[(ch * 2 * MS + MS + n) * 8 + o] = __double2half(xs - (double)__half2float(h));
     }
-    *reinterpret_cast<uint4*>(Bc + (ch * 2 * MS + n) * 8) = *reinterpret_cast<const uint4*>(h);
-    *reinterpret_cast<uint4*>(Bc + (ch * 2 * MS + MS + n) * 8) = *reinterpret_cast<const uint4*>(l);
   }
   fence_async_smem();
   if (tid == 0) {
