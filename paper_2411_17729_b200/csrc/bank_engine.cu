@@ -81,6 +81,8 @@ struct BankWs {
   int* meta;      // Neff | Kc | parity | order | iota   (kMetaInts n ints)
   double* Kr64;   // [n][m][128]
   float* krT;     // [n][2][m][128]
+  void* kr16;     // m = 64: [n][16][2m][8] fp16 head weights (R33)
+  float* kinv;    // m = 64: [n][m] their inverse column scales
   double* w64;    // [n][m]
   float *w32, *c32, *d32;
   float* pvec;   // [n][kMaxParts][m] output-part row vectors (R24-R26)
@@ -98,6 +100,8 @@ static BankWs carve_bank(void* ws, int n, int m, int64_t L, int batch, int qslot
   w.meta = c.take<int>((size_t)kMetaInts * n);
   w.Kr64 = c.take<double>((size_t)n * m * 128);
   w.krT = c.take<float>((size_t)n * 2 * m * 128);
+  w.kr16 = c.take<uint16_t>(m == 64 ? (size_t)n * 2 * m * 128 : 0);
+  w.kinv = c.take<float>(m == 64 ? (size_t)n * m : 0);
   w.w64 = c.take<double>((size_t)n * m);
   w.w32 = c.take<float>((size_t)n * m);
   w.c32 = c.take<float>((size_t)n * m);
@@ -473,6 +477,7 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     if ((rc = launch_bank_derived(P.p64, N_max + 1, Bbar, C, D, dNeff, dKc, w.Kr64, w.krT, w.w64, w.w32, w.c32,
                                   w.d32, use_ab ? w.pvec : nullptr, w.tri, fold, n, m, st)))
       return rc;
+    if (m == 64 && (rc = launch_bank_head_weights(w.Kr64, w.kr16, w.kinv, n, st))) return rc;
     for (int j = 0; j < qslots; ++j) {          // Q_k = P_{k+1} P_k for pass j (k = 7 + 2j)
       const int k = kHeadK + 2 * j;
       if (count_lp_ge(k + 2) == 0) continue;
@@ -538,7 +543,7 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     if (chunked) CASC_TRY(cudaStreamWaitEvent(st, bs->u_events[ci], 0));
     const int hc0 = chunked ? bs->bounds[ci] : 0, hcn = chunked ? bs->bounds[ci + 1] - hc0 : n;
     BankHeadArg a{};
-    a.u = static_cast<const float*>(u); a.krT = w.krT; a.kr64 = w.Kr64; a.V = static_cast<float*>(w.Va);
+    a.u = static_cast<const float*>(u); a.krT = w.krT; a.kr16 = static_cast<const __half*>(w.kr16); a.kinv = w.kinv; a.V = static_cast<float*>(w.Va);
     a.sys_list = chunked ? diota + hc0 : dorder; a.n_list = hcn; a.L = L; a.batch = batch;
     if (use_ab) a.op = op;
     ProfScope ps(st, K_BANK_HEAD, (double)hcn * batch * L * (1 + m) * 4.0,

@@ -40,6 +40,10 @@ __device__ __forceinline__ void tma_store_3d_h(const CUtensorMap* map, const voi
 __device__ __forceinline__ void bulk_commit_h() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
 }  // namespace
 
 template <int MS>
@@ -52,7 +56,7 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
   __half* Bc = reinterpret_cast<__half*>(Stg + TM * 32);       // [BCH][hi MS | lo MS][8] fp16, 32 KB
   __half* Zb = Bc + 2 * KL * MS;                               // [2 slots][hi|lo][ZR][8] fp16
   float* Us = reinterpret_cast<float*>(Zb + 2 * 2 * ZR * 8);   // [2 slots][264] u window
-  __shared__ uint64_t z_full[2], z_empty[2], tfull[2], tempty[2], sc_full[4];
+  __shared__ uint64_t z_full[2], z_empty[2], tfull[2], tempty[2], sc_full[4], w_full;
   __shared__ uint32_t tmem_base;
   __shared__ float col_inv[MS], tile_inv[4];                   // inverse scales (powers of two)
 
@@ -62,29 +66,15 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
   const int seq = c * a.batch + b;
   const float* u = a.u + (int64_t)seq * a.L;
 
-  // Krylov weights W[n][j] (float64, lag j; one warp per column n, coalesced) -> exponent e_n with
-  // max_j |W_nj| in [2^e_n, 2^(e_n + 1)), then fp16 hi / lo of W * 2^(14 - e_n) at k' = 127 - j
-  const double* kr = a.kr64 + (int64_t)c * MS * KL;
-  for (int n = warp; n < MS; n += 6) {
-    double x[4], mx = 0.0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      x[q] = __ldg(kr + n * KL + lane + 32 * q);
-      mx = fmax(mx, fabs(x[q]));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const int e = mx > 0.0 ? max(-110, min(110, ilogb(mx))) : 0;
-    if (lane == 0) col_inv[n] = ldexpf(1.f, e - 14);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int kp = KL - 1 - (lane + 32 * q), ch = kp / 8, o = kp % 8;
-      const double xs = ldexp(x[q], 14 - e);
-      const __half h = __double2half(xs);
-      Bc[(ch * 2 * MS + n) * 8 + o] = h;
-      Bc[(ch * 2 * MS + MS + n) * 8 + o] = __double2half(xs - (double)__half2float(h));
-    }
+  // the channel's fp16 Krylov weights (bank_head_weights_kernel): 32 KB by one bulk copy
+  const __half* kw = a.kr16 + (int64_t)c * 2 * KL * MS;
+  if (tid == 0) {
+    mbar_init(&w_full, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(&w_full, 2 * KL * MS * 2);
+    bulk_g2s(Bc, kw, 2 * KL * MS * 2, &w_full);
   }
+  if (tid < MS) col_inv[tid] = __ldg(a.kinv + (int64_t)c * MS + tid);
   fence_async_smem();
   if (tid == 0) {
     for (int s = 0; s < 2; ++s) {
@@ -180,6 +170,7 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
     {                                             // whole warp: operands stay in uniform registers
       const uint32_t idesc = make_idesc(FMT_F16, TM, MS), idesc2 = make_idesc(FMT_F16, TM, 2 * MS);
       const uint32_t bc = smem_u32(Bc);
+      mbar_wait_u(&w_full, 0);                     // weights landed (async proxy: visible to the MMAs)
       for (int i = 0; i < nt; ++i) {
         const int slot = i & 1;
         mbar_wait_u(&z_full[slot], (uint32_t)((i >> 1) & 1));
@@ -263,6 +254,43 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
   }
   __syncthreads();
   if (warp == 1) tmem_dealloc<4 * MS>(tbase);
+}
+
+// Per channel, once per call: the Krylov weights W[n][j] (float64, lag j) -> exponent e_n with
+// max_j |W_nj| in [2^e_n, 2^(e_n + 1)), fp16 hi / lo of W * 2^(14 - e_n) at k' = 127 - j in the head's
+// shared-memory layout ([K chunk of 8][hi 64 | lo 64 rows][8]), and 2^(e_n - 14) (R33).
+__global__ void __launch_bounds__(256) bank_head_weights_kernel(const double* kr64, __half* kr16, float* kinv) {
+  constexpr int MS = 64;
+  const int c = blockIdx.x, warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const double* kr = kr64 + (int64_t)c * MS * KL;
+  __half* Bc = kr16 + (int64_t)c * 2 * KL * MS;
+  for (int n = warp; n < MS; n += 8) {
+    double x[4], mx = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      x[q] = kr[n * KL + lane + 32 * q];
+      mx = fmax(mx, fabs(x[q]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int e = mx > 0.0 ? max(-110, min(110, ilogb(mx))) : 0;
+    if (lane == 0) kinv[(int64_t)c * MS + n] = ldexpf(1.f, e - 14);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int kp = KL - 1 - (lane + 32 * q), ch = kp / 8, o = kp % 8;
+      const double xs = ldexp(x[q], 14 - e);
+      const __half h = __double2half(xs);
+      Bc[(ch * 2 * MS + n) * 8 + o] = h;
+      Bc[(ch * 2 * MS + MS + n) * 8 + o] = __double2half(xs - (double)__half2float(h));
+    }
+  }
+}
+
+int launch_bank_head_weights(const double* kr64, void* kr16, float* kinv, int n, cudaStream_t st) {
+  if (n <= 0) return CASC_OK;
+  bank_head_weights_kernel<<<n, 256, 0, st>>>(kr64, static_cast<__half*>(kr16), kinv);
+  CASC_LAUNCHED();
+  return CASC_OK;
 }
 
 int launch_bank_head_ws(int m, const BankHeadArg& a, int64_t n_seq_total, cudaStream_t st) {

@@ -1,13 +1,15 @@
 // Tensor-core bank path (SISO channels, fp32 mode): argument blocks and launchers.
 #pragma once
 #include "common.cuh"
+#include <cuda_fp16.h>
 
 namespace casc {
 
 struct BankHeadArg {
   const float* u;          // [n_ch][batch][L]
   const float* krT;        // [n_ch][2][MS][128]  hi | lo of Kr^T (k' = 127 - lag; CUDA-core head)
-  const double* kr64;      // [n_ch][MS][128]     Kr in float64 (lag j; the m = 64 fp16 head splits it)
+  const __half* kr16;      // [n_ch][16][2 * MS][8] fp16 hi | lo of the scaled weights (m = 64 head, R33)
+  const float* kinv;       // [n_ch][MS]          their inverse column scales 2^(e_n - 14)
   float* V;                // [n_ch][batch][L][MS]
   const int* sys_list; int n_list;
   int64_t L; int batch; int tiles_per_cta;
@@ -40,6 +42,7 @@ struct BankTailArg {
 bool bank_tc_supported(int m);
 int launch_bank_head(int m, const BankHeadArg& a, cudaStream_t st);
 int launch_bank_head_ws(int m, const BankHeadArg& a, int64_t n_seq_total, cudaStream_t st);
+int launch_bank_head_weights(const double* kr64, void* kr16, float* kinv, int n, cudaStream_t st);
 int launch_bank_stage_rp(int m, const BankStageArg& a, cudaStream_t st);
 int launch_bank_tail(int m, const BankTailArg& a, cudaStream_t st);
 int launch_bank_ab_tail(const BankAbTailArg& a, cudaStream_t st);
