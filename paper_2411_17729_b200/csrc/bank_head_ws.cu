@@ -134,8 +134,12 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
         if (lane + 32 * r < 255) mb = max(mb, __float_as_uint(fabsf(us[lane + 32 * r])));
       mb = __reduce_max_sync(0xffffffffu, mb);
       const float mx = __uint_as_float(mb);
+      // (exponents clamped to +-110 so that the scale and its inverse stay normal fp32 numbers: a
+      // window below 2^-110 in magnitude keeps only fp16's subnormal precision; inf / NaN propagate)
       const int et = mx > 0.f ? max(-110, min(110, ilogbf(mx))) : 0;
       const float sc = ldexpf(1.f, 14 - et);
+      // 4-deep ring: this write (tile i) follows z_empty of tile i - 2 (the MMA warp's commit), whose
+      // MMAs waited for tempty of tile i - 4, which the epilogue arrives after reading tile_inv[i & 3]
       if (lane == 0) tile_inv[i & 3] = ldexpf(1.f, et - 14);
 #pragma unroll
       for (int r = 0; r < 8; ++r) {               // Z-row w = (u[t0-127+w+q] * 2^(14 - et), q = 0..7)
