@@ -475,9 +475,8 @@ static int bank_wave(int n, int m, int64_t L, int batch, const int* N_host, int 
     CASC_TRY(cudaStreamWaitEvent(qs, q_start, 0));
     ProfScope ps(st, K_DERIVED, 0.0, 2.0 * n * (double)m * m * 128);
     if ((rc = launch_bank_derived(P.p64, N_max + 1, Bbar, C, D, dNeff, dKc, w.Kr64, w.krT, w.w64, w.w32, w.c32,
-                                  w.d32, use_ab ? w.pvec : nullptr, w.tri, fold, n, m, st)))
+                                  w.d32, use_ab ? w.pvec : nullptr, w.tri, fold, n, m, st, w.kr16, w.kinv)))
       return rc;
-    if (m == 64 && (rc = launch_bank_head_weights(w.Kr64, w.kr16, w.kinv, n, st))) return rc;
     for (int j = 0; j < qslots; ++j) {          // Q_k = P_{k+1} P_k for pass j (k = 7 + 2j)
       const int k = kHeadK + 2 * j;
       if (count_lp_ge(k + 2) == 0) continue;

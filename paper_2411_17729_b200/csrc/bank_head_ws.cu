@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
   const int seq = c * a.batch + b;
   const float* u = a.u + (int64_t)seq * a.L;
 
-  // the channel's fp16 Krylov weights (bank_head_weights_kernel): 32 KB by one bulk copy
+  // the channel's fp16 Krylov weights (bank_derived_kernel): 32 KB by one bulk copy
   const __half* kw = a.kr16 + (int64_t)c * 2 * KL * MS;
   if (tid == 0) {
     mbar_init(&w_full, 1);
@@ -258,43 +258,6 @@ __global__ void __launch_bounds__(192, 2) bank_head_ws_kernel(const __grid_const
   }
   __syncthreads();
   if (warp == 1) tmem_dealloc<4 * MS>(tbase);
-}
-
-// Per channel, once per call: the Krylov weights W[n][j] (float64, lag j) -> exponent e_n with
-// max_j |W_nj| in [2^e_n, 2^(e_n + 1)), fp16 hi / lo of W * 2^(14 - e_n) at k' = 127 - j in the head's
-// shared-memory layout ([K chunk of 8][hi 64 | lo 64 rows][8]), and 2^(e_n - 14) (R33).
-__global__ void __launch_bounds__(256) bank_head_weights_kernel(const double* kr64, __half* kr16, float* kinv) {
-  constexpr int MS = 64;
-  const int c = blockIdx.x, warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const double* kr = kr64 + (int64_t)c * MS * KL;
-  __half* Bc = kr16 + (int64_t)c * 2 * KL * MS;
-  for (int n = warp; n < MS; n += 8) {
-    double x[4], mx = 0.0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      x[q] = kr[n * KL + lane + 32 * q];
-      mx = fmax(mx, fabs(x[q]));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const int e = mx > 0.0 ? max(-110, min(110, ilogb(mx))) : 0;
-    if (lane == 0) kinv[(int64_t)c * MS + n] = ldexpf(1.f, e - 14);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int kp = KL - 1 - (lane + 32 * q), ch = kp / 8, o = kp % 8;
-      const double xs = ldexp(x[q], 14 - e);
-      const __half h = __double2half(xs);
-      Bc[(ch * 2 * MS + n) * 8 + o] = h;
-      Bc[(ch * 2 * MS + MS + n) * 8 + o] = __double2half(xs - (double)__half2float(h));
-    }
-  }
-}
-
-int launch_bank_head_weights(const double* kr64, void* kr16, float* kinv, int n, cudaStream_t st) {
-  if (n <= 0) return CASC_OK;
-  bank_head_weights_kernel<<<n, 256, 0, st>>>(kr64, static_cast<__half*>(kr16), kinv);
-  CASC_LAUNCHED();
-  return CASC_OK;
 }
 
 int launch_bank_head_ws(int m, const BankHeadArg& a, int64_t n_seq_total, cudaStream_t st) {

@@ -20,6 +20,7 @@
 #include "kernels.cuh"
 #include "sm100.cuh"
 #include "bank_tc.cuh"
+#include <cuda_fp16.h>
 #include "bank_common.cuh"
 
 namespace casc {
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(256) bank_derived_kernel(const double* p64, in
                                                            const double* C, const double* D, const int* Neff,
                                                            const int* Kc, double* Kr64, float* krT, double* w64,
                                                            float* w32, float* c32, float* d32, float* pvec,
-                                                           int* tri, int fold, int ms) {
+                                                           int* tri, int fold, int ms, __half* kr16, float* kinv) {
   extern __shared__ double dsm[];
   double* Ps = dsm;                         // [ms][ms+1]
   double* Kr = Ps + ms * (ms + 1);          // [ms][129]
@@ -289,6 +290,34 @@ __global__ void __launch_bounds__(256) bank_derived_kernel(const double* p64, in
     krT[(int64_t)s * 2 * ms * 128 + r * 128 + kp] = hi;
     krT[(int64_t)s * 2 * ms * 128 + ms * 128 + r * 128 + kp] = tf32_rna((float)(v - (double)hi));
   }
+  // m = 64: the head's fp16 weights (R33) from the same Kr in shared memory: per column n
+  // the exponent e_n of max_j |W_nj|, fp16 hi / lo of W * 2^(14 - e_n) at k' = 127 - j in the head's
+  // shared-memory layout ([K chunk of 8][hi 64 | lo 64 rows][8]), and 2^(e_n - 14)
+  if (kr16 != nullptr && ms == 64) {
+    const int warp = tid / 32, lane = tid % 32;
+    __half* Bh = kr16 + (int64_t)s * 2 * 128 * 64;
+    for (int n = warp; n < 64; n += 8) {
+      double x[4], mx = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = lane + 32 * q;
+        x[q] = (j < (1 << kc)) ? Kr[n * 129 + j] : 0.0;
+        mx = fmax(mx, fabs(x[q]));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const int e = mx > 0.0 ? max(-110, min(110, ilogb(mx))) : 0;
+      if (lane == 0) kinv[(int64_t)s * 64 + n] = ldexpf(1.f, e - 14);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int kp = 127 - (lane + 32 * q), ch = kp / 8, o = kp % 8;
+        const double xs = ldexp(x[q], 14 - e);
+        const __half h = __double2half(xs);
+        Bh[(ch * 128 + n) * 8 + o] = h;
+        Bh[(ch * 128 + 64 + n) * 8 + o] = __double2half(xs - (double)__half2float(h));
+      }
+    }
+  }
   // w = C P_Ne (row vector times matrix), and fp32 copies; P_Ne staged through shared memory
   const double* PN = Ps0 + (int64_t)Neff[s] * mm;
   __syncthreads();                                 // Ps (the last P_i) and Kr reads done
@@ -328,12 +357,13 @@ __global__ void __launch_bounds__(256) bank_derived_kernel(const double* p64, in
 
 int launch_bank_derived(const double* p64, int slots, const double* Bbar, const double* C, const double* D,
                         const int* Neff, const int* Kc, double* Kr64, float* krT, double* w64, float* w32,
-                        float* c32, float* d32, float* pvec, int* tri, int fold, int n, int ms, cudaStream_t st) {
+                        float* c32, float* d32, float* pvec, int* tri, int fold, int n, int ms, cudaStream_t st,
+                        void* kr16, float* kinv) {
   const size_t smem = (size_t)(ms * (ms + 1) + ms * 129) * sizeof(double);
   if (cudaFuncSetAttribute(bank_derived_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return CASC_ERR_CUDA;
   bank_derived_kernel<<<n, 256, smem, st>>>(p64, slots, Bbar, C, D, Neff, Kc, Kr64, krT, w64, w32, c32, d32, pvec,
-                                            tri, fold, ms);
+                                            tri, fold, ms, static_cast<__half*>(kr16), kinv);
   CASC_LAUNCHED();
   return CASC_OK;
 }

@@ -42,12 +42,12 @@ struct BankTailArg {
 bool bank_tc_supported(int m);
 int launch_bank_head(int m, const BankHeadArg& a, cudaStream_t st);
 int launch_bank_head_ws(int m, const BankHeadArg& a, int64_t n_seq_total, cudaStream_t st);
-int launch_bank_head_weights(const double* kr64, void* kr16, float* kinv, int n, cudaStream_t st);
 int launch_bank_stage_rp(int m, const BankStageArg& a, cudaStream_t st);
 int launch_bank_tail(int m, const BankTailArg& a, cudaStream_t st);
 int launch_bank_ab_tail(const BankAbTailArg& a, cudaStream_t st);
 int launch_bank_derived(const double* p64, int slots, const double* Bbar, const double* C, const double* D,
                         const int* Neff, const int* Kc, double* Kr64, float* krT, double* w64, float* w32,
-                        float* c32, float* d32, float* pvec, int* tri, int fold, int n, int ms, cudaStream_t st);
+                        float* c32, float* d32, float* pvec, int* tri, int fold, int n, int ms, cudaStream_t st,
+                        void* kr16 = nullptr, float* kinv = nullptr);
 
 }  // namespace casc
